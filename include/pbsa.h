@@ -1,0 +1,150 @@
+/*
+ * pbsa.h -- C ABI of the B200-native p-bit simulated-annealing sweep.
+ *
+ * Drop-in boundary for the reference's one hot loop,
+ *   pbitsa._kernels.anneal_loop(indptr, indices, values, h, me_i, me_j, me_w,
+ *                               ge_i, ge_j, ge_w, lam, delta, period, i0_min,
+ *                               beta, cycles, t_res, algo, alpha, p_stall, key)
+ *   (/root/reference/pkg/src/pbitsa/_kernels.py:68-175, called from
+ *    annealer.run_anneal, annealer.py:216-238, one trial per call)
+ * generalised to T independent trials per call, which is how
+ * engine.run_trials (engine.py:82-127) fans it out.  Every argument keeps the
+ * reference's meaning and dtype; outputs are the same 8 arrays stacked over
+ * trials.  Plain pointers and sizes only; all buffers are HOST memory unless
+ * a function says otherwise.  Every function returns PBSA_OK (0) or a
+ * negative status; pbsa_last_error() then describes the failure (thread-local).
+ * Thread-safe: no global mutable state; a plan is used by one thread at a time.
+ */
+#ifndef PBSA_H
+#define PBSA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBSA_ABI_VERSION 1
+
+enum {
+    PBSA_OK = 0,
+    PBSA_EINVAL = -1, /* invalid argument (ValueError on the Python side) */
+    PBSA_ECUDA = -2,  /* CUDA runtime error                                */
+    PBSA_ENOMEM = -3, /* host or device allocation failed                  */
+};
+
+/* Input rule codes, identical to _kernels.py:38-41 (ALGO_PSA/TAPSA/SPSA). */
+enum { PBSA_ALGO_PSA = 0, PBSA_ALGO_TAPSA = 1, PBSA_ALGO_SPSA = 2 };
+
+/* Which device path a plan runs (pbsa_plan_info). */
+enum { PBSA_PATH_PACKED = 1, PBSA_PATH_GENERAL = 2 };
+
+typedef struct pbsa_plan pbsa_plan;
+
+int pbsa_abi_version(void);
+const char *pbsa_last_error(void);
+int pbsa_device_count(int *count);
+
+/*
+ * Upload one batch of trials to `device` and build its device-resident
+ * state (CSR adjacency, per-trial key prefixes, profiles, schedule tables).
+ *
+ *   n, indptr[n+1], indices[nnz], values[nnz], h[n]      IsingModel CSR
+ *        (model.py:21-33, 84-128; int64 / float64 exactly as the reference)
+ *   mm, me_i/me_j[mm], me_w[mm]                          model edges (energy)
+ *   gm, ge_i/ge_j/ge_w[gm]                               graph edges (cut);
+ *        gm = 0 means "no graph" (annealer.py:208-213): cut outputs are 0
+ *   lam, delta (float64), period (int64)                 VariabilityProfile;
+ *        rows of n, `profile_stride` = 0 (one profile shared by all trials)
+ *        or n (row t belongs to trial t).  NULL for all three = ideal.
+ *   i0_min, beta, cycles, t_res                          AnnealSchedule
+ *   algo, alpha, p_stall                                 AlgorithmConfig
+ *        (alpha = 1 unless TAPSA, annealer.py:235)
+ *   trials, keys[trials]                                 run_key(seed) per trial
+ *        (streams.py:58-60)
+ */
+int pbsa_plan_create(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                     const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                     const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                     const int64_t *ge_j, const int64_t *ge_w, const double *lam,
+                     const double *delta, const int64_t *period, int64_t profile_stride,
+                     double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                     int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                     pbsa_plan **out);
+
+/*
+ * Run the whole anneal on the device from the initial spins: `cycles` main
+ * cycles of `t_res` synchronous sub-steps each, per-cycle energy/cut traces.
+ * Inputs are already resident; nothing crosses PCIe.  *device_ms (optional)
+ * receives the CUDA-event time of the run on the plan's stream.
+ */
+int pbsa_plan_run(pbsa_plan *plan, float *device_ms);
+
+/*
+ * Copy the results of the last run back, in anneal_loop's return order
+ * (_kernels.py:175), stacked over trials (row t = trial t):
+ *   spins[T*n] int8, inputs[T*n] f64, hist[T*n*alpha] f64, counts[T*n] i64,
+ *   trace_i0[T*cycles] f64, trace_energy[T*cycles] f64,
+ *   trace_cut[T*cycles] i64, best_cut[T] i64.
+ * Any output pointer may be NULL to skip it.
+ */
+int pbsa_plan_download(pbsa_plan *plan, int8_t *spins, double *inputs, double *hist,
+                       int64_t *counts, double *trace_i0, double *trace_energy,
+                       int64_t *trace_cut, int64_t *best_cut);
+
+/*
+ * Device-side summary of the last run without downloading traces:
+ * final_cut_sum = sum over trials of the last-cycle cut, best_cut_max = max
+ * over trials of best cut, updates = total p-bit updates performed.
+ */
+int pbsa_plan_summary(pbsa_plan *plan, int64_t *final_cut_sum, int64_t *best_cut_max,
+                      int64_t *updates);
+
+/*
+ * Plan facts: path (PBSA_PATH_*), launches per run, the dominant sweep
+ * kernel's mean per-launch time of the last run in ms (CUDA events on the
+ * plan stream) and its launch count, and the trial-word count.
+ */
+int pbsa_plan_info(const pbsa_plan *plan, int *path, int64_t *launches_per_run,
+                   double *sweep_ms_mean, int64_t *sweep_launches, int64_t *words);
+
+int pbsa_plan_destroy(pbsa_plan *plan);
+
+/*
+ * One-shot batched anneal_loop: create + run + download + destroy, all host
+ * buffers (the end-to-end path engine.run_trials / annealer.run_anneal use).
+ * Output layout as pbsa_plan_download; *device_ms as pbsa_plan_run.
+ */
+int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                           const double *values, const double *h, int64_t mm,
+                           const int64_t *me_i, const int64_t *me_j, const double *me_w,
+                           int64_t gm, const int64_t *ge_i, const int64_t *ge_j,
+                           const int64_t *ge_w, const double *lam, const double *delta,
+                           const int64_t *period, int64_t profile_stride, double i0_min,
+                           double beta, int64_t cycles, int64_t t_res, int algo, int64_t alpha,
+                           double p_stall, int64_t trials, const uint64_t *keys, int8_t *spins,
+                           double *inputs, double *hist, int64_t *counts, double *trace_i0,
+                           double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
+                           float *device_ms);
+
+/*
+ * Device self-checks (used by the parity tests): evaluate the device
+ * counter hash stream_u64(key, tag, a, b) (streams.py:41-45) and the device
+ * tanh on `count` host inputs.
+ */
+int pbsa_debug_stream_u64(int device, int64_t count, const uint64_t *key, const uint64_t *tag,
+                          const uint64_t *a, const uint64_t *b, uint64_t *out);
+int pbsa_debug_tanh(int device, int64_t count, const double *x, double *out);
+
+/* Host builds of device-side pieces (no GPU needed):
+ *   pbsa_libm_tanh_host  -- the device tanh (same source, libm_tanh.cuh);
+ *   pbsa_threshold_host  -- the packed path's activation threshold for a
+ *     tanh value t: the update is +1 iff hash >= threshold, exactly when
+ *     r + t >= 0 with r = 2 u01 - 1 (_kernels.py:149-152); ~0 means never. */
+double pbsa_libm_tanh_host(double x);
+uint64_t pbsa_threshold_host(double t);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBSA_H */

@@ -1,0 +1,241 @@
+"""ctypes binding of the C ABI in include/pbsa.h (libpbsa.so, built in-tree).
+
+This is the only route from the Python API to the compute: there is no CPU
+fallback.  If the library is missing or no CUDA device is visible, every
+compute entry point raises ``RuntimeError``.  ctypes releases the GIL for the
+duration of each call, so trials sharded over threads/devices overlap.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpbsa.so"
+
+PBSA_OK = 0
+PATH_PACKED, PATH_GENERAL = 1, 2
+
+_lib: ctypes.CDLL | None = None
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_F64 = ctypes.c_double
+
+# (name, restype, argtypes)
+_SIGNATURES = [
+    ("pbsa_abi_version", ctypes.c_int, []),
+    ("pbsa_last_error", ctypes.c_char_p, []),
+    ("pbsa_device_count", ctypes.c_int, [ctypes.POINTER(ctypes.c_int)]),
+    ("pbsa_plan_create", ctypes.c_int,
+     [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
+      _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.POINTER(_P)]),
+    ("pbsa_plan_run", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_float)]),
+    ("pbsa_plan_download", ctypes.c_int, [_P] + [_P] * 8),
+    ("pbsa_plan_summary", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                                         ctypes.POINTER(_I64)]),
+    ("pbsa_plan_info", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_I64),
+                                      ctypes.POINTER(_F64), ctypes.POINTER(_I64),
+                                      ctypes.POINTER(_I64)]),
+    ("pbsa_plan_destroy", ctypes.c_int, [_P]),
+    ("pbsa_anneal_loop_batch", ctypes.c_int,
+     [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
+      _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P] + [_P] * 8
+     + [ctypes.POINTER(ctypes.c_float)]),
+    ("pbsa_debug_stream_u64", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P, _P, _P]),
+    ("pbsa_debug_tanh", ctypes.c_int, [ctypes.c_int, _I64, _P, _P]),
+    ("pbsa_libm_tanh_host", _F64, [_F64]),
+    ("pbsa_threshold_host", ctypes.c_uint64, [_F64]),
+]
+
+EXPORTED = [name for name, _, _ in _SIGNATURES]
+
+
+def load() -> ctypes.CDLL:
+    """Load libpbsa.so; raises RuntimeError (never falls back) if it is absent."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"CUDA library {LIB_PATH} is not built; run __graft_entry__.build() "
+                "(there is no CPU fallback for the annealing sweep)")
+        lib = ctypes.CDLL(str(LIB_PATH))
+        for name, res, args in _SIGNATURES:
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != PBSA_OK:
+        msg = load().pbsa_last_error().decode(errors="replace")
+        if rc == -1:
+            raise ValueError(msg)
+        raise RuntimeError(f"pbsa error {rc}: {msg}")
+
+
+def device_count() -> int:
+    c = ctypes.c_int(0)
+    rc = load().pbsa_device_count(ctypes.byref(c))
+    return c.value if rc == PBSA_OK else 0
+
+
+def require_device(device: int) -> None:
+    n = device_count()
+    if n < 1:
+        raise RuntimeError("no CUDA device visible: the p-bit sweep runs only on the GPU "
+                           "(libpbsa.so, sm_100a); there is no CPU fallback")
+    if not 0 <= device < n:
+        raise RuntimeError(f"device {device} out of range (have {n})")
+
+
+def _ptr(a) -> int:
+    return 0 if a is None or a.size == 0 else a.ctypes.data
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+class Batch:
+    """Host-side arguments of one batched anneal_loop call (_kernels.py:69-91)."""
+
+    def __init__(self, model, schedule, keys, profile_rows=None, graph=None, algo_code=0,
+                 alpha=1, p_stall=0.5):
+        self.n = int(model.n)
+        self.indptr = _c(model.indptr, np.int64)
+        self.indices = _c(model.indices, np.int64)
+        self.values = _c(model.values, np.float64)
+        self.h = _c(model.h, np.float64)
+        self.me_i = _c(model.edge_i, np.int64)
+        self.me_j = _c(model.edge_j, np.int64)
+        self.me_w = _c(model.edge_w, np.float64)
+        if graph is not None:
+            self.ge_i = _c(graph.edge_i, np.int64)
+            self.ge_j = _c(graph.edge_j, np.int64)
+            self.ge_w = _c(graph.edge_w, np.int64)
+        else:
+            self.ge_i = self.ge_j = self.ge_w = np.empty(0, np.int64)
+        self.keys = np.asarray(keys, dtype=np.uint64)
+        self.T = int(self.keys.size)
+        # profile_rows: None (ideal), or (lam, delta, period, stride)
+        if profile_rows is None:
+            self.lam = self.delta = self.period = None
+            self.stride = 0
+        else:
+            lam, delta, period, stride = profile_rows
+            self.lam, self.delta = _c(lam, np.float64), _c(delta, np.float64)
+            self.period, self.stride = _c(period, np.int64), int(stride)
+        self.i0_min, self.beta = float(schedule.i0_min), float(schedule.beta)
+        self.cycles, self.t_res = int(schedule.cycles), int(schedule.t_res)
+        self.algo, self.alpha, self.p_stall = int(algo_code), int(alpha), float(p_stall)
+
+    def _args(self):
+        return (self.n, _ptr(self.indptr), _ptr(self.indices), _ptr(self.values), _ptr(self.h),
+                int(self.me_i.size), _ptr(self.me_i), _ptr(self.me_j), _ptr(self.me_w),
+                int(self.ge_i.size), _ptr(self.ge_i), _ptr(self.ge_j), _ptr(self.ge_w),
+                _ptr(self.lam), _ptr(self.delta), _ptr(self.period), self.stride,
+                self.i0_min, self.beta, self.cycles, self.t_res, self.algo, self.alpha,
+                self.p_stall, self.T, _ptr(self.keys))
+
+    def alloc_outputs(self) -> dict:
+        T, n, C = self.T, self.n, self.cycles
+        return dict(spins=np.empty((T, n), np.int8), inputs=np.empty((T, n)),
+                    hist=np.empty((T, n, self.alpha)), counts=np.empty((T, n), np.int64),
+                    i0_trace=np.empty((T, C)), energy_trace=np.empty((T, C)),
+                    cut_trace=np.empty((T, C), np.int64), best_cut=np.empty(T, np.int64))
+
+
+OUT_ORDER = ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "cut_trace",
+             "best_cut")
+
+
+def anneal_batch(batch: Batch, device: int = 0) -> tuple[dict, float]:
+    """One-shot pbsa_anneal_loop_batch; returns (outputs, device milliseconds)."""
+    lib = load()
+    require_device(device)
+    out = batch.alloc_outputs()
+    ms = ctypes.c_float(0.0)
+    _check(lib.pbsa_anneal_loop_batch(device, *batch._args(),
+                                      *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))
+    return out, float(ms.value)
+
+
+class Plan:
+    """Device-resident batch: create once, run many times (bench `value` path)."""
+
+    def __init__(self, batch: Batch, device: int = 0):
+        lib = load()
+        require_device(device)
+        self.batch, self.device = batch, device
+        h = _P()
+        _check(lib.pbsa_plan_create(device, *batch._args(), ctypes.byref(h)))
+        self._h = h
+
+    def run(self) -> float:
+        ms = ctypes.c_float(0.0)
+        _check(load().pbsa_plan_run(self._h, ctypes.byref(ms)))
+        return float(ms.value)
+
+    def download(self) -> dict:
+        out = self.batch.alloc_outputs()
+        _check(load().pbsa_plan_download(self._h, *(_ptr(out[k]) for k in OUT_ORDER)))
+        return out
+
+    def summary(self) -> tuple[int, int, int]:
+        a, b, c = _I64(), _I64(), _I64()
+        _check(load().pbsa_plan_summary(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def info(self) -> dict:
+        path, launches, sweeps, words = ctypes.c_int(), _I64(), _I64(), _I64()
+        ms = _F64()
+        _check(load().pbsa_plan_info(self._h, ctypes.byref(path), ctypes.byref(launches),
+                                     ctypes.byref(ms), ctypes.byref(sweeps), ctypes.byref(words)))
+        return dict(path={1: "packed", 2: "general"}.get(path.value, "?"),
+                    launches=launches.value, sweep_ms_mean=ms.value,
+                    sweep_launches=sweeps.value, words=words.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            load().pbsa_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def debug_stream_u64(keys, tags, a, b, device: int = 0) -> np.ndarray:
+    lib = load()
+    require_device(device)
+    arrs = [np.ascontiguousarray(x, dtype=np.uint64) for x in (keys, tags, a, b)]
+    out = np.empty(arrs[0].size, np.uint64)
+    _check(lib.pbsa_debug_stream_u64(device, out.size, *(x.ctypes.data for x in arrs),
+                                     out.ctypes.data))
+    return out
+
+
+def debug_tanh(x, device: int = 0) -> np.ndarray:
+    lib = load()
+    require_device(device)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    _check(lib.pbsa_debug_tanh(device, x.size, x.ctypes.data, out.ctypes.data))
+    return out
+
+
+def default_device() -> int:
+    """Device ordinal from PBSA_DEVICE or LOCAL_RANK (one process per GPU), else 0."""
+    for var in ("PBSA_DEVICE", "LOCAL_RANK"):
+        v = os.environ.get(var)
+        if v is not None and v.strip():
+            return int(v)
+    return 0

@@ -1,0 +1,917 @@
+// pbsa.cu -- host runtime and C ABI (include/pbsa.h) of the B200 pSA sweep.
+//
+// A plan owns one batch of trials on one device: the device CSR, per-trial
+// key prefixes, profiles, schedule tables, double-buffered spin state and the
+// per-cycle accumulators.  pbsa_plan_run replays one CUDA graph containing
+// the whole anneal (init, one sweep launch per active sub-step, per-cycle
+// statistics, trace finalisation), so a 1000-cycle run is a single graph
+// launch.  The reference loop being replaced is
+// /root/reference/pkg/src/pbitsa/_kernels.py:68-175 (see pbsa_device.cuh).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pbsa.h"
+#include "pbsa_device.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw Error(code, buf);
+}
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            fail(e_ == cudaErrorMemoryAllocation ? PBSA_ENOMEM : PBSA_ECUDA, "%s: %s (%s:%d)", \
+                 #call, cudaGetErrorString(e_), __FILE__, __LINE__);                    \
+    } while (0)
+
+template <typename F>
+int guarded(F &&f) {
+    try {
+        f();
+        return PBSA_OK;
+    } catch (const Error &e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        g_last_error = "host allocation failed";
+        return PBSA_ENOMEM;
+    } catch (const std::exception &e) {
+        g_last_error = e.what();
+        return PBSA_EINVAL;
+    }
+}
+
+// -------------------------------------------------------------- host hash
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
+uint64_t hmix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D4A04C32684F87ULL;
+    return z ^ (z >> 31);
+}
+uint64_t habsorb(uint64_t h, uint64_t w) { return hmix64((h + kGamma) ^ w); }
+
+// Smallest integer U with U * 2^-52 - 1 + t >= 0, i.e. ceil((1 - t) * 2^52),
+// computed exactly from t's binary representation (t in [-1, 1]).
+uint64_t threshold_u53(double t) {
+    if (t == 0.0) return 1ULL << 52;
+    int e;
+    const double f = std::frexp(t, &e);                  // t = f 2^e, |f| in [0.5, 1)
+    const int64_t M = (int64_t)std::ldexp(f, 53);        // exact 53-bit integer
+    const int sh = e - 1;                                // t * 2^52 = M * 2^sh
+    const int64_t two52 = 1LL << 52;
+    if (sh >= 0) return (uint64_t)(two52 - (M << sh));
+    const int k = -sh;
+    if (M > 0) {
+        if (k >= 63) return (uint64_t)two52;             // ceil(2^52 - tiny)
+        return (uint64_t)(two52 - (M >> k));
+    }
+    const int64_t A = -M;
+    if (k >= 63) return (uint64_t)two52 + 1;
+    const int64_t q = (A >> k) + ((A & ((1LL << k) - 1)) ? 1 : 0);
+    return (uint64_t)(two52 + q);
+}
+
+uint64_t threshold_h64(double t) {
+    const uint64_t u = threshold_u53(t);
+    if (u >= (1ULL << 53)) return ~0ULL;  // never +1
+    return u << 11;
+}
+
+int next_pow2(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+template <typename T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void upload(const T *src, size_t count, cudaStream_t st) {
+        alloc(count);
+        if (count) CK(cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
+    }
+    void upload(const std::vector<T> &v, cudaStream_t st) { upload(v.data(), v.size(), st); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+};
+
+int64_t grid_for(int64_t work, int threads) { return (work + threads - 1) / threads; }
+
+}  // namespace
+
+struct pbsa_plan {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_sweep0 = nullptr, ev_sweep1 = nullptr, ev_end = nullptr;
+    bool ran = false;
+
+    // problem
+    int64_t n = 0, T = 0, Tp = 0, W = 0, cycles = 0, t_res = 0, alpha = 1, nnz = 0;
+    int algo = 0;
+    double p_stall = 0.5;
+    int path = 0;
+    bool has_graph = false;
+    bool int_energy = true;
+    bool tapsa_hist_from_raw = false;  // TAPSA alpha=1 routed to the packed path
+    int64_t total_w = 0;
+    std::vector<double> i0;
+    std::vector<uint32_t> active_counts;  // general path: sub-steps with any update
+    int64_t launches = 0, sweep_launches = 0;
+    int64_t updates_per_run = 0;
+
+    // packed path
+    int L = 1, dmax = 0, K = 1;
+    int warps_per_word = 1, chunks = 1, packed_blocks = 1;
+    DevBuf<uint32_t> p_spins[2], rowptr, adj;
+    DevBuf<uint64_t> thr, krg;
+    DevBuf<unsigned long long> pacc;  // [(C+1)][Tp]
+    DevBuf<int16_t> raw_last;         // [n][Tp]
+
+    // general path
+    DevBuf<int8_t> g_spins[2];
+    DevBuf<uint32_t> col, me_i, me_j, ge_i, ge_j;
+    DevBuf<double> val, h, me_w, lam, delta, inputs, hist, e_f64;
+    DevBuf<int64_t> me_wi, h_int, ge_w;
+    DevBuf<int32_t> period, counts;
+    DevBuf<uint64_t> kr, kst;
+    DevBuf<unsigned long long> cut_acc, e_acc;  // [C][Tp]
+    int shared_profile = 0;
+    bool has_lam = false, has_delta = false, has_period = false;
+
+    DevBuf<uint64_t> kspin;
+    // outputs
+    DevBuf<int64_t> trace_cut, best;
+    DevBuf<double> trace_energy;
+    int final_parity = 0;  // which spin buffer holds the final state
+
+    ~pbsa_plan() {
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        for (cudaEvent_t e : {ev_start, ev_sweep0, ev_sweep1, ev_end})
+            if (e) cudaEventDestroy(e);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        CK(cudaGetDevice(&prev));
+        CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+bool is_integral(double x) { return std::isfinite(x) && x == std::nearbyint(x) && std::fabs(x) < 2147483647.0; }
+
+template <typename K>
+void set_packed_smem(K kernel, size_t bytes) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+using PackedKernel = void (*)(pbsa::PackedArgs);
+PackedKernel packed_kernel_for(int L) {
+    switch (L) {
+        case 1: return pbsa::packed_sweep<1>;
+        case 2: return pbsa::packed_sweep<2>;
+        case 3: return pbsa::packed_sweep<3>;
+        case 4: return pbsa::packed_sweep<4>;
+        case 5: return pbsa::packed_sweep<5>;
+        case 6: return pbsa::packed_sweep<6>;
+        case 7: return pbsa::packed_sweep<7>;
+        default: fail(PBSA_EINVAL, "packed path supports degree <= 127");
+    }
+}
+
+void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
+                 const int64_t *indices, const double *values, const double *hv, int64_t mm,
+                 const int64_t *mei, const int64_t *mej, const double *mew, int64_t gm,
+                 const int64_t *gei, const int64_t *gej, const int64_t *gew, const double *lam,
+                 const double *delta, const int64_t *period, int64_t pstride, double i0_min,
+                 double beta, int64_t cycles, int64_t t_res, int algo, int64_t alpha,
+                 double p_stall, int64_t trials, const uint64_t *keys) {
+    // ------------------------------------------------------- validation
+    if (n < 1 || n > INT32_MAX / 2) fail(PBSA_EINVAL, "n must be in [1, 2^30), got %lld", (long long)n);
+    if (trials < 1 || trials > (1LL << 24)) fail(PBSA_EINVAL, "trials must be in [1, 2^24]");
+    if (cycles < 1) fail(PBSA_EINVAL, "cycles must be >= 1");
+    if (t_res < 1) fail(PBSA_EINVAL, "t_res must be >= 1");
+    if (cycles * t_res >= (1LL << 31)) fail(PBSA_EINVAL, "cycles * t_res must be < 2^31");
+    if (algo < 0 || algo > 2) fail(PBSA_EINVAL, "algo must be 0 (psa), 1 (tapsa) or 2 (spsa)");
+    if (alpha < 1 || alpha > 4096) fail(PBSA_EINVAL, "alpha must be in [1, 4096]");
+    if (!(p_stall >= 0.0 && p_stall <= 1.0)) fail(PBSA_EINVAL, "p_stall must lie in [0, 1]");
+    if (!(i0_min > 0.0) || !(beta > 0.0)) fail(PBSA_EINVAL, "i0_min and beta must be > 0");
+    if (!indptr || !hv || !keys) fail(PBSA_EINVAL, "null model/keys pointer");
+    if (indptr[n] > 0 && (!indices || !values)) fail(PBSA_EINVAL, "null CSR pointer");
+    if ((mm > 0 && (!mei || !mej || !mew)) || (gm > 0 && (!gei || !gej || !gew)))
+        fail(PBSA_EINVAL, "null edge pointer");
+    if (pstride != 0 && pstride != n) fail(PBSA_EINVAL, "profile_stride must be 0 or n");
+    if ((lam == nullptr) != (delta == nullptr) || (lam == nullptr) != (period == nullptr))
+        fail(PBSA_EINVAL, "lam, delta and period must all be given or all be NULL");
+    if (indptr[0] != 0) fail(PBSA_EINVAL, "indptr[0] must be 0");
+    for (int64_t i = 0; i < n; ++i)
+        if (indptr[i + 1] < indptr[i]) fail(PBSA_EINVAL, "indptr must be non-decreasing");
+    const int64_t nnz = indptr[n];
+    if (nnz >= (1LL << 31)) fail(PBSA_EINVAL, "too many couplings");
+    for (int64_t k = 0; k < nnz; ++k)
+        if (indices[k] < 0 || indices[k] >= n) fail(PBSA_EINVAL, "CSR index out of range");
+    for (int64_t k = 0; k < mm; ++k)
+        if (mei[k] < 0 || mei[k] >= n || mej[k] < 0 || mej[k] >= n)
+            fail(PBSA_EINVAL, "model edge out of range");
+    for (int64_t k = 0; k < gm; ++k)
+        if (gei[k] < 0 || gei[k] >= n || gej[k] < 0 || gej[k] >= n)
+            fail(PBSA_EINVAL, "graph edge out of range");
+    const int64_t prow = pstride ? trials : 1;
+    if (period)
+        for (int64_t k = 0; k < prow * n; ++k)
+            if (period[k] < 1) fail(PBSA_EINVAL, "period entries must be >= 1");
+
+    P.device = device;
+    P.n = n;
+    P.T = trials;
+    P.W = (trials + 31) / 32;
+    P.Tp = P.W * 32;
+    P.cycles = cycles;
+    P.t_res = t_res;
+    P.algo = algo;
+    P.alpha = alpha;
+    P.p_stall = p_stall;
+    P.nnz = nnz;
+    P.has_graph = gm > 0;
+
+    P.i0.resize(cycles);
+    {
+        double x = i0_min;  // repeated division, as run (_kernels.py:118, 172-173)
+        for (int64_t c = 0; c < cycles; ++c) {
+            P.i0[c] = x;
+            if (c < cycles - 1) x = x / beta;
+        }
+    }
+
+    // --------------------------------------------------- path selection
+    bool unit_J = true, zero_h = true;
+    int64_t dmax = 0;
+    for (int64_t k = 0; k < nnz; ++k)
+        if (values[k] != 1.0 && values[k] != -1.0) { unit_J = false; break; }
+    for (int64_t i = 0; i < n; ++i) {
+        if (hv[i] != 0.0) zero_h = false;
+        dmax = std::max<int64_t>(dmax, indptr[i + 1] - indptr[i]);
+    }
+    bool ideal = true;
+    if (lam) {
+        for (int64_t k = 0; k < prow * n && ideal; ++k)
+            if (lam[k] != 1.0 || delta[k] != 0.0 || period[k] != t_res) ideal = false;
+    }
+    bool graph_is_model = true;
+    if (P.has_graph) {
+        if (gm != mm) graph_is_model = false;
+        for (int64_t k = 0; k < gm && graph_is_model; ++k)
+            if (gei[k] != mei[k] || gej[k] != mej[k] || (double)(-gew[k]) != mew[k])
+                graph_is_model = false;
+        for (int64_t k = 0; k < gm; ++k) P.total_w += gew[k];
+    }
+    const bool rule_is_psa = algo == 0 || (algo == 1 && alpha == 1) || (algo == 2 && p_stall == 0.0);
+    const bool packed = rule_is_psa && unit_J && zero_h && ideal && graph_is_model && dmax <= 127;
+    P.tapsa_hist_from_raw = packed && algo == 1;
+    P.path = packed ? PBSA_PATH_PACKED : PBSA_PATH_GENERAL;
+
+    DeviceGuard dg(device);
+    CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+    for (cudaEvent_t *e : {&P.ev_start, &P.ev_sweep0, &P.ev_sweep1, &P.ev_end}) CK(cudaEventCreate(e));
+    cudaStream_t st = P.stream;
+
+    // per-trial key prefixes (streams.py: draws are absorb^3(key, tag, a, b))
+    std::vector<uint64_t> kspin(P.Tp, 0), kr(P.Tp, 0), kst(P.Tp, 0);
+    for (int64_t t = 0; t < trials; ++t) {
+        kspin[t] = habsorb(keys[t], 2);
+        kr[t] = habsorb(keys[t], 3);
+        kst[t] = habsorb(keys[t], 4);
+    }
+    P.kspin.upload(kspin, st);
+
+    std::vector<uint32_t> rowptr(n + 1);
+    for (int64_t i = 0; i <= n; ++i) rowptr[i] = (uint32_t)indptr[i];
+    P.rowptr.upload(rowptr, st);
+
+    if (packed) {
+        // ---------------------------------------------------- packed setup
+        P.dmax = (int)dmax;
+        P.L = 1;
+        while ((1 << P.L) - 1 < dmax) ++P.L;
+        P.K = 2 * P.dmax + 1;
+        std::vector<uint32_t> adjv(nnz);
+        for (int64_t k = 0; k < nnz; ++k)
+            adjv[k] = (uint32_t)indices[k] | (values[k] < 0 ? 0x80000000u : 0u);
+        P.adj.upload(adjv, st);
+        std::vector<uint64_t> krg(P.Tp);
+        for (int64_t t = 0; t < P.Tp; ++t) krg[t] = kr[t] + kGamma;
+        P.krg.upload(krg, st);
+        // thresholds per (cycle, raw): inp = i0 * raw; act = r + tanh(inp) (lam = 1, delta = 0)
+        std::vector<uint64_t> thr((size_t)cycles * P.K);
+        for (int64_t c = 0; c < cycles; ++c)
+            for (int raw = -P.dmax; raw <= P.dmax; ++raw)
+                thr[(size_t)c * P.K + raw + P.dmax] =
+                    threshold_h64(pb_libm_tanh(P.i0[c] * (double)raw));
+        P.thr.upload(thr, st);
+        for (auto &b : P.p_spins) b.alloc((size_t)P.W * n);
+        P.pacc.alloc((size_t)(cycles + 1) * P.Tp);
+        P.raw_last.alloc((size_t)n * P.Tp);
+
+        // launch shape: one wave of resident warps, each owning one word
+        PackedKernel kern = packed_kernel_for(P.L);
+        const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8;
+        set_packed_smem(kern, smem);
+        int occ = 0, sms = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pbsa::kPackedThreads, smem));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        occ = std::max(occ, 1);
+        P.chunks = (int)((n + 31) / 32);
+        const int64_t target_warps = (int64_t)sms * occ * pbsa::kPackedWarps;
+        int64_t wpw = std::max<int64_t>(1, target_warps / P.W);
+        wpw = std::min<int64_t>(wpw, P.chunks);
+        P.warps_per_word = (int)wpw;
+        P.packed_blocks = (int)grid_for(P.W * wpw, pbsa::kPackedWarps);
+        P.updates_per_run = (int64_t)n * trials * cycles;
+    } else {
+        // --------------------------------------------------- general setup
+        std::vector<uint32_t> colv(nnz);
+        for (int64_t k = 0; k < nnz; ++k) colv[k] = (uint32_t)indices[k];
+        P.col.upload(colv, st);
+        P.val.upload(values, nnz, st);
+        P.h.upload(hv, n, st);
+        P.kr.upload(kr, st);
+        P.kst.upload(kst, st);
+        for (auto &b : P.g_spins) b.alloc((size_t)n * P.Tp);
+        P.inputs.alloc((size_t)n * P.Tp);
+        P.counts.alloc((size_t)n * P.Tp);
+        if (algo == 1) P.hist.alloc((size_t)n * alpha * P.Tp);
+        // profiles: [n] shared or [n][Tp] transposed from [T][n]
+        std::vector<int64_t> distinct_periods;
+        if (lam) {
+            P.has_lam = P.has_delta = P.has_period = true;
+            P.shared_profile = pstride == 0;
+            const int64_t rows = P.shared_profile ? 1 : P.Tp;
+            std::vector<double> l((size_t)n * rows, 1.0), d((size_t)n * rows, 0.0);
+            std::vector<int32_t> p((size_t)n * rows, (int32_t)t_res);
+            std::set<int64_t> ps;
+            for (int64_t t = 0; t < (P.shared_profile ? 1 : trials); ++t)
+                for (int64_t i = 0; i < n; ++i) {
+                    const size_t src = (size_t)t * n + i;
+                    const size_t dst = P.shared_profile ? (size_t)i : (size_t)i * P.Tp + t;
+                    l[dst] = lam[src];
+                    d[dst] = delta[src];
+                    // periods beyond the last sub-step only ever fire at count 0
+                    const int64_t pv = std::min<int64_t>(period[src], INT32_MAX);
+                    p[dst] = (int32_t)pv;
+                    ps.insert(pv);
+                }
+            P.lam.upload(l, st);
+            P.delta.upload(d, st);
+            P.period.upload(p, st);
+            distinct_periods.assign(ps.begin(), ps.end());
+        } else {
+            distinct_periods.push_back(t_res);
+        }
+        // sub-steps where at least one p-bit of one trial fires
+        for (int64_t c = 0; c < cycles; ++c)
+            for (int64_t s = 0; s < t_res; ++s) {
+                const int64_t count = c * t_res + s;
+                for (int64_t pv : distinct_periods)
+                    if (count % pv == 0) {
+                        P.active_counts.push_back((uint32_t)count);
+                        break;
+                    }
+            }
+        // energy mode: exact integer accumulation when every term is integral
+        double mag = 0.0;
+        bool integral = true;
+        for (int64_t k = 0; k < mm && integral; ++k) {
+            integral = is_integral(mew[k]);
+            mag += std::fabs(mew[k]);
+        }
+        for (int64_t i = 0; i < n && integral; ++i) {
+            integral = is_integral(hv[i]);
+            mag += std::fabs(hv[i]);
+        }
+        P.int_energy = integral && mag < 9.0e15;
+        std::vector<uint32_t> a32(mm), b32(mm);
+        for (int64_t k = 0; k < mm; ++k) {
+            a32[k] = (uint32_t)mei[k];
+            b32[k] = (uint32_t)mej[k];
+        }
+        P.me_i.upload(a32, st);
+        P.me_j.upload(b32, st);
+        if (P.int_energy) {
+            std::vector<int64_t> wi(mm), hi(n);
+            bool any_h = false;
+            for (int64_t k = 0; k < mm; ++k) wi[k] = (int64_t)mew[k];
+            for (int64_t i = 0; i < n; ++i) {
+                hi[i] = (int64_t)hv[i];
+                any_h |= hi[i] != 0;
+            }
+            P.me_wi.upload(wi, st);
+            if (any_h) P.h_int.upload(hi, st);
+            P.e_acc.alloc((size_t)cycles * P.Tp);
+        } else {
+            P.me_w.upload(mew, mm, st);
+            P.e_f64.alloc((size_t)cycles * P.Tp);
+        }
+        std::vector<uint32_t> g32i(gm), g32j(gm);
+        for (int64_t k = 0; k < gm; ++k) {
+            g32i[k] = (uint32_t)gei[k];
+            g32j[k] = (uint32_t)gej[k];
+        }
+        P.ge_i.upload(g32i, st);
+        P.ge_j.upload(g32j, st);
+        if (gm) P.ge_w.upload(gew, gm, st);
+        P.cut_acc.alloc((size_t)cycles * P.Tp);
+        // updates: sum over (trial, node) of ceil(cycles * t_res / period)
+        const int64_t total = cycles * t_res;
+        int64_t ups = 0;
+        if (lam) {
+            for (int64_t t = 0; t < trials; ++t)
+                for (int64_t i = 0; i < n; ++i) {
+                    const int64_t pv = period[(pstride ? t * n : 0) + i];
+                    ups += (total + pv - 1) / pv;
+                }
+        } else {
+            ups = trials * n * ((total + t_res - 1) / t_res);
+        }
+        P.updates_per_run = ups;
+    }
+    // mm/gm metadata for stats
+    P.trace_cut.alloc((size_t)trials * cycles);
+    P.trace_energy.alloc((size_t)trials * cycles);
+    P.best.alloc((size_t)trials);
+    CK(cudaStreamSynchronize(st));
+    (void)mm;
+}
+
+void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
+    cudaStream_t st = P.stream;
+    const int TB = 256;
+    P.launches = 0;
+    P.sweep_launches = 0;
+    if (P.path == PBSA_PATH_PACKED) {
+        pbsa::init_packed<<<grid_for(P.n * P.W, TB), TB, 0, st>>>(P.p_spins[0].p, P.kspin.p,
+                                                                   (int)P.n, (int)P.W);
+        CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
+        P.launches += 1;
+        PackedKernel kern = packed_kernel_for(P.L);
+        const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8;
+        CK(cudaEventRecord(P.ev_sweep0, st));
+        int cur = 0;
+        for (int64_t c = 0; c <= P.cycles; ++c) {
+            pbsa::PackedArgs a{};
+            a.sold = P.p_spins[cur].p;
+            a.snew = P.p_spins[cur ^ 1].p;
+            a.rowptr = P.rowptr.p;
+            a.adj = P.adj.p;
+            a.krg = P.krg.p;
+            const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
+            a.thr = P.thr.p + (size_t)cc * P.K;
+            a.pacc = P.pacc.p + (size_t)c * P.Tp;
+            a.raw_out = (c == P.cycles - 1) ? P.raw_last.p : nullptr;
+            a.n = (int)P.n;
+            a.W = (int)P.W;
+            a.Tp = (int)P.Tp;
+            a.K = P.K;
+            a.dmax = P.dmax;
+            a.warps_per_word = P.warps_per_word;
+            a.chunks = P.chunks;
+            a.count = (uint32_t)(c * P.t_res);
+            a.do_update = c < P.cycles;
+            kern<<<P.packed_blocks, pbsa::kPackedThreads, smem, st>>>(a);
+            CK(cudaGetLastError());
+            ++P.launches;
+            if (c < P.cycles) {
+                ++P.sweep_launches;
+                cur ^= 1;
+            }
+        }
+        CK(cudaEventRecord(P.ev_sweep1, st));
+        P.final_parity = cur;
+        pbsa::FinalArgs f{};
+        f.pacc = P.pacc.p;
+        f.total_w = P.total_w;
+        f.mode = 0;
+        f.has_graph = P.has_graph;
+        f.C = (int)P.cycles;
+        f.Tp = (int)P.Tp;
+        f.T = (int)P.T;
+        f.trace_cut = P.trace_cut.p;
+        f.trace_energy = P.trace_energy.p;
+        f.best = P.best.p;
+        pbsa::finalize_traces<<<grid_for(P.T, TB), TB, 0, st>>>(f);
+        ++P.launches;
+    } else {
+        pbsa::init_general<<<grid_for(P.n * P.Tp, TB), TB, 0, st>>>(P.g_spins[0].p, P.kspin.p,
+                                                                    (int)P.n, (int)P.Tp);
+        CK(cudaMemsetAsync(P.inputs.p, 0, P.inputs.n * sizeof(double), st));
+        CK(cudaMemsetAsync(P.counts.p, 0, P.counts.n * sizeof(int32_t), st));
+        if (P.hist.n) CK(cudaMemsetAsync(P.hist.p, 0, P.hist.n * sizeof(double), st));
+        CK(cudaMemsetAsync(P.cut_acc.p, 0, P.cut_acc.n * sizeof(unsigned long long), st));
+        if (P.e_acc.n) CK(cudaMemsetAsync(P.e_acc.p, 0, P.e_acc.n * sizeof(unsigned long long), st));
+        P.launches += 1;
+        CK(cudaEventRecord(P.ev_sweep0, st));
+        int cur = 0;
+        size_t ai = 0;
+        const int sm_chunks = std::max<int64_t>(1, std::min<int64_t>(64, (std::max(mm, gm) + 255) / 256));
+        for (int64_t c = 0; c < P.cycles; ++c) {
+            while (ai < P.active_counts.size() && P.active_counts[ai] < (uint64_t)(c + 1) * P.t_res) {
+                pbsa::GeneralArgs a{};
+                a.sold = P.g_spins[cur].p;
+                a.snew = P.g_spins[cur ^ 1].p;
+                a.rowptr = P.rowptr.p;
+                a.col = P.col.p;
+                a.val = P.val.p;
+                a.h = P.h.p;
+                a.lam = P.has_lam ? P.lam.p : nullptr;
+                a.delta = P.has_delta ? P.delta.p : nullptr;
+                a.period = P.has_period ? P.period.p : nullptr;
+                a.shared_profile = P.shared_profile;
+                a.inputs = P.inputs.p;
+                a.counts = P.counts.p;
+                a.hist = P.hist.p;
+                a.kr = P.kr.p;
+                a.kst = P.kst.p;
+                a.n = (int)P.n;
+                a.Tp = (int)P.Tp;
+                a.T = (int)P.T;
+                a.algo = P.algo;
+                a.alpha = (int)P.alpha;
+                a.t_res = (int)P.t_res;
+                a.i0 = P.i0[c];
+                a.p_stall = P.p_stall;
+                a.count = P.active_counts[ai];
+                pbsa::general_substep<<<grid_for(P.n * P.Tp, TB), TB, 0, st>>>(a);
+                CK(cudaGetLastError());
+                ++P.launches;
+                ++P.sweep_launches;
+                cur ^= 1;
+                ++ai;
+            }
+            pbsa::StatsArgs s{};
+            s.s = P.g_spins[cur].p;
+            s.ge_i = P.ge_i.p;
+            s.ge_j = P.ge_j.p;
+            s.ge_w = P.ge_w.p;
+            s.me_i = P.me_i.p;
+            s.me_j = P.me_j.p;
+            s.me_wi = P.me_wi.p;
+            s.hi = P.h_int.p;
+            s.gm = gm;
+            s.mm = mm;
+            s.n = (int)P.n;
+            s.Tp = (int)P.Tp;
+            s.T = (int)P.T;
+            s.chunks = sm_chunks;
+            s.cut_acc = P.cut_acc.p + (size_t)c * P.Tp;
+            s.e_acc = P.int_energy ? P.e_acc.p + (size_t)c * P.Tp : nullptr;
+            dim3 grid(sm_chunks, (unsigned)grid_for(P.T, TB));
+            pbsa::general_stats<<<grid, TB, 0, st>>>(s);
+            ++P.launches;
+            if (!P.int_energy) {
+                pbsa::general_energy_f64<<<grid_for(P.T, 128), 128, 0, st>>>(
+                    P.g_spins[cur].p, P.h.p, P.me_i.p, P.me_j.p, P.me_w.p, mm, (int)P.n,
+                    (int)P.Tp, (int)P.T, P.e_f64.p + (size_t)c * P.Tp);
+                ++P.launches;
+            }
+        }
+        CK(cudaEventRecord(P.ev_sweep1, st));
+        P.final_parity = cur;
+        pbsa::FinalArgs f{};
+        f.cut_acc = P.cut_acc.p;
+        f.e_acc = P.e_acc.p;
+        f.e_f64 = P.e_f64.p;
+        f.mode = P.int_energy ? 1 : 2;
+        f.has_graph = P.has_graph;
+        f.C = (int)P.cycles;
+        f.Tp = (int)P.Tp;
+        f.T = (int)P.T;
+        f.trace_cut = P.trace_cut.p;
+        f.trace_energy = P.trace_energy.p;
+        f.best = P.best.p;
+        pbsa::finalize_traces<<<grid_for(P.T, TB), TB, 0, st>>>(f);
+        ++P.launches;
+    }
+    CK(cudaGetLastError());
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int pbsa_abi_version(void) { return PBSA_ABI_VERSION; }
+
+const char *pbsa_last_error(void) { return g_last_error.c_str(); }
+
+int pbsa_device_count(int *count) {
+    return guarded([&] {
+        if (!count) fail(PBSA_EINVAL, "null count");
+        CK(cudaGetDeviceCount(count));
+    });
+}
+
+int pbsa_plan_create(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                     const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                     const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                     const int64_t *ge_j, const int64_t *ge_w, const double *lam,
+                     const double *delta, const int64_t *period, int64_t profile_stride,
+                     double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                     int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                     pbsa_plan **out) {
+    return guarded([&] {
+        if (!out) fail(PBSA_EINVAL, "null plan out-pointer");
+        *out = nullptr;
+        if (mm < 0 || gm < 0) fail(PBSA_EINVAL, "negative edge count");
+        std::unique_ptr<pbsa_plan> P(new pbsa_plan());
+        create_plan(*P, device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm, ge_i,
+                    ge_j, ge_w, lam, delta, period, profile_stride, i0_min, beta, cycles, t_res,
+                    algo, alpha, p_stall, trials, keys);
+        DeviceGuard dg(device);
+        // capture the whole anneal into one graph
+        CK(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_run(*P, mm, gm);
+        } catch (...) {
+            cudaGraph_t g;
+            cudaStreamEndCapture(P->stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        cudaGraph_t graph;
+        CK(cudaStreamEndCapture(P->stream, &graph));
+        cudaError_t e = cudaGraphInstantiate(&P->graph_exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(e);
+        *out = P.release();
+    });
+}
+
+int pbsa_plan_run(pbsa_plan *P, float *device_ms) {
+    return guarded([&] {
+        if (!P) fail(PBSA_EINVAL, "null plan");
+        DeviceGuard dg(P->device);
+        CK(cudaEventRecord(P->ev_start, P->stream));
+        CK(cudaGraphLaunch(P->graph_exec, P->stream));
+        CK(cudaEventRecord(P->ev_end, P->stream));
+        CK(cudaEventSynchronize(P->ev_end));
+        P->ran = true;
+        if (device_ms) CK(cudaEventElapsedTime(device_ms, P->ev_start, P->ev_end));
+    });
+}
+
+int pbsa_plan_info(const pbsa_plan *P, int *path, int64_t *launches_per_run,
+                   double *sweep_ms_mean, int64_t *sweep_launches, int64_t *words) {
+    return guarded([&] {
+        if (!P) fail(PBSA_EINVAL, "null plan");
+        if (path) *path = P->path;
+        if (launches_per_run) *launches_per_run = P->launches;
+        if (sweep_launches) *sweep_launches = P->sweep_launches;
+        if (words) *words = P->W;
+        if (sweep_ms_mean) {
+            *sweep_ms_mean = 0.0;
+            if (P->ran && P->sweep_launches) {
+                float ms = 0.f;
+                CK(cudaEventElapsedTime(&ms, P->ev_sweep0, P->ev_sweep1));
+                // the packed phase also holds the final cut-only pass
+                const int64_t k = P->path == PBSA_PATH_PACKED ? P->sweep_launches + 1
+                                                               : P->sweep_launches;
+                *sweep_ms_mean = (double)ms / (double)k;
+            }
+        }
+    });
+}
+
+int pbsa_plan_summary(pbsa_plan *P, int64_t *final_cut_sum, int64_t *best_cut_max,
+                      int64_t *updates) {
+    return guarded([&] {
+        if (!P) fail(PBSA_EINVAL, "null plan");
+        if (!P->ran) fail(PBSA_EINVAL, "plan has not been run");
+        DeviceGuard dg(P->device);
+        std::vector<int64_t> last(P->T), best(P->T);
+        // last-cycle cut of every trial: column C-1 of [T][C]
+        CK(cudaMemcpy2DAsync(last.data(), sizeof(int64_t), P->trace_cut.p + (P->cycles - 1),
+                             P->cycles * sizeof(int64_t), sizeof(int64_t), P->T,
+                             cudaMemcpyDeviceToHost, P->stream));
+        CK(cudaMemcpyAsync(best.data(), P->best.p, P->T * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                           P->stream));
+        CK(cudaStreamSynchronize(P->stream));
+        int64_t s = 0, b = -(1LL << 62);
+        for (int64_t t = 0; t < P->T; ++t) {
+            s += last[t];
+            b = std::max(b, best[t]);
+        }
+        if (final_cut_sum) *final_cut_sum = s;
+        if (best_cut_max) *best_cut_max = b;
+        if (updates) *updates = P->updates_per_run;
+    });
+}
+
+int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist, int64_t *counts,
+                       double *trace_i0, double *trace_energy, int64_t *trace_cut,
+                       int64_t *best_cut) {
+    return guarded([&] {
+        if (!P) fail(PBSA_EINVAL, "null plan");
+        if (!P->ran) fail(PBSA_EINVAL, "plan has not been run");
+        DeviceGuard dg(P->device);
+        cudaStream_t st = P->stream;
+        const int64_t n = P->n, T = P->T, C = P->cycles;
+        const int TB = 256;
+        if (trace_cut)
+            CK(cudaMemcpyAsync(trace_cut, P->trace_cut.p, T * C * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, st));
+        if (trace_energy)
+            CK(cudaMemcpyAsync(trace_energy, P->trace_energy.p, T * C * sizeof(double),
+                               cudaMemcpyDeviceToHost, st));
+        if (best_cut)
+            CK(cudaMemcpyAsync(best_cut, P->best.p, T * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        DevBuf<int8_t> dspins;
+        DevBuf<double> dinputs, dhist;
+        DevBuf<int32_t> dcounts;
+        if (P->path == PBSA_PATH_PACKED) {
+            if (spins) {
+                dspins.alloc((size_t)T * n);
+                pbsa::unpack_spins<<<grid_for(n * T, TB), TB, 0, st>>>(
+                    P->p_spins[P->final_parity].p, dspins.p, (int)n, (int)P->W, (int)T);
+                CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
+            }
+            if (inputs || (hist && P->tapsa_hist_from_raw)) {
+                dinputs.alloc((size_t)T * n);
+                pbsa::inputs_from_raw<<<grid_for(n * T, TB), TB, 0, st>>>(
+                    P->raw_last.p, dinputs.p, P->i0[C - 1], (int)n, (int)P->Tp, (int)T);
+                if (inputs)
+                    CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double),
+                                       cudaMemcpyDeviceToHost, st));
+            }
+            if (hist && P->tapsa_hist_from_raw) {
+                // TAPSA with alpha = 1: the history holds the last raw field
+                dhist.alloc((size_t)T * n);
+                pbsa::inputs_from_raw<<<grid_for(n * T, TB), TB, 0, st>>>(
+                    P->raw_last.p, dhist.p, 1.0, (int)n, (int)P->Tp, (int)T);
+                CK(cudaMemcpyAsync(hist, dhist.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+            }
+            CK(cudaStreamSynchronize(st));
+            if (hist && !P->tapsa_hist_from_raw) std::memset(hist, 0, T * n * P->alpha * sizeof(double));
+            if (counts)
+                for (int64_t k = 0; k < T * n; ++k) counts[k] = C;
+        } else {
+            dim3 tb(32, 8);
+            if (spins) {
+                dspins.alloc((size_t)T * n);
+                dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
+                pbsa::transpose_tile<int8_t><<<g, tb, 0, st>>>(P->g_spins[P->final_parity].p,
+                                                               dspins.p, (int)n, (int)P->Tp, (int)T);
+                CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
+            }
+            if (inputs) {
+                dinputs.alloc((size_t)T * n);
+                dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
+                pbsa::transpose_tile<double><<<g, tb, 0, st>>>(P->inputs.p, dinputs.p, (int)n,
+                                                               (int)P->Tp, (int)T);
+                CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double),
+                                   cudaMemcpyDeviceToHost, st));
+            }
+            if (counts) {
+                dcounts.alloc((size_t)T * n);
+                dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
+                pbsa::transpose_tile<int32_t><<<g, tb, 0, st>>>(P->counts.p, dcounts.p, (int)n,
+                                                                (int)P->Tp, (int)T);
+            }
+            if (hist && P->algo == 1) {
+                const int64_t rows = n * P->alpha;
+                dhist.alloc((size_t)T * rows);
+                dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(rows, 32));
+                pbsa::transpose_tile<double><<<g, tb, 0, st>>>(P->hist.p, dhist.p, (int)rows,
+                                                               (int)P->Tp, (int)T);
+                CK(cudaMemcpyAsync(hist, dhist.p, T * rows * sizeof(double),
+                                   cudaMemcpyDeviceToHost, st));
+            }
+            std::vector<int32_t> c32;
+            if (counts) {
+                c32.resize((size_t)T * n);
+                CK(cudaMemcpyAsync(c32.data(), dcounts.p, T * n * sizeof(int32_t),
+                                   cudaMemcpyDeviceToHost, st));
+            }
+            CK(cudaStreamSynchronize(st));
+            if (counts)
+                for (int64_t k = 0; k < T * n; ++k) counts[k] = c32[k];
+            if (hist && P->algo != 1) std::memset(hist, 0, T * n * P->alpha * sizeof(double));
+        }
+        if (trace_i0)
+            for (int64_t t = 0; t < T; ++t) std::memcpy(trace_i0 + t * C, P->i0.data(), C * sizeof(double));
+        CK(cudaGetLastError());
+    });
+}
+
+int pbsa_plan_destroy(pbsa_plan *P) {
+    return guarded([&] {
+        if (!P) return;
+        DeviceGuard dg(P->device);
+        delete P;
+    });
+}
+
+int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                           const double *values, const double *h, int64_t mm,
+                           const int64_t *me_i, const int64_t *me_j, const double *me_w,
+                           int64_t gm, const int64_t *ge_i, const int64_t *ge_j,
+                           const int64_t *ge_w, const double *lam, const double *delta,
+                           const int64_t *period, int64_t profile_stride, double i0_min,
+                           double beta, int64_t cycles, int64_t t_res, int algo, int64_t alpha,
+                           double p_stall, int64_t trials, const uint64_t *keys, int8_t *spins,
+                           double *inputs, double *hist, int64_t *counts, double *trace_i0,
+                           double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
+                           float *device_ms) {
+    pbsa_plan *P = nullptr;
+    int rc = pbsa_plan_create(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm,
+                              ge_i, ge_j, ge_w, lam, delta, period, profile_stride, i0_min, beta,
+                              cycles, t_res, algo, alpha, p_stall, trials, keys, &P);
+    if (rc != PBSA_OK) return rc;
+    rc = pbsa_plan_run(P, device_ms);
+    if (rc == PBSA_OK)
+        rc = pbsa_plan_download(P, spins, inputs, hist, counts, trace_i0, trace_energy, trace_cut,
+                                best_cut);
+    const std::string err = g_last_error;
+    pbsa_plan_destroy(P);
+    if (rc != PBSA_OK) g_last_error = err;
+    return rc;
+}
+
+int pbsa_debug_stream_u64(int device, int64_t count, const uint64_t *key, const uint64_t *tag,
+                          const uint64_t *a, const uint64_t *b, uint64_t *out) {
+    return guarded([&] {
+        if (count < 0) fail(PBSA_EINVAL, "negative count");
+        if (count == 0) return;
+        DeviceGuard dg(device);
+        DevBuf<uint64_t> dk, dt, da, db, dout;
+        dk.upload(key, count, 0);
+        dt.upload(tag, count, 0);
+        da.upload(a, count, 0);
+        db.upload(b, count, 0);
+        dout.alloc(count);
+        pbsa::debug_stream<<<grid_for(count, 256), 256>>>(count, dk.p, dt.p, da.p, db.p, dout.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, dout.p, count * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    });
+}
+
+int pbsa_debug_tanh(int device, int64_t count, const double *x, double *out) {
+    return guarded([&] {
+        if (count < 0) fail(PBSA_EINVAL, "negative count");
+        if (count == 0) return;
+        DeviceGuard dg(device);
+        DevBuf<double> dx, dout;
+        dx.upload(x, count, 0);
+        dout.alloc(count);
+        pbsa::debug_tanh<<<grid_for(count, 256), 256>>>(count, dx.p, dout.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, dout.p, count * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+double pbsa_libm_tanh_host(double x) { return pb_libm_tanh(x); }
+
+uint64_t pbsa_threshold_host(double t) { return threshold_h64(t); }
+
+}  // extern "C"

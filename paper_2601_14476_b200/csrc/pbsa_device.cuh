@@ -1,0 +1,411 @@
+// pbsa_device.cuh -- device kernels of the B200-native pSA sweep.
+//
+// Restates, for sm_100a, the reference hot loop
+//   /root/reference/pkg/src/pbitsa/_kernels.py:68-175  (anneal_loop)
+// batched over trials.  Two paths:
+//
+//  * PACKED (the production path for MAX-CUT-shaped work: J in {+1,-1}, h = 0,
+//    ideal profile, plain pSA rule).  Spins are bit-packed, 32 trials per
+//    uint32 word, layout [node][word]; one thread owns one (node, word) task
+//    = 32 p-bit updates.  The local field of all 32 trials is formed with a
+//    bit-sliced adder over the neighbour words; the activation is an exact
+//    integer threshold on the 64-bit counter hash (thresholds derived on the
+//    host from libm-exact tanh per (cycle, raw field)), so no tanh runs on the
+//    device and the result is bit-identical to the reference.  The per-cycle
+//    cut is fused into the next sweep's gather (sum_i s_i raw_i).
+//
+//  * GENERAL (any real J/h, any variability profile, all three input rules).
+//    int8 spins, layout [node][trial]; one thread per (node, trial); fp64
+//    arithmetic in the reference's exact operation order with contraction
+//    disabled, and a tanh that rounds like the host libm (libm_tanh.cuh).
+//
+// Both paths draw every random number from the same splitmix-style counter
+// hash as streams.py:29-55, regenerated in-kernel from (key, tag, node, count).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "libm_tanh.cuh"
+
+#define PB_GAMMA 0x9E3779B97F4A7C15ULL
+#define PB_M1 0xBF58476D1CE4E5B9ULL
+#define PB_M2 0x94D4A04C32684F87ULL
+
+namespace pbsa {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * PB_M1;
+    z = (z ^ (z >> 27)) * PB_M2;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t absorb(uint64_t h, uint64_t w) {
+    return mix64((h + PB_GAMMA) ^ w);
+}
+
+// u01 = (h >> 11) * 2^-53 exactly (streams.py:48-50).
+__device__ __forceinline__ double u01_of(uint64_t h) {
+    return __dmul_rn(__ull2double_rn(h >> 11), 0x1p-53);
+}
+
+// ------------------------------------------------------------------ init
+// Initial spins: u01(key, TAG_SPIN, i, 0) < 0.5  <=>  stream word < 2^63
+// (_kernels.py:94-97).  kspin[t] = absorb(key_t, TAG_SPIN) (host prefix).
+
+__global__ void init_packed(uint32_t *__restrict__ s, const uint64_t *__restrict__ kspin,
+                            int n, int W) {
+    const int64_t task = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (task >= (int64_t)n * W) return;
+    const int w = (int)(task / n), i = (int)(task % n);
+    uint32_t word = 0;
+#pragma unroll 4
+    for (int b = 0; b < 32; ++b) {
+        const uint64_t h = absorb(absorb(kspin[w * 32 + b], (uint64_t)i), 0);
+        word |= (uint32_t)((h >> 63) == 0) << b;
+    }
+    s[task] = word;
+}
+
+__global__ void init_general(int8_t *__restrict__ s, const uint64_t *__restrict__ kspin, int n,
+                             int Tp) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)n * Tp) return;
+    const int i = (int)(g / Tp), t = (int)(g % Tp);
+    const uint64_t h = absorb(absorb(kspin[t], (uint64_t)i), 0);
+    s[g] = (h >> 63) == 0 ? 1 : -1;
+}
+
+// ---------------------------------------------------------- packed sweep
+// Layout: spins uint32 [W][n] (word-major, node-fast): bit b of word (w, i) is
+// trial 32w+b's spin at node i, 1 = +1.  A warp owns one word index w for its
+// whole life and walks 32-node chunks of it (lane = node), so the 32 trial
+// keys of the warp are uniform (broadcast from shared memory), neighbour
+// words of consecutive nodes are coalesced on lattice-like graphs, and the
+// per-trial cut partials reduce with one 32x32 butterfly per warp.
+struct PackedArgs {
+    const uint32_t *sold;
+    uint32_t *snew;
+    const uint32_t *rowptr;   // [n+1]
+    const uint32_t *adj;      // [nnz] column | (J < 0) << 31
+    const uint64_t *krg;      // [Tp] absorb(key, TAG_R) + GAMMA
+    const uint64_t *thr;      // [K] thresholds of this cycle (H >= thr -> +1)
+    unsigned long long *pacc; // [Tp] += sum_i s_i * raw_i of the sub-step's input state
+    int16_t *raw_out;         // [n][Tp] raw field of this update, or null
+    int n, W, Tp, K, dmax;
+    int warps_per_word;       // warps sharing one word index
+    int chunks;               // ceil(n / 32)
+    uint32_t count;           // global sub-step counter c * t_res
+    int do_update;            // 0: only accumulate pacc (final cut pass)
+};
+
+// H >= thr for H = mix64(x), evaluated high word first: the low word is only
+// needed when the high words tie (probability ~2^-32).  thr == ~0 encodes
+// "never" (tanh == -1 exactly), which no genuine threshold equals because
+// genuine thresholds have their low 11 bits clear.
+__device__ __forceinline__ bool hash_ge(uint64_t x, uint64_t thr) {
+    uint64_t z = (x ^ (x >> 30)) * PB_M1;
+    z = (z ^ (z >> 27)) * PB_M2;
+    const uint32_t zhi = (uint32_t)(z >> 32);
+    const uint32_t hhi = zhi ^ (zhi >> 31);
+    const uint32_t thi = (uint32_t)(thr >> 32);
+    if (hhi != thi) return hhi > thi;
+    const uint64_t h = z ^ (z >> 31);
+    return h >= thr && thr != ~0ULL;
+}
+
+constexpr int kPackedThreads = 256;
+constexpr int kPackedWarps = kPackedThreads / 32;
+
+template <int L>
+__global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) {
+    extern __shared__ unsigned long long smem_u64[];
+    uint64_t *sthr = reinterpret_cast<uint64_t *>(smem_u64);   // [K]
+    uint64_t *skey = sthr + a.K;                                // [warps][32]
+
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int gwarp = blockIdx.x * kPackedWarps + wib;
+    const int w = gwarp / a.warps_per_word;
+    const int q = gwarp % a.warps_per_word;
+    const bool live = w < a.W;
+
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) sthr[k] = a.thr[k];
+    uint64_t *key = skey + wib * 32;
+    key[lane] = live ? a.krg[(size_t)w * 32 + lane] : 0;
+    __syncthreads();
+
+    int acc[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) acc[b] = 0;
+
+    if (live) {
+        const uint32_t *sw = a.sold + (size_t)w * a.n;
+        for (int ch = q; ch < a.chunks; ch += a.warps_per_word) {
+            const int i = ch * 32 + lane;
+            if (i >= a.n) continue;
+            const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
+            // bit-sliced count of neighbours with J_ik * s_k == +1
+            uint32_t p[L];
+#pragma unroll
+            for (int b = 0; b < L; ++b) p[b] = 0;
+            for (uint32_t k = beg; k < end; ++k) {
+                const uint32_t e = __ldg(a.adj + k);
+                uint32_t carry = __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
+#pragma unroll
+                for (int b = 0; b < L; ++b) {
+                    const uint32_t nc = p[b] & carry;
+                    p[b] ^= carry;
+                    carry = nc;
+                }
+            }
+            const int d = (int)(end - beg);
+            const uint32_t own = __ldg(sw + i);
+            uint32_t word = 0;
+#pragma unroll
+            for (int b = 0; b < 32; ++b) {
+                int pop = 0;
+#pragma unroll
+                for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                const int raw = 2 * pop - d;
+                if (a.do_update) {
+                    const uint64_t x1 = key[b] ^ (uint64_t)i;
+                    const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)a.count;
+                    word |= (uint32_t)hash_ge(x2, sthr[raw + a.dmax]) << b;
+                }
+                acc[b] += ((own >> b) & 1u) ? raw : -raw;
+                if (a.raw_out) a.raw_out[(size_t)i * a.Tp + w * 32 + b] = (int16_t)raw;
+            }
+            if (a.do_update) a.snew[(size_t)w * a.n + i] = word;
+        }
+    }
+    // 32x32 transpose-reduce: lane b ends with the warp's sum for trial 32w+b.
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        const bool upper = (lane & off) != 0;
+#pragma unroll
+        for (int b = 0; b < off; ++b) {
+            const int send = upper ? acc[b] : acc[b + off];
+            const int keep = upper ? acc[b + off] : acc[b];
+            acc[b] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        }
+    }
+    if (live && acc[0]) atomicAdd(a.pacc + (size_t)w * 32 + lane, (unsigned long long)(long long)acc[0]);
+}
+
+// Packed spins [W][n] -> int8 [T][n]
+__global__ void unpack_spins(const uint32_t *__restrict__ s, int8_t *__restrict__ out, int n,
+                             int W, int T) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)n * T) return;
+    const int t = (int)(g / n), i = (int)(g % n);
+    out[g] = ((s[(size_t)(t >> 5) * n + i] >> (t & 31)) & 1u) ? 1 : -1;
+}
+
+// inputs[t][i] = i0_last * raw_last[i][t]  (pSA: inp = i0 * raw, _kernels.py:146)
+__global__ void inputs_from_raw(const int16_t *__restrict__ raw, double *__restrict__ out,
+                                double i0_last, int n, int Tp, int T) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)n * T) return;
+    const int t = (int)(g / n), i = (int)(g % n);
+    out[g] = __dmul_rn(i0_last, (double)raw[(size_t)i * Tp + t]);
+}
+
+// ----------------------------------------------------------- general path
+struct GeneralArgs {
+    const int8_t *sold;
+    int8_t *snew;
+    const uint32_t *rowptr;
+    const uint32_t *col;
+    const double *val;
+    const double *h;
+    const double *lam;     // [n][Tp] or [n] (shared) or null (1.0)
+    const double *delta;   // same layout, null = 0.0
+    const int32_t *period; // same layout, null = t_res
+    int shared_profile;
+    double *inputs;        // [n][Tp]
+    int32_t *counts;       // [n][Tp]
+    double *hist;          // [n][alpha][Tp] (TAPSA only)
+    const uint64_t *kr;    // [Tp] absorb(key, TAG_R)
+    const uint64_t *kst;   // [Tp] absorb(key, TAG_STALL)
+    int n, Tp, T, algo, alpha, t_res;
+    double i0, p_stall;
+    uint32_t count;
+};
+
+__global__ void __launch_bounds__(256) general_substep(GeneralArgs a) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)a.n * a.Tp) return;
+    const int i = (int)(g / a.Tp), t = (int)(g % a.Tp);
+    const int8_t cur = a.sold[g];
+    const int64_t pidx = a.shared_profile ? i : g;
+    const uint32_t per = a.period ? (uint32_t)a.period[pidx] : (uint32_t)a.t_res;
+    if (t >= a.T || a.count % per != 0) {
+        a.snew[g] = cur;
+        return;
+    }
+    // raw = h_i + sum_k values[k] * spins[indices[k]], CSR order (_kernels.py:128-130)
+    double raw = a.h[i];
+    const uint32_t beg = a.rowptr[i], end = a.rowptr[i + 1];
+    for (uint32_t k = beg; k < end; ++k)
+        raw = __dadd_rn(raw, __dmul_rn(a.val[k], (double)a.sold[(size_t)a.col[k] * a.Tp + t]));
+    const int32_t cnt = a.counts[g];
+    double inp;
+    if (a.algo == 1) {  // TAPSA (_kernels.py:131-138)
+        const size_t base = (size_t)i * a.alpha;
+        a.hist[(base + cnt % a.alpha) * a.Tp + t] = raw;
+        const int filled = cnt + 1 < a.alpha ? cnt + 1 : a.alpha;
+        double acc = 0.0;
+        for (int q = 0; q < filled; ++q) acc = __dadd_rn(acc, a.hist[(base + q) * a.Tp + t]);
+        inp = __dmul_rn(a.i0, __ddiv_rn(acc, (double)filled));
+    } else if (a.algo == 2) {  // SPSA (_kernels.py:139-144)
+        if (cnt == 0) {
+            inp = __dmul_rn(a.i0, raw);
+        } else {
+            const double u = u01_of(absorb(absorb(a.kst[t], (uint64_t)i), (uint64_t)a.count));
+            inp = u < a.p_stall ? a.inputs[g] : __dmul_rn(a.i0, raw);
+        }
+    } else {
+        inp = __dmul_rn(a.i0, raw);
+    }
+    a.inputs[g] = inp;
+    a.counts[g] = cnt + 1;
+    const double lam = a.lam ? a.lam[pidx] : 1.0;
+    const double del = a.delta ? a.delta[pidx] : 0.0;
+    const double r = __dsub_rn(__dmul_rn(2.0, u01_of(absorb(absorb(a.kr[t], (uint64_t)i),
+                                                            (uint64_t)a.count))), 1.0);
+    const double act = __dadd_rn(r, pb_libm_tanh(__dmul_rn(lam, __dadd_rn(inp, del))));
+    a.snew[g] = act >= 0.0 ? 1 : -1;
+}
+
+// Per-cycle cut and integer energy over edges, spins int8 [n][Tp].
+// grid.x chunks the edge range, threads cover trials.
+struct StatsArgs {
+    const int8_t *s;
+    const uint32_t *ge_i, *ge_j;
+    const int64_t *ge_w;
+    const uint32_t *me_i, *me_j;
+    const int64_t *me_wi;   // integer couplings (int_energy mode)
+    const int64_t *hi;      // integer fields (int_energy mode), null if all zero
+    int64_t gm, mm;
+    int n, Tp, T;
+    int chunks;
+    unsigned long long *cut_acc;   // [Tp] for this cycle
+    unsigned long long *e_acc;     // [Tp] for this cycle (sum_e J s s + sum_i h s)
+};
+
+__global__ void general_stats(StatsArgs a) {
+    const int t = blockIdx.y * blockDim.x + threadIdx.x;
+    if (t >= a.T) return;
+    const int ch = blockIdx.x;
+    long long cut = 0, e = 0;
+    {
+        const int64_t per = (a.gm + a.chunks - 1) / a.chunks;
+        const int64_t lo = ch * per, hi = min(a.gm, lo + per);
+        for (int64_t k = lo; k < hi; ++k)
+            if (a.s[(size_t)a.ge_i[k] * a.Tp + t] != a.s[(size_t)a.ge_j[k] * a.Tp + t])
+                cut += a.ge_w[k];
+    }
+    if (a.e_acc) {
+        const int64_t per = (a.mm + a.chunks - 1) / a.chunks;
+        const int64_t lo = ch * per, hi = min(a.mm, lo + per);
+        for (int64_t k = lo; k < hi; ++k)
+            e += a.me_wi[k] * (long long)(a.s[(size_t)a.me_i[k] * a.Tp + t] *
+                                          a.s[(size_t)a.me_j[k] * a.Tp + t]);
+        if (a.hi) {
+            const int64_t pn = (a.n + a.chunks - 1) / a.chunks;
+            const int64_t lo2 = ch * pn, hi2 = min((int64_t)a.n, lo2 + pn);
+            for (int64_t i = lo2; i < hi2; ++i) e += a.hi[i] * (long long)a.s[(size_t)i * a.Tp + t];
+        }
+    }
+    if (cut) atomicAdd(a.cut_acc + t, (unsigned long long)cut);
+    if (a.e_acc && e) atomicAdd(a.e_acc + t, (unsigned long long)e);
+}
+
+// Exact fp64 energy in the reference's sequential order (_kernels.py:157-161),
+// one thread per trial; used only when couplings/fields are not integers.
+__global__ void general_energy_f64(const int8_t *__restrict__ s, const double *__restrict__ h,
+                                   const uint32_t *__restrict__ me_i,
+                                   const uint32_t *__restrict__ me_j,
+                                   const double *__restrict__ me_w, int64_t mm, int n, int Tp,
+                                   int T, double *__restrict__ e_out /* [Tp] this cycle */) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    double e = 0.0;
+    for (int i = 0; i < n; ++i)
+        e = __dsub_rn(e, __dmul_rn(h[i], (double)s[(size_t)i * Tp + t]));
+    for (int64_t k = 0; k < mm; ++k)
+        e = __dsub_rn(e, __dmul_rn(__dmul_rn(me_w[k], (double)s[(size_t)me_i[k] * Tp + t]),
+                                   (double)s[(size_t)me_j[k] * Tp + t]));
+    e_out[t] = e;
+}
+
+// ---------------------------------------------------------------- finalise
+// Per (trial, cycle): trace_cut, trace_energy from the accumulators, [T][C].
+//   mode 0 (packed):  P = pacc[c+1][t]: cut = (2W + P)/4, E = -P/2
+//   mode 1 (general, integer energy): cut = cut_acc[c][t], E = -e_acc[c][t]
+//   mode 2 (general, fp64 energy):    cut = cut_acc[c][t], E = e_f64[c][t]
+struct FinalArgs {
+    const unsigned long long *pacc;
+    const unsigned long long *cut_acc;
+    const unsigned long long *e_acc;
+    const double *e_f64;
+    int64_t total_w;
+    int mode, has_graph;
+    int C, Tp, T;
+    int64_t *trace_cut;     // [T][C]
+    double *trace_energy;   // [T][C]
+    int64_t *best;          // [T]
+};
+
+__global__ void finalize_traces(FinalArgs a) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.T) return;
+    long long best = -(1LL << 62);
+    for (int c = 0; c < a.C; ++c) {
+        long long cut;
+        double e;
+        if (a.mode == 0) {
+            const long long P = (long long)a.pacc[(size_t)(c + 1) * a.Tp + t];
+            cut = a.has_graph ? (2 * a.total_w + P) / 4 : 0;
+            e = (double)(-(P / 2));
+        } else {
+            cut = a.has_graph ? (long long)a.cut_acc[(size_t)c * a.Tp + t] : 0;
+            e = a.mode == 1 ? (double)(-(long long)a.e_acc[(size_t)c * a.Tp + t])
+                            : a.e_f64[(size_t)c * a.Tp + t];
+        }
+        a.trace_cut[(size_t)t * a.C + c] = cut;
+        a.trace_energy[(size_t)t * a.C + c] = e;
+        if (cut > best) best = cut;
+    }
+    a.best[t] = best;
+}
+
+// Generic tiled transpose: src [R][Cc] -> dst [Cc_used][R] (first Cc_used columns)
+template <typename T>
+__global__ void transpose_tile(const T *__restrict__ src, T *__restrict__ dst, int R, int Cc,
+                               int Cc_used) {
+    __shared__ T tile[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int r = r0 + y, c = c0 + threadIdx.x;
+        if (r < R && c < Cc_used) tile[y][threadIdx.x] = src[(size_t)r * Cc + c];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int c = c0 + y, r = r0 + threadIdx.x;
+        if (c < Cc_used && r < R) dst[(size_t)c * R + r] = tile[threadIdx.x][y];
+    }
+}
+
+// Debug: device hash and tanh on arbitrary inputs.
+__global__ void debug_stream(int64_t cnt, const uint64_t *key, const uint64_t *tag,
+                             const uint64_t *x, const uint64_t *y, uint64_t *out) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < cnt) out[g] = absorb(absorb(absorb(key[g], tag[g]), x[g]), y[g]);
+}
+
+__global__ void debug_tanh(int64_t cnt, const double *x, double *out) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < cnt) out[g] = pb_libm_tanh(x[g]);
+}
+
+}  // namespace pbsa

@@ -1,0 +1,195 @@
+"""CUDA path vs the reference (golden fixtures) and the oracle, bit-for-bit.
+
+Every test here calls the product through the C ABI (libpbsa.so via the
+package API) on a real GPU.  Bar: spins, cut traces, update counts, inputs,
+histories, best cuts and i0 traces are bit-identical; energies are compared
+exactly too (they are integer sums for every integer-weight case, and the
+fp64 case keeps the reference's accumulation order).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from cases import BENCH_CASES, bench_inputs, random_graph, small_case
+from paper_2601_14476_b200 import _native, engine, streams
+from paper_2601_14476_b200.annealer import (Algorithm, AlgorithmConfig, AnnealSchedule,
+                                            derive_schedule, profile_rows, run_anneal)
+from paper_2601_14476_b200.model import IsingModel, maxcut_to_ising
+from paper_2601_14476_b200.pbit import VariabilityConfig, VariabilityProfile, sample_variability
+
+pytestmark = pytest.mark.gpu
+
+M64 = (1 << 64) - 1
+
+
+def _batch(model, sch, cfg, keys, profs, graph):
+    b = _native.Batch(model, sch, keys, profile_rows=profile_rows(profs, model.n), graph=graph,
+                      algo_code=cfg.kind.code, alpha=cfg.kernel_alpha, p_stall=cfg.p_stall)
+    return _native.anneal_batch(b)[0]
+
+
+def test_device_hash_matches_reference_kats(golden_streams):
+    rows = golden_streams["grid"]
+    keys = [int(r[0]) for r in rows]
+    tags = [r[1] for r in rows]
+    a = [int(r[2]) for r in rows]
+    b = [r[3] for r in rows]
+    got = _native.debug_stream_u64(keys, tags, a, b)
+    assert [int(x) for x in got] == [int(r[4]) for r in rows]
+    kat = _native.debug_stream_u64([42, 0], [3, 1], [7, 0], [123, 0])
+    assert int(kat[0]) == 0xB71C3C338A17B8FA and int(kat[1]) == 0x9D9A85784BF1C21D
+
+
+def test_device_tanh_matches_host_libm():
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.uniform(-25, 25, 400_000), rng.uniform(-1.5, 1.5, 400_000),
+                        rng.standard_normal(200_000) * 1e-9,
+                        np.ldexp(rng.uniform(0.5, 1, 200_000), rng.integers(-60, 5, 200_000))])
+    got = _native.debug_tanh(x)
+    want = np.array([math.tanh(v) for v in x])
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("pname", ["ideal", "varied"])
+@pytest.mark.parametrize("kind", list(Algorithm))
+def test_small_case_matches_reference(golden_small, pname, kind):
+    g, model, sch, profiles = small_case()
+    cfg = AlgorithmConfig(kind, alpha=3, p_stall=0.4)
+    for seed in (0, 1):
+        r = run_anneal(model, sch, cfg, profiles[pname], seed=seed, graph=g)
+        p = f"{pname}_{kind.value}_{seed}_"
+        assert np.array_equal(r.final_state.spins, golden_small[p + "spins"])
+        assert np.array_equal(r.final_state.inputs, golden_small[p + "inputs"])
+        assert np.array_equal(r.final_state.ti_history, golden_small[p + "hist"])
+        assert np.array_equal(r.update_counts, golden_small[p + "counts"])
+        assert np.array_equal(r.i0_trace, golden_small[p + "i0"])
+        assert np.array_equal(r.energy_trace, golden_small[p + "energy"])
+        assert np.array_equal(r.cut_trace, golden_small[p + "cut"])
+        assert r.best_cut == golden_small[p + "best"]
+
+
+@pytest.mark.parametrize("tag", list(BENCH_CASES))
+def test_benchmark_trials_match_reference(golden_bench, bench_graphs, tag):
+    name, kind, sig, trials = BENCH_CASES[tag]
+    graph = bench_graphs(name)
+    model, sch, cfg, seeds, profs, keys = bench_inputs(graph, kind, sig, trials)
+    out = _batch(model, sch, cfg, keys, profs, graph)
+    for idx, k in enumerate(trials):
+        p = f"{tag}_{k}_"
+        assert np.array_equal(out["spins"][idx], golden_bench[p + "spins"]), p
+        assert np.array_equal(out["cut_trace"][idx], golden_bench[p + "cut"]), p
+        assert out["best_cut"][idx] == golden_bench[p + "best"], p
+        assert out["counts"][idx].sum() == golden_bench[p + "counts_sum"], p
+        assert np.array_equal(out["inputs"][idx], golden_bench[p + "inputs"]), p
+        W = graph.total_weight()
+        assert np.array_equal(out["energy_trace"][idx], W - 2.0 * out["cut_trace"][idx])
+
+
+@pytest.mark.parametrize("kind", list(Algorithm))
+def test_g1_hundred_trial_summaries_match_reference(golden_bench, bench_graphs, kind):
+    # acceptance criterion 3 numbers (/root/reference/pkg/test_output.txt:148)
+    spec = engine.ExperimentSpec(graph="G1", algo=AlgorithmConfig(kind), cycles=1000, trials=100)
+    s = engine.run_trials(spec, {"G1": bench_graphs("G1")})
+    assert np.array_equal([r.final_cut for r in s.results],
+                          golden_bench[f"g1_{kind.value}_s0_final_cuts100"])
+    assert np.array_equal([r.best_cut for r in s.results],
+                          golden_bench[f"g1_{kind.value}_s0_best_cuts100"])
+    want = {"psa": 0.0, "tapsa": 0.9973, "spsa": 0.7418}[kind.value]
+    assert round(s.mean_cut / 11605, 4) == want
+
+
+def _oracle_compare(oracle, model, sch, cfg, profs, keys, graph):
+    got = _batch(model, sch, cfg, keys, profs, graph)
+    ref_profs = profs if profs is not None else VariabilityProfile.ideal(model.n, sch.t_res)
+    want = oracle.anneal_batch(model, sch, cfg.kind.value, ref_profs, keys, graph=graph,
+                               alpha=cfg.kernel_alpha, p_stall=cfg.p_stall)
+    for k in ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
+    if graph is not None:
+        assert np.array_equal(got["cut_trace"], want["cut_trace"])
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_specs_match_oracle(oracle, case):
+    # criterion-2-style random specs (test_acceptance.py:82-118), all rules
+    rng = np.random.default_rng(7000 + case)
+    n = int(rng.integers(4, 60))
+    g = random_graph(n, int(rng.integers(0, 1 << 30)), weights=(-2, -1, 1, 2) if case % 2 else (-1, 1),
+                     p_edge=float(rng.uniform(0.1, 0.8)))
+    model = maxcut_to_ising(g)
+    t_res = int(rng.choice([1, 3, 10]))
+    sch = derive_schedule(model, cycles=int(rng.integers(5, 80)), t_res=t_res)
+    kind = list(Algorithm)[case % 3]
+    cfg = AlgorithmConfig(kind, alpha=int(rng.integers(1, 6)), p_stall=float(rng.uniform(0, 1)))
+    T = int(rng.integers(1, 70))
+    keys = [streams.run_key(int(rng.integers(0, 1 << 62))) for _ in range(T)]
+    if case % 4 == 0:
+        profs = None
+    else:
+        vc = VariabilityConfig(*(float(x) for x in rng.uniform(0, 0.8, 3)), t_res=t_res)
+        profs = [sample_variability(vc, n, np.random.default_rng(int(rng.integers(0, 1 << 30))))
+                 for _ in range(T)]
+    _oracle_compare(oracle, model, sch, cfg, profs, keys, g)
+
+
+def test_fractional_model_without_graph_matches_oracle(oracle):
+    # non-integer couplings and fields, no graph: fp64 field/energy order path
+    rng = np.random.default_rng(3)
+    n = 25
+    edges = [(i, j, float(rng.normal())) for i in range(n) for j in range(i + 1, n)
+             if rng.random() < 0.3]
+    model = IsingModel.from_edges(n, edges, h=rng.normal(size=n) * 0.3)
+    sch = derive_schedule(model, cycles=40, t_res=4)
+    for kind in Algorithm:
+        cfg = AlgorithmConfig(kind, alpha=2, p_stall=0.3)
+        keys = [streams.run_key(s) for s in range(9)]
+        _oracle_compare(oracle, model, sch, cfg, None, keys, None)
+
+
+def test_single_spin_bias_saturates_to_plus_one():
+    # /root/reference/pkg/tests/test_annealer.py:182-190
+    model = IsingModel.from_edges(1, [], h=[2.0])
+    sch = AnnealSchedule(i0_min=0.5, i0_max=50.0, beta=0.01 ** (1.0 / 9.0), cycles=10, t_res=3)
+    res = run_anneal(model, sch, AlgorithmConfig(Algorithm.PSA),
+                     VariabilityProfile.ideal(1, t_res=3), seed=5)
+    assert res.final_state.spins[0] == 1
+    assert res.final_energy == -2.0
+    assert res.cut_trace is None and res.final_cut is None and res.best_cut is None
+
+
+def test_degenerate_rules_are_bitwise_plain_rule(bench_graphs):
+    # alpha=1 TApSA and p=0 SpSA collapse onto pSA (criterion 2), on the packed path
+    g = bench_graphs("G81")
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 60, 10)
+    keys = [streams.run_key(s) for s in range(64)]
+    base = _batch(model, sch, AlgorithmConfig(Algorithm.PSA), keys, None, g)
+    for cfg in (AlgorithmConfig(Algorithm.TAPSA, alpha=1), AlgorithmConfig(Algorithm.SPSA, p_stall=0.0)):
+        other = _batch(model, sch, cfg, keys, None, g)
+        for k in ("spins", "cut_trace", "energy_trace", "counts", "inputs"):
+            assert np.array_equal(base[k], other[k]), (cfg, k)
+
+
+def test_full_size_g81_properties_and_shard_invariance(bench_graphs, golden_bench):
+    """BASELINE config C4 at full size (4096 trials): recorded trials match the
+    reference, E = W - 2 cut on every trace entry, and any trial split (the
+    multi-GPU sharding) gives identical per-trial results."""
+    g = bench_graphs("G81")
+    spec = engine.ExperimentSpec(graph="G81", algo=AlgorithmConfig(Algorithm.PSA), cycles=1000,
+                                 trials=4096)
+    full, _ = engine.run_trial_range(spec, g, 0, 4096)
+    half, _ = engine.run_trial_range(spec, g, 2048, 4096)
+    for k in (0, 1, 2047, 4095):
+        assert np.array_equal(full[k].cut_trace, golden_bench[f"g81_psa_s0_{k}_cut"])
+        assert np.array_equal(full[k].final_state.spins, golden_bench[f"g81_psa_s0_{k}_spins"])
+    for k in range(2048, 4096, 97):
+        assert np.array_equal(full[k].final_state.spins, half[k - 2048].final_state.spins)
+        assert np.array_equal(full[k].cut_trace, half[k - 2048].cut_trace)
+    W = g.total_weight()
+    for r in full[::256]:
+        assert np.array_equal(r.energy_trace, W - 2.0 * r.cut_trace)
+        assert r.best_cut == r.cut_trace.max()

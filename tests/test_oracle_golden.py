@@ -1,0 +1,89 @@
+"""Pin the CPU oracle (oracle/psa_oracle.c) to the reference's own outputs.
+
+The golden fixtures were produced by importing the reference package
+(tests/golden/make_golden.py); the oracle must reproduce them bit-for-bit
+before it is trusted as the checker for the CUDA path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from cases import BENCH_CASES, bench_inputs, small_case
+
+
+def test_oracle_stream_kats(oracle, golden_streams):
+    # pinned values of /root/reference/pkg/tests/test_streams.py:26-45
+    assert oracle.mix64(1) == 0x10A81D8AD3D870A3
+    assert oracle.stream_u64(42, 3, 7, 123) == 0xB71C3C338A17B8FA
+    assert oracle.run_key(0) == 0x9D9A85784BF1C21D
+    assert oracle.trial_seed(0, 0) == 0x805BF55D41EBCFB0
+    assert oracle.trial_seed(0, 1) == 0xDA28150A69217582
+    assert oracle.profile_seed(12345) == 0xB62E0384700FB443
+    assert oracle.uniform01(9, 3, 5, 17) == 0.2934698501022247
+    for z, want in golden_streams["mix64"].items():
+        assert oracle.mix64(int(z)) == int(want)
+    for key, tag, a, b, want, u in golden_streams["grid"]:
+        assert oracle.stream_u64(int(key), tag, int(a), b) == int(want)
+        assert oracle.uniform01(int(key), tag, int(a), b) == float.fromhex(u)
+
+
+@pytest.mark.parametrize("pname", ["ideal", "varied"])
+@pytest.mark.parametrize("kind", ["psa", "tapsa", "spsa"])
+def test_oracle_small_case_matches_reference(oracle, golden_small, pname, kind):
+    g, model, sch, profiles = small_case()
+    assert np.array_equal(np.stack([g.edge_i, g.edge_j, g.edge_w]), golden_small["edges"])
+    prof = profiles[pname]
+    alpha = 3 if kind == "tapsa" else 1
+    for seed in (0, 1):
+        from paper_2601_14476_b200 import streams
+        out = oracle.anneal_batch(model, sch, kind, prof, [streams.run_key(seed)], graph=g,
+                                  alpha=alpha, p_stall=0.4, threads=1)
+        p = f"{pname}_{kind}_{seed}_"
+        assert np.array_equal(out["spins"][0], golden_small[p + "spins"])
+        assert np.array_equal(out["inputs"][0], golden_small[p + "inputs"])
+        assert np.array_equal(out["hist"][0], golden_small[p + "hist"])
+        assert np.array_equal(out["counts"][0], golden_small[p + "counts"])
+        assert np.array_equal(out["i0_trace"][0], golden_small[p + "i0"])
+        assert np.array_equal(out["energy_trace"][0], golden_small[p + "energy"])
+        assert np.array_equal(out["cut_trace"][0], golden_small[p + "cut"])
+        assert out["best_cut"][0] == golden_small[p + "best"]
+
+
+# one representative trial per benchmark config keeps the CPU suite short
+ORACLE_BENCH = [("g1_psa_s0", [0, 3]), ("g1_psa_s5", [1]), ("g1_tapsa_s0", [0]),
+                ("g1_spsa_s0", [1]), ("g22_psa_s5", [1024]), ("g55_psa_s5", [0, 4095]),
+                ("g81_psa_s0", [2047]), ("g81_psa_s5", [0])]
+
+
+@pytest.mark.parametrize("tag,trials", ORACLE_BENCH)
+def test_oracle_benchmark_runs_match_reference(oracle, golden_bench, bench_graphs, tag, trials):
+    name, kind, sig, _ = BENCH_CASES[tag]
+    graph = bench_graphs(name)
+    model, sch, cfg, seeds, profs, keys = bench_inputs(graph, kind, sig, trials)
+    out = oracle.anneal_batch(model, sch, kind.value, profs if profs else _ideal(graph.n), keys,
+                              graph=graph, alpha=cfg.kernel_alpha, p_stall=cfg.p_stall)
+    for idx, k in enumerate(trials):
+        p = f"{tag}_{k}_"
+        assert np.array_equal(out["spins"][idx], golden_bench[p + "spins"]), p
+        assert np.array_equal(out["cut_trace"][idx], golden_bench[p + "cut"]), p
+        assert out["best_cut"][idx] == golden_bench[p + "best"]
+        assert out["counts"][idx].sum() == golden_bench[p + "counts_sum"]
+        assert np.array_equal(out["inputs"][idx], golden_bench[p + "inputs"]), p
+
+
+def _ideal(n):
+    from paper_2601_14476_b200.pbit import VariabilityProfile
+    return VariabilityProfile.ideal(n)
+
+
+def test_profile_golden_prefix(golden_bench, bench_graphs):
+    # host profile sampling reproduces the reference draws (pbit.py:57-75)
+    for tag in ("g55_psa_s5", "g22_psa_s5", "g81_psa_s5"):
+        name, kind, sig, _ = BENCH_CASES[tag]
+        *_, profs, _ = bench_inputs(bench_graphs(name), kind, sig, [0])
+        p = f"{tag}_0_"
+        assert np.array_equal(profs[0].lam[:3], golden_bench[p + "lam3"])
+        assert np.array_equal(profs[0].delta[:3], golden_bench[p + "delta3"])
+        assert np.array_equal(profs[0].period[:8], golden_bench[p + "period8"])
