@@ -108,6 +108,13 @@ int pbsa_plan_summary(pbsa_plan *plan, int64_t *final_cut_sum, int64_t *best_cut
 int pbsa_plan_info(const pbsa_plan *plan, int *path, int64_t *launches_per_run,
                    double *sweep_ms_mean, int64_t *sweep_launches, int64_t *words);
 
+/*
+ * Bytes one end-to-end call moves: host->device at plan creation (CSR,
+ * edges, keys, profiles, schedule tables) and device->host for a full
+ * pbsa_plan_download of all eight outputs.
+ */
+int pbsa_plan_bytes(const pbsa_plan *plan, int64_t *h2d_bytes, int64_t *d2h_bytes);
+
 int pbsa_plan_destroy(pbsa_plan *plan);
 
 /*

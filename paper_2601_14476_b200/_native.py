@@ -40,6 +40,7 @@ _SIGNATURES = [
     ("pbsa_plan_info", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_I64),
                                       ctypes.POINTER(_F64), ctypes.POINTER(_I64),
                                       ctypes.POINTER(_I64)]),
+    ("pbsa_plan_bytes", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("pbsa_plan_destroy", ctypes.c_int, [_P]),
     ("pbsa_anneal_loop_batch", ctypes.c_int,
      [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
@@ -200,6 +201,12 @@ class Plan:
         return dict(path={1: "packed", 2: "general"}.get(path.value, "?"),
                     launches=launches.value, sweep_ms_mean=ms.value,
                     sweep_launches=sweeps.value, words=words.value)
+
+    def transfer_bytes(self) -> tuple[int, int]:
+        """(host->device bytes at creation, device->host bytes of a full download)."""
+        a, b = _I64(), _I64()
+        _check(load().pbsa_plan_bytes(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
 
     def close(self) -> None:
         if getattr(self, "_h", None):

@@ -112,6 +112,7 @@ template <typename T>
 struct DevBuf {
     T *p = nullptr;
     size_t n = 0;
+    size_t bytes_up = 0;  // host->device bytes of the last upload
     void alloc(size_t count) {
         release();
         n = count;
@@ -119,6 +120,7 @@ struct DevBuf {
     }
     void upload(const T *src, size_t count, cudaStream_t st) {
         alloc(count);
+        bytes_up = count * sizeof(T);
         if (count) CK(cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
     }
     void upload(const std::vector<T> &v, cudaStream_t st) { upload(v.data(), v.size(), st); }
@@ -126,6 +128,7 @@ struct DevBuf {
         if (p) cudaFree(p);
         p = nullptr;
         n = 0;
+        bytes_up = 0;
     }
     ~DevBuf() { release(); }
 };
@@ -160,6 +163,7 @@ struct pbsa_plan {
     int warps_per_word = 1, chunks = 1, packed_blocks = 1;
     DevBuf<uint32_t> p_spins[2], rowptr, adj;
     DevBuf<uint64_t> thr, krg;
+    DevBuf<uint2> kfc;
     DevBuf<unsigned long long> pacc;  // [(C+1)][Tp]
     DevBuf<int16_t> raw_last;         // [n][Tp]
 
@@ -309,7 +313,11 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         for (int64_t k = 0; k < gm; ++k) P.total_w += gew[k];
     }
     const bool rule_is_psa = algo == 0 || (algo == 1 && alpha == 1) || (algo == 2 && p_stall == 0.0);
-    const bool packed = rule_is_psa && unit_J && zero_h && ideal && graph_is_model && dmax <= 127;
+    // i < 2^30 and count < 2^30 let the packed kernel fold the first xorshift
+    // of each absorb into per-trial constants (pbsa_device.cuh)
+    const bool small_counters = n <= (1LL << 30) && cycles * t_res <= (1LL << 30);
+    const bool packed = rule_is_psa && unit_J && zero_h && ideal && graph_is_model && dmax <= 127 &&
+                        small_counters;
     P.tapsa_hist_from_raw = packed && algo == 1;
     P.path = packed ? PBSA_PATH_PACKED : PBSA_PATH_GENERAL;
 
@@ -342,8 +350,15 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             adjv[k] = (uint32_t)indices[k] | (values[k] < 0 ? 0x80000000u : 0u);
         P.adj.upload(adjv, st);
         std::vector<uint64_t> krg(P.Tp);
-        for (int64_t t = 0; t < P.Tp; ++t) krg[t] = kr[t] + kGamma;
+        std::vector<uint2> kfc(P.Tp);
+        for (int64_t t = 0; t < P.Tp; ++t) {
+            krg[t] = kr[t] + kGamma;
+            const uint32_t lo = (uint32_t)krg[t], hi = (uint32_t)(krg[t] >> 32);
+            const uint32_t Y = hi ^ (hi >> 30);
+            kfc[t] = make_uint2(lo ^ ((lo >> 30) | (hi << 2)), Y * 0x1CE4E5B9u);
+        }
         P.krg.upload(krg, st);
+        P.kfc.upload(kfc, st);
         // thresholds per (cycle, raw): inp = i0 * raw; act = r + tanh(inp) (lam = 1, delta = 0)
         std::vector<uint64_t> thr((size_t)cycles * P.K);
         for (int64_t c = 0; c < cycles; ++c)
@@ -357,7 +372,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
 
         // launch shape: one wave of resident warps, each owning one word
         PackedKernel kern = packed_kernel_for(P.L);
-        const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8;
+        const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8 + 16;
         set_packed_smem(kern, smem);
         int occ = 0, sms = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pbsa::kPackedThreads, smem));
@@ -496,8 +511,8 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
         PackedKernel kern = packed_kernel_for(P.L);
-        const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8;
-        CK(cudaEventRecord(P.ev_sweep0, st));
+        const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8 + 16;
+        CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
         int cur = 0;
         for (int64_t c = 0; c <= P.cycles; ++c) {
             pbsa::PackedArgs a{};
@@ -506,6 +521,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             a.rowptr = P.rowptr.p;
             a.adj = P.adj.p;
             a.krg = P.krg.p;
+            a.kfc = P.kfc.p;
             const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
             a.thr = P.thr.p + (size_t)cc * P.K;
             a.pacc = P.pacc.p + (size_t)c * P.Tp;
@@ -527,7 +543,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                 cur ^= 1;
             }
         }
-        CK(cudaEventRecord(P.ev_sweep1, st));
+        CK(cudaEventRecordWithFlags(P.ev_sweep1, st, cudaEventRecordExternal));
         P.final_parity = cur;
         pbsa::FinalArgs f{};
         f.pacc = P.pacc.p;
@@ -551,7 +567,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         CK(cudaMemsetAsync(P.cut_acc.p, 0, P.cut_acc.n * sizeof(unsigned long long), st));
         if (P.e_acc.n) CK(cudaMemsetAsync(P.e_acc.p, 0, P.e_acc.n * sizeof(unsigned long long), st));
         P.launches += 1;
-        CK(cudaEventRecord(P.ev_sweep0, st));
+        CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
         int cur = 0;
         size_t ai = 0;
         const int sm_chunks = std::max<int64_t>(1, std::min<int64_t>(64, (std::max(mm, gm) + 255) / 256));
@@ -616,7 +632,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                 ++P.launches;
             }
         }
-        CK(cudaEventRecord(P.ev_sweep1, st));
+        CK(cudaEventRecordWithFlags(P.ev_sweep1, st, cudaEventRecordExternal));
         P.final_parity = cur;
         pbsa::FinalArgs f{};
         f.cut_acc = P.cut_acc.p;
@@ -841,6 +857,29 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
         if (trace_i0)
             for (int64_t t = 0; t < T; ++t) std::memcpy(trace_i0 + t * C, P->i0.data(), C * sizeof(double));
         CK(cudaGetLastError());
+    });
+}
+
+int pbsa_plan_bytes(const pbsa_plan *P, int64_t *h2d_bytes, int64_t *d2h_bytes) {
+    return guarded([&] {
+        if (!P) fail(PBSA_EINVAL, "null plan");
+        const size_t up = P->p_spins[0].bytes_up + P->rowptr.bytes_up + P->adj.bytes_up + P->kfc.bytes_up +
+                          P->thr.bytes_up + P->krg.bytes_up + P->col.bytes_up + P->me_i.bytes_up +
+                          P->me_j.bytes_up + P->ge_i.bytes_up + P->ge_j.bytes_up +
+                          P->val.bytes_up + P->h.bytes_up + P->me_w.bytes_up + P->lam.bytes_up +
+                          P->delta.bytes_up + P->me_wi.bytes_up + P->h_int.bytes_up +
+                          P->ge_w.bytes_up + P->period.bytes_up + P->kr.bytes_up +
+                          P->kst.bytes_up + P->kspin.bytes_up;
+        const int64_t T = P->T, n = P->n, C = P->cycles;
+        int64_t down = T * n + T * n * 8 + 2 * T * C * 8 + T * 8;  // spins, inputs, traces, best
+        if (P->path == PBSA_PATH_GENERAL) {
+            down += T * n * 4;                                        // counts (int32 on device)
+            if (P->algo == 1) down += T * n * P->alpha * 8;           // history
+        } else if (P->tapsa_hist_from_raw) {
+            down += T * n * 8;
+        }
+        if (h2d_bytes) *h2d_bytes = (int64_t)up;
+        if (d2h_bytes) *d2h_bytes = down;
     });
 }
 

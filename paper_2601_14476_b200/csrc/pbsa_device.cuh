@@ -79,48 +79,94 @@ __global__ void init_general(int8_t *__restrict__ s, const uint64_t *__restrict_
 // Layout: spins uint32 [W][n] (word-major, node-fast): bit b of word (w, i) is
 // trial 32w+b's spin at node i, 1 = +1.  A warp owns one word index w for its
 // whole life and walks 32-node chunks of it (lane = node), so the 32 trial
-// keys of the warp are uniform (broadcast from shared memory), neighbour
+// constants of the warp are uniform (broadcast from shared memory), neighbour
 // words of consecutive nodes are coalesced on lattice-like graphs, and the
 // per-trial cut partials reduce with one 32x32 butterfly per warp.
+//
+// The per-update draw is H = absorb(absorb(K, i), count) with
+// K = absorb(key, TAG_R) (streams.py:41-45, _kernels.py:149).  Two exact
+// algebraic reductions shorten it (both need i < 2^30 and count < 2^30, which
+// the host checks before choosing this path):
+//   * the first xorshift of absorb(K, i) only sees i in bits < 30, so
+//     y = (F_t ^ i, Y_t) with per-trial constants, and the high word of
+//     y * M1 is umulhi(y_lo, M1lo) + y_lo * M1hi + C_t with C_t = Y_t * M1lo;
+//   * likewise count enters the first xorshift of the second absorb as a
+//     plain XOR on the low word.
+// The activation decision "H >= thr" is taken on the high word of the last
+// multiply (before the final xorshift) through the carry of zhi + ~thi; the
+// only inputs where that can differ from the exact 64-bit test are
+// (zhi >> 1) == (thi >> 1), which flag the word for an exact recomputation.
 struct PackedArgs {
     const uint32_t *sold;
     uint32_t *snew;
     const uint32_t *rowptr;   // [n+1]
     const uint32_t *adj;      // [nnz] column | (J < 0) << 31
-    const uint64_t *krg;      // [Tp] absorb(key, TAG_R) + GAMMA
+    const uint2 *kfc;         // [Tp] per-trial (F_t, C_t)
+    const uint64_t *krg;      // [Tp] absorb(key, TAG_R) + GAMMA (exact slow path)
     const uint64_t *thr;      // [K] thresholds of this cycle (H >= thr -> +1)
     unsigned long long *pacc; // [Tp] += sum_i s_i * raw_i of the sub-step's input state
     int16_t *raw_out;         // [n][Tp] raw field of this update, or null
     int n, W, Tp, K, dmax;
     int warps_per_word;       // warps sharing one word index
     int chunks;               // ceil(n / 32)
-    uint32_t count;           // global sub-step counter c * t_res
+    uint32_t count;           // global sub-step counter c * t_res (< 2^30)
     int do_update;            // 0: only accumulate pacc (final cut pass)
 };
 
-// H >= thr for H = mix64(x), evaluated high word first: the low word is only
-// needed when the high words tie (probability ~2^-32).  thr == ~0 encodes
-// "never" (tanh == -1 exactly), which no genuine threshold equals because
-// genuine thresholds have their low 11 bits clear.
-__device__ __forceinline__ bool hash_ge(uint64_t x, uint64_t thr) {
-    uint64_t z = (x ^ (x >> 30)) * PB_M1;
-    z = (z ^ (z >> 27)) * PB_M2;
-    const uint32_t zhi = (uint32_t)(z >> 32);
-    const uint32_t hhi = zhi ^ (zhi >> 31);
-    const uint32_t thi = (uint32_t)(thr >> 32);
-    if (hhi != thi) return hhi > thi;
-    const uint64_t h = z ^ (z >> 31);
-    return h >= thr && thr != ~0ULL;
+// Exact H >= thr for H = mix64(x); thr == ~0 encodes "never" (tanh == -1),
+// which no genuine threshold equals (their low 11 bits are clear).
+__device__ __forceinline__ bool hash_ge_exact(uint64_t x, uint64_t thr) {
+    return mix64(x) >= thr && thr != ~0ULL;
 }
 
 constexpr int kPackedThreads = 256;
 constexpr int kPackedWarps = kPackedThreads / 32;
 
+__device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
+
+// One trial's decision bit, shifted into `word` through the carry flag.
+// Returns the (zhi ^ thi) tie witness (< 2 means "recompute exactly").
+__device__ __forceinline__ uint32_t packed_decide(uint32_t ylo, uint32_t C, uint32_t count,
+                                                  uint2 t, uint32_t &word) {
+    constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
+    constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
+    constexpr uint32_t GL = 0x7F4A7C15u, GH = 0x9E3779B9u;
+    // first absorb: z = y * M1 with y = (ylo, Y), Y * M1L folded into C.
+    // Right shifts of high words go through IMAD.HI (x >> s == umulhi(x, 2^(32-s)))
+    // so the FMA pipe takes part of the load of the saturated ALU pipe.
+    uint32_t zl = ylo * M1L;
+    uint32_t zh = mulhi(ylo, M1L) + ylo * M1H + C;
+    // z ^= z >> 27 ; z *= M2
+    uint32_t yl = zl ^ __funnelshift_r(zl, zh, 27);
+    uint32_t yh = zh ^ mulhi(zh, 1u << 5);
+    zl = yl * M2L;
+    zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
+    // z ^= z >> 31  -> A ; s = A + GAMMA
+    yl = zl ^ __funnelshift_r(zl, zh, 31);
+    yh = zh ^ mulhi(zh, 1u << 1);
+    uint32_t sl, sh;
+    asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
+        : "=r"(sl), "=r"(sh) : "r"(yl), "r"(yh), "r"(GL), "r"(GH));
+    // second absorb: x = s ^ count ; z ^= z >> 30 (count < 2^30 only touches the low word)
+    yl = sl ^ count ^ __funnelshift_r(sl, sh, 30);
+    yh = sh ^ mulhi(sh, 1u << 2);
+    zl = yl * M1L;
+    zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
+    yl = zl ^ __funnelshift_r(zl, zh, 27);
+    yh = zh ^ mulhi(zh, 1u << 5);
+    zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
+    // carry(zh + ~thi) == (zh > thi); word = 2 word + carry
+    uint32_t dummy;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %4;"
+        : "=r"(dummy), "=r"(word) : "r"(zh), "r"(t.x), "r"(word));
+    return zh ^ t.y;
+}
+
 template <int L>
 __global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) {
     extern __shared__ unsigned long long smem_u64[];
-    uint64_t *sthr = reinterpret_cast<uint64_t *>(smem_u64);   // [K]
-    uint64_t *skey = sthr + a.K;                                // [warps][32]
+    uint2 *sthr = reinterpret_cast<uint2 *>(smem_u64);   // [K] {~thi, thi}
+    uint2 *skey = sthr + a.K;                             // [warps][32] {F, C}
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int gwarp = blockIdx.x * kPackedWarps + wib;
@@ -128,14 +174,22 @@ __global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) 
     const int q = gwarp % a.warps_per_word;
     const bool live = w < a.W;
 
-    for (int k = threadIdx.x; k < a.K; k += blockDim.x) sthr[k] = a.thr[k];
-    uint64_t *key = skey + wib * 32;
-    key[lane] = live ? a.krg[(size_t)w * 32 + lane] : 0;
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+        const uint32_t thi = (uint32_t)(a.thr[k] >> 32);
+        sthr[k] = make_uint2(~thi, thi);
+    }
+    uint2 *key = skey + wib * 32;
+    key[lane] = live ? a.kfc[(size_t)w * 32 + lane] : make_uint2(0, 0);
+    uint32_t *scount = reinterpret_cast<uint32_t *>(skey + kPackedWarps * 32);
+    if (threadIdx.x == 0) scount[0] = a.count;
     __syncthreads();
 
     int acc[32];
 #pragma unroll
     for (int b = 0; b < 32; ++b) acc[b] = 0;
+    // read back through shared memory so the counter lives in a vector
+    // register (a kernel-parameter operand is re-fetched with LDCU per trial)
+    const uint32_t count = scount[0];
 
     if (live) {
         const uint32_t *sw = a.sold + (size_t)w * a.n;
@@ -146,35 +200,48 @@ __global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) 
             // bit-sliced count of neighbours with J_ik * s_k == +1
             uint32_t p[L];
 #pragma unroll
-            for (int b = 0; b < L; ++b) p[b] = 0;
+            for (int r = 0; r < L; ++r) p[r] = 0;
             for (uint32_t k = beg; k < end; ++k) {
                 const uint32_t e = __ldg(a.adj + k);
                 uint32_t carry = __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
 #pragma unroll
-                for (int b = 0; b < L; ++b) {
-                    const uint32_t nc = p[b] & carry;
-                    p[b] ^= carry;
+                for (int r = 0; r < L; ++r) {
+                    const uint32_t nc = p[r] & carry;
+                    p[r] ^= carry;
                     carry = nc;
                 }
             }
             const int d = (int)(end - beg);
             const uint32_t own = __ldg(sw + i);
-            uint32_t word = 0;
+            const uint2 *tb = sthr + (a.dmax - d);   // entry for raw = 2 pop - d
+            uint32_t word = 0, tie = 0xffffffffu;
+            const uint32_t ui = (uint32_t)i;
 #pragma unroll
-            for (int b = 0; b < 32; ++b) {
+            for (int b = 31; b >= 0; --b) {
                 int pop = 0;
 #pragma unroll
                 for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                 const int raw = 2 * pop - d;
                 if (a.do_update) {
-                    const uint64_t x1 = key[b] ^ (uint64_t)i;
-                    const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)a.count;
-                    word |= (uint32_t)hash_ge(x2, sthr[raw + a.dmax]) << b;
+                    const uint2 kc = key[b];
+                    tie = min(tie, packed_decide(kc.x ^ ui, kc.y, count, tb[2 * pop], word));
                 }
                 acc[b] += ((own >> b) & 1u) ? raw : -raw;
                 if (a.raw_out) a.raw_out[(size_t)i * a.Tp + w * 32 + b] = (int16_t)raw;
             }
-            if (a.do_update) a.snew[(size_t)w * a.n + i] = word;
+            if (a.do_update) {
+                if (tie < 2) {  // rare: some trial's high words nearly tie -> exact 64-bit test
+                    word = 0;
+                    for (int b = 0; b < 32; ++b) {
+                        int pop = 0;
+                        for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                        const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
+                        const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                        word |= (uint32_t)hash_ge_exact(x2, a.thr[2 * pop - d + a.dmax]) << b;
+                    }
+                }
+                a.snew[(size_t)w * a.n + i] = word;
+            }
         }
     }
     // 32x32 transpose-reduce: lane b ends with the warp's sum for trial 32w+b.
