@@ -213,17 +213,20 @@ void set_packed_smem(K kernel, size_t bytes) {
 }
 
 using PackedKernel = void (*)(pbsa::PackedArgs);
-PackedKernel packed_kernel_for(int L) {
+PackedKernel packed_kernel_for(int L, bool update) {
+#define PBSA_CASE(l) \
+    case l: return update ? pbsa::packed_sweep<l, true> : pbsa::packed_sweep<l, false>;
     switch (L) {
-        case 1: return pbsa::packed_sweep<1>;
-        case 2: return pbsa::packed_sweep<2>;
-        case 3: return pbsa::packed_sweep<3>;
-        case 4: return pbsa::packed_sweep<4>;
-        case 5: return pbsa::packed_sweep<5>;
-        case 6: return pbsa::packed_sweep<6>;
-        case 7: return pbsa::packed_sweep<7>;
+        PBSA_CASE(1)
+        PBSA_CASE(2)
+        PBSA_CASE(3)
+        PBSA_CASE(4)
+        PBSA_CASE(5)
+        PBSA_CASE(6)
+        PBSA_CASE(7)
         default: fail(PBSA_EINVAL, "packed path supports degree <= 127");
     }
+#undef PBSA_CASE
 }
 
 void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
@@ -371,9 +374,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.raw_last.alloc((size_t)n * P.Tp);
 
         // launch shape: one wave of resident warps, each owning one word
-        PackedKernel kern = packed_kernel_for(P.L);
+        PackedKernel kern = packed_kernel_for(P.L, true);
         const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8 + 16;
         set_packed_smem(kern, smem);
+        set_packed_smem(packed_kernel_for(P.L, false), smem);
         int occ = 0, sms = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pbsa::kPackedThreads, smem));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -382,6 +386,11 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         const int64_t target_warps = (int64_t)sms * occ * pbsa::kPackedWarps;
         int64_t wpw = std::max<int64_t>(1, target_warps / P.W);
         wpw = std::min<int64_t>(wpw, P.chunks);
+        // the per-thread bit-sliced cut counter holds sum(degree) < 2^kCutPlanes
+        const int64_t need = (P.chunks * std::max<int64_t>(dmax, 1)) / ((1LL << pbsa::kCutPlanes) - 1) + 1;
+        wpw = std::max<int64_t>(wpw, std::min<int64_t>(need, P.chunks));
+        if ((P.chunks + wpw - 1) / wpw * std::max<int64_t>(dmax, 1) >= (1LL << pbsa::kCutPlanes))
+            fail(PBSA_EINVAL, "graph too large for the packed cut counter");
         P.warps_per_word = (int)wpw;
         P.packed_blocks = (int)grid_for(P.W * wpw, pbsa::kPackedWarps);
         P.updates_per_run = (int64_t)n * trials * cycles;
@@ -510,7 +519,8 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                                                    (int)P.n, (int)P.W);
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
-        PackedKernel kern = packed_kernel_for(P.L);
+        PackedKernel kern_up = packed_kernel_for(P.L, true);
+        PackedKernel kern_cut = packed_kernel_for(P.L, false);
         const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
         int cur = 0;
@@ -535,7 +545,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             a.chunks = P.chunks;
             a.count = (uint32_t)(c * P.t_res);
             a.do_update = c < P.cycles;
-            kern<<<P.packed_blocks, pbsa::kPackedThreads, smem, st>>>(a);
+            (c < P.cycles ? kern_up : kern_cut)<<<P.packed_blocks, pbsa::kPackedThreads, smem, st>>>(a);
             CK(cudaGetLastError());
             ++P.launches;
             if (c < P.cycles) {

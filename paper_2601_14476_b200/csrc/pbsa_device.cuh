@@ -162,7 +162,22 @@ __device__ __forceinline__ uint32_t packed_decide(uint32_t ylo, uint32_t C, uint
     return zh ^ t.y;
 }
 
-template <int L>
+// Bit-sliced counter: add the L-bit per-trial numbers x[] into C[] (CL planes).
+template <int L, int CL>
+__device__ __forceinline__ void vc_add(uint32_t (&C)[CL], const uint32_t (&x)[L]) {
+    uint32_t carry = 0;
+#pragma unroll
+    for (int r = 0; r < CL; ++r) {
+        const uint32_t v = r < L ? x[r] : 0u;
+        const uint32_t s = C[r] ^ v ^ carry;
+        carry = (C[r] & v) | (carry & (C[r] ^ v));
+        C[r] = s;
+    }
+}
+
+constexpr int kCutPlanes = 16;  // per-thread cut counter width (host keeps tasks*dmax < 2^16)
+
+template <int L, bool UPDATE>
 __global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) {
     extern __shared__ unsigned long long smem_u64[];
     uint2 *sthr = reinterpret_cast<uint2 *>(smem_u64);   // [K] {~thi, thi}
@@ -183,13 +198,17 @@ __global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) 
     uint32_t *scount = reinterpret_cast<uint32_t *>(skey + kPackedWarps * 32);
     if (threadIdx.x == 0) scount[0] = a.count;
     __syncthreads();
-
-    int acc[32];
-#pragma unroll
-    for (int b = 0; b < 32; ++b) acc[b] = 0;
     // read back through shared memory so the counter lives in a vector
     // register (a kernel-parameter operand is re-fetched with LDCU per trial)
     const uint32_t count = scount[0];
+
+    // Per-trial sum over this thread's nodes of q_i = #{k : J_ik s_i s_k = +1},
+    // kept bit-sliced; s_i raw_i = 2 q_i - d_i, so the cut partial is
+    // 2 * C - dsum (h = 0).
+    uint32_t C[kCutPlanes];
+#pragma unroll
+    for (int r = 0; r < kCutPlanes; ++r) C[r] = 0;
+    int dsum = 0;
 
     if (live) {
         const uint32_t *sw = a.sold + (size_t)w * a.n;
@@ -197,39 +216,39 @@ __global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) 
             const int i = ch * 32 + lane;
             if (i >= a.n) continue;
             const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
-            // bit-sliced count of neighbours with J_ik * s_k == +1
-            uint32_t p[L];
+            const uint32_t own = __ldg(sw + i);
+            // bit-sliced counts: p = #{J_ik s_k = +1} (local field), g = #{J_ik s_i s_k = +1} (cut)
+            uint32_t p[L], g[L];
 #pragma unroll
-            for (int r = 0; r < L; ++r) p[r] = 0;
+            for (int r = 0; r < L; ++r) p[r] = g[r] = 0;
             for (uint32_t k = beg; k < end; ++k) {
                 const uint32_t e = __ldg(a.adj + k);
-                uint32_t carry = __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
+                uint32_t cp = __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
+                uint32_t cg = ~(cp ^ own);
 #pragma unroll
                 for (int r = 0; r < L; ++r) {
-                    const uint32_t nc = p[r] & carry;
-                    p[r] ^= carry;
-                    carry = nc;
+                    const uint32_t np = p[r] & cp, ng = g[r] & cg;
+                    p[r] ^= cp;
+                    g[r] ^= cg;
+                    cp = np;
+                    cg = ng;
                 }
             }
             const int d = (int)(end - beg);
-            const uint32_t own = __ldg(sw + i);
-            const uint2 *tb = sthr + (a.dmax - d);   // entry for raw = 2 pop - d
-            uint32_t word = 0, tie = 0xffffffffu;
-            const uint32_t ui = (uint32_t)i;
+            dsum += d;
+            vc_add<L, kCutPlanes>(C, g);
+            if (UPDATE) {
+                const uint2 *tb = sthr + (a.dmax - d);   // entry for raw = 2 pop - d
+                uint32_t word = 0, tie = 0xffffffffu;
+                const uint32_t ui = (uint32_t)i;
 #pragma unroll
-            for (int b = 31; b >= 0; --b) {
-                int pop = 0;
+                for (int b = 31; b >= 0; --b) {
+                    int pop = 0;
 #pragma unroll
-                for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
-                const int raw = 2 * pop - d;
-                if (a.do_update) {
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                     const uint2 kc = key[b];
                     tie = min(tie, packed_decide(kc.x ^ ui, kc.y, count, tb[2 * pop], word));
                 }
-                acc[b] += ((own >> b) & 1u) ? raw : -raw;
-                if (a.raw_out) a.raw_out[(size_t)i * a.Tp + w * 32 + b] = (int16_t)raw;
-            }
-            if (a.do_update) {
                 if (tie < 2) {  // rare: some trial's high words nearly tie -> exact 64-bit test
                     word = 0;
                     for (int b = 0; b < 32; ++b) {
@@ -241,10 +260,26 @@ __global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) 
                     }
                 }
                 a.snew[(size_t)w * a.n + i] = word;
+                if (a.raw_out) {  // last cycle only: the raw field each trial's update used
+                    for (int b = 0; b < 32; ++b) {
+                        int pop = 0;
+                        for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                        a.raw_out[(size_t)i * a.Tp + w * 32 + b] = (int16_t)(2 * pop - d);
+                    }
+                }
             }
         }
     }
-    // 32x32 transpose-reduce: lane b ends with the warp's sum for trial 32w+b.
+    // Unpack the per-trial totals and transpose-reduce over the warp:
+    // lane b ends with the warp's sum for trial 32w+b.
+    int acc[32];
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+        int v = 0;
+#pragma unroll
+        for (int r = 0; r < kCutPlanes; ++r) v |= (int)((C[r] >> b) & 1u) << r;
+        acc[b] = 2 * v - dsum;
+    }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
         const bool upper = (lane & off) != 0;
