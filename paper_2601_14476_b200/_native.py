@@ -14,7 +14,8 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libpbsa.so"
+LIB_PATH = Path(os.environ.get("PBSA_LIB") or
+                Path(__file__).resolve().parent / "_lib" / "libpbsa.so")
 
 PBSA_OK = 0
 PATH_PACKED, PATH_GENERAL = 1, 2

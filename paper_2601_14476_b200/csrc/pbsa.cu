@@ -387,10 +387,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         int64_t wpw = std::max<int64_t>(1, target_warps / P.W);
         wpw = std::min<int64_t>(wpw, P.chunks);
         // the per-thread bit-sliced cut counter holds sum(degree) < 2^kCutPlanes
-        const int64_t need = (P.chunks * std::max<int64_t>(dmax, 1)) / ((1LL << pbsa::kCutPlanes) - 1) + 1;
-        wpw = std::max<int64_t>(wpw, std::min<int64_t>(need, P.chunks));
-        if ((P.chunks + wpw - 1) / wpw * std::max<int64_t>(dmax, 1) >= (1LL << pbsa::kCutPlanes))
-            fail(PBSA_EINVAL, "graph too large for the packed cut counter");
+        const int64_t cap = (1LL << pbsa::kCutPlanes) - 1, dm = std::max<int64_t>(dmax, 1);
+        if (dm > cap) fail(PBSA_EINVAL, "degree too large for the packed cut counter");
+        const int64_t max_tasks = cap / dm;  // chunks one warp may take
+        wpw = std::max<int64_t>(wpw, std::min<int64_t>((P.chunks + max_tasks - 1) / max_tasks, P.chunks));
         P.warps_per_word = (int)wpw;
         P.packed_blocks = (int)grid_for(P.W * wpw, pbsa::kPackedWarps);
         P.updates_per_run = (int64_t)n * trials * cycles;

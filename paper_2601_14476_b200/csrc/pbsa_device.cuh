@@ -175,10 +175,15 @@ __device__ __forceinline__ void vc_add(uint32_t (&C)[CL], const uint32_t (&x)[L]
     }
 }
 
-constexpr int kCutPlanes = 16;  // per-thread cut counter width (host keeps tasks*dmax < 2^16)
+constexpr int kCutPlanes = 8;       // per-thread cut counter width (host keeps tasks*dmax < 2^8)
+constexpr int kWarpCutPlanes = 13;  // after the warp-level add (32 * 255 < 2^13)
+
+#ifndef PBSA_PACKED_MIN_BLOCKS
+#define PBSA_PACKED_MIN_BLOCKS 4
+#endif
 
 template <int L, bool UPDATE>
-__global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) {
+__global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed_sweep(PackedArgs a) {
     extern __shared__ unsigned long long smem_u64[];
     uint2 *sthr = reinterpret_cast<uint2 *>(smem_u64);   // [K] {~thi, thi}
     uint2 *skey = sthr + a.K;                             // [warps][32] {F, C}
@@ -270,26 +275,27 @@ __global__ void __launch_bounds__(kPackedThreads, 3) packed_sweep(PackedArgs a) 
             }
         }
     }
-    // Unpack the per-trial totals and transpose-reduce over the warp:
-    // lane b ends with the warp's sum for trial 32w+b.
-    int acc[32];
+    // Warp-level bit-sliced add of the 32 lanes' counters (all lanes of the
+    // warp hold the same 32 trials), then lane b unpacks trial 32w+b.
+    uint32_t W13[kWarpCutPlanes];
 #pragma unroll
-    for (int b = 0; b < 32; ++b) {
-        int v = 0;
-#pragma unroll
-        for (int r = 0; r < kCutPlanes; ++r) v |= (int)((C[r] >> b) & 1u) << r;
-        acc[b] = 2 * v - dsum;
-    }
+    for (int r = 0; r < kWarpCutPlanes; ++r) W13[r] = r < kCutPlanes ? C[r] : 0u;
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
-        const bool upper = (lane & off) != 0;
+        uint32_t carry = 0;
 #pragma unroll
-        for (int b = 0; b < off; ++b) {
-            const int send = upper ? acc[b] : acc[b + off];
-            const int keep = upper ? acc[b + off] : acc[b];
-            acc[b] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+        for (int r = 0; r < kWarpCutPlanes; ++r) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, W13[r], off);
+            const uint32_t sum = W13[r] ^ o ^ carry;
+            carry = (W13[r] & o) | (carry & (W13[r] ^ o));
+            W13[r] = sum;
         }
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, off);
     }
+    int acc0 = 0;
+#pragma unroll
+    for (int r = 0; r < kWarpCutPlanes; ++r) acc0 |= (int)((W13[r] >> lane) & 1u) << r;
+    int acc[1] = {2 * acc0 - dsum};
     if (live && acc[0]) atomicAdd(a.pacc + (size_t)w * 32 + lane, (unsigned long long)(long long)acc[0]);
 }
 
