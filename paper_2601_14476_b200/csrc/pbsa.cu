@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <set>
@@ -163,7 +164,8 @@ struct pbsa_plan {
     int warps_per_word = 1, chunks = 1, packed_blocks = 1;
     DevBuf<uint32_t> p_spins[2], rowptr, adj;
     DevBuf<uint64_t> thr, krg;
-    DevBuf<uint2> kfc;
+    DevBuf<uint2> kfc, acache;
+    bool use_cache = false;
     DevBuf<unsigned long long> pacc;  // [(C+1)][Tp]
     DevBuf<int16_t> raw_last;         // [n][Tp]
 
@@ -213,9 +215,12 @@ void set_packed_smem(K kernel, size_t bytes) {
 }
 
 using PackedKernel = void (*)(pbsa::PackedArgs);
-PackedKernel packed_kernel_for(int L, bool update) {
-#define PBSA_CASE(l) \
-    case l: return update ? pbsa::packed_sweep<l, true> : pbsa::packed_sweep<l, false>;
+PackedKernel packed_kernel_for(int L, bool update, bool cached) {
+#define PBSA_CASE(l)                                                                  \
+    case l:                                                                           \
+        return update ? (cached ? pbsa::packed_sweep<l, true, true>                   \
+                                : pbsa::packed_sweep<l, true, false>)                 \
+                      : pbsa::packed_sweep<l, false, false>;
     switch (L) {
         PBSA_CASE(1)
         PBSA_CASE(2)
@@ -374,10 +379,16 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.raw_last.alloc((size_t)n * P.Tp);
 
         // launch shape: one wave of resident warps, each owning one word
-        PackedKernel kern = packed_kernel_for(P.L, true);
+        // cache the sub-step-independent first absorb of every (trial, node)
+        // draw when it fits the budget (PBSA_PACKED_CACHE=0/1 overrides)
+        const size_t cache_entries = (size_t)P.W * ((n + 31) / 32) * 1024;
+        P.use_cache = cache_entries * 8 <= (32ULL << 30);
+        if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1';
+        if (P.use_cache) P.acache.alloc(cache_entries);
+        PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache);
         const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8 + 16;
         set_packed_smem(kern, smem);
-        set_packed_smem(packed_kernel_for(P.L, false), smem);
+        set_packed_smem(packed_kernel_for(P.L, false, false), smem);
         int occ = 0, sms = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pbsa::kPackedThreads, smem));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -519,8 +530,11 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                                                    (int)P.n, (int)P.W);
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
-        PackedKernel kern_up = packed_kernel_for(P.L, true);
-        PackedKernel kern_cut = packed_kernel_for(P.L, false);
+        if (P.use_cache)
+            pbsa::packed_cache_init<<<grid_for((int64_t)P.acache.n, TB), TB, 0, st>>>(
+                P.acache.p, P.krg.p, (int)P.n, P.chunks, (int)P.W);
+        PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache);
+        PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
         const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
         int cur = 0;
@@ -532,6 +546,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             a.adj = P.adj.p;
             a.krg = P.krg.p;
             a.kfc = P.kfc.p;
+            a.acache = P.use_cache ? P.acache.p : nullptr;
             const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
             a.thr = P.thr.p + (size_t)cc * P.K;
             a.pacc = P.pacc.p + (size_t)c * P.Tp;

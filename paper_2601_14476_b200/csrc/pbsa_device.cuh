@@ -75,6 +75,23 @@ __global__ void init_general(int8_t *__restrict__ s, const uint64_t *__restrict_
     s[g] = (h >> 63) == 0 ? 1 : -1;
 }
 
+// Per-(trial, node) first absorb of the TAG_R draw, which does not depend on
+// the sub-step: absorb(K_t, i) + GAMMA (K_t = absorb(key, TAG_R)), stored in
+// 8 KB tiles per (word w, 32-node chunk) laid out [trial b][lane] so the sweep
+// reads trial b of its node at a fixed offset and every load is 256 B coalesced.
+__global__ void packed_cache_init(uint2 *__restrict__ acache, const uint64_t *__restrict__ krg,
+                                  int n, int chunks, int W) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)W * chunks * 1024) return;
+    const int lane = (int)(g & 31), b = (int)((g >> 5) & 31);
+    const int64_t tile = g >> 10;
+    const int ch = (int)(tile % chunks), w = (int)(tile / chunks);
+    const int i = ch * 32 + lane;
+    uint64_t s = 0;
+    if (i < n) s = mix64(krg[w * 32 + b] ^ (uint64_t)i) + PB_GAMMA;
+    acache[g] = make_uint2((uint32_t)s, (uint32_t)(s >> 32));
+}
+
 // ---------------------------------------------------------- packed sweep
 // Layout: spins uint32 [W][n] (word-major, node-fast): bit b of word (w, i) is
 // trial 32w+b's spin at node i, 1 = +1.  A warp owns one word index w for its
@@ -102,6 +119,7 @@ struct PackedArgs {
     const uint32_t *rowptr;   // [n+1]
     const uint32_t *adj;      // [nnz] column | (J < 0) << 31
     const uint2 *kfc;         // [Tp] per-trial (F_t, C_t)
+    const uint2 *acache;      // [W][chunks][32 trials][32 lanes] absorb(K_t, i) + GAMMA, or null
     const uint64_t *krg;      // [Tp] absorb(key, TAG_R) + GAMMA (exact slow path)
     const uint64_t *thr;      // [K] thresholds of this cycle (H >= thr -> +1)
     unsigned long long *pacc; // [Tp] += sum_i s_i * raw_i of the sub-step's input state
@@ -124,16 +142,15 @@ constexpr int kPackedWarps = kPackedThreads / 32;
 
 __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
 
-// One trial's decision bit, shifted into `word` through the carry flag.
-// Returns the (zhi ^ thi) tie witness (< 2 means "recompute exactly").
-__device__ __forceinline__ uint32_t packed_decide(uint32_t ylo, uint32_t C, uint32_t count,
-                                                  uint2 t, uint32_t &word) {
+// First absorb of a trial's draw: s = absorb(K, i) + GAMMA, as (lo, hi).
+// y = (ylo, Y) with ylo = F_t ^ i; Y * M1L is folded into C = C_t.
+// Right shifts of high words go through IMAD.HI (x >> s == umulhi(x, 2^(32-s)))
+// so the FMA pipe takes part of the load of the saturated ALU pipe.
+__device__ __forceinline__ void packed_first_absorb(uint32_t ylo, uint32_t C, uint32_t &sl,
+                                                    uint32_t &sh) {
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
     constexpr uint32_t GL = 0x7F4A7C15u, GH = 0x9E3779B9u;
-    // first absorb: z = y * M1 with y = (ylo, Y), Y * M1L folded into C.
-    // Right shifts of high words go through IMAD.HI (x >> s == umulhi(x, 2^(32-s)))
-    // so the FMA pipe takes part of the load of the saturated ALU pipe.
     uint32_t zl = ylo * M1L;
     uint32_t zh = mulhi(ylo, M1L) + ylo * M1H + C;
     // z ^= z >> 27 ; z *= M2
@@ -144,18 +161,25 @@ __device__ __forceinline__ uint32_t packed_decide(uint32_t ylo, uint32_t C, uint
     // z ^= z >> 31  -> A ; s = A + GAMMA
     yl = zl ^ __funnelshift_r(zl, zh, 31);
     yh = zh ^ mulhi(zh, 1u << 1);
-    uint32_t sl, sh;
     asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
         : "=r"(sl), "=r"(sh) : "r"(yl), "r"(yh), "r"(GL), "r"(GH));
-    // second absorb: x = s ^ count ; z ^= z >> 30 (count < 2^30 only touches the low word)
-    yl = sl ^ count ^ __funnelshift_r(sl, sh, 30);
-    yh = sh ^ mulhi(sh, 1u << 2);
-    zl = yl * M1L;
-    zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
+}
+
+// Second absorb (x = s ^ count) up to the high word of the last multiply,
+// then the decision bit shifted into `word` through the carry of zh + ~thi.
+// Returns the (zh ^ thi) tie witness (< 2 means "recompute exactly").
+__device__ __forceinline__ uint32_t packed_second_decide(uint32_t sl, uint32_t sh, uint32_t count,
+                                                         uint2 t, uint32_t &word) {
+    constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
+    constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
+    // z ^= z >> 30 (count < 2^30 only touches the low word)
+    uint32_t yl = sl ^ count ^ __funnelshift_r(sl, sh, 30);
+    uint32_t yh = sh ^ mulhi(sh, 1u << 2);
+    uint32_t zl = yl * M1L;
+    uint32_t zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
     yl = zl ^ __funnelshift_r(zl, zh, 27);
     yh = zh ^ mulhi(zh, 1u << 5);
     zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
-    // carry(zh + ~thi) == (zh > thi); word = 2 word + carry
     uint32_t dummy;
     asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %4;"
         : "=r"(dummy), "=r"(word) : "r"(zh), "r"(t.x), "r"(word));
@@ -182,7 +206,7 @@ constexpr int kWarpCutPlanes = 13;  // after the warp-level add (32 * 255 < 2^13
 #define PBSA_PACKED_MIN_BLOCKS 4
 #endif
 
-template <int L, bool UPDATE>
+template <int L, bool UPDATE, bool CACHED>
 __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed_sweep(PackedArgs a) {
     extern __shared__ unsigned long long smem_u64[];
     uint2 *sthr = reinterpret_cast<uint2 *>(smem_u64);   // [K] {~thi, thi}
@@ -244,6 +268,9 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             vc_add<L, kCutPlanes>(C, g);
             if (UPDATE) {
                 const uint2 *tb = sthr + (a.dmax - d);   // entry for raw = 2 pop - d
+                // cache tile of (word w, chunk ch): [b][lane], so trial b of this
+                // lane sits at a compile-time offset b * 256 B
+                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
                 uint32_t word = 0, tie = 0xffffffffu;
                 const uint32_t ui = (uint32_t)i;
 #pragma unroll
@@ -251,8 +278,16 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     int pop = 0;
 #pragma unroll
                     for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
-                    const uint2 kc = key[b];
-                    tie = min(tie, packed_decide(kc.x ^ ui, kc.y, count, tb[2 * pop], word));
+                    uint32_t sl, sh;
+                    if (CACHED) {
+                        const uint2 v = __ldcs(ctile + b * 32);
+                        sl = v.x;
+                        sh = v.y;
+                    } else {
+                        const uint2 kc = key[b];
+                        packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                    }
+                    tie = min(tie, packed_second_decide(sl, sh, count, tb[2 * pop], word));
                 }
                 if (tie < 2) {  // rare: some trial's high words nearly tie -> exact 64-bit test
                     word = 0;
