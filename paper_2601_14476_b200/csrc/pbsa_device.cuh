@@ -76,7 +76,8 @@ __global__ void init_general(int8_t *__restrict__ s, const uint64_t *__restrict_
 }
 
 // Per-(trial, node) first absorb of the TAG_R draw, which does not depend on
-// the sub-step: absorb(K_t, i) + GAMMA (K_t = absorb(key, TAG_R)), stored in
+// the sub-step: s = absorb(K_t, i) + GAMMA (K_t = absorb(key, TAG_R)), plus the
+// count-independent part of the next xorshift, stored in
 // 8 KB tiles per (word w, 32-node chunk) laid out [trial b][lane] so the sweep
 // reads trial b of its node at a fixed offset and every load is 256 B coalesced.
 __global__ void packed_cache_init(uint2 *__restrict__ acache, const uint64_t *__restrict__ krg,
@@ -89,7 +90,10 @@ __global__ void packed_cache_init(uint2 *__restrict__ acache, const uint64_t *__
     const int i = ch * 32 + lane;
     uint64_t s = 0;
     if (i < n) s = mix64(krg[w * 32 + b] ^ (uint64_t)i) + PB_GAMMA;
-    acache[g] = make_uint2((uint32_t)s, (uint32_t)(s >> 32));
+    // store y' = s ^ (s >> 30): the sweep only XORs the sub-step counter into
+    // its low word (count < 2^30 never reaches the shifted bits)
+    const uint64_t y = s ^ (s >> 30);
+    acache[g] = make_uint2((uint32_t)y, (uint32_t)(y >> 32));
 }
 
 // ---------------------------------------------------------- packed sweep
@@ -165,16 +169,13 @@ __device__ __forceinline__ void packed_first_absorb(uint32_t ylo, uint32_t C, ui
         : "=r"(sl), "=r"(sh) : "r"(yl), "r"(yh), "r"(GL), "r"(GH));
 }
 
-// Second absorb (x = s ^ count) up to the high word of the last multiply,
-// then the decision bit shifted into `word` through the carry of zh + ~thi.
-// Returns the (zh ^ thi) tie witness (< 2 means "recompute exactly").
-__device__ __forceinline__ uint32_t packed_second_decide(uint32_t sl, uint32_t sh, uint32_t count,
-                                                         uint2 t, uint32_t &word) {
+// Second absorb from y = x ^ (x >> 30), x = s ^ count, up to the high word of
+// the last multiply, then the decision bit shifted into `word` through the
+// carry of zh + ~thi.  Returns the (zh ^ thi) tie witness (< 2: recompute).
+__device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t yh, uint2 t,
+                                                    uint32_t &word) {
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
-    // z ^= z >> 30 (count < 2^30 only touches the low word)
-    uint32_t yl = sl ^ count ^ __funnelshift_r(sl, sh, 30);
-    uint32_t yh = sh ^ mulhi(sh, 1u << 2);
     uint32_t zl = yl * M1L;
     uint32_t zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
     yl = zl ^ __funnelshift_r(zl, zh, 27);
@@ -184,6 +185,13 @@ __device__ __forceinline__ uint32_t packed_second_decide(uint32_t sl, uint32_t s
     asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %4;"
         : "=r"(dummy), "=r"(word) : "r"(zh), "r"(t.x), "r"(word));
     return zh ^ t.y;
+}
+
+// Second absorb (x = s ^ count; count < 2^30 only touches the low word).
+__device__ __forceinline__ uint32_t packed_second_decide(uint32_t sl, uint32_t sh, uint32_t count,
+                                                         uint2 t, uint32_t &word) {
+    return packed_decide_y(sl ^ count ^ __funnelshift_r(sl, sh, 30), sh ^ mulhi(sh, 1u << 2), t,
+                           word);
 }
 
 // Bit-sliced counter: add the L-bit per-trial numbers x[] into C[] (CL planes).
@@ -278,16 +286,15 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     int pop = 0;
 #pragma unroll
                     for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
-                    uint32_t sl, sh;
                     if (CACHED) {
                         const uint2 v = __ldcs(ctile + b * 32);
-                        sl = v.x;
-                        sh = v.y;
+                        tie = min(tie, packed_decide_y(v.x ^ count, v.y, tb[2 * pop], word));
                     } else {
                         const uint2 kc = key[b];
+                        uint32_t sl, sh;
                         packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                        tie = min(tie, packed_second_decide(sl, sh, count, tb[2 * pop], word));
                     }
-                    tie = min(tie, packed_second_decide(sl, sh, count, tb[2 * pop], word));
                 }
                 if (tie < 2) {  // rare: some trial's high words nearly tie -> exact 64-bit test
                     word = 0;
