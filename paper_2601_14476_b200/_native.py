@@ -157,11 +157,14 @@ OUT_ORDER = ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "c
              "best_cut")
 
 
-def anneal_batch(batch: Batch, device: int = 0) -> tuple[dict, float]:
-    """One-shot pbsa_anneal_loop_batch; returns (outputs, device milliseconds)."""
+def anneal_batch(batch: Batch, device: int = 0, out: dict | None = None) -> tuple[dict, float]:
+    """One-shot pbsa_anneal_loop_batch; returns (outputs, device milliseconds).
+    ``out`` may supply preallocated (e.g. page-locked) output arrays shaped
+    like ``batch.alloc_outputs()``."""
     lib = load()
     require_device(device)
-    out = batch.alloc_outputs()
+    if out is None:
+        out = batch.alloc_outputs()
     ms = ctypes.c_float(0.0)
     _check(lib.pbsa_anneal_loop_batch(device, *batch._args(),
                                       *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))

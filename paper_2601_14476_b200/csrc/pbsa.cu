@@ -16,6 +16,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -109,24 +111,37 @@ int next_pow2(int x) {
     return p;
 }
 
+// Stream-ordered device buffers from the device's default memory pool (its
+// release threshold is raised once per device, so repeated one-shot calls
+// reuse memory instead of paying cudaMalloc/cudaFree each time).
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
+struct AllocStream {
+    cudaStream_t prev;
+    explicit AllocStream(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+    ~AllocStream() { g_alloc_stream = prev; }
+};
+
 template <typename T>
 struct DevBuf {
     T *p = nullptr;
     size_t n = 0;
     size_t bytes_up = 0;  // host->device bytes of the last upload
+    cudaStream_t st = nullptr;
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+        st = g_alloc_stream;
+        if (count) CK(cudaMallocAsync(reinterpret_cast<void **>(&p), count * sizeof(T), st));
     }
-    void upload(const T *src, size_t count, cudaStream_t st) {
+    void upload(const T *src, size_t count, cudaStream_t s) {
         alloc(count);
         bytes_up = count * sizeof(T);
-        if (count) CK(cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, st));
+        if (count) CK(cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
     }
-    void upload(const std::vector<T> &v, cudaStream_t st) { upload(v.data(), v.size(), st); }
+    void upload(const std::vector<T> &v, cudaStream_t s) { upload(v.data(), v.size(), s); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
         p = nullptr;
         n = 0;
         bytes_up = 0;
@@ -134,11 +149,56 @@ struct DevBuf {
     ~DevBuf() { release(); }
 };
 
+void raise_pool_threshold(int device) {
+    static std::mutex mu;
+    static std::set<int> done;
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count(device)) return;
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    done.insert(device);
+}
+
+// Fill a large host array with several threads (output buffers of a full
+// 4096-trial G81 download are ~0.7 GB each).
+template <typename T>
+void parallel_fill(T *dst, size_t count, T value) {
+    const size_t bytes = count * sizeof(T);
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (bytes < (32u << 20) || nt == 1) {
+        std::fill(dst, dst + count, value);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t per = (count + nt - 1) / nt;
+    for (unsigned k = 0; k < nt; ++k) {
+        const size_t lo = k * per, hi = std::min(count, lo + per);
+        if (lo >= hi) break;
+        pool.emplace_back([=] { std::fill(dst + lo, dst + hi, value); });
+    }
+    for (auto &t : pool) t.join();
+}
+
 int64_t grid_for(int64_t work, int threads) { return (work + threads - 1) / threads; }
 
 }  // namespace
 
+struct StreamHolder {
+    cudaStream_t s = nullptr;
+    ~StreamHolder() {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+};
+
 struct pbsa_plan {
+    // declared first so it is destroyed last, after every buffer has been
+    // released onto it
+    StreamHolder stream_holder;
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
@@ -190,7 +250,6 @@ struct pbsa_plan {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         for (cudaEvent_t e : {ev_start, ev_sweep0, ev_sweep1, ev_end})
             if (e) cudaEventDestroy(e);
-        if (stream) cudaStreamDestroy(stream);
     }
 };
 
@@ -331,6 +390,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
 
     DeviceGuard dg(device);
     CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+    P.stream_holder.s = P.stream;
+    raise_pool_threshold(device);
+    AllocStream as(P.stream);
     for (cudaEvent_t *e : {&P.ev_start, &P.ev_sweep0, &P.ev_sweep1, &P.ev_end}) CK(cudaEventCreate(e));
     cudaStream_t st = P.stream;
 
@@ -807,35 +869,37 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                                cudaMemcpyDeviceToHost, st));
         if (best_cut)
             CK(cudaMemcpyAsync(best_cut, P->best.p, T * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        AllocStream as(st);
         DevBuf<int8_t> dspins;
         DevBuf<double> dinputs, dhist;
         DevBuf<int32_t> dcounts;
+        DevBuf<int64_t> dcounts64;
         if (P->path == PBSA_PATH_PACKED) {
             if (spins) {
                 dspins.alloc((size_t)T * n);
                 pbsa::unpack_spins<<<grid_for(n * T, TB), TB, 0, st>>>(
                     P->p_spins[P->final_parity].p, dspins.p, (int)n, (int)P->W, (int)T);
-                CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
             }
             if (inputs || (hist && P->tapsa_hist_from_raw)) {
                 dinputs.alloc((size_t)T * n);
                 pbsa::inputs_from_raw<<<grid_for(n * T, TB), TB, 0, st>>>(
                     P->raw_last.p, dinputs.p, P->i0[C - 1], (int)n, (int)P->Tp, (int)T);
-                if (inputs)
-                    CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double),
-                                       cudaMemcpyDeviceToHost, st));
             }
             if (hist && P->tapsa_hist_from_raw) {
                 // TAPSA with alpha = 1: the history holds the last raw field
                 dhist.alloc((size_t)T * n);
                 pbsa::inputs_from_raw<<<grid_for(n * T, TB), TB, 0, st>>>(
                     P->raw_last.p, dhist.p, 1.0, (int)n, (int)P->Tp, (int)T);
-                CK(cudaMemcpyAsync(hist, dhist.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
             }
+            // host-side constant outputs overlap the device work above
+            if (hist && !P->tapsa_hist_from_raw) parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
+            if (counts) parallel_fill(counts, (size_t)(T * n), (int64_t)C);  // every p-bit fires once per cycle
+            if (spins) CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
+            if (inputs)
+                CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+            if (hist && P->tapsa_hist_from_raw)
+                CK(cudaMemcpyAsync(hist, dhist.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
-            if (hist && !P->tapsa_hist_from_raw) std::memset(hist, 0, T * n * P->alpha * sizeof(double));
-            if (counts)
-                for (int64_t k = 0; k < T * n; ++k) counts[k] = C;
         } else {
             dim3 tb(32, 8);
             if (spins) {
@@ -843,21 +907,20 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                 dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
                 pbsa::transpose_tile<int8_t><<<g, tb, 0, st>>>(P->g_spins[P->final_parity].p,
                                                                dspins.p, (int)n, (int)P->Tp, (int)T);
-                CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
             }
             if (inputs) {
                 dinputs.alloc((size_t)T * n);
                 dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
                 pbsa::transpose_tile<double><<<g, tb, 0, st>>>(P->inputs.p, dinputs.p, (int)n,
                                                                (int)P->Tp, (int)T);
-                CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double),
-                                   cudaMemcpyDeviceToHost, st));
             }
             if (counts) {
                 dcounts.alloc((size_t)T * n);
+                dcounts64.alloc((size_t)T * n);
                 dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
                 pbsa::transpose_tile<int32_t><<<g, tb, 0, st>>>(P->counts.p, dcounts.p, (int)n,
                                                                 (int)P->Tp, (int)T);
+                pbsa::widen_i32<<<grid_for(T * n, TB), TB, 0, st>>>(dcounts.p, dcounts64.p, T * n);
             }
             if (hist && P->algo == 1) {
                 const int64_t rows = n * P->alpha;
@@ -865,19 +928,17 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                 dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(rows, 32));
                 pbsa::transpose_tile<double><<<g, tb, 0, st>>>(P->hist.p, dhist.p, (int)rows,
                                                                (int)P->Tp, (int)T);
-                CK(cudaMemcpyAsync(hist, dhist.p, T * rows * sizeof(double),
-                                   cudaMemcpyDeviceToHost, st));
             }
-            std::vector<int32_t> c32;
-            if (counts) {
-                c32.resize((size_t)T * n);
-                CK(cudaMemcpyAsync(c32.data(), dcounts.p, T * n * sizeof(int32_t),
-                                   cudaMemcpyDeviceToHost, st));
-            }
-            CK(cudaStreamSynchronize(st));
+            if (hist && P->algo != 1) parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
+            if (spins) CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
+            if (inputs)
+                CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
             if (counts)
-                for (int64_t k = 0; k < T * n; ++k) counts[k] = c32[k];
-            if (hist && P->algo != 1) std::memset(hist, 0, T * n * P->alpha * sizeof(double));
+                CK(cudaMemcpyAsync(counts, dcounts64.p, T * n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+            if (hist && P->algo == 1)
+                CK(cudaMemcpyAsync(hist, dhist.p, T * n * P->alpha * sizeof(double),
+                                   cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
         }
         if (trace_i0)
             for (int64_t t = 0; t < T; ++t) std::memcpy(trace_i0 + t * C, P->i0.data(), C * sizeof(double));

@@ -529,6 +529,11 @@ __global__ void finalize_traces(FinalArgs a) {
     a.best[t] = best;
 }
 
+__global__ void widen_i32(const int32_t *__restrict__ src, int64_t *__restrict__ dst, int64_t n) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n) dst[g] = src[g];
+}
+
 // Generic tiled transpose: src [R][Cc] -> dst [Cc_used][R] (first Cc_used columns)
 template <typename T>
 __global__ void transpose_tile(const T *__restrict__ src, T *__restrict__ dst, int R, int Cc,
