@@ -1,0 +1,89 @@
+"""The C-ABI library (CPU-side checks, no GPU compute).
+
+* libpbsa.so loads and exports every function include/pbsa.h declares;
+* the host build of the device tanh (libm_tanh.cuh) equals the system libm
+  bit-for-bit -- the property that makes varied-profile runs replay the
+  reference exactly;
+* the packed path's integer activation threshold equals the reference's
+  floating-point decision ``r + t >= 0`` (_kernels.py:149-152) exactly;
+* compute entry points fail loudly (no CPU fallback) without a GPU.
+"""
+
+from __future__ import annotations
+
+import math
+import re
+from fractions import Fraction
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2601_14476_b200 import _native
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "pbsa.h"
+
+
+def declared_functions() -> list[str]:
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(pbsa_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.load()
+    names = declared_functions()
+    assert len(names) >= 14
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_native.EXPORTED)
+    assert lib.pbsa_abi_version() == 1
+
+
+def test_host_tanh_port_equals_libm():
+    lib = _native.load()
+    rng = np.random.default_rng(11)
+    xs = np.concatenate([rng.uniform(-25, 25, 60_000), rng.uniform(-1.5, 1.5, 60_000),
+                         np.ldexp(rng.uniform(0.5, 1.0, 30_000), rng.integers(-70, 6, 30_000)),
+                         -np.ldexp(rng.uniform(0.5, 1.0, 30_000), rng.integers(-70, 6, 30_000)),
+                         np.array([0.0, -0.0, 22.0, -22.0, 21.99999, 1.0, -1.0, 0.5 * math.log(3)])])
+    bad = [x for x in xs if lib.pbsa_libm_tanh_host(float(x)).hex() != math.tanh(float(x)).hex()]
+    assert not bad, bad[:5]
+
+
+def _decision_exact(t: float, u53: int) -> bool:
+    """The reference decision r + t >= 0 with r = 2 (u / 2^53) - 1."""
+    r = 2.0 * (u53 * 2.0 ** -53) - 1.0
+    return r + t >= 0.0
+
+
+def test_threshold_matches_reference_decision():
+    lib = _native.load()
+    rng = np.random.default_rng(12)
+    ts = [math.tanh(x) for x in np.concatenate([rng.normal(0, 2, 3000), rng.normal(0, 1e-6, 500)])]
+    ts += [1.0, -1.0, 0.0, -0.0, math.tanh(20.0), math.tanh(-20.0), 2.0 ** -60, -(2.0 ** -60)]
+    for t in ts:
+        thr = int(lib.pbsa_threshold_host(t))
+        if thr == (1 << 64) - 1:  # never +1
+            assert not _decision_exact(t, (1 << 53) - 1)
+            continue
+        assert thr % 2048 == 0
+        U = thr >> 11
+        # exact rational threshold
+        assert U == max(0, math.ceil((1 - Fraction(t)) * 2 ** 52))
+        for u in (U - 1, U, U + 1):
+            if 0 <= u < (1 << 53):
+                assert _decision_exact(t, u) == (u >= U), (t, u)
+
+
+def test_compute_calls_fail_loudly_without_gpu():
+    if _native.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(RuntimeError, match="no CUDA device"):
+        _native.require_device(0)
+    from paper_2601_14476_b200 import annealer, model, pbit
+    g = model.MaxCutGraph.from_edges(3, [(0, 1, 1), (1, 2, 1)])
+    m = model.maxcut_to_ising(g)
+    sch = annealer.derive_schedule(m, 5)
+    with pytest.raises(RuntimeError):
+        annealer.run_anneal(m, sch, annealer.AlgorithmConfig(annealer.Algorithm.PSA),
+                            pbit.VariabilityProfile.ideal(3), seed=0, graph=g)
