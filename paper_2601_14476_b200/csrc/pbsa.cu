@@ -203,6 +203,9 @@ struct pbsa_plan {
     cudaStream_t stream = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     cudaEvent_t ev_start = nullptr, ev_sweep0 = nullptr, ev_sweep1 = nullptr, ev_end = nullptr;
+    cudaEvent_t ev_fork = nullptr;
+    std::vector<cudaEvent_t> ev_join;
+    std::vector<cudaStream_t> chain_streams;  // packed path: extra concurrent word groups
     bool ran = false;
 
     // problem
@@ -248,8 +251,10 @@ struct pbsa_plan {
 
     ~pbsa_plan() {
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
-        for (cudaEvent_t e : {ev_start, ev_sweep0, ev_sweep1, ev_end})
+        for (cudaEvent_t e : {ev_start, ev_sweep0, ev_sweep1, ev_end, ev_fork})
             if (e) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
+        for (cudaStream_t cs : chain_streams) cudaStreamDestroy(cs);
     }
 };
 
@@ -465,6 +470,19 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         const int64_t max_tasks = cap / dm;  // chunks one warp may take
         wpw = std::max<int64_t>(wpw, std::min<int64_t>((P.chunks + max_tasks - 1) / max_tasks, P.chunks));
         P.warps_per_word = (int)wpw;
+        // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
+        int chains = 4;
+        if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
+        chains = (int)std::min<int64_t>(chains, P.W);
+        if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
+        for (int g = 1; g < chains; ++g) {
+            cudaStream_t cs;
+            CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            P.chain_streams.push_back(cs);
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            P.ev_join.push_back(e);
+        }
         P.packed_blocks = (int)grid_for(P.W * wpw, pbsa::kPackedWarps);
         P.updates_per_run = (int64_t)n * trials * cycles;
     } else {
@@ -599,35 +617,54 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
         const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
+        // Independent word groups run as concurrent chains (graph branches):
+        // one chain's launch gaps and tail are filled by the other's blocks.
+        const int G = (int)P.chain_streams.size() + 1;
+        const int64_t per = (P.W + G - 1) / G;
+        if (G > 1) {
+            CK(cudaEventRecord(P.ev_fork, st));
+            for (cudaStream_t cs : P.chain_streams) CK(cudaStreamWaitEvent(cs, P.ev_fork, 0));
+        }
         int cur = 0;
-        for (int64_t c = 0; c <= P.cycles; ++c) {
-            pbsa::PackedArgs a{};
-            a.sold = P.p_spins[cur].p;
-            a.snew = P.p_spins[cur ^ 1].p;
-            a.rowptr = P.rowptr.p;
-            a.adj = P.adj.p;
-            a.krg = P.krg.p;
-            a.kfc = P.kfc.p;
-            a.acache = P.use_cache ? P.acache.p : nullptr;
-            const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
-            a.thr = P.thr.p + (size_t)cc * P.K;
-            a.pacc = P.pacc.p + (size_t)c * P.Tp;
-            a.raw_out = (c == P.cycles - 1) ? P.raw_last.p : nullptr;
-            a.n = (int)P.n;
-            a.W = (int)P.W;
-            a.Tp = (int)P.Tp;
-            a.K = P.K;
-            a.dmax = P.dmax;
-            a.warps_per_word = P.warps_per_word;
-            a.chunks = P.chunks;
-            a.count = (uint32_t)(c * P.t_res);
-            a.do_update = c < P.cycles;
-            (c < P.cycles ? kern_up : kern_cut)<<<P.packed_blocks, pbsa::kPackedThreads, smem, st>>>(a);
-            CK(cudaGetLastError());
-            ++P.launches;
-            if (c < P.cycles) {
-                ++P.sweep_launches;
-                cur ^= 1;
+        for (int g = 0; g < G; ++g) {
+            const int64_t w0 = g * per, w1 = std::min<int64_t>(P.W, w0 + per);
+            if (w0 >= w1) continue;
+            cudaStream_t cs = g == 0 ? st : P.chain_streams[g - 1];
+            const int blocks = (int)grid_for((w1 - w0) * P.warps_per_word, pbsa::kPackedWarps);
+            cur = 0;
+            for (int64_t c = 0; c <= P.cycles; ++c) {
+                pbsa::PackedArgs a{};
+                a.sold = P.p_spins[cur].p + w0 * P.n;
+                a.snew = P.p_spins[cur ^ 1].p + w0 * P.n;
+                a.rowptr = P.rowptr.p;
+                a.adj = P.adj.p;
+                a.krg = P.krg.p + w0 * 32;
+                a.kfc = P.kfc.p + w0 * 32;
+                a.acache = P.use_cache ? P.acache.p + (size_t)w0 * P.chunks * 1024 : nullptr;
+                const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
+                a.thr = P.thr.p + (size_t)cc * P.K;
+                a.pacc = P.pacc.p + (size_t)c * P.Tp + w0 * 32;
+                a.raw_out = (c == P.cycles - 1) ? P.raw_last.p + w0 * 32 : nullptr;
+                a.n = (int)P.n;
+                a.W = (int)(w1 - w0);
+                a.Tp = (int)P.Tp;
+                a.K = P.K;
+                a.dmax = P.dmax;
+                a.warps_per_word = P.warps_per_word;
+                a.chunks = P.chunks;
+                a.count = (uint32_t)(c * P.t_res);
+                a.do_update = c < P.cycles;
+                (c < P.cycles ? kern_up : kern_cut)<<<blocks, pbsa::kPackedThreads, smem, cs>>>(a);
+                CK(cudaGetLastError());
+                ++P.launches;
+                if (c < P.cycles) {
+                    if (g == 0) ++P.sweep_launches;
+                    cur ^= 1;
+                }
+            }
+            if (g > 0) {
+                CK(cudaEventRecord(P.ev_join[g - 1], cs));
+                CK(cudaStreamWaitEvent(st, P.ev_join[g - 1], 0));
             }
         }
         CK(cudaEventRecordWithFlags(P.ev_sweep1, st, cudaEventRecordExternal));
