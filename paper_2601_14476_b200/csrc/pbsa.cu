@@ -229,6 +229,7 @@ struct pbsa_plan {
     DevBuf<uint64_t> thr, krg;
     DevBuf<uint2> kfc, acache;
     bool use_cache = false;
+    int64_t phase_words = 1;
     DevBuf<unsigned long long> pacc;  // [(C+1)][Tp]
     DevBuf<int16_t> raw_last;         // [n][Tp]
 
@@ -448,12 +449,16 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // launch shape: one wave of resident warps, each owning one word
         // cache the sub-step-independent first absorb of every (trial, node)
         // draw when it fits the budget (PBSA_PACKED_CACHE=0/1 overrides)
-        const size_t cache_entries = (size_t)P.W * ((n + 31) / 32) * 1024;
+        // phase width in words (PBSA_PACKED_PHASE_WORDS overrides; 0 = all)
+        P.phase_words = 0;
+        if (const char *env = std::getenv("PBSA_PACKED_PHASE_WORDS")) P.phase_words = std::atoi(env);
+        if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;
+        const size_t cache_entries = (size_t)P.phase_words * ((n + 31) / 32) * 1024;
         P.use_cache = cache_entries * 8 <= (32ULL << 30);
         if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1';
         if (P.use_cache) P.acache.alloc(cache_entries);
         PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache);
-        const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8 + 16;
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 128 + pbsa::kPackedWarps * 32 * 8 + 16;
         set_packed_smem(kern, smem);
         set_packed_smem(packed_kernel_for(P.L, false, false), smem);
         int occ = 0, sms = 0;
@@ -462,7 +467,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         occ = std::max(occ, 1);
         P.chunks = (int)((n + 31) / 32);
         const int64_t target_warps = (int64_t)sms * occ * pbsa::kPackedWarps;
-        int64_t wpw = std::max<int64_t>(1, target_warps / P.W);
+        int64_t wpw = std::max<int64_t>(1, target_warps / P.phase_words);  // one phase at a time
         wpw = std::min<int64_t>(wpw, P.chunks);
         // the per-thread bit-sliced cut counter holds sum(degree) < 2^kCutPlanes
         const int64_t cap = (1LL << pbsa::kCutPlanes) - 1, dm = std::max<int64_t>(dmax, 1);
@@ -610,61 +615,69 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                                                    (int)P.n, (int)P.W);
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
-        if (P.use_cache)
-            pbsa::packed_cache_init<<<grid_for((int64_t)P.acache.n, TB), TB, 0, st>>>(
-                P.acache.p, P.krg.p, (int)P.n, P.chunks, (int)P.W);
         PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
-        const size_t smem = (size_t)P.K * 8 + pbsa::kPackedWarps * 32 * 8 + 16;
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 128 + pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
-        // Independent word groups run as concurrent chains (graph branches):
-        // one chain's launch gaps and tail are filled by the other's blocks.
+        // Word phases run one after another so that a phase's first-absorb
+        // cache (PW words x n x 256 B) stays L2-resident across its cycles;
+        // inside a phase, independent word groups run as concurrent chains
+        // (graph branches) so one chain's launch gaps and tail are filled by
+        // the others' blocks.
         const int G = (int)P.chain_streams.size() + 1;
-        const int64_t per = (P.W + G - 1) / G;
-        if (G > 1) {
-            CK(cudaEventRecord(P.ev_fork, st));
-            for (cudaStream_t cs : P.chain_streams) CK(cudaStreamWaitEvent(cs, P.ev_fork, 0));
-        }
         int cur = 0;
-        for (int g = 0; g < G; ++g) {
-            const int64_t w0 = g * per, w1 = std::min<int64_t>(P.W, w0 + per);
-            if (w0 >= w1) continue;
-            cudaStream_t cs = g == 0 ? st : P.chain_streams[g - 1];
-            const int blocks = (int)grid_for((w1 - w0) * P.warps_per_word, pbsa::kPackedWarps);
-            cur = 0;
-            for (int64_t c = 0; c <= P.cycles; ++c) {
-                pbsa::PackedArgs a{};
-                a.sold = P.p_spins[cur].p + w0 * P.n;
-                a.snew = P.p_spins[cur ^ 1].p + w0 * P.n;
-                a.rowptr = P.rowptr.p;
-                a.adj = P.adj.p;
-                a.krg = P.krg.p + w0 * 32;
-                a.kfc = P.kfc.p + w0 * 32;
-                a.acache = P.use_cache ? P.acache.p + (size_t)w0 * P.chunks * 1024 : nullptr;
-                const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
-                a.thr = P.thr.p + (size_t)cc * P.K;
-                a.pacc = P.pacc.p + (size_t)c * P.Tp + w0 * 32;
-                a.raw_out = (c == P.cycles - 1) ? P.raw_last.p + w0 * 32 : nullptr;
-                a.n = (int)P.n;
-                a.W = (int)(w1 - w0);
-                a.Tp = (int)P.Tp;
-                a.K = P.K;
-                a.dmax = P.dmax;
-                a.warps_per_word = P.warps_per_word;
-                a.chunks = P.chunks;
-                a.count = (uint32_t)(c * P.t_res);
-                a.do_update = c < P.cycles;
-                (c < P.cycles ? kern_up : kern_cut)<<<blocks, pbsa::kPackedThreads, smem, cs>>>(a);
-                CK(cudaGetLastError());
+        for (int64_t p0 = 0; p0 < P.W; p0 += P.phase_words) {
+            const int64_t p1 = std::min<int64_t>(P.W, p0 + P.phase_words);
+            if (P.use_cache) {
+                pbsa::packed_cache_init<<<grid_for((p1 - p0) * P.chunks * 1024, TB), TB, 0, st>>>(
+                    P.acache.p, P.krg.p + p0 * 32, (int)P.n, P.chunks, (int)(p1 - p0));
                 ++P.launches;
-                if (c < P.cycles) {
-                    if (g == 0) ++P.sweep_launches;
-                    cur ^= 1;
-                }
             }
-            if (g > 0) {
-                CK(cudaEventRecord(P.ev_join[g - 1], cs));
-                CK(cudaStreamWaitEvent(st, P.ev_join[g - 1], 0));
+            if (G > 1) {
+                CK(cudaEventRecord(P.ev_fork, st));
+                for (cudaStream_t cs : P.chain_streams) CK(cudaStreamWaitEvent(cs, P.ev_fork, 0));
+            }
+            const int64_t per = (p1 - p0 + G - 1) / G;
+            for (int g = 0; g < G; ++g) {
+                const int64_t w0 = p0 + g * per, w1 = std::min<int64_t>(p1, w0 + per);
+                if (w0 >= w1) continue;
+                cudaStream_t cs = g == 0 ? st : P.chain_streams[g - 1];
+                const int blocks = (int)grid_for((w1 - w0) * P.warps_per_word, pbsa::kPackedWarps);
+                cur = 0;
+                for (int64_t c = 0; c <= P.cycles; ++c) {
+                    pbsa::PackedArgs a{};
+                    a.sold = P.p_spins[cur].p + w0 * P.n;
+                    a.snew = P.p_spins[cur ^ 1].p + w0 * P.n;
+                    a.rowptr = P.rowptr.p;
+                    a.adj = P.adj.p;
+                    a.krg = P.krg.p + w0 * 32;
+                    a.kfc = P.kfc.p + w0 * 32;
+                    a.acache = P.use_cache ? P.acache.p + (size_t)(w0 - p0) * P.chunks * 1024 : nullptr;
+                    const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
+                    a.thr = P.thr.p + (size_t)cc * P.K;
+                    a.pacc = P.pacc.p + (size_t)c * P.Tp + w0 * 32;
+                    a.raw_out = (c == P.cycles - 1) ? P.raw_last.p + w0 * 32 : nullptr;
+                    a.n = (int)P.n;
+                    a.W = (int)(w1 - w0);
+                    a.Tp = (int)P.Tp;
+                    a.K = P.K;
+                    a.dmax = P.dmax;
+                    a.warps_per_word = P.warps_per_word;
+                    a.chunks = P.chunks;
+                    a.count = (uint32_t)(c * P.t_res);
+                    a.do_update = c < P.cycles;
+                    (c < P.cycles ? kern_up : kern_cut)<<<blocks, pbsa::kPackedThreads, smem, cs>>>(a);
+                    CK(cudaGetLastError());
+                    ++P.launches;
+                    if (c < P.cycles) {
+                        if (g == 0 && p0 == 0) ++P.sweep_launches;
+                        cur ^= 1;
+                    }
+                }
+                if (g > 0) {
+                    CK(cudaEventRecord(P.ev_join[g - 1], cs));
+                    CK(cudaStreamWaitEvent(st, P.ev_join[g - 1], 0));
+                }
             }
         }
         CK(cudaEventRecordWithFlags(P.ev_sweep1, st, cudaEventRecordExternal));

@@ -217,8 +217,15 @@ constexpr int kWarpCutPlanes = 13;  // after the warp-level add (32 * 255 < 2^13
 template <int L, bool UPDATE, bool CACHED>
 __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed_sweep(PackedArgs a) {
     extern __shared__ unsigned long long smem_u64[];
-    uint2 *sthr = reinterpret_cast<uint2 *>(smem_u64);   // [K] {~thi, thi}
-    uint2 *skey = sthr + a.K;                             // [warps][32] {F, C}
+    // Threshold table, 128 B aligned.  L <= 4 (degree <= 15): one 16-entry row
+    // per degree d indexed by the neighbour count p (raw = 2p - d), so a
+    // trial's entry address is (p * 8) | row base, formed with one LOP3.
+    // Larger degrees: entries indexed by raw + dmax.
+    constexpr bool NIB = L <= 4;
+    uint2 *sthr = reinterpret_cast<uint2 *>(
+        (reinterpret_cast<uintptr_t>(smem_u64) + 127) & ~(uintptr_t)127);
+    const int tab_entries = NIB ? (a.dmax + 1) * 16 : a.K;
+    uint2 *skey = sthr + tab_entries;                     // [warps][32] {F, C}
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int gwarp = blockIdx.x * kPackedWarps + wib;
@@ -226,8 +233,15 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     const int q = gwarp % a.warps_per_word;
     const bool live = w < a.W;
 
-    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
-        const uint32_t thi = (uint32_t)(a.thr[k] >> 32);
+    for (int k = threadIdx.x; k < tab_entries; k += blockDim.x) {
+        int raw = k - a.dmax;
+        bool ok = true;
+        if (NIB) {
+            const int d = k >> 4, pp = k & 15;
+            raw = 2 * pp - d;
+            ok = pp <= d;
+        }
+        const uint32_t thi = ok ? (uint32_t)(a.thr[raw + a.dmax] >> 32) : 0u;
         sthr[k] = make_uint2(~thi, thi);
     }
     uint2 *key = skey + wib * 32;
@@ -281,19 +295,46 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
                 uint32_t word = 0, tie = 0xffffffffu;
                 const uint32_t ui = (uint32_t)i;
+                // NIB: transpose the L count planes into 32 nibbles (N[k] nibble j =
+                // count of trial 8k + j), a few ops per 32 trials instead of 2L per trial
+                uint32_t N[4] = {0u, 0u, 0u, 0u};
+                uint32_t rb = 0;
+                if (NIB) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                        for (int r = 0; r < L; ++r) {
+                            uint32_t x = (p[r] >> (8 * k)) & 0xFFu;
+                            x = (x | (x << 12)) & 0x000F000Fu;
+                            x = (x | (x << 6)) & 0x03030303u;
+                            x = (x | (x << 3)) & 0x11111111u;
+                            N[k] |= x << r;
+                        }
+                    }
+                    rb = (uint32_t)__cvta_generic_to_shared(sthr) + (uint32_t)d * 128u;
+                }
 #pragma unroll
                 for (int b = 31; b >= 0; --b) {
-                    int pop = 0;
+                    uint2 t;
+                    if (NIB) {
+                        const int k = b >> 3, j = b & 7;
+                        const uint32_t x = j == 0 ? (N[k] << 3) : (N[k] >> (4 * j - 3));
+                        const uint32_t addr = (x & 0x78u) | rb;
+                        asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "r"(addr));
+                    } else {
+                        int pop = 0;
 #pragma unroll
-                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                        for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                        t = tb[2 * pop];
+                    }
                     if (CACHED) {
                         const uint2 v = __ldcs(ctile + b * 32);
-                        tie = min(tie, packed_decide_y(v.x ^ count, v.y, tb[2 * pop], word));
+                        tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
                     } else {
                         const uint2 kc = key[b];
                         uint32_t sl, sh;
                         packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
-                        tie = min(tie, packed_second_decide(sl, sh, count, tb[2 * pop], word));
+                        tie = min(tie, packed_second_decide(sl, sh, count, t, word));
                     }
                 }
                 if (tie < 2) {  // rare: some trial's high words nearly tie -> exact 64-bit test
