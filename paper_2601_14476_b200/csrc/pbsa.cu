@@ -476,7 +476,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         wpw = std::max<int64_t>(wpw, std::min<int64_t>((P.chunks + max_tasks - 1) / max_tasks, P.chunks));
         P.warps_per_word = (int)wpw;
         // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
-        int chains = 4;
+        int chains = 16;
         if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
         chains = (int)std::min<int64_t>(chains, P.W);
         if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
