@@ -240,9 +240,27 @@ struct pbsa_plan {
     DevBuf<int64_t> me_wi, h_int, ge_w;
     DevBuf<int32_t> period, counts;
     DevBuf<uint64_t> kr, kst;
-    DevBuf<unsigned long long> cut_acc, e_acc;  // [C][Tp]
+    DevBuf<unsigned long long> cut_acc, e_acc, dj_acc;  // [C][Tp]
+    DevBuf<int32_t> ge_w32, me_w32;
+    int64_t sum_j = 0;
+    bool graph_is_model = false;
     int shared_profile = 0;
     bool has_lam = false, has_delta = false, has_period = false;
+    // active-list mode (integer-valued models): per-sub-step lists of firing p-bits
+    struct ALaunch {
+        uint32_t count;
+        int64_t cycle, desc_off;
+        int ndesc, total;
+    };
+    bool active_mode = false;
+    std::vector<ALaunch> alaunch;
+    DevBuf<uint32_t> alist, st_g;
+    DevBuf<int8_t> st_v;
+    DevBuf<int4> adesc;
+    DevBuf<int32_t> vali, hi32, hist_i;
+    DevBuf<uint64_t> athr;  // [cycles][Kt] thresholds (lam = 1, delta = 0, plain rule), or empty
+    int tshift = 0, rawmin = 0, Kt = 0;
+    uint32_t tmask = 0;
 
     DevBuf<uint64_t> kspin;
     // outputs
@@ -297,6 +315,105 @@ PackedKernel packed_kernel_for(int L, bool update, bool cached) {
         default: fail(PBSA_EINVAL, "packed path supports degree <= 127");
     }
 #undef PBSA_CASE
+}
+
+// Active-list setup for integer-valued models (see general_active).
+void setup_active(pbsa_plan &P, int64_t n, const int64_t *indptr, const int64_t *indices,
+                  const double *values, const double *hv, const double *lam, const double *delta,
+                  const int64_t *period, int64_t pstride, int64_t trials, int64_t cycles,
+                  int64_t t_res, int algo, int64_t alpha, double p_stall) {
+    const int64_t nnz = indptr[n];
+    int tshift = 0;
+    while ((1LL << tshift) < P.Tp) ++tshift;
+    if ((n << tshift) > (int64_t)UINT32_MAX || n * P.Tp > (int64_t)UINT32_MAX) return;
+    for (int64_t k = 0; k < nnz; ++k)
+        if (!is_integral(values[k])) return;
+    cudaStream_t st = P.stream;
+    std::vector<int32_t> vi(nnz), hi(n);
+    bool any_h = false;
+    int64_t rawmin = INT64_MAX, rawmax = INT64_MIN;
+    for (int64_t i = 0; i < n; ++i) {
+        hi[i] = (int32_t)hv[i];
+        any_h |= hi[i] != 0;
+        int64_t span = 0;
+        for (int64_t k = indptr[i]; k < indptr[i + 1]; ++k) span += std::llabs((int64_t)values[k]);
+        rawmin = std::min(rawmin, hi[i] - span);
+        rawmax = std::max(rawmax, hi[i] + span);
+    }
+    if (rawmax - rawmin > (1LL << 30)) return;
+    for (int64_t k = 0; k < nnz; ++k) vi[k] = (int32_t)values[k];
+    P.vali.upload(vi, st);
+    if (any_h) P.hi32.upload(hi, st);
+    if (algo == 1) P.hist_i.alloc((size_t)n * alpha * P.Tp);
+    // table mode: plain rule (or a degenerate rule) with an ideal lam/delta
+    bool ideal_ld = true;
+    const int64_t prow = pstride ? trials : 1;
+    if (lam)
+        for (int64_t k = 0; k < prow * n && ideal_ld; ++k)
+            ideal_ld = lam[k] == 1.0 && delta[k] == 0.0;
+    const bool plain = algo == 0 || (algo == 1 && alpha == 1) || (algo == 2 && p_stall == 0.0);
+    if (plain && ideal_ld && rawmax - rawmin < 65536) {
+        P.rawmin = (int)rawmin;
+        P.Kt = (int)(rawmax - rawmin + 1);
+        std::vector<uint64_t> thr((size_t)cycles * P.Kt);
+        for (int64_t c = 0; c < cycles; ++c)
+            for (int64_t r = rawmin; r <= rawmax; ++r)
+                thr[(size_t)c * P.Kt + (r - rawmin)] = threshold_h64(pb_libm_tanh(P.i0[c] * (double)r));
+        P.athr.upload(thr, st);
+    }
+    // bucket every (trial, node) pair by its period; order inside a bucket is
+    // node-major so neighbouring threads share CSR rows
+    const int64_t maxcount = cycles * t_res;
+    auto per_of = [&](int64_t t, int64_t i) -> int64_t {
+        const int64_t pv = period ? period[(pstride ? t * n : 0) + i] : t_res;
+        return std::min<int64_t>(pv, maxcount + 1);
+    };
+    std::vector<int64_t> bucket_of(maxcount + 2, -1), periods;
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t t = 0; t < trials; ++t) {
+            const int64_t pv = per_of(t, i);
+            if (bucket_of[pv] < 0) {
+                bucket_of[pv] = 0;
+                periods.push_back(pv);
+            }
+        }
+    std::sort(periods.begin(), periods.end());
+    for (size_t b = 0; b < periods.size(); ++b) bucket_of[periods[b]] = (int64_t)b;
+    std::vector<int64_t> bstart(periods.size() + 1, 0);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t t = 0; t < trials; ++t) ++bstart[bucket_of[per_of(t, i)] + 1];
+    for (size_t b = 0; b < periods.size(); ++b) bstart[b + 1] += bstart[b];
+    std::vector<uint32_t> list((size_t)bstart.back());
+    std::vector<int64_t> fill(bstart.begin(), bstart.end() - 1);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t t = 0; t < trials; ++t)
+            list[fill[bucket_of[per_of(t, i)]]++] = (uint32_t)((i << tshift) | t);
+    P.alist.upload(list, st);
+    // per active sub-step: descriptors of the buckets whose period divides the counter
+    std::vector<int4> desc;
+    int64_t maxtotal = 0;
+    for (int64_t count = 0; count < maxcount; ++count) {
+        pbsa_plan::ALaunch L{(uint32_t)count, count / t_res, (int64_t)desc.size(), 0, 0};
+        int64_t cum = 0;
+        for (size_t b = 0; b < periods.size(); ++b) {
+            if (count % periods[b] != 0) continue;
+            const int64_t len = bstart[b + 1] - bstart[b];
+            desc.push_back(make_int4((int)bstart[b], (int)cum, (int)len, 0));
+            cum += len;
+        }
+        L.ndesc = (int)(desc.size() - L.desc_off);
+        if (L.ndesc > pbsa::kMaxActiveDesc) return;  // fall back to the full-pass kernel
+        L.total = (int)cum;
+        if (cum > 0) P.alaunch.push_back(L);
+        maxtotal = std::max(maxtotal, cum);
+    }
+    P.adesc.upload(desc, st);
+    P.st_g.alloc((size_t)maxtotal);
+    P.st_v.alloc((size_t)maxtotal);
+    P.tshift = tshift;
+    P.tmask = (uint32_t)((1u << tshift) - 1u);
+    P.active_mode = true;
+    P.hist.release();  // the integer ring replaces the fp64 history
 }
 
 void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
@@ -560,16 +677,27 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.me_i.upload(a32, st);
         P.me_j.upload(b32, st);
         if (P.int_energy) {
-            std::vector<int64_t> wi(mm), hi(n);
+            // energy from per-edge disagreement counts: sum J s s = sum J - 2 sum_{differ} J;
+            // for the MAX-CUT mapping (J = -w) the cut count alone gives it
+            std::vector<int64_t> hi(n);
+            std::vector<int32_t> wj(mm);
             bool any_h = false;
-            for (int64_t k = 0; k < mm; ++k) wi[k] = (int64_t)mew[k];
+            for (int64_t k = 0; k < mm; ++k) {
+                wj[k] = (int32_t)mew[k];
+                P.sum_j += (int64_t)mew[k];
+            }
             for (int64_t i = 0; i < n; ++i) {
                 hi[i] = (int64_t)hv[i];
                 any_h |= hi[i] != 0;
             }
-            P.me_wi.upload(wi, st);
-            if (any_h) P.h_int.upload(hi, st);
-            P.e_acc.alloc((size_t)cycles * P.Tp);
+            if (!(P.has_graph && graph_is_model)) {
+                P.me_w32.upload(wj, st);
+                P.dj_acc.alloc((size_t)cycles * P.Tp);
+            }
+            if (any_h) {
+                P.h_int.upload(hi, st);
+                P.e_acc.alloc((size_t)cycles * P.Tp);
+            }
         } else {
             P.me_w.upload(mew, mm, st);
             P.e_f64.alloc((size_t)cycles * P.Tp);
@@ -582,6 +710,15 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.ge_i.upload(g32i, st);
         P.ge_j.upload(g32j, st);
         if (gm) P.ge_w.upload(gew, gm, st);
+        if (gm && P.int_energy) {
+            std::vector<int32_t> w32(gm);
+            for (int64_t k = 0; k < gm; ++k) {
+                if (gew[k] > INT32_MAX || gew[k] < INT32_MIN) fail(PBSA_EINVAL, "graph weight exceeds int32");
+                w32[k] = (int32_t)gew[k];
+            }
+            P.ge_w32.upload(w32, st);
+        }
+        P.graph_is_model = P.has_graph && graph_is_model;
         P.cut_acc.alloc((size_t)cycles * P.Tp);
         // updates: sum over (trial, node) of ceil(cycles * t_res / period)
         const int64_t total = cycles * t_res;
@@ -596,6 +733,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             ups = trials * n * ((total + t_res - 1) / t_res);
         }
         P.updates_per_run = ups;
+        if (P.int_energy)
+            setup_active(P, n, indptr, indices, values, hv, lam, delta, period, pstride, trials,
+                         cycles, t_res, algo, alpha, p_stall);
     }
     // mm/gm metadata for stats
     P.trace_cut.alloc((size_t)trials * cycles);
@@ -701,15 +841,58 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         CK(cudaMemsetAsync(P.inputs.p, 0, P.inputs.n * sizeof(double), st));
         CK(cudaMemsetAsync(P.counts.p, 0, P.counts.n * sizeof(int32_t), st));
         if (P.hist.n) CK(cudaMemsetAsync(P.hist.p, 0, P.hist.n * sizeof(double), st));
+        if (P.hist_i.n) CK(cudaMemsetAsync(P.hist_i.p, 0, P.hist_i.n * sizeof(int32_t), st));
         CK(cudaMemsetAsync(P.cut_acc.p, 0, P.cut_acc.n * sizeof(unsigned long long), st));
         if (P.e_acc.n) CK(cudaMemsetAsync(P.e_acc.p, 0, P.e_acc.n * sizeof(unsigned long long), st));
+        if (P.dj_acc.n) CK(cudaMemsetAsync(P.dj_acc.p, 0, P.dj_acc.n * sizeof(unsigned long long), st));
         P.launches += 1;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
         int cur = 0;
-        size_t ai = 0;
+        size_t ai = 0, li = 0;
         const int sm_chunks = std::max<int64_t>(1, std::min<int64_t>(64, (std::max(mm, gm) + 255) / 256));
         for (int64_t c = 0; c < P.cycles; ++c) {
-            while (ai < P.active_counts.size() && P.active_counts[ai] < (uint64_t)(c + 1) * P.t_res) {
+            // active-list mode: in-place spins, staged + scattered per sub-step
+            while (P.active_mode && li < P.alaunch.size() && P.alaunch[li].cycle == c) {
+                const pbsa_plan::ALaunch &L = P.alaunch[li];
+                pbsa::ActiveArgs a{};
+                a.s = P.g_spins[0].p;
+                a.st_g = P.st_g.p;
+                a.st_v = P.st_v.p;
+                a.list = P.alist.p;
+                a.desc = P.adesc.p + L.desc_off;
+                a.ndesc = L.ndesc;
+                a.total = L.total;
+                a.rowptr = P.rowptr.p;
+                a.col = P.col.p;
+                a.vali = P.vali.p;
+                a.hi = P.hi32.n ? P.hi32.p : nullptr;
+                a.lam = P.has_lam ? P.lam.p : nullptr;
+                a.delta = P.has_delta ? P.delta.p : nullptr;
+                a.shared_profile = P.shared_profile;
+                a.inputs = P.inputs.p;
+                a.counts = P.counts.p;
+                a.hist = P.hist_i.p;
+                a.kr = P.kr.p;
+                a.kst = P.kst.p;
+                a.thr = P.athr.n ? P.athr.p + (size_t)c * P.Kt : nullptr;
+                a.rawmin = P.rawmin;
+                a.tshift = P.tshift;
+                a.tmask = P.tmask;
+                a.Tp = (int)P.Tp;
+                a.alpha = (int)P.alpha;
+                a.algo = P.algo;
+                a.i0 = P.i0[c];
+                a.p_stall = P.p_stall;
+                a.count = L.count;
+                pbsa::general_active<<<grid_for(L.total, TB), TB, 0, st>>>(a);
+                CK(cudaGetLastError());
+                pbsa::general_scatter<<<grid_for(L.total, TB), TB, 0, st>>>(P.g_spins[0].p, P.st_g.p,
+                                                                           P.st_v.p, L.total);
+                P.launches += 2;
+                ++P.sweep_launches;
+                ++li;
+            }
+            while (!P.active_mode && ai < P.active_counts.size() && P.active_counts[ai] < (uint64_t)(c + 1) * P.t_res) {
                 pbsa::GeneralArgs a{};
                 a.sold = P.g_spins[cur].p;
                 a.snew = P.g_spins[cur ^ 1].p;
@@ -742,26 +925,52 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                 cur ^= 1;
                 ++ai;
             }
-            pbsa::StatsArgs s{};
-            s.s = P.g_spins[cur].p;
-            s.ge_i = P.ge_i.p;
-            s.ge_j = P.ge_j.p;
-            s.ge_w = P.ge_w.p;
-            s.me_i = P.me_i.p;
-            s.me_j = P.me_j.p;
-            s.me_wi = P.me_wi.p;
-            s.hi = P.h_int.p;
-            s.gm = gm;
-            s.mm = mm;
-            s.n = (int)P.n;
-            s.Tp = (int)P.Tp;
-            s.T = (int)P.T;
-            s.chunks = sm_chunks;
-            s.cut_acc = P.cut_acc.p + (size_t)c * P.Tp;
-            s.e_acc = P.int_energy ? P.e_acc.p + (size_t)c * P.Tp : nullptr;
-            dim3 grid(sm_chunks, (unsigned)grid_for(P.T, TB));
-            pbsa::general_stats<<<grid, TB, 0, st>>>(s);
-            ++P.launches;
+            if (P.int_energy) {
+                const int64_t mx = std::max(gm, P.graph_is_model ? (int64_t)0 : mm);
+                const int chunks = (int)std::max<int64_t>(1, std::min<int64_t>(256, mx / 256));
+                dim3 grid(chunks, (unsigned)grid_for(P.Tp / 4, TB));
+                if (gm) {
+                    pbsa::differ_count<<<grid, TB, 0, st>>>(P.g_spins[cur].p, P.ge_i.p, P.ge_j.p,
+                                                            P.ge_w32.p, gm, (int)(P.Tp / 4), chunks,
+                                                            P.cut_acc.p + (size_t)c * P.Tp);
+                    ++P.launches;
+                }
+                if (!P.graph_is_model && mm) {
+                    pbsa::differ_count<<<grid, TB, 0, st>>>(P.g_spins[cur].p, P.me_i.p, P.me_j.p,
+                                                            P.me_w32.p, mm, (int)(P.Tp / 4), chunks,
+                                                            P.dj_acc.p + (size_t)c * P.Tp);
+                    ++P.launches;
+                }
+                if (P.e_acc.n) {  // sum_i h_i s_i
+                    pbsa::StatsArgs s{};
+                    s.s = P.g_spins[cur].p;
+                    s.hi = P.h_int.p;
+                    s.n = (int)P.n;
+                    s.Tp = (int)P.Tp;
+                    s.T = (int)P.T;
+                    s.chunks = sm_chunks;
+                    s.cut_acc = P.cut_acc.p + (size_t)c * P.Tp;
+                    s.e_acc = P.e_acc.p + (size_t)c * P.Tp;
+                    dim3 g2(sm_chunks, (unsigned)grid_for(P.T, TB));
+                    pbsa::general_stats<<<g2, TB, 0, st>>>(s);
+                    ++P.launches;
+                }
+            } else {
+                pbsa::StatsArgs s{};
+                s.s = P.g_spins[cur].p;
+                s.ge_i = P.ge_i.p;
+                s.ge_j = P.ge_j.p;
+                s.ge_w = P.ge_w.p;
+                s.gm = gm;
+                s.n = (int)P.n;
+                s.Tp = (int)P.Tp;
+                s.T = (int)P.T;
+                s.chunks = sm_chunks;
+                s.cut_acc = P.cut_acc.p + (size_t)c * P.Tp;
+                dim3 grid(sm_chunks, (unsigned)grid_for(P.T, TB));
+                pbsa::general_stats<<<grid, TB, 0, st>>>(s);
+                ++P.launches;
+            }
             if (!P.int_energy) {
                 pbsa::general_energy_f64<<<grid_for(P.T, 128), 128, 0, st>>>(
                     P.g_spins[cur].p, P.h.p, P.me_i.p, P.me_j.p, P.me_w.p, mm, (int)P.n,
@@ -773,7 +982,10 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         P.final_parity = cur;
         pbsa::FinalArgs f{};
         f.cut_acc = P.cut_acc.p;
-        f.e_acc = P.e_acc.p;
+        f.e_acc = P.e_acc.n ? P.e_acc.p : nullptr;
+        f.dj_acc = P.dj_acc.p;
+        f.sum_j = P.sum_j;
+        f.graph_is_model = P.graph_is_model;
         f.e_f64 = P.e_f64.p;
         f.mode = P.int_energy ? 1 : 2;
         f.has_graph = P.has_graph;
@@ -976,8 +1188,16 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                 const int64_t rows = n * P->alpha;
                 dhist.alloc((size_t)T * rows);
                 dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(rows, 32));
-                pbsa::transpose_tile<double><<<g, tb, 0, st>>>(P->hist.p, dhist.p, (int)rows,
-                                                               (int)P->Tp, (int)T);
+                if (P->active_mode) {  // integer ring -> fp64 (exact: the raws are integers)
+                    DevBuf<int32_t> hi32;
+                    hi32.alloc((size_t)T * rows);
+                    pbsa::transpose_tile<int32_t><<<g, tb, 0, st>>>(P->hist_i.p, hi32.p, (int)rows,
+                                                                    (int)P->Tp, (int)T);
+                    pbsa::widen_hist<<<grid_for(T * rows, TB), TB, 0, st>>>(hi32.p, dhist.p, T * rows);
+                } else {
+                    pbsa::transpose_tile<double><<<g, tb, 0, st>>>(P->hist.p, dhist.p, (int)rows,
+                                                                   (int)P->Tp, (int)T);
+                }
             }
             if (hist && P->algo != 1) parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
             if (spins) CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));

@@ -467,6 +467,113 @@ __global__ void __launch_bounds__(256) general_substep(GeneralArgs a) {
     a.snew[g] = act >= 0.0 ? 1 : -1;
 }
 
+// ------------------------------------------------- general path, active lists
+// For integer-valued models (every MAX-CUT instance) the sub-step touches only
+// the p-bits that fire: (trial, node) pairs are bucketed by update period on
+// the host, and a sub-step with counter `count` processes the concatenation of
+// the buckets whose period divides it (descriptors {start, cum, len}).  One
+// thread per firing p-bit; the local field is an exact integer sum (equal to
+// the reference's fp64 CSR-order sum because every partial sum is an integer
+// below 2^53).  New spins are staged and scattered by a second kernel, which
+// keeps the synchronous snapshot semantics of _kernels.py:151-155.
+struct ActiveArgs {
+    const int8_t *s;          // [n][Tp]
+    uint32_t *st_g;           // staged pair index
+    int8_t *st_v;             // staged new spin
+    const uint32_t *list;     // all (node << tshift | trial) entries, bucketed by period
+    const int4 *desc;         // [ndesc] {start in list, cumulative offset, length, 0}
+    int ndesc, total;
+    const uint32_t *rowptr, *col;
+    const int32_t *vali;      // integer couplings, CSR order
+    const int32_t *hi;        // integer fields or null
+    const double *lam, *delta;
+    int shared_profile;
+    double *inputs;           // [n][Tp]
+    int32_t *counts;          // [n][Tp]
+    int32_t *hist;            // [n][alpha][Tp] raw fields (TAPSA)
+    const uint64_t *kr, *kst;
+    const uint64_t *thr;      // [K] this cycle's thresholds (table mode) or null
+    int rawmin;
+    int tshift;
+    uint32_t tmask;
+    int Tp, alpha, algo;
+    double i0, p_stall;
+    uint32_t count;
+};
+
+constexpr int kMaxActiveDesc = 512;
+
+__global__ void __launch_bounds__(256) general_active(ActiveArgs a) {
+    __shared__ int4 sdesc[kMaxActiveDesc];
+    for (int k = threadIdx.x; k < a.ndesc; k += blockDim.x) sdesc[k] = a.desc[k];
+    __syncthreads();
+    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= a.total) return;
+    int lo = 0, hi = a.ndesc - 1;  // last descriptor with cum <= pos
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sdesc[mid].y <= pos) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t e = a.list[sdesc[lo].x + (pos - sdesc[lo].y)];
+    const int i = (int)(e >> a.tshift), t = (int)(e & a.tmask);
+    const size_t g = (size_t)i * a.Tp + t;
+    int raw = a.hi ? a.hi[i] : 0;
+    const uint32_t beg = a.rowptr[i], end = a.rowptr[i + 1];
+    for (uint32_t k = beg; k < end; ++k) raw += a.vali[k] * (int)a.s[(size_t)a.col[k] * a.Tp + t];
+    const int32_t cnt = a.counts[g];
+    double inp;
+    if (a.algo == 1) {  // TAPSA (_kernels.py:131-138); integer partial sums are exact in fp64
+        int32_t *ring = a.hist + (size_t)i * a.alpha * a.Tp + t;
+        ring[(size_t)(cnt % a.alpha) * a.Tp] = raw;
+        const int filled = cnt + 1 < a.alpha ? cnt + 1 : a.alpha;
+        long long acc = 0;
+        for (int q = 0; q < filled; ++q) acc += ring[(size_t)q * a.Tp];
+        inp = __dmul_rn(a.i0, __ddiv_rn((double)acc, (double)filled));
+    } else if (a.algo == 2 && cnt > 0) {  // SPSA (_kernels.py:139-144)
+        const double u = u01_of(absorb(absorb(a.kst[t], (uint64_t)i), (uint64_t)a.count));
+        inp = u < a.p_stall ? a.inputs[g] : __dmul_rn(a.i0, (double)raw);
+    } else {
+        inp = __dmul_rn(a.i0, (double)raw);
+    }
+    a.inputs[g] = inp;
+    a.counts[g] = cnt + 1;
+    const uint64_t h = absorb(absorb(a.kr[t], (uint64_t)i), (uint64_t)a.count);
+    bool up;
+    if (a.thr) {  // lam = 1, delta = 0, plain rule: exact integer threshold per (cycle, raw)
+        const uint64_t thr = a.thr[raw - a.rawmin];
+        up = h >= thr && thr != ~0ULL;
+    } else {
+        double x = inp;
+        if (a.lam) {
+            const size_t pidx = a.shared_profile ? (size_t)i : g;
+            x = __dmul_rn(a.lam[pidx], __dadd_rn(inp, a.delta[pidx]));
+        }
+        const double r = __dsub_rn(__dmul_rn(2.0, u01_of(h)), 1.0);
+        // Prefilter with single-precision tanhf (<= 2 ulp) of x rounded to
+        // float: |tanhf((float)x) - tanh(x)| < 2^-21 for every x, so whenever
+        // |r + tanhf| >= 2^-16 the sign equals the sign of r + libm tanh(x).
+        // Only the rare near-ties evaluate the libm-exact fp64 tanh.
+        const double s = __dadd_rn(r, (double)tanhf(__double2float_rn(x)));
+        if (fabs(s) >= 0x1p-16)
+            up = s >= 0.0;
+        else
+            up = __dadd_rn(r, pb_libm_tanh(x)) >= 0.0;
+    }
+    a.st_g[pos] = (uint32_t)g;
+    a.st_v[pos] = up ? 1 : -1;
+}
+
+__global__ void general_scatter(int8_t *__restrict__ s, const uint32_t *__restrict__ st_g,
+                                const int8_t *__restrict__ st_v, int total) {
+    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos < total) s[st_g[pos]] = st_v[pos];
+}
+
+__global__ void widen_hist(const int32_t *__restrict__ src, double *__restrict__ dst, int64_t n) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n) dst[g] = (double)src[g];
+}
+
 // Per-cycle cut and integer energy over edges, spins int8 [n][Tp].
 // grid.x chunks the edge range, threads cover trials.
 struct StatsArgs {
@@ -511,6 +618,48 @@ __global__ void general_stats(StatsArgs a) {
     if (a.e_acc && e) atomicAdd(a.e_acc + t, (unsigned long long)e);
 }
 
+// Per-trial sum over an edge list of w_e [s_a != s_b], spins int8 [n][Tp]
+// read four trials per 32-bit word.  Unit weights accumulate in packed bytes
+// (flushed every 255 edges); other weights per byte.  Used per cycle for the
+// cut (graph weights) and, when the model is not the graph's MAX-CUT mapping,
+// for sum_e J_e [s_a != s_b] (energy = sum J - 2 * that).
+__global__ void differ_count(const int8_t *__restrict__ s, const uint32_t *__restrict__ ei,
+                             const uint32_t *__restrict__ ej, const int32_t *__restrict__ w,
+                             int64_t m, int Tq, int chunks, unsigned long long *__restrict__ out) {
+    const int q = blockIdx.y * blockDim.x + threadIdx.x;
+    if (q >= Tq) return;
+    const uint32_t *s32 = reinterpret_cast<const uint32_t *>(s);
+    const int64_t per = (m + chunks - 1) / chunks;
+    const int64_t lo = blockIdx.x * per, hi = min(m, lo + per);
+    long long c[4] = {0, 0, 0, 0};
+    uint32_t accP = 0, accN = 0;
+    int k = 0;
+    for (int64_t e = lo; e < hi; ++e) {
+        const uint32_t d = ((s32[(size_t)ei[e] * Tq + q] ^ s32[(size_t)ej[e] * Tq + q]) >> 1) & 0x01010101u;
+        const int wv = w[e];
+        if (wv == 1) {
+            accP += d;
+        } else if (wv == -1) {
+            accN += d;
+        } else {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) c[b] += (long long)wv * ((d >> (8 * b)) & 1u);
+        }
+        if (++k == 255) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                c[b] += (long long)((accP >> (8 * b)) & 0xFFu) - (long long)((accN >> (8 * b)) & 0xFFu);
+            accP = accN = 0;
+            k = 0;
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        c[b] += (long long)((accP >> (8 * b)) & 0xFFu) - (long long)((accN >> (8 * b)) & 0xFFu);
+        if (c[b]) atomicAdd(out + 4 * q + b, (unsigned long long)c[b]);
+    }
+}
+
 // Exact fp64 energy in the reference's sequential order (_kernels.py:157-161),
 // one thread per trial; used only when couplings/fields are not integers.
 __global__ void general_energy_f64(const int8_t *__restrict__ s, const double *__restrict__ h,
@@ -537,9 +686,12 @@ __global__ void general_energy_f64(const int8_t *__restrict__ s, const double *_
 struct FinalArgs {
     const unsigned long long *pacc;
     const unsigned long long *cut_acc;
-    const unsigned long long *e_acc;
+    const unsigned long long *e_acc;   // mode 1: sum_i h_i s_i, or null
+    const unsigned long long *dj_acc;  // mode 1, model != graph: sum_e J [s_a != s_b]
     const double *e_f64;
     int64_t total_w;
+    int64_t sum_j;
+    int graph_is_model;
     int mode, has_graph;
     int C, Tp, T;
     int64_t *trace_cut;     // [T][C]
@@ -559,9 +711,15 @@ __global__ void finalize_traces(FinalArgs a) {
             cut = a.has_graph ? (2 * a.total_w + P) / 4 : 0;
             e = (double)(-(P / 2));
         } else {
-            cut = a.has_graph ? (long long)a.cut_acc[(size_t)c * a.Tp + t] : 0;
-            e = a.mode == 1 ? (double)(-(long long)a.e_acc[(size_t)c * a.Tp + t])
-                            : a.e_f64[(size_t)c * a.Tp + t];
+            const size_t at = (size_t)c * a.Tp + t;
+            cut = a.has_graph ? (long long)a.cut_acc[at] : 0;
+            if (a.mode == 1) {  // integer energy: sum J s s + sum h s, from differ counts
+                long long es = a.sum_j + (a.graph_is_model ? 2 * cut : -2 * (long long)a.dj_acc[at]);
+                if (a.e_acc) es += (long long)a.e_acc[at];
+                e = (double)(-es);
+            } else {
+                e = a.e_f64[at];
+            }
         }
         a.trace_cut[(size_t)t * a.C + c] = cut;
         a.trace_energy[(size_t)t * a.C + c] = e;
