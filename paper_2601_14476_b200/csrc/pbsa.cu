@@ -257,7 +257,8 @@ struct pbsa_plan {
     DevBuf<uint32_t> alist, st_g;
     DevBuf<int8_t> st_v;
     DevBuf<int4> adesc;
-    DevBuf<int32_t> vali, hi32, hist_i;
+    DevBuf<int32_t> vali, hi32, hist_i, a_counts;  // hist_i: [alpha][Np], list order
+    DevBuf<double> a_inputs;                        // [Np], list order
     DevBuf<uint64_t> athr;  // [cycles][Kt] thresholds (lam = 1, delta = 0, plain rule), or empty
     int tshift = 0, rawmin = 0, Kt = 0;
     uint32_t tmask = 0;
@@ -344,7 +345,7 @@ void setup_active(pbsa_plan &P, int64_t n, const int64_t *indptr, const int64_t 
     for (int64_t k = 0; k < nnz; ++k) vi[k] = (int32_t)values[k];
     P.vali.upload(vi, st);
     if (any_h) P.hi32.upload(hi, st);
-    if (algo == 1) P.hist_i.alloc((size_t)n * alpha * P.Tp);
+    if (algo == 1) P.hist_i.alloc((size_t)n * alpha * trials);
     // table mode: plain rule (or a degenerate rule) with an ideal lam/delta
     bool ideal_ld = true;
     const int64_t prow = pstride ? trials : 1;
@@ -410,6 +411,23 @@ void setup_active(pbsa_plan &P, int64_t n, const int64_t *indptr, const int64_t 
     P.adesc.upload(desc, st);
     P.st_g.alloc((size_t)maxtotal);
     P.st_v.alloc((size_t)maxtotal);
+    // per-p-bit state in list order (coalesced per launch); per-trial profiles
+    // are gathered into list order too
+    const size_t Np = list.size();
+    P.a_inputs.alloc(Np);
+    P.a_counts.alloc(Np);
+    if (lam && pstride) {
+        std::vector<double> l(Np), d(Np);
+        for (size_t li = 0; li < Np; ++li) {
+            const int64_t i = list[li] >> tshift, t = list[li] & ((1u << tshift) - 1u);
+            l[li] = lam[t * n + i];
+            d[li] = delta[t * n + i];
+        }
+        P.lam.upload(l, st);
+        P.delta.upload(d, st);
+    }
+    P.inputs.release();
+    P.counts.release();
     P.tshift = tshift;
     P.tmask = (uint32_t)((1u << tshift) - 1u);
     P.active_mode = true;
@@ -838,8 +856,10 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
     } else {
         pbsa::init_general<<<grid_for(P.n * P.Tp, TB), TB, 0, st>>>(P.g_spins[0].p, P.kspin.p,
                                                                     (int)P.n, (int)P.Tp);
-        CK(cudaMemsetAsync(P.inputs.p, 0, P.inputs.n * sizeof(double), st));
-        CK(cudaMemsetAsync(P.counts.p, 0, P.counts.n * sizeof(int32_t), st));
+        if (P.inputs.n) CK(cudaMemsetAsync(P.inputs.p, 0, P.inputs.n * sizeof(double), st));
+        if (P.counts.n) CK(cudaMemsetAsync(P.counts.p, 0, P.counts.n * sizeof(int32_t), st));
+        if (P.a_inputs.n) CK(cudaMemsetAsync(P.a_inputs.p, 0, P.a_inputs.n * sizeof(double), st));
+        if (P.a_counts.n) CK(cudaMemsetAsync(P.a_counts.p, 0, P.a_counts.n * sizeof(int32_t), st));
         if (P.hist.n) CK(cudaMemsetAsync(P.hist.p, 0, P.hist.n * sizeof(double), st));
         if (P.hist_i.n) CK(cudaMemsetAsync(P.hist_i.p, 0, P.hist_i.n * sizeof(int32_t), st));
         CK(cudaMemsetAsync(P.cut_acc.p, 0, P.cut_acc.n * sizeof(unsigned long long), st));
@@ -869,9 +889,10 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                 a.lam = P.has_lam ? P.lam.p : nullptr;
                 a.delta = P.has_delta ? P.delta.p : nullptr;
                 a.shared_profile = P.shared_profile;
-                a.inputs = P.inputs.p;
-                a.counts = P.counts.p;
+                a.inputs = P.a_inputs.p;
+                a.counts = P.a_counts.p;
                 a.hist = P.hist_i.p;
+                a.Np = (int64_t)P.alist.n;
                 a.kr = P.kr.p;
                 a.kst = P.kst.p;
                 a.thr = P.athr.n ? P.athr.p + (size_t)c * P.Kt : nullptr;
@@ -1170,30 +1191,39 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                 pbsa::transpose_tile<int8_t><<<g, tb, 0, st>>>(P->g_spins[P->final_parity].p,
                                                                dspins.p, (int)n, (int)P->Tp, (int)T);
             }
+            const int64_t Np = (int64_t)P->alist.n;
+            const int tsh = P->tshift;
             if (inputs) {
                 dinputs.alloc((size_t)T * n);
-                dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
-                pbsa::transpose_tile<double><<<g, tb, 0, st>>>(P->inputs.p, dinputs.p, (int)n,
-                                                               (int)P->Tp, (int)T);
+                if (P->active_mode) {
+                    pbsa::list_to_trial_major<double, double><<<grid_for(Np, TB), TB, 0, st>>>(
+                        P->a_inputs.p, P->alist.p, Np, tsh, P->tmask, (int)n, 1, dinputs.p);
+                } else {
+                    dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
+                    pbsa::transpose_tile<double><<<g, tb, 0, st>>>(P->inputs.p, dinputs.p, (int)n,
+                                                                   (int)P->Tp, (int)T);
+                }
             }
             if (counts) {
-                dcounts.alloc((size_t)T * n);
                 dcounts64.alloc((size_t)T * n);
-                dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
-                pbsa::transpose_tile<int32_t><<<g, tb, 0, st>>>(P->counts.p, dcounts.p, (int)n,
-                                                                (int)P->Tp, (int)T);
-                pbsa::widen_i32<<<grid_for(T * n, TB), TB, 0, st>>>(dcounts.p, dcounts64.p, T * n);
+                if (P->active_mode) {
+                    pbsa::list_to_trial_major<int32_t, int64_t><<<grid_for(Np, TB), TB, 0, st>>>(
+                        P->a_counts.p, P->alist.p, Np, tsh, P->tmask, (int)n, 1, dcounts64.p);
+                } else {
+                    dcounts.alloc((size_t)T * n);
+                    dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(n, 32));
+                    pbsa::transpose_tile<int32_t><<<g, tb, 0, st>>>(P->counts.p, dcounts.p, (int)n,
+                                                                    (int)P->Tp, (int)T);
+                    pbsa::widen_i32<<<grid_for(T * n, TB), TB, 0, st>>>(dcounts.p, dcounts64.p, T * n);
+                }
             }
             if (hist && P->algo == 1) {
                 const int64_t rows = n * P->alpha;
                 dhist.alloc((size_t)T * rows);
                 dim3 g((unsigned)grid_for(T, 32), (unsigned)grid_for(rows, 32));
                 if (P->active_mode) {  // integer ring -> fp64 (exact: the raws are integers)
-                    DevBuf<int32_t> hi32;
-                    hi32.alloc((size_t)T * rows);
-                    pbsa::transpose_tile<int32_t><<<g, tb, 0, st>>>(P->hist_i.p, hi32.p, (int)rows,
-                                                                    (int)P->Tp, (int)T);
-                    pbsa::widen_hist<<<grid_for(T * rows, TB), TB, 0, st>>>(hi32.p, dhist.p, T * rows);
+                    pbsa::list_to_trial_major<int32_t, double><<<grid_for(Np, TB), TB, 0, st>>>(
+                        P->hist_i.p, P->alist.p, Np, tsh, P->tmask, (int)n, (int)P->alpha, dhist.p);
                 } else {
                     pbsa::transpose_tile<double><<<g, tb, 0, st>>>(P->hist.p, dhist.p, (int)rows,
                                                                    (int)P->Tp, (int)T);

@@ -488,9 +488,10 @@ struct ActiveArgs {
     const int32_t *hi;        // integer fields or null
     const double *lam, *delta;
     int shared_profile;
-    double *inputs;           // [n][Tp]
-    int32_t *counts;          // [n][Tp]
-    int32_t *hist;            // [n][alpha][Tp] raw fields (TAPSA)
+    double *inputs;           // [Np] list order
+    int32_t *counts;          // [Np] list order
+    int32_t *hist;            // [alpha][Np] raw fields (TAPSA), list order
+    int64_t Np;               // list length (= trials * n)
     const uint64_t *kr, *kst;
     const uint64_t *thr;      // [K] this cycle's thresholds (table mode) or null
     int rawmin;
@@ -514,29 +515,32 @@ __global__ void __launch_bounds__(256) general_active(ActiveArgs a) {
         const int mid = (lo + hi + 1) >> 1;
         if (sdesc[mid].y <= pos) lo = mid; else hi = mid - 1;
     }
-    const uint32_t e = a.list[sdesc[lo].x + (pos - sdesc[lo].y)];
+    // per-p-bit state lives in list order: a firing p-bit always sits at the
+    // same list position, so state loads/stores of a launch are coalesced
+    const uint32_t li = (uint32_t)(sdesc[lo].x + (pos - sdesc[lo].y));
+    const uint32_t e = a.list[li];
     const int i = (int)(e >> a.tshift), t = (int)(e & a.tmask);
     const size_t g = (size_t)i * a.Tp + t;
     int raw = a.hi ? a.hi[i] : 0;
     const uint32_t beg = a.rowptr[i], end = a.rowptr[i + 1];
     for (uint32_t k = beg; k < end; ++k) raw += a.vali[k] * (int)a.s[(size_t)a.col[k] * a.Tp + t];
-    const int32_t cnt = a.counts[g];
+    const int32_t cnt = a.counts[li];
     double inp;
     if (a.algo == 1) {  // TAPSA (_kernels.py:131-138); integer partial sums are exact in fp64
-        int32_t *ring = a.hist + (size_t)i * a.alpha * a.Tp + t;
-        ring[(size_t)(cnt % a.alpha) * a.Tp] = raw;
+        int32_t *ring = a.hist + li;
+        ring[(size_t)(cnt % a.alpha) * a.Np] = raw;
         const int filled = cnt + 1 < a.alpha ? cnt + 1 : a.alpha;
         long long acc = 0;
-        for (int q = 0; q < filled; ++q) acc += ring[(size_t)q * a.Tp];
+        for (int q = 0; q < filled; ++q) acc += ring[(size_t)q * a.Np];
         inp = __dmul_rn(a.i0, __ddiv_rn((double)acc, (double)filled));
     } else if (a.algo == 2 && cnt > 0) {  // SPSA (_kernels.py:139-144)
         const double u = u01_of(absorb(absorb(a.kst[t], (uint64_t)i), (uint64_t)a.count));
-        inp = u < a.p_stall ? a.inputs[g] : __dmul_rn(a.i0, (double)raw);
+        inp = u < a.p_stall ? a.inputs[li] : __dmul_rn(a.i0, (double)raw);
     } else {
         inp = __dmul_rn(a.i0, (double)raw);
     }
-    a.inputs[g] = inp;
-    a.counts[g] = cnt + 1;
+    a.inputs[li] = inp;
+    a.counts[li] = cnt + 1;
     const uint64_t h = absorb(absorb(a.kr[t], (uint64_t)i), (uint64_t)a.count);
     bool up;
     if (a.thr) {  // lam = 1, delta = 0, plain rule: exact integer threshold per (cycle, raw)
@@ -545,7 +549,7 @@ __global__ void __launch_bounds__(256) general_active(ActiveArgs a) {
     } else {
         double x = inp;
         if (a.lam) {
-            const size_t pidx = a.shared_profile ? (size_t)i : g;
+            const size_t pidx = a.shared_profile ? (size_t)i : (size_t)li;
             x = __dmul_rn(a.lam[pidx], __dadd_rn(inp, a.delta[pidx]));
         }
         const double r = __dsub_rn(__dmul_rn(2.0, u01_of(h)), 1.0);
@@ -553,14 +557,26 @@ __global__ void __launch_bounds__(256) general_active(ActiveArgs a) {
         // float: |tanhf((float)x) - tanh(x)| < 2^-21 for every x, so whenever
         // |r + tanhf| >= 2^-16 the sign equals the sign of r + libm tanh(x).
         // Only the rare near-ties evaluate the libm-exact fp64 tanh.
-        const double s = __dadd_rn(r, (double)tanhf(__double2float_rn(x)));
-        if (fabs(s) >= 0x1p-16)
-            up = s >= 0.0;
+        const double sres = __dadd_rn(r, (double)tanhf(__double2float_rn(x)));
+        if (fabs(sres) >= 0x1p-16)
+            up = sres >= 0.0;
         else
             up = __dadd_rn(r, pb_libm_tanh(x)) >= 0.0;
     }
     a.st_g[pos] = (uint32_t)g;
     a.st_v[pos] = up ? 1 : -1;
+}
+
+// list-order per-p-bit state -> [trial][node][k] output rows
+template <typename TS, typename TD>
+__global__ void list_to_trial_major(const TS *__restrict__ src, const uint32_t *__restrict__ list,
+                                    int64_t Np, int tshift, uint32_t tmask, int n, int K,
+                                    TD *__restrict__ dst) {
+    const int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= Np) return;
+    const uint32_t e = list[li];
+    const int64_t row = (int64_t)(e & tmask) * n + (e >> tshift);
+    for (int k = 0; k < K; ++k) dst[row * K + k] = (TD)src[(size_t)k * Np + li];
 }
 
 __global__ void general_scatter(int8_t *__restrict__ s, const uint32_t *__restrict__ st_g,
