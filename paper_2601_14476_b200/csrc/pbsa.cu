@@ -216,6 +216,8 @@ struct pbsa_plan {
     bool has_graph = false;
     bool int_energy = true;
     bool tapsa_hist_from_raw = false;  // TAPSA alpha=1 routed to the packed path
+    bool tapsa_packed = false;         // TAPSA alpha>=2 on the packed path (bit-sliced ring)
+    DevBuf<uint32_t> ring;             // [W][alpha][L][n]
     int64_t total_w = 0;
     std::vector<double> i0;
     std::vector<uint32_t> active_counts;  // general path: sub-steps with any update
@@ -299,12 +301,26 @@ void set_packed_smem(K kernel, size_t bytes) {
 }
 
 using PackedKernel = void (*)(pbsa::PackedArgs);
-PackedKernel packed_kernel_for(int L, bool update, bool cached) {
+PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false) {
 #define PBSA_CASE(l)                                                                  \
     case l:                                                                           \
         return update ? (cached ? pbsa::packed_sweep<l, true, true>                   \
                                 : pbsa::packed_sweep<l, true, false>)                 \
                       : pbsa::packed_sweep<l, false, false>;
+#define PBSA_TCASE(l)                                                                 \
+    case l:                                                                           \
+        return cached ? pbsa::packed_sweep<l, true, true, 1>                          \
+                      : pbsa::packed_sweep<l, true, false, 1>;
+    if (update && tapsa) {
+        switch (L) {
+            PBSA_TCASE(1)
+            PBSA_TCASE(2)
+            PBSA_TCASE(3)
+            PBSA_TCASE(4)
+            PBSA_TCASE(5)
+            default: fail(PBSA_EINVAL, "packed TApSA supports degree <= 31");
+        }
+    }
     switch (L) {
         PBSA_CASE(1)
         PBSA_CASE(2)
@@ -316,6 +332,14 @@ PackedKernel packed_kernel_for(int L, bool update, bool cached) {
         default: fail(PBSA_EINVAL, "packed path supports degree <= 127");
     }
 #undef PBSA_CASE
+#undef PBSA_TCASE
+}
+
+template <int L>
+void launch_hist_from_ring(const uint32_t *ring, const uint32_t *rowptr, int n, int T, int alpha,
+                           int written, double *out, cudaStream_t st) {
+    pbsa::hist_from_ring<L><<<grid_for((int64_t)n * T, 256), 256, 0, st>>>(ring, rowptr, n, T, alpha,
+                                                                          written, out);
 }
 
 // Active-list setup for integer-valued models (see general_active).
@@ -524,9 +548,12 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     // i < 2^30 and count < 2^30 let the packed kernel fold the first xorshift
     // of each absorb into per-trial constants (pbsa_device.cuh)
     const bool small_counters = n <= (1LL << 30) && cycles * t_res <= (1LL << 30);
-    const bool packed = rule_is_psa && unit_J && zero_h && ideal && graph_is_model && dmax <= 127 &&
-                        small_counters;
-    P.tapsa_hist_from_raw = packed && algo == 1;
+    // time-averaged rule on the packed path: sum of alpha counts must stay < 64
+    const bool tapsa_packed = algo == 1 && alpha >= 2 && alpha * dmax <= 63 && dmax <= 31;
+    const bool packed = (rule_is_psa || tapsa_packed) && unit_J && zero_h && ideal &&
+                        graph_is_model && dmax <= 127 && small_counters;
+    P.tapsa_packed = packed && tapsa_packed;
+    P.tapsa_hist_from_raw = packed && algo == 1 && !P.tapsa_packed;
     P.path = packed ? PBSA_PATH_PACKED : PBSA_PATH_GENERAL;
 
     DeviceGuard dg(device);
@@ -570,13 +597,31 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         }
         P.krg.upload(krg, st);
         P.kfc.upload(kfc, st);
-        // thresholds per (cycle, raw): inp = i0 * raw; act = r + tanh(inp) (lam = 1, delta = 0)
-        std::vector<uint64_t> thr((size_t)cycles * P.K);
-        for (int64_t c = 0; c < cycles; ++c)
-            for (int raw = -P.dmax; raw <= P.dmax; ++raw)
-                thr[(size_t)c * P.K + raw + P.dmax] =
-                    threshold_h64(pb_libm_tanh(P.i0[c] * (double)raw));
-        P.thr.upload(thr, st);
+        if (P.tapsa_packed) {
+            // thresholds per (cycle, degree d, S): acc = 2 S - f d, f = min(c+1, alpha),
+            // inp = i0 * (acc / f) exactly as _kernels.py:138 evaluates it
+            P.K = (P.dmax + 1) * 64;
+            std::vector<uint64_t> thr((size_t)cycles * P.K, ~0ULL);
+            for (int64_t c = 0; c < cycles; ++c) {
+                const int64_t f = std::min<int64_t>(c + 1, alpha);
+                for (int d = 0; d <= P.dmax; ++d)
+                    for (int64_t S = 0; S <= f * d && S < 64; ++S) {
+                        const double acc = (double)(2 * S - f * d);
+                        thr[(size_t)c * P.K + d * 64 + S] =
+                            threshold_h64(pb_libm_tanh(P.i0[c] * (acc / (double)f)));
+                    }
+            }
+            P.thr.upload(thr, st);
+            P.ring.alloc((size_t)P.W * alpha * P.L * n);
+        } else {
+            // thresholds per (cycle, raw): inp = i0 * raw; act = r + tanh(inp) (lam = 1, delta = 0)
+            std::vector<uint64_t> thr((size_t)cycles * P.K);
+            for (int64_t c = 0; c < cycles; ++c)
+                for (int raw = -P.dmax; raw <= P.dmax; ++raw)
+                    thr[(size_t)c * P.K + raw + P.dmax] =
+                        threshold_h64(pb_libm_tanh(P.i0[c] * (double)raw));
+            P.thr.upload(thr, st);
+        }
         for (auto &b : P.p_spins) b.alloc((size_t)P.W * n);
         P.pacc.alloc((size_t)(cycles + 1) * P.Tp);
         P.raw_last.alloc((size_t)n * P.Tp);
@@ -592,8 +637,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.use_cache = cache_entries * 8 <= (32ULL << 30);
         if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1';
         if (P.use_cache) P.acache.alloc(cache_entries);
-        PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache);
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 128 + pbsa::kPackedWarps * 32 * 8 + 16;
+        PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed);
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
         set_packed_smem(kern, smem);
         set_packed_smem(packed_kernel_for(P.L, false, false), smem);
         int occ = 0, sms = 0;
@@ -773,9 +818,9 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                                                    (int)P.n, (int)P.W);
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
-        PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache);
+        PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 128 + pbsa::kPackedWarps * 32 * 8 + 16;
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
         // Word phases run one after another so that a phase's first-absorb
         // cache (PW words x n x 256 B) stays L2-resident across its cycles;
@@ -824,6 +869,12 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     a.chunks = P.chunks;
                     a.count = (uint32_t)(c * P.t_res);
                     a.do_update = c < P.cycles;
+                    if (P.tapsa_packed) {
+                        a.ring = P.ring.p + (size_t)w0 * P.alpha * P.L * P.n;
+                        a.alpha = (int)P.alpha;
+                        a.slot = (int)(cc % P.alpha);
+                        a.filled = (int)std::min<int64_t>(cc + 1, P.alpha);
+                    }
                     (c < P.cycles ? kern_up : kern_cut)<<<blocks, pbsa::kPackedThreads, smem, cs>>>(a);
                     CK(cudaGetLastError());
                     ++P.launches;
@@ -1163,25 +1214,39 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                 pbsa::unpack_spins<<<grid_for(n * T, TB), TB, 0, st>>>(
                     P->p_spins[P->final_parity].p, dspins.p, (int)n, (int)P->W, (int)T);
             }
-            if (inputs || (hist && P->tapsa_hist_from_raw)) {
+            const double f_last = P->tapsa_packed ? (double)std::min<int64_t>(C, P->alpha) : 1.0;
+            if (inputs) {
                 dinputs.alloc((size_t)T * n);
                 pbsa::inputs_from_raw<<<grid_for(n * T, TB), TB, 0, st>>>(
-                    P->raw_last.p, dinputs.p, P->i0[C - 1], (int)n, (int)P->Tp, (int)T);
+                    P->raw_last.p, dinputs.p, P->i0[C - 1], (int)n, (int)P->Tp, (int)T, f_last);
             }
             if (hist && P->tapsa_hist_from_raw) {
                 // TAPSA with alpha = 1: the history holds the last raw field
                 dhist.alloc((size_t)T * n);
                 pbsa::inputs_from_raw<<<grid_for(n * T, TB), TB, 0, st>>>(
-                    P->raw_last.p, dhist.p, 1.0, (int)n, (int)P->Tp, (int)T);
+                    P->raw_last.p, dhist.p, 1.0, (int)n, (int)P->Tp, (int)T, 1.0);
+            }
+            if (hist && P->tapsa_packed) {
+                dhist.alloc((size_t)T * n * P->alpha);
+                const int written = (int)std::min<int64_t>(C, P->alpha);
+                switch (P->L) {
+                    case 1: launch_hist_from_ring<1>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
+                    case 2: launch_hist_from_ring<2>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
+                    case 3: launch_hist_from_ring<3>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
+                    case 4: launch_hist_from_ring<4>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
+                    default: launch_hist_from_ring<5>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
+                }
             }
             // host-side constant outputs overlap the device work above
-            if (hist && !P->tapsa_hist_from_raw) parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
+            if (hist && !P->tapsa_hist_from_raw && !P->tapsa_packed)
+                parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
             if (counts) parallel_fill(counts, (size_t)(T * n), (int64_t)C);  // every p-bit fires once per cycle
             if (spins) CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
             if (inputs)
                 CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
-            if (hist && P->tapsa_hist_from_raw)
-                CK(cudaMemcpyAsync(hist, dhist.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+            if (hist && (P->tapsa_hist_from_raw || P->tapsa_packed))
+                CK(cudaMemcpyAsync(hist, dhist.p, T * n * (P->tapsa_packed ? P->alpha : 1) * sizeof(double),
+                                   cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
         } else {
             dim3 tb(32, 8);
@@ -1259,10 +1324,12 @@ int pbsa_plan_bytes(const pbsa_plan *P, int64_t *h2d_bytes, int64_t *d2h_bytes) 
         const int64_t T = P->T, n = P->n, C = P->cycles;
         int64_t down = T * n + T * n * 8 + 2 * T * C * 8 + T * 8;  // spins, inputs, traces, best
         if (P->path == PBSA_PATH_GENERAL) {
-            down += T * n * 4;                                        // counts (int32 on device)
+            down += T * n * 8;                                        // counts (int64)
             if (P->algo == 1) down += T * n * P->alpha * 8;           // history
         } else if (P->tapsa_hist_from_raw) {
             down += T * n * 8;
+        } else if (P->tapsa_packed) {
+            down += T * n * P->alpha * 8;
         }
         if (h2d_bytes) *h2d_bytes = (int64_t)up;
         if (d2h_bytes) *d2h_bytes = down;

@@ -133,6 +133,8 @@ struct PackedArgs {
     int chunks;               // ceil(n / 32)
     uint32_t count;           // global sub-step counter c * t_res (< 2^30)
     int do_update;            // 0: only accumulate pacc (final cut pass)
+    uint32_t *ring;           // TApSA: [W][alpha][L][n] bit-sliced neighbour counts
+    int alpha, slot, filled;  // TApSA: ring length, this cycle's slot, min(c+1, alpha)
 };
 
 // Exact H >= thr for H = mix64(x); thr == ~0 encodes "never" (tanh == -1),
@@ -214,17 +216,27 @@ constexpr int kWarpCutPlanes = 13;  // after the warp-level add (32 * 255 < 2^13
 #define PBSA_PACKED_MIN_BLOCKS 4
 #endif
 
-template <int L, bool UPDATE, bool CACHED>
+// TApSA (time-averaged rule, _kernels.py:131-138) on the packed path: every
+// p-bit fires once per cycle, so the history slot (c % alpha) and the fill
+// count min(c+1, alpha) are the same for the whole launch.  The ring keeps the
+// bit-sliced neighbour counts p of the last alpha cycles ([W][alpha][L][n]);
+// the drive is i0 * (acc / filled) with acc = 2 S - filled * d and
+// S = sum of p over the filled slots (< 64), so the threshold is a per-cycle
+// table lookup by (degree, S), exactly like the plain rule.
+constexpr int kTapsaPlanes = 6;
+
+template <int L, bool UPDATE, bool CACHED, int ALG = 0>
 __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed_sweep(PackedArgs a) {
     extern __shared__ unsigned long long smem_u64[];
     // Threshold table, 128 B aligned.  L <= 4 (degree <= 15): one 16-entry row
     // per degree d indexed by the neighbour count p (raw = 2p - d), so a
     // trial's entry address is (p * 8) | row base, formed with one LOP3.
-    // Larger degrees: entries indexed by raw + dmax.
-    constexpr bool NIB = L <= 4;
+    // Larger degrees: entries indexed by raw + dmax.  TApSA: 64-entry rows by S.
+    constexpr bool TAPSA = ALG == 1;
+    constexpr bool NIB = L <= 4 && !TAPSA;
     uint2 *sthr = reinterpret_cast<uint2 *>(
-        (reinterpret_cast<uintptr_t>(smem_u64) + 127) & ~(uintptr_t)127);
-    const int tab_entries = NIB ? (a.dmax + 1) * 16 : a.K;
+        (reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
+    const int tab_entries = TAPSA ? (a.dmax + 1) * 64 : NIB ? (a.dmax + 1) * 16 : a.K;
     uint2 *skey = sthr + tab_entries;                     // [warps][32] {F, C}
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -234,14 +246,19 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     const bool live = w < a.W;
 
     for (int k = threadIdx.x; k < tab_entries; k += blockDim.x) {
-        int raw = k - a.dmax;
-        bool ok = true;
-        if (NIB) {
-            const int d = k >> 4, pp = k & 15;
-            raw = 2 * pp - d;
-            ok = pp <= d;
+        uint32_t thi;
+        if (TAPSA) {
+            thi = (uint32_t)(a.thr[k] >> 32);  // host table is already [degree][S]
+        } else {
+            int raw = k - a.dmax;
+            bool ok = true;
+            if (NIB) {
+                const int d = k >> 4, pp = k & 15;
+                raw = 2 * pp - d;
+                ok = pp <= d;
+            }
+            thi = ok ? (uint32_t)(a.thr[raw + a.dmax] >> 32) : 0u;
         }
-        const uint32_t thi = ok ? (uint32_t)(a.thr[raw + a.dmax] >> 32) : 0u;
         sthr[k] = make_uint2(~thi, thi);
     }
     uint2 *key = skey + wib * 32;
@@ -288,7 +305,73 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             const int d = (int)(end - beg);
             dsum += d;
             vc_add<L, kCutPlanes>(C, g);
-            if (UPDATE) {
+            if (UPDATE && TAPSA) {
+                // S = p of this cycle + the other filled slots of the ring
+                uint32_t S[kTapsaPlanes];
+#pragma unroll
+                for (int r = 0; r < kTapsaPlanes; ++r) S[r] = r < L ? p[r] : 0u;
+                uint32_t *ring = a.ring + (size_t)w * a.alpha * L * a.n + i;
+                for (int qs = 0; qs < a.filled; ++qs) {
+                    if (qs == a.slot) continue;
+                    uint32_t x[L];
+#pragma unroll
+                    for (int r = 0; r < L; ++r) x[r] = ring[(size_t)(qs * L + r) * a.n];
+                    vc_add<L, kTapsaPlanes>(S, x);
+                }
+#pragma unroll
+                for (int r = 0; r < L; ++r) ring[(size_t)(a.slot * L + r) * a.n] = p[r];
+                // byte-transpose S: B[k] byte j = S of trial 4k + j (the shifted
+                // copies of a 4-bit group never overlap, so the multiply is a spread)
+                uint32_t B[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    B[k] = 0;
+#pragma unroll
+                    for (int r = 0; r < kTapsaPlanes; ++r) {
+                        const uint32_t x4 = (S[r] >> (4 * k)) & 0xFu;
+                        B[k] |= (x4 * (0x00204081u << r)) & (0x01010101u << r);
+                    }
+                }
+                const uint32_t rb = (uint32_t)__cvta_generic_to_shared(sthr) + (uint32_t)d * 512u;
+                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
+                uint32_t word = 0, tie = 0xffffffffu;
+                const uint32_t ui = (uint32_t)i;
+#pragma unroll
+                for (int b = 31; b >= 0; --b) {
+                    const int k = b >> 2, j = b & 3;
+                    const uint32_t x = j == 0 ? (B[k] << 3) : (B[k] >> (8 * j - 3));
+                    const uint32_t addr = (x & 0x1F8u) | rb;
+                    uint2 t;
+                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "r"(addr));
+                    if (CACHED) {
+                        const uint2 v = __ldcs(ctile + b * 32);
+                        tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
+                    } else {
+                        const uint2 kc = key[b];
+                        uint32_t sl, sh;
+                        packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                        tie = min(tie, packed_second_decide(sl, sh, count, t, word));
+                    }
+                }
+                if (tie < 2) {  // rare near-tie: exact 64-bit test
+                    word = 0;
+                    for (int b = 0; b < 32; ++b) {
+                        int sb = 0;
+                        for (int r = 0; r < kTapsaPlanes; ++r) sb |= (int)((S[r] >> b) & 1u) << r;
+                        const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
+                        const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                        word |= (uint32_t)hash_ge_exact(x2, a.thr[d * 64 + sb]) << b;
+                    }
+                }
+                a.snew[(size_t)w * a.n + i] = word;
+                if (a.raw_out) {  // last cycle only: acc = sum of the filled raw fields
+                    for (int b = 0; b < 32; ++b) {
+                        int sb = 0;
+                        for (int r = 0; r < kTapsaPlanes; ++r) sb |= (int)((S[r] >> b) & 1u) << r;
+                        a.raw_out[(size_t)i * a.Tp + w * 32 + b] = (int16_t)(2 * sb - a.filled * d);
+                    }
+                }
+            } else if (UPDATE) {
                 const uint2 *tb = sthr + (a.dmax - d);   // entry for raw = 2 pop - d
                 // cache tile of (word w, chunk ch): [b][lane], so trial b of this
                 // lane sits at a compile-time offset b * 256 B
@@ -391,13 +474,37 @@ __global__ void unpack_spins(const uint32_t *__restrict__ s, int8_t *__restrict_
     out[g] = ((s[(size_t)(t >> 5) * n + i] >> (t & 31)) & 1u) ? 1 : -1;
 }
 
-// inputs[t][i] = i0_last * raw_last[i][t]  (pSA: inp = i0 * raw, _kernels.py:146)
+// inputs[t][i] = i0_last * (acc_last[i][t] / filled): the last drive of the
+// plain rule (filled = 1, acc = raw; _kernels.py:146) or the time-averaged
+// rule (_kernels.py:138); raw_last is the packed kernel's last-cycle output.
 __global__ void inputs_from_raw(const int16_t *__restrict__ raw, double *__restrict__ out,
-                                double i0_last, int n, int Tp, int T) {
+                                double i0_last, int n, int Tp, int T, double filled) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= (int64_t)n * T) return;
     const int t = (int)(g / n), i = (int)(g % n);
-    out[g] = __dmul_rn(i0_last, (double)raw[(size_t)i * Tp + t]);
+    out[g] = __dmul_rn(i0_last, __ddiv_rn((double)raw[(size_t)i * Tp + t], filled));
+}
+
+// TApSA history output [T][n][alpha] from the packed ring: slot q holds the
+// raw field 2p - d of the last cycle that wrote it (0.0 if never written).
+template <int L>
+__global__ void hist_from_ring(const uint32_t *__restrict__ ring, const uint32_t *__restrict__ rowptr,
+                               int n, int T, int alpha, int written, double *__restrict__ out) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)n * T) return;
+    const int t = (int)(g / n), i = (int)(g % n);
+    const int w = t >> 5, b = t & 31;
+    const int d = (int)(rowptr[i + 1] - rowptr[i]);
+    for (int q = 0; q < alpha; ++q) {
+        double v = 0.0;
+        if (q < written) {
+            int p = 0;
+            for (int r = 0; r < L; ++r)
+                p |= (int)((ring[((size_t)(w * alpha + q) * L + r) * n + i] >> b) & 1u) << r;
+            v = (double)(2 * p - d);
+        }
+        out[g * alpha + q] = v;
+    }
 }
 
 // ----------------------------------------------------------- general path

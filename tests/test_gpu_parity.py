@@ -193,3 +193,23 @@ def test_full_size_g81_properties_and_shard_invariance(bench_graphs, golden_benc
     for r in full[::256]:
         assert np.array_equal(r.energy_trace, W - 2.0 * r.cut_trace)
         assert r.best_cut == r.cut_trace.max()
+
+
+@pytest.mark.parametrize("name,alpha,cycles", [("G81", 4, 200), ("G55", 4, 120), ("G48", 7, 150)])
+def test_packed_tapsa_matches_oracle(oracle, bench_graphs, name, alpha, cycles):
+    """Time-averaged rule on the packed path (bit-sliced history ring)."""
+    g = bench_graphs(name)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, cycles, 10)
+    cfg = AlgorithmConfig(Algorithm.TAPSA, alpha=alpha)
+    keys = [streams.run_key(streams.trial_seed(3, k)) for k in range(5)]
+    b = _native.Batch(model, sch, keys, graph=g, algo_code=cfg.kind.code, alpha=cfg.kernel_alpha)
+    plan = _native.Plan(b)
+    assert plan.info()["path"] == "packed"
+    plan.run()
+    got = plan.download()
+    plan.close()
+    want = oracle.anneal_batch(model, sch, "tapsa", VariabilityProfile.ideal(model.n), keys, graph=g,
+                               alpha=alpha)
+    for k in ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
