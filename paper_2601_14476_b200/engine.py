@@ -24,6 +24,7 @@ from .annealer import (AlgorithmConfig, TrialResult, derive_schedule, profile_ro
                        results_from_batch)
 from .model import MaxCutGraph, maxcut_to_ising
 from .pbit import VariabilityConfig, sample_variability
+from .profiles import sample_profiles
 
 SWEEP_AXES = ("sigma_lambda", "sigma_delta", "sigma_nu")
 
@@ -83,8 +84,9 @@ def trial_profiles(spec: ExperimentSpec, n: int, seeds: Sequence[int]):
     if not spec.resample_variability:
         fixed = sample_variability(cfg, n, np.random.default_rng(streams.profile_seed(seeds[0])))
         return fixed
-    return [sample_variability(cfg, n, np.random.default_rng(streams.profile_seed(s)))
-            for s in seeds]
+    # stacked [trials][n] rows, sampled by parallel worker processes (profiles.py)
+    lam, delta, period = sample_profiles(cfg, n, seeds)
+    return (lam, delta, period, n)
 
 
 def run_trial_range(spec: ExperimentSpec, graph: MaxCutGraph, start: int, stop: int,
@@ -136,5 +138,42 @@ def sweep(spec: ExperimentSpec, axis: str, values: Sequence[float],
     for v in values:
         if v < 0:
             raise ValueError(f"sweep value must be >= 0, got {v}")
-    return [run_trials(replace(spec, variability=replace(spec.variability, **{axis: float(v)})),
-                       graphs, registry) for v in values]
+    try:
+        graph = graphs[spec.graph]
+    except KeyError:
+        raise KeyError(f"unknown graph {spec.graph!r}; have {sorted(graphs)}") from None
+    specs = [replace(spec, variability=replace(spec.variability, **{axis: float(v)}))
+             for v in values]
+    best_known = registry.get(spec.graph) if registry is not None else None
+    out: list[ExperimentSummary | None] = [None] * len(specs)
+    # Points with variability share the device path, so they run as ONE batch
+    # of len(points) * trials trials (same seeds per point, so the sweep stays
+    # paired exactly as in the reference).  The ideal point, if any, runs alone
+    # on the packed path.
+    grouped = [k for k, s in enumerate(specs)
+               if not s.variability.is_ideal and s.resample_variability]
+    for k, s in enumerate(specs):
+        if k not in grouped:
+            out[k] = run_trials(s, graphs, registry)
+    if len(grouped) == 1:
+        out[grouped[0]] = run_trials(specs[grouped[0]], graphs, registry)
+    elif grouped:
+        model = maxcut_to_ising(graph)
+        schedule = derive_schedule(model, spec.cycles, spec.variability.t_res)
+        seeds = streams.trial_seeds(spec.base_seed, spec.trials, 0)
+        t0 = time.perf_counter()
+        rows = [trial_profiles(specs[k], model.n, seeds) for k in grouped]
+        lam = np.concatenate([r[0] for r in rows])
+        delta = np.concatenate([r[1] for r in rows])
+        period = np.concatenate([r[2] for r in rows])
+        keys = np.tile(streams.run_keys(seeds), len(grouped))
+        batch = _native.Batch(model, schedule, keys, profile_rows=(lam, delta, period, model.n),
+                              graph=graph, algo_code=spec.algo.kind.code,
+                              alpha=spec.algo.kernel_alpha, p_stall=spec.algo.p_stall)
+        res, _ = _native.anneal_batch(batch, device=_native.default_device())
+        elapsed = (time.perf_counter() - t0) / len(grouped)
+        T = spec.trials
+        for j, k in enumerate(grouped):
+            part = {name: arr[j * T:(j + 1) * T] for name, arr in res.items()}
+            out[k] = summarize(results_from_batch(part, seeds, schedule, True), best_known, elapsed)
+    return out

@@ -195,6 +195,28 @@ def test_full_size_g81_properties_and_shard_invariance(bench_graphs, golden_benc
         assert r.best_cut == r.cut_trace.max()
 
 
+def test_batched_sweep_is_paired_with_single_runs():
+    # /root/reference/pkg/tests/test_engine.py:118-134: a sweep point equals the
+    # standalone run at that sigma; here all varied points share one device batch
+    g = random_graph(80, 14, p_edge=0.15)
+    graphs = {"toy": g}
+    spec = engine.ExperimentSpec(graph="toy", algo=AlgorithmConfig(Algorithm.TAPSA), cycles=80,
+                                 trials=6)
+    values = [0.0, 0.4, 0.7]
+    sums = engine.sweep(spec, "sigma_delta", values, graphs, registry={"toy": 100})
+    for v, s in zip(values, sums):
+        alone = engine.run_trials(engine.ExperimentSpec(
+            graph="toy", algo=AlgorithmConfig(Algorithm.TAPSA), cycles=80, trials=6,
+            variability=VariabilityConfig(sigma_delta=v)), graphs, registry={"toy": 100})
+        assert [r.final_cut for r in s.results] == [r.final_cut for r in alone.results]
+        for a, b in zip(s.results, alone.results):
+            assert np.array_equal(a.energy_trace, b.energy_trace)
+            assert np.array_equal(a.final_state.spins, b.final_state.spins)
+            assert np.array_equal(a.final_state.ti_history, b.final_state.ti_history)
+        assert s.mean_cut == alone.mean_cut and s.std_cut == alone.std_cut
+        assert s.normalized_mean_cut == alone.normalized_mean_cut
+
+
 @pytest.mark.parametrize("name,alpha,cycles", [("G81", 4, 200), ("G55", 4, 120), ("G48", 7, 150)])
 def test_packed_tapsa_matches_oracle(oracle, bench_graphs, name, alpha, cycles):
     """Time-averaged rule on the packed path (bit-sliced history ring)."""
