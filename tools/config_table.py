@@ -1,0 +1,147 @@
+"""Measure every BASELINE.json config (C1-C5) on the GPU next to the CPU
+reference port, and write profiles/<tag>_configs.{md,json}.
+
+    python tools/config_table.py [--tag r01] [--quick]
+
+GPU numbers: device time of one whole anneal (CUDA events, inputs resident,
+second of two runs).  CPU numbers: the oracle port (C restatement of
+_kernels.anneal_loop, all host threads) on a bounded sample of the same trials,
+scaled to updates/s.  Quality: mean final cut over the trials / the analog
+denominator (tests/golden/analogs.json) or the G-set registry.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+from oracle import oracle as orc  # noqa: E402  (CPU reference leg only)
+from paper_2601_14476_b200 import _native, benchmarks, streams  # noqa: E402
+from paper_2601_14476_b200.annealer import (Algorithm, AlgorithmConfig, derive_schedule,  # noqa: E402
+                                            profile_rows)
+from paper_2601_14476_b200.engine import ExperimentSpec, trial_profiles  # noqa: E402
+from paper_2601_14476_b200.model import maxcut_to_ising  # noqa: E402
+from paper_2601_14476_b200.pbit import VariabilityConfig, VariabilityProfile  # noqa: E402
+
+PEAK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+
+
+def bytes_per_update(g):
+    n, nnz = g.n, 2 * g.m
+    return nnz / n + 1 + (2.125 * nnz + 4 * (n + 1)) / (32 * n)
+
+
+def gpu_run(g, kind, sig, T, cycles=1000, alpha=4):
+    m = maxcut_to_ising(g)
+    sch = derive_schedule(m, cycles, 10)
+    spec = ExperimentSpec(graph="x", algo=AlgorithmConfig(kind, alpha=alpha),
+                          variability=VariabilityConfig(*sig), cycles=cycles, trials=T)
+    seeds = streams.trial_seeds(0, T)
+    t0 = time.perf_counter()
+    profs = trial_profiles(spec, m.n, seeds)
+    t_prof = time.perf_counter() - t0
+    b = _native.Batch(m, sch, streams.run_keys(seeds), profile_rows=profile_rows(profs, m.n), graph=g,
+                      algo_code=kind.code, alpha=spec.algo.kernel_alpha, p_stall=0.5)
+    plan = _native.Plan(b)
+    plan.run()
+    ms = plan.run()
+    cut_sum, best, ups = plan.summary()
+    info = plan.info()
+    plan.close()
+    return dict(ms=ms, updates=ups, upd_s=ups / ms * 1e3, path=info["path"], mean_cut=cut_sum / T,
+                best=best, profile_s=t_prof)
+
+
+def cpu_run(g, kind, sig, T_sample, cycles=1000, alpha=4):
+    m = maxcut_to_ising(g)
+    sch = derive_schedule(m, cycles, 10)
+    spec = ExperimentSpec(graph="x", algo=AlgorithmConfig(kind, alpha=alpha),
+                          variability=VariabilityConfig(*sig), cycles=cycles, trials=T_sample)
+    seeds = streams.trial_seeds(0, T_sample)
+    profs = trial_profiles(spec, m.n, seeds)
+    if profs is None:
+        plist = VariabilityProfile.ideal(m.n)
+    else:
+        lam, delta, period, _ = profs
+        plist = [VariabilityProfile(lam[k], delta[k], period[k], 10) for k in range(T_sample)]
+    threads = len(os.sched_getaffinity(0))
+    t0 = time.perf_counter()
+    out = orc.anneal_batch(m, sch, kind.value, plist, streams.run_keys(seeds), graph=g,
+                           alpha=spec.algo.kernel_alpha, p_stall=0.5, threads=threads)
+    dt = time.perf_counter() - t0
+    return dict(upd_s=float(out["counts"].sum()) / dt, seconds=dt, threads=threads, trials=T_sample,
+                mean_cut=float(out["cut_trace"][:, -1].mean()))
+
+
+def denom(name):
+    gold = json.loads((ROOT / "tests" / "golden" / "analogs.json").read_text())
+    return gold.get(name, {}).get("best_known_analog")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tag", default="r01")
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    orc.build()
+    threads = len(os.sched_getaffinity(0))
+    rows = []
+
+    def add(cfg, name, kind, sig, T, cpu_T, note=""):
+        g, _ = benchmarks.load(name)
+        gpu = gpu_run(g, kind, sig, T)
+        cpu = cpu_run(g, kind, sig, cpu_T) if cpu_T else None
+        d = denom(name)
+        B = bytes_per_update(g)
+        row = dict(config=cfg, graph=name, n=g.n, m=g.m, algo=kind.value, sigma=list(sig), trials=T,
+                   path=gpu["path"], gpu_ms=gpu["ms"], gpu_upd_s=gpu["upd_s"],
+                   roofline_frac=gpu["upd_s"] * B / (PEAK * 1e9), bytes_per_update=B,
+                   cpu_upd_s=cpu["upd_s"] if cpu else None, cpu_threads=threads,
+                   cpu_sample_trials=cpu_T, speedup=(gpu["upd_s"] / cpu["upd_s"]) if cpu else None,
+                   mean_cut=gpu["mean_cut"], normalized=(gpu["mean_cut"] / d) if d else None,
+                   profile_sampling_s=gpu["profile_s"], note=note)
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+
+    q = args.quick
+    add("C1", "G1", Algorithm.PSA, (0, 0, 0), 100, 16 if q else 100)
+    for axis in range(3):
+        for v in ((0.5,) if q else (0.5, 1.0)):
+            sig = [0.0, 0.0, 0.0]
+            sig[axis] = v
+            add("C2", "G1", Algorithm.PSA, tuple(sig), 1024, 16)
+    add("C2", "G1", Algorithm.PSA, (0, 0, 0), 1024, 0, "sigma = 0 reference point")
+    add("C3", "G22", Algorithm.PSA, (0.5, 0.5, 0.5), 4096, 16)
+    add("C3", "G55", Algorithm.PSA, (0.5, 0.5, 0.5), 4096, 16)
+    add("C4", "G81", Algorithm.PSA, (0, 0, 0), 4096, 16)
+    add("C3'", "G1", Algorithm.TAPSA, (0, 0, 0), 1024, 16, "time-averaged rule (alpha=4)")
+    add("C3'", "G81", Algorithm.TAPSA, (0, 0, 0), 4096, 16, "time-averaged rule (alpha=4)")
+    add("C3'", "G1", Algorithm.SPSA, (0, 0, 0), 1024, 16, "stalled rule (p=0.5)")
+    for name in ([] if q else ["G1", "G47", "G22", "G48", "G55", "G60", "G67", "G77", "G81"]):
+        add("C5", name, Algorithm.PSA, (0, 0, 0), 1024, 8)
+
+    out = ROOT / "profiles" / f"{args.tag}_configs.json"
+    out.write_text(json.dumps(rows, indent=1))
+    lines = [f"# {args.tag}: BASELINE configs on one B200 vs the CPU reference port ({threads} threads)", "",
+             "| cfg | graph (n) | rule | sigma | trials | path | GPU ms/run | GPU upd/s | frac of HBM roofline | CPU upd/s | GPU/CPU | mean cut / best-known |",
+             "|---|---|---|---|---:|---|---:|---:|---:|---:|---:|---:|"]
+    for r in rows:
+        lines.append(
+            f"| {r['config']} | {r['graph']} ({r['n']}) | {r['algo']} | {tuple(r['sigma'])} | {r['trials']} | "
+            f"{r['path']} | {r['gpu_ms']:.1f} | {r['gpu_upd_s']:.3g} | {r['roofline_frac']:.3f} | "
+            f"{(r['cpu_upd_s'] or 0):.3g} | {(r['speedup'] or 0):.0f} | "
+            f"{(r['normalized'] if r['normalized'] is not None else float('nan')):.4f} |")
+    (ROOT / "profiles" / f"{args.tag}_configs.md").write_text("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    main()
