@@ -217,6 +217,12 @@ struct pbsa_plan {
     bool int_energy = true;
     bool tapsa_hist_from_raw = false;  // TAPSA alpha=1 routed to the packed path
     bool tapsa_packed = false;         // TAPSA alpha>=2 on the packed path (bit-sliced ring)
+    bool spsa_packed = false;          // SPSA p>0 on the packed path (per-p-bit drive index)
+    DevBuf<uint32_t> sidx, sthi;       // [W][32][n]
+    DevBuf<uint2> kfs;                 // [Tp] (F, C) of absorb(key, TAG_STALL) + GAMMA
+    DevBuf<uint64_t> kstg;             // [Tp] absorb(key, TAG_STALL) + GAMMA
+    DevBuf<double> i0_dev;             // [cycles]
+    uint64_t p_stall64 = 0;
     DevBuf<uint32_t> ring;             // [W][alpha][L][n]
     int64_t total_w = 0;
     std::vector<double> i0;
@@ -301,7 +307,8 @@ void set_packed_smem(K kernel, size_t bytes) {
 }
 
 using PackedKernel = void (*)(pbsa::PackedArgs);
-PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false) {
+PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false,
+                               bool spsa = false) {
 #define PBSA_CASE(l)                                                                  \
     case l:                                                                           \
         return update ? (cached ? pbsa::packed_sweep<l, true, true>                   \
@@ -311,6 +318,10 @@ PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = fal
     case l:                                                                           \
         return cached ? pbsa::packed_sweep<l, true, true, 1>                          \
                       : pbsa::packed_sweep<l, true, false, 1>;
+#define PBSA_SCASE(l)                                                                 \
+    case l:                                                                           \
+        return cached ? pbsa::packed_sweep<l, true, true, 2>                          \
+                      : pbsa::packed_sweep<l, true, false, 2>;
     if (update && tapsa) {
         switch (L) {
             PBSA_TCASE(1)
@@ -321,6 +332,19 @@ PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = fal
             default: fail(PBSA_EINVAL, "packed TApSA supports degree <= 31");
         }
     }
+    if (update && spsa) {
+        switch (L) {
+            PBSA_SCASE(1)
+            PBSA_SCASE(2)
+            PBSA_SCASE(3)
+            PBSA_SCASE(4)
+            PBSA_SCASE(5)
+            PBSA_SCASE(6)
+            PBSA_SCASE(7)
+            default: fail(PBSA_EINVAL, "packed SpSA supports degree <= 127");
+        }
+    }
+#undef PBSA_SCASE
     switch (L) {
         PBSA_CASE(1)
         PBSA_CASE(2)
@@ -550,9 +574,12 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     const bool small_counters = n <= (1LL << 30) && cycles * t_res <= (1LL << 30);
     // time-averaged rule on the packed path: sum of alpha counts must stay < 64
     const bool tapsa_packed = algo == 1 && alpha >= 2 && alpha * dmax <= 63 && dmax <= 31;
-    const bool packed = (rule_is_psa || tapsa_packed) && unit_J && zero_h && ideal &&
+    // stalled rule on the packed path: per-p-bit threshold index into all cycles' tables
+    const bool spsa_packed = algo == 2 && p_stall > 0.0 && cycles * (2 * dmax + 1) < (1LL << 31);
+    const bool packed = (rule_is_psa || tapsa_packed || spsa_packed) && unit_J && zero_h && ideal &&
                         graph_is_model && dmax <= 127 && small_counters;
     P.tapsa_packed = packed && tapsa_packed;
+    P.spsa_packed = packed && spsa_packed && !rule_is_psa;
     P.tapsa_hist_from_raw = packed && algo == 1 && !P.tapsa_packed;
     P.path = packed ? PBSA_PATH_PACKED : PBSA_PATH_GENERAL;
 
@@ -597,6 +624,24 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         }
         P.krg.upload(krg, st);
         P.kfc.upload(kfc, st);
+        if (P.spsa_packed) {
+            std::vector<uint64_t> kg(P.Tp);
+            std::vector<uint2> kf(P.Tp);
+            for (int64_t t = 0; t < P.Tp; ++t) {
+                kg[t] = kst[t] + kGamma;
+                const uint32_t lo = (uint32_t)kg[t], hi = (uint32_t)(kg[t] >> 32);
+                const uint32_t Y = hi ^ (hi >> 30);
+                kf[t] = make_uint2(lo ^ ((lo >> 30) | (hi << 2)), Y * 0x1CE4E5B9u);
+            }
+            P.kstg.upload(kg, st);
+            P.kfs.upload(kf, st);
+            // u = (H >> 11) 2^-53 < p  <=>  H < ceil(p 2^53) << 11   (p * 2^53 is exact)
+            const double ps = std::ceil(std::ldexp(p_stall, 53));
+            P.p_stall64 = ps >= 0x1p53 ? ~0ULL : ((uint64_t)ps << 11);
+            P.sidx.alloc((size_t)P.W * 32 * n);
+            P.sthi.alloc((size_t)P.W * 32 * n);
+            P.i0_dev.upload(P.i0, st);
+        }
         if (P.tapsa_packed) {
             // thresholds per (cycle, degree d, S): acc = 2 S - f d, f = min(c+1, alpha),
             // inp = i0 * (acc / f) exactly as _kernels.py:138 evaluates it
@@ -637,7 +682,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.use_cache = cache_entries * 8 <= (32ULL << 30);
         if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1';
         if (P.use_cache) P.acache.alloc(cache_entries);
-        PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed);
+        PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
         set_packed_smem(kern, smem);
         set_packed_smem(packed_kernel_for(P.L, false, false), smem);
@@ -818,7 +863,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                                                    (int)P.n, (int)P.W);
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
-        PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed);
+        PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
@@ -869,6 +914,16 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     a.chunks = P.chunks;
                     a.count = (uint32_t)(c * P.t_res);
                     a.do_update = c < P.cycles;
+                    if (P.spsa_packed) {
+                        a.sidx = P.sidx.p + (size_t)w0 * 32 * P.n;
+                        a.sthi = P.sthi.p + (size_t)w0 * 32 * P.n;
+                        a.kfs = P.kfs.p + w0 * 32;
+                        a.kst = P.kstg.p + w0 * 32;
+                        a.thr_all = P.thr.p;
+                        a.p_stall64 = P.p_stall64;
+                        a.cycle = (int)cc;
+                        a.Kc = P.K;
+                    }
                     if (P.tapsa_packed) {
                         a.ring = P.ring.p + (size_t)w0 * P.alpha * P.L * P.n;
                         a.alpha = (int)P.alpha;
@@ -1217,8 +1272,12 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
             const double f_last = P->tapsa_packed ? (double)std::min<int64_t>(C, P->alpha) : 1.0;
             if (inputs) {
                 dinputs.alloc((size_t)T * n);
-                pbsa::inputs_from_raw<<<grid_for(n * T, TB), TB, 0, st>>>(
-                    P->raw_last.p, dinputs.p, P->i0[C - 1], (int)n, (int)P->Tp, (int)T, f_last);
+                if (P->spsa_packed)
+                    pbsa::inputs_from_sidx<<<grid_for(n * T, TB), TB, 0, st>>>(
+                        P->sidx.p, P->i0_dev.p, dinputs.p, (int)n, (int)T, P->K, P->dmax);
+                else
+                    pbsa::inputs_from_raw<<<grid_for(n * T, TB), TB, 0, st>>>(
+                        P->raw_last.p, dinputs.p, P->i0[C - 1], (int)n, (int)P->Tp, (int)T, f_last);
             }
             if (hist && P->tapsa_hist_from_raw) {
                 // TAPSA with alpha = 1: the history holds the last raw field

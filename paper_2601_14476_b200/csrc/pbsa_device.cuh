@@ -133,6 +133,13 @@ struct PackedArgs {
     int chunks;               // ceil(n / 32)
     uint32_t count;           // global sub-step counter c * t_res (< 2^30)
     int do_update;            // 0: only accumulate pacc (final cut pass)
+    uint32_t *sidx;           // SpSA: [W][32][n] threshold-table index of each p-bit's drive
+    uint32_t *sthi;           // SpSA: [W][32][n] high word of that threshold
+    const uint2 *kfs;         // SpSA: [Tp] per-trial (F, C) of absorb(key, TAG_STALL)
+    const uint64_t *kst;      // SpSA: [Tp] absorb(key, TAG_STALL) + GAMMA (exact slow path)
+    const uint64_t *thr_all;  // SpSA: [cycles][K] all thresholds
+    uint64_t p_stall64;       // SpSA: stall iff H_stall < p_stall64 (~0: always)
+    int cycle, Kc;            // SpSA: this cycle, entries per cycle
     uint32_t *ring;           // TApSA: [W][alpha][L][n] bit-sliced neighbour counts
     int alpha, slot, filled;  // TApSA: ring length, this cycle's slot, min(c+1, alpha)
 };
@@ -233,6 +240,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     // trial's entry address is (p * 8) | row base, formed with one LOP3.
     // Larger degrees: entries indexed by raw + dmax.  TApSA: 64-entry rows by S.
     constexpr bool TAPSA = ALG == 1;
+    constexpr bool SPSA = ALG == 2;
     constexpr bool NIB = L <= 4 && !TAPSA;
     uint2 *sthr = reinterpret_cast<uint2 *>(
         (reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
@@ -371,6 +379,77 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         a.raw_out[(size_t)i * a.Tp + w * 32 + b] = (int16_t)(2 * sb - a.filled * d);
                     }
                 }
+            } else if (UPDATE && SPSA) {
+                // Stalled rule (_kernels.py:139-144): the drive is i0[c'] * raw' of the
+                // p-bit's last fresh update, so its threshold is thr_all[c' * K + raw' + dmax];
+                // sidx keeps that index per (trial, node).  A fresh draw refreshes it unless
+                // u = u01(key, TAG_STALL, i, count) < p_stall; the first update is always fresh.
+                uint32_t *sidx = a.sidx + (size_t)w * 32 * a.n + i;
+                const int base = a.cycle * a.Kc + a.dmax - d;      // fresh index = base + 2 pop
+                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
+                const uint32_t ui = (uint32_t)i;
+                // pass 1: stall bits of the 32 trials (exactly, before any index is replaced)
+                uint32_t stallw = 0;
+                if (a.cycle > 0) {
+                    const uint2 pst = make_uint2(~(uint32_t)(a.p_stall64 >> 32),
+                                                 (uint32_t)(a.p_stall64 >> 32));
+                    uint32_t gew = 0, ties = 0xffffffffu;
+#pragma unroll 4
+                    for (int b = 31; b >= 0; --b) {
+                        const uint2 ks = a.kfs[(size_t)w * 32 + b];
+                        uint32_t sl, sh;
+                        packed_first_absorb(ks.x ^ ui, ks.y, sl, sh);
+                        ties = min(ties, packed_second_decide(sl, sh, count, pst, gew));
+                    }
+                    stallw = ~gew;  // H_stall < p_stall64 -> stall
+                    if (ties < 2) {
+                        stallw = 0;
+                        for (int b = 0; b < 32; ++b) {
+                            const uint64_t xs = (a.kst[(size_t)w * 32 + b]) ^ (uint64_t)ui;
+                            const uint64_t xs2 = (mix64(xs) + PB_GAMMA) ^ (uint64_t)count;
+                            stallw |= (uint32_t)!hash_ge_exact(xs2, a.p_stall64) << b;
+                        }
+                    }
+                }
+                // pass 2: drive (stalled: the stored threshold word, an independent
+                // coalesced load; fresh: this cycle's shared-memory table, stored
+                // together with its index), then the activation decision
+                uint32_t *sthi = a.sthi + (size_t)w * 32 * a.n + i;
+                uint32_t word = 0, tie = 0xffffffffu;
+#pragma unroll 8
+                for (int b = 31; b >= 0; --b) {
+                    int pop = 0;
+#pragma unroll
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                    uint2 t;
+                    if ((stallw >> b) & 1u) {
+                        const uint32_t thi = sthi[(size_t)b * a.n];
+                        t = make_uint2(~thi, thi);
+                    } else {
+                        t = NIB ? sthr[d * 16 + pop] : sthr[2 * pop - d + a.dmax];
+                        sidx[(size_t)b * a.n] = (uint32_t)(base + 2 * pop);
+                        sthi[(size_t)b * a.n] = t.y;
+                    }
+                    if (CACHED) {
+                        const uint2 v = __ldcs(ctile + b * 32);
+                        tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
+                    } else {
+                        const uint2 kc = key[b];
+                        uint32_t sl, sh;
+                        packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                        tie = min(tie, packed_second_decide(sl, sh, count, t, word));
+                    }
+                }
+                if (tie < 2) {  // rare near-tie in an activation draw: exact 64-bit test
+                    word = 0;
+                    for (int b = 0; b < 32; ++b) {
+                        const uint32_t idx = sidx[(size_t)b * a.n];
+                        const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
+                        const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                        word |= (uint32_t)hash_ge_exact(x2, a.thr_all[idx]) << b;
+                    }
+                }
+                a.snew[(size_t)w * a.n + i] = word;
             } else if (UPDATE) {
                 const uint2 *tb = sthr + (a.dmax - d);   // entry for raw = 2 pop - d
                 // cache tile of (word w, chunk ch): [b][lane], so trial b of this
@@ -483,6 +562,18 @@ __global__ void inputs_from_raw(const int16_t *__restrict__ raw, double *__restr
     if (g >= (int64_t)n * T) return;
     const int t = (int)(g / n), i = (int)(g % n);
     out[g] = __dmul_rn(i0_last, __ddiv_rn((double)raw[(size_t)i * Tp + t], filled));
+}
+
+// SpSA last drive inputs[t][i] = i0[c'] * raw' from the packed drive index
+// c' * K + raw' + dmax (_kernels.py:144, 147).
+__global__ void inputs_from_sidx(const uint32_t *__restrict__ sidx, const double *__restrict__ i0,
+                                 double *__restrict__ out, int n, int T, int K, int dmax) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= (int64_t)n * T) return;
+    const int t = (int)(g / n), i = (int)(g % n);
+    const uint32_t idx = sidx[(size_t)t * n + i];  // [W][32][n] == [trial][n]
+    const int c = (int)(idx / (uint32_t)K), raw = (int)(idx % (uint32_t)K) - dmax;
+    out[g] = __dmul_rn(i0[c], (double)raw);
 }
 
 // TApSA history output [T][n][alpha] from the packed ring: slot q holds the

@@ -217,6 +217,27 @@ def test_batched_sweep_is_paired_with_single_runs():
         assert s.normalized_mean_cut == alone.normalized_mean_cut
 
 
+@pytest.mark.parametrize("name,p_stall,cycles", [("G81", 0.5, 150), ("G55", 0.3, 120),
+                                                  ("G48", 1.0, 60), ("G22", 0.7, 80)])
+def test_packed_spsa_matches_oracle(oracle, bench_graphs, name, p_stall, cycles):
+    """Stalled rule on the packed path (per-p-bit drive index, two hashes per update)."""
+    g = bench_graphs(name)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, cycles, 10)
+    cfg = AlgorithmConfig(Algorithm.SPSA, p_stall=p_stall)
+    keys = [streams.run_key(streams.trial_seed(5, k)) for k in range(5)]
+    b = _native.Batch(model, sch, keys, graph=g, algo_code=cfg.kind.code, alpha=1, p_stall=p_stall)
+    plan = _native.Plan(b)
+    assert plan.info()["path"] == "packed"
+    plan.run()
+    got = plan.download()
+    plan.close()
+    want = oracle.anneal_batch(model, sch, "spsa", VariabilityProfile.ideal(model.n), keys, graph=g,
+                               alpha=1, p_stall=p_stall)
+    for k in ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
+
+
 @pytest.mark.parametrize("name,alpha,cycles", [("G81", 4, 200), ("G55", 4, 120), ("G48", 7, 150)])
 def test_packed_tapsa_matches_oracle(oracle, bench_graphs, name, alpha, cycles):
     """Time-averaged rule on the packed path (bit-sliced history ring)."""
