@@ -701,7 +701,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         wpw = std::max<int64_t>(wpw, std::min<int64_t>((P.chunks + max_tasks - 1) / max_tasks, P.chunks));
         P.warps_per_word = (int)wpw;
         // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
-        int chains = 16;
+        // small batches need many chains to hide launch gaps; large ones only a
+        // couple (fewer graph nodes to instantiate)
+        int chains = (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.W));
         if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
         chains = (int)std::min<int64_t>(chains, P.W);
         if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
@@ -1296,16 +1298,17 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                     default: launch_hist_from_ring<5>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
                 }
             }
-            // host-side constant outputs overlap the device work above
-            if (hist && !P->tapsa_hist_from_raw && !P->tapsa_packed)
-                parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
-            if (counts) parallel_fill(counts, (size_t)(T * n), (int64_t)C);  // every p-bit fires once per cycle
+            // copies first (asynchronous into page-locked buffers), then the
+            // host-side constant outputs while the DMA and kernels run
             if (spins) CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
             if (inputs)
                 CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
             if (hist && (P->tapsa_hist_from_raw || P->tapsa_packed))
                 CK(cudaMemcpyAsync(hist, dhist.p, T * n * (P->tapsa_packed ? P->alpha : 1) * sizeof(double),
                                    cudaMemcpyDeviceToHost, st));
+            if (hist && !P->tapsa_hist_from_raw && !P->tapsa_packed)
+                parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
+            if (counts) parallel_fill(counts, (size_t)(T * n), (int64_t)C);  // every p-bit fires once per cycle
             CK(cudaStreamSynchronize(st));
         } else {
             dim3 tb(32, 8);
