@@ -237,6 +237,7 @@ struct pbsa_plan {
     DevBuf<uint64_t> thr, krg;
     DevBuf<uint2> kfc, acache;
     bool use_cache = false;
+    bool use_pdl = true;  // PBSA_PDL=0 disables programmatic dependent launch
     int64_t phase_words = 1;
     DevBuf<unsigned long long> pacc;  // [(C+1)][Tp]
     DevBuf<int16_t> raw_last;         // [n][Tp]
@@ -677,6 +678,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // phase width in words (PBSA_PACKED_PHASE_WORDS overrides; 0 = all)
         P.phase_words = 0;
         if (const char *env = std::getenv("PBSA_PACKED_PHASE_WORDS")) P.phase_words = std::atoi(env);
+        if (const char *env = std::getenv("PBSA_PDL")) P.use_pdl = env[0] != '0';
         if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;
         const size_t cache_entries = (size_t)P.phase_words * ((n + 31) / 32) * 1024;
         P.use_cache = cache_entries * 8 <= (32ULL << 30);
@@ -703,7 +705,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
         // small batches need many chains to hide launch gaps; large ones only a
         // couple (fewer graph nodes to instantiate)
-        int chains = (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.W));
+        int chains = (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
         if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
         chains = (int)std::min<int64_t>(chains, P.W);
         if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
@@ -932,7 +934,21 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                         a.slot = (int)(cc % P.alpha);
                         a.filled = (int)std::min<int64_t>(cc + 1, P.alpha);
                     }
-                    (c < P.cycles ? kern_up : kern_cut)<<<blocks, pbsa::kPackedThreads, smem, cs>>>(a);
+                    {
+                        // programmatic dependent launch: the next sub-step's prologue
+                        // overlaps this one's tail (the kernel waits on griddepcontrol)
+                        cudaLaunchConfig_t cfg{};
+                        cfg.gridDim = dim3((unsigned)blocks);
+                        cfg.blockDim = dim3(pbsa::kPackedThreads);
+                        cfg.dynamicSmemBytes = smem;
+                        cfg.stream = cs;
+                        cudaLaunchAttribute attr[1];
+                        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                        attr[0].val.programmaticStreamSerializationAllowed = P.use_pdl ? 1 : 0;
+                        cfg.attrs = attr;
+                        cfg.numAttrs = 1;
+                        CK(cudaLaunchKernelEx(&cfg, c < P.cycles ? kern_up : kern_cut, a));
+                    }
                     CK(cudaGetLastError());
                     ++P.launches;
                     if (c < P.cycles) {

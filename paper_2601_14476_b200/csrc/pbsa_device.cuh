@@ -234,6 +234,7 @@ constexpr int kTapsaPlanes = 6;
 
 template <int L, bool UPDATE, bool CACHED, int ALG = 0>
 __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed_sweep(PackedArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;");
     extern __shared__ unsigned long long smem_u64[];
     // Threshold table, 128 B aligned.  L <= 4 (degree <= 15): one 16-entry row
     // per degree d indexed by the neighbour count p (raw = 2p - d), so a
@@ -274,6 +275,10 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     uint32_t *scount = reinterpret_cast<uint32_t *>(skey + kPackedWarps * 32);
     if (threadIdx.x == 0) scount[0] = a.count;
     __syncthreads();
+    // Programmatic dependent launch: everything above reads only host-written
+    // constants, so it overlaps the previous sub-step's tail; the spin state
+    // of that sub-step is read only after its grid has completed.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // read back through shared memory so the counter lives in a vector
     // register (a kernel-parameter operand is re-fetched with LDCU per trial)
     const uint32_t count = scount[0];
