@@ -1,0 +1,41 @@
+"""bench.py contract pieces that run without a GPU: the reference arm (the
+CPU port on the host cores) prints one well-formed JSON line, and the
+roofline arithmetic follows SURVEY.md 8(d)."""
+
+from __future__ import annotations
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_reference_arm_prints_one_json_line(oracle):
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
+         "--warmup", "0", "--cycles", "50", "--cpu-sample-trials", "2"],
+        capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference"
+    assert d["unit"] == "updates/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "port"
+    assert d["e2e"] == {"value": d["value"], "unit": "updates/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["config"]["graph"] == "G81" and d["config"]["trials"] == 4096
+
+
+def test_algorithmic_bytes_per_update_matches_survey():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_2601_14476_b200 import benchmarks
+    # G1 52.25, G22 22.44, G55 6.46, G81 5.39 bytes/update
+    for name, want in (("G1", 52.25), ("G22", 22.44), ("G55", 6.46), ("G81", 5.39)):
+        g = benchmarks.load(name)[0]
+        assert bench.algorithmic_bytes_per_update(g) == pytest.approx(want, abs=0.01)
