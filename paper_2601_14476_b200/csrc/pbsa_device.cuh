@@ -298,24 +298,36 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             if (i >= a.n) continue;
             const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
             const uint32_t own = __ldg(sw + i);
-            // bit-sliced counts: p = #{J_ik s_k = +1} (local field), g = #{J_ik s_i s_k = +1} (cut)
-            uint32_t p[L], g[L];
+            // bit-sliced count p = #{J_ik s_k = +1} (local field) over the d neighbours
+            uint32_t p[L];
 #pragma unroll
-            for (int r = 0; r < L; ++r) p[r] = g[r] = 0;
+            for (int r = 0; r < L; ++r) p[r] = 0;
             for (uint32_t k = beg; k < end; ++k) {
                 const uint32_t e = __ldg(a.adj + k);
                 uint32_t cp = __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
-                uint32_t cg = ~(cp ^ own);
 #pragma unroll
                 for (int r = 0; r < L; ++r) {
-                    const uint32_t np = p[r] & cp, ng = g[r] & cg;
+                    const uint32_t np = p[r] & cp;
                     p[r] ^= cp;
-                    g[r] ^= cg;
                     cp = np;
-                    cg = ng;
                 }
             }
             const int d = (int)(end - beg);
+            // cut count g = #{J_ik s_i s_k = +1} = (s_i = +1) ? p : d - p, bit-sliced:
+            // d - p = ~p + (d + 1) mod 2^L (p <= d < 2^L), then a per-trial select
+            uint32_t g[L];
+            {
+                const uint32_t dp1 = (uint32_t)(d + 1);
+                uint32_t carry = 0;
+#pragma unroll
+                for (int r = 0; r < L; ++r) {
+                    const uint32_t m = 0u - ((dp1 >> r) & 1u);
+                    const uint32_t x = ~p[r];
+                    const uint32_t sum = x ^ m ^ carry;
+                    carry = (x & m) | (carry & (x ^ m));
+                    g[r] = (p[r] & own) | (sum & ~own);
+                }
+            }
             dsum += d;
             vc_add<L, kCutPlanes>(C, g);
             if (UPDATE && TAPSA) {
