@@ -29,6 +29,10 @@
 namespace {
 
 thread_local std::string g_last_error;
+// set while pbsa_anneal_loop_batch builds its single-use plan: such plans skip
+// word phasing, whose graph (phases x chains x cycles nodes) costs more to
+// instantiate than a single run saves
+thread_local bool g_oneshot = false;
 
 struct Error : std::runtime_error {
     int code;
@@ -676,7 +680,11 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // cache the sub-step-independent first absorb of every (trial, node)
         // draw when it fits the budget (PBSA_PACKED_CACHE=0/1 overrides)
         // phase width in words (PBSA_PACKED_PHASE_WORDS overrides; 0 = all)
-        P.phase_words = 0;
+        // Large batches run in word phases of 13 words (416 trials): each phase's
+        // cache (~67 MB for G81) stays L2-resident across its cycles, which keeps
+        // HBM (and the 1 kW power cap) out of the loop; 13 words x ~315 warps
+        // per word fill one wave with ~2 tasks per warp.  Small batches: one phase.
+        P.phase_words = (P.W > 16 && !g_oneshot) ? 13 : 0;
         if (const char *env = std::getenv("PBSA_PACKED_PHASE_WORDS")) P.phase_words = std::atoi(env);
         if (const char *env = std::getenv("PBSA_PDL")) P.use_pdl = env[0] != '0';
         if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;
@@ -1434,9 +1442,11 @@ int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const i
                            double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
                            float *device_ms) {
     pbsa_plan *P = nullptr;
+    g_oneshot = true;
     int rc = pbsa_plan_create(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm,
                               ge_i, ge_j, ge_w, lam, delta, period, profile_stride, i0_min, beta,
                               cycles, t_res, algo, alpha, p_stall, trials, keys, &P);
+    g_oneshot = false;
     if (rc != PBSA_OK) return rc;
     rc = pbsa_plan_run(P, device_ms);
     if (rc == PBSA_OK)
