@@ -185,6 +185,25 @@ void parallel_fill(T *dst, size_t count, T value) {
     for (auto &t : pool) t.join();
 }
 
+// Run f(lo, hi) over [0, count) split across host threads (large layouts only).
+template <typename F>
+void parallel_for(int64_t count, int64_t min_per_thread, F &&f) {
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    nt = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nt, count / std::max<int64_t>(1, min_per_thread)));
+    if (nt == 1) {
+        f((int64_t)0, count);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const int64_t per = (count + nt - 1) / nt;
+    for (unsigned k = 0; k < nt; ++k) {
+        const int64_t lo = k * per, hi = std::min(count, lo + per);
+        if (lo >= hi) break;
+        pool.emplace_back([&f, lo, hi] { f(lo, hi); });
+    }
+    for (auto &t : pool) t.join();
+}
+
 int64_t grid_for(int64_t work, int threads) { return (work + threads - 1) / threads; }
 
 }  // namespace
@@ -245,6 +264,26 @@ struct pbsa_plan {
     int64_t phase_words = 1;
     DevBuf<unsigned long long> pacc;  // [(C+1)][Tp]
     DevBuf<int16_t> raw_last;         // [n][Tp]
+    // packed VAR mode: per-p-bit variability profile under the plain rule
+    bool var_mode = false, var_uniform = true;
+    DevBuf<float2> prof;               // [Tp][n] {fl32(lam), fl32(lam * delta)}
+    DevBuf<double> lam64, del64;       // [Tp][n]
+    DevBuf<double> inp_var;            // [Tp][n] last i0 * raw of every p-bit
+    DevBuf<uint32_t> pplanes;          // [W][nplanes][n]
+    DevBuf<uint8_t> vdivs;             // divisor lists of all sub-steps
+    int nplanes = 0;
+    int64_t pmax = 0;
+    float var_margin = 1.0f;
+    std::vector<uint8_t> pcl;          // [T][n] clamped periods (timing spread only)
+    // packed launch sequence (one entry per sweep launch, the last one cut-only)
+    struct PLaunch {
+        uint32_t count;
+        int64_t cycle;
+        int do_cut, ndiv;
+        int64_t div_off;
+        bool update, inp;
+    };
+    std::vector<PLaunch> plaunch;
 
     // general path
     DevBuf<int8_t> g_spins[2];
@@ -313,7 +352,19 @@ void set_packed_smem(K kernel, size_t bytes) {
 
 using PackedKernel = void (*)(pbsa::PackedArgs);
 PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false,
-                               bool spsa = false) {
+                               bool spsa = false, bool var = false) {
+    if (update && var) {
+        switch (L) {
+            case 1: return pbsa::packed_sweep<1, true, false, 3>;
+            case 2: return pbsa::packed_sweep<2, true, false, 3>;
+            case 3: return pbsa::packed_sweep<3, true, false, 3>;
+            case 4: return pbsa::packed_sweep<4, true, false, 3>;
+            case 5: return pbsa::packed_sweep<5, true, false, 3>;
+            case 6: return pbsa::packed_sweep<6, true, false, 3>;
+            case 7: return pbsa::packed_sweep<7, true, false, 3>;
+            default: fail(PBSA_EINVAL, "packed variability path supports degree <= 127");
+        }
+    }
 #define PBSA_CASE(l)                                                                  \
     case l:                                                                           \
         return update ? (cached ? pbsa::packed_sweep<l, true, true>                   \
@@ -581,8 +632,27 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     const bool tapsa_packed = algo == 1 && alpha >= 2 && alpha * dmax <= 63 && dmax <= 31;
     // stalled rule on the packed path: per-p-bit threshold index into all cycles' tables
     const bool spsa_packed = algo == 2 && p_stall > 0.0 && cycles * (2 * dmax + 1) < (1LL << 31);
-    const bool packed = (rule_is_psa || tapsa_packed || spsa_packed) && unit_J && zero_h && ideal &&
-                        graph_is_model && dmax <= 127 && small_counters;
+    // variability profile on the packed path: plain rule, finite lam/delta,
+    // clamped periods below 256 (bit-sliced in at most 8 planes)
+    const int64_t maxcount = cycles * t_res;
+    bool var_ok = lam && !ideal && (algo == 0 || (algo == 2 && p_stall == 0.0));
+    if (const char *env = std::getenv("PBSA_PACKED_VAR")) var_ok = var_ok && env[0] != '0';
+    int64_t pmax = 0;
+    bool var_uniform = true;
+    if (var_ok) {
+        for (int64_t k = 0; k < prow * n && var_ok; ++k) {
+            var_ok = std::isfinite(lam[k]) && std::isfinite(delta[k]);
+            const int64_t pc = std::min<int64_t>(period[k], maxcount);
+            pmax = std::max(pmax, pc);
+            var_uniform = var_uniform && period[k] == t_res;
+        }
+        var_ok = var_ok && pmax < 256;
+    }
+    const bool packed = (((rule_is_psa || tapsa_packed || spsa_packed) && ideal) || var_ok) && unit_J &&
+                        zero_h && graph_is_model && dmax <= 127 && small_counters;
+    P.var_mode = packed && var_ok;
+    P.var_uniform = var_uniform;
+    P.pmax = pmax;
     P.tapsa_packed = packed && tapsa_packed;
     P.spsa_packed = packed && spsa_packed && !rule_is_psa;
     P.tapsa_hist_from_raw = packed && algo == 1 && !P.tapsa_packed;
@@ -674,7 +744,77 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         }
         for (auto &b : P.p_spins) b.alloc((size_t)P.W * n);
         P.pacc.alloc((size_t)(cycles + 1) * P.Tp);
-        P.raw_last.alloc((size_t)n * P.Tp);
+        if (!P.var_mode) P.raw_last.alloc((size_t)n * P.Tp);
+
+        // launch sequence: one sweep per cycle (counter c * t_res) ...
+        std::vector<uint8_t> divs;
+        if (!P.var_mode || P.var_uniform) {
+            for (int64_t c = 0; c < cycles; ++c)
+                P.plaunch.push_back({(uint32_t)(c * t_res), c, 1, 0, 0, true,
+                                     c == cycles - 1});
+        }
+        if (P.var_mode) {
+            // per-p-bit profile, trial-major [Tp][n] (padding trials: ideal)
+            const int64_t Tp = P.Tp;
+            std::vector<float2> pf((size_t)Tp * n, make_float2(1.0f, 0.0f));
+            std::vector<double> l64((size_t)Tp * n, 1.0), d64((size_t)Tp * n, 0.0);
+            parallel_for(trials, 16, [&](int64_t t0, int64_t t1) {
+                for (int64_t t = t0; t < t1; ++t)
+                    for (int64_t i = 0; i < n; ++i) {
+                        const size_t src = (size_t)(pstride ? t * n : 0) + i, dst = (size_t)t * n + i;
+                        l64[dst] = lam[src];
+                        d64[dst] = delta[src];
+                        pf[dst] = make_float2((float)lam[src], (float)(lam[src] * delta[src]));
+                    }
+            });
+            P.prof.upload(pf, st);
+            P.lam64.upload(l64, st);
+            P.del64.upload(d64, st);
+            P.inp_var.alloc((size_t)Tp * n);
+            if (const char *env = std::getenv("PBSA_VAR_MARGIN")) P.var_margin = (float)std::atof(env);
+            if (!P.var_uniform) {
+                // clamped periods (a period >= cycles * t_res fires only at count 0),
+                // bit-sliced per word: plane k bit b = bit k of trial 32w+b's period
+                P.nplanes = 1;
+                while ((1LL << P.nplanes) <= P.pmax) ++P.nplanes;
+                P.pcl.assign((size_t)trials * n, 0);
+                std::vector<uint32_t> planes((size_t)P.W * P.nplanes * n, 0u);
+                parallel_for(P.W, 1, [&](int64_t w0, int64_t w1) {
+                    for (int64_t w = w0; w < w1; ++w)
+                        for (int b = 0; b < 32; ++b) {
+                            const int64_t t = w * 32 + b;
+                            for (int64_t i = 0; i < n; ++i) {
+                                int64_t pc = t_res;
+                                if (t < trials) {
+                                    pc = std::min<int64_t>(period[(pstride ? t * n : 0) + i], maxcount);
+                                    P.pcl[(size_t)t * n + i] = (uint8_t)pc;
+                                }
+                                for (int k = 0; k < P.nplanes; ++k)
+                                    planes[((size_t)w * P.nplanes + k) * n + i] |= (uint32_t)((pc >> k) & 1) << b;
+                            }
+                        }
+                });
+                P.pplanes.upload(planes, st);
+                std::vector<char> present(256, 0);
+                for (uint8_t pc : P.pcl) present[pc] = 1;  // (padding trials never matter)
+                // ... or, with a timing spread, every sub-step some present period
+                // divides (the first sub-step of each cycle always runs: it takes the cut)
+                for (int64_t c = 0; c < cycles; ++c)
+                    for (int64_t s = 0; s < t_res; ++s) {
+                        const int64_t count = c * t_res + s;
+                        const int64_t off = (int64_t)divs.size();
+                        for (int64_t pc = 1; pc <= P.pmax; ++pc)
+                            if (present[pc] && count % pc == 0) divs.push_back((uint8_t)pc);
+                        const int nd = (int)((int64_t)divs.size() - off);
+                        if (s == 0 || nd > 0)
+                            P.plaunch.push_back({(uint32_t)count, c, s == 0, nd, off, true,
+                                                 count >= maxcount - P.pmax});
+                    }
+                if (divs.empty()) divs.push_back(0);
+                P.vdivs.upload(divs, st);
+            }
+        }
+        P.plaunch.push_back({(uint32_t)(cycles * t_res), cycles, 1, 0, 0, false, false});
 
         // launch shape: one wave of resident warps, each owning one word
         // cache the sub-step-independent first absorb of every (trial, node)
@@ -684,15 +824,18 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // cache (~67 MB for G81) stays L2-resident across its cycles, which keeps
         // HBM (and the 1 kW power cap) out of the loop; 13 words x ~315 warps
         // per word fill one wave with ~2 tasks per warp.  Small batches: one phase.
-        P.phase_words = (P.W > 16 && !g_oneshot) ? 13 : 0;
+        // A timing spread multiplies the launches by t_res: one phase, one chain.
+        const bool many_launches = P.var_mode && !P.var_uniform;
+        P.phase_words = (P.W > 16 && !g_oneshot && !many_launches) ? 13 : 0;
         if (const char *env = std::getenv("PBSA_PACKED_PHASE_WORDS")) P.phase_words = std::atoi(env);
         if (const char *env = std::getenv("PBSA_PDL")) P.use_pdl = env[0] != '0';
         if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;
         const size_t cache_entries = (size_t)P.phase_words * ((n + 31) / 32) * 1024;
-        P.use_cache = cache_entries * 8 <= (32ULL << 30);
-        if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1';
+        P.use_cache = cache_entries * 8 <= (32ULL << 30) && !P.var_mode;
+        if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1' && !P.var_mode;
         if (P.use_cache) P.acache.alloc(cache_entries);
-        PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed);
+        PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
+                                              P.var_mode);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
         set_packed_smem(kern, smem);
         set_packed_smem(packed_kernel_for(P.L, false, false), smem);
@@ -713,7 +856,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
         // small batches need many chains to hide launch gaps; large ones only a
         // couple (fewer graph nodes to instantiate)
-        int chains = (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
+        int chains = many_launches ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
         if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
         chains = (int)std::min<int64_t>(chains, P.W);
         if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
@@ -727,6 +870,11 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         }
         P.packed_blocks = (int)grid_for(P.W * wpw, pbsa::kPackedWarps);
         P.updates_per_run = (int64_t)n * trials * cycles;
+        if (many_launches) {  // sum over p-bits of #{count < cycles t_res : period | count}
+            int64_t ups = 0;
+            for (uint8_t pc : P.pcl) ups += (maxcount + pc - 1) / pc;
+            P.updates_per_run = ups;
+        }
     } else {
         // --------------------------------------------------- general setup
         std::vector<uint32_t> colv(nnz);
@@ -875,7 +1023,8 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                                                    (int)P.n, (int)P.W);
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
-        PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed);
+        PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
+                                                 P.var_mode);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
@@ -904,7 +1053,8 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                 cudaStream_t cs = g == 0 ? st : P.chain_streams[g - 1];
                 const int blocks = (int)grid_for((w1 - w0) * P.warps_per_word, pbsa::kPackedWarps);
                 cur = 0;
-                for (int64_t c = 0; c <= P.cycles; ++c) {
+                for (const pbsa_plan::PLaunch &pl : P.plaunch) {
+                    const int64_t c = pl.cycle;
                     pbsa::PackedArgs a{};
                     a.sold = P.p_spins[cur].p + w0 * P.n;
                     a.snew = P.p_spins[cur ^ 1].p + w0 * P.n;
@@ -916,7 +1066,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
                     a.thr = P.thr.p + (size_t)cc * P.K;
                     a.pacc = P.pacc.p + (size_t)c * P.Tp + w0 * 32;
-                    a.raw_out = (c == P.cycles - 1) ? P.raw_last.p + w0 * 32 : nullptr;
+                    a.raw_out = (c == P.cycles - 1 && !P.var_mode) ? P.raw_last.p + w0 * 32 : nullptr;
                     a.n = (int)P.n;
                     a.W = (int)(w1 - w0);
                     a.Tp = (int)P.Tp;
@@ -924,8 +1074,23 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     a.dmax = P.dmax;
                     a.warps_per_word = P.warps_per_word;
                     a.chunks = P.chunks;
-                    a.count = (uint32_t)(c * P.t_res);
-                    a.do_update = c < P.cycles;
+                    a.count = pl.count;
+                    a.do_update = pl.update;
+                    a.do_cut = pl.do_cut;
+                    if (P.var_mode) {
+                        const size_t off = (size_t)w0 * 32 * P.n;
+                        a.prof = P.prof.p + off;
+                        a.lam64 = P.lam64.p + off;
+                        a.del64 = P.del64.p + off;
+                        a.pplanes = P.var_uniform ? nullptr : P.pplanes.p + (size_t)w0 * P.nplanes * P.n;
+                        a.divs = P.var_uniform ? nullptr : P.vdivs.p + pl.div_off;
+                        a.ndiv = pl.ndiv;
+                        a.nplanes = P.nplanes;
+                        a.i0 = P.i0[cc];
+                        a.i0f = (float)P.i0[cc];
+                        a.margin = P.var_margin;
+                        a.inp_out = pl.inp ? P.inp_var.p + off : nullptr;
+                    }
                     if (P.spsa_packed) {
                         a.sidx = P.sidx.p + (size_t)w0 * 32 * P.n;
                         a.sthi = P.sthi.p + (size_t)w0 * 32 * P.n;
@@ -955,11 +1120,11 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                         attr[0].val.programmaticStreamSerializationAllowed = P.use_pdl ? 1 : 0;
                         cfg.attrs = attr;
                         cfg.numAttrs = 1;
-                        CK(cudaLaunchKernelEx(&cfg, c < P.cycles ? kern_up : kern_cut, a));
+                        CK(cudaLaunchKernelEx(&cfg, pl.update ? kern_up : kern_cut, a));
                     }
                     CK(cudaGetLastError());
                     ++P.launches;
-                    if (c < P.cycles) {
+                    if (pl.update) {
                         if (g == 0 && p0 == 0) ++P.sweep_launches;
                         cur ^= 1;
                     }
@@ -1296,7 +1461,7 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                     P->p_spins[P->final_parity].p, dspins.p, (int)n, (int)P->W, (int)T);
             }
             const double f_last = P->tapsa_packed ? (double)std::min<int64_t>(C, P->alpha) : 1.0;
-            if (inputs) {
+            if (inputs && !P->var_mode) {
                 dinputs.alloc((size_t)T * n);
                 if (P->spsa_packed)
                     pbsa::inputs_from_sidx<<<grid_for(n * T, TB), TB, 0, st>>>(
@@ -1325,14 +1490,23 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
             // copies first (asynchronous into page-locked buffers), then the
             // host-side constant outputs while the DMA and kernels run
             if (spins) CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
-            if (inputs)
-                CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+            if (inputs)  // VAR: i0 * raw of each p-bit's last update, already [T][n]
+                CK(cudaMemcpyAsync(inputs, P->var_mode ? P->inp_var.p : dinputs.p, T * n * sizeof(double),
+                                   cudaMemcpyDeviceToHost, st));
             if (hist && (P->tapsa_hist_from_raw || P->tapsa_packed))
                 CK(cudaMemcpyAsync(hist, dhist.p, T * n * (P->tapsa_packed ? P->alpha : 1) * sizeof(double),
                                    cudaMemcpyDeviceToHost, st));
             if (hist && !P->tapsa_hist_from_raw && !P->tapsa_packed)
                 parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
-            if (counts) parallel_fill(counts, (size_t)(T * n), (int64_t)C);  // every p-bit fires once per cycle
+            if (counts && P->pcl.empty()) {
+                parallel_fill(counts, (size_t)(T * n), (int64_t)C);  // every p-bit fires once per cycle
+            } else if (counts) {  // timing spread: #{count < C t_res : period | count}
+                const int64_t mc = C * P->t_res;
+                const uint8_t *pc = P->pcl.data();
+                parallel_for(T * n, 1 << 20, [&](int64_t lo, int64_t hi) {
+                    for (int64_t k = lo; k < hi; ++k) counts[k] = (mc + pc[k] - 1) / pc[k];
+                });
+            }
             CK(cudaStreamSynchronize(st));
         } else {
             dim3 tb(32, 8);
@@ -1406,7 +1580,11 @@ int pbsa_plan_bytes(const pbsa_plan *P, int64_t *h2d_bytes, int64_t *d2h_bytes) 
                           P->val.bytes_up + P->h.bytes_up + P->me_w.bytes_up + P->lam.bytes_up +
                           P->delta.bytes_up + P->me_wi.bytes_up + P->h_int.bytes_up +
                           P->ge_w.bytes_up + P->period.bytes_up + P->kr.bytes_up +
-                          P->kst.bytes_up + P->kspin.bytes_up;
+                          P->kst.bytes_up + P->kspin.bytes_up + P->prof.bytes_up + P->lam64.bytes_up +
+                          P->del64.bytes_up + P->pplanes.bytes_up + P->vdivs.bytes_up +
+                          P->kfs.bytes_up + P->kstg.bytes_up + P->vali.bytes_up + P->hi32.bytes_up +
+                          P->alist.bytes_up + P->adesc.bytes_up + P->athr.bytes_up + P->i0_dev.bytes_up +
+                          P->ge_w32.bytes_up + P->me_w32.bytes_up;
         const int64_t T = P->T, n = P->n, C = P->cycles;
         int64_t down = T * n + T * n * 8 + 2 * T * C * 8 + T * 8;  // spins, inputs, traces, best
         if (P->path == PBSA_PATH_GENERAL) {

@@ -142,6 +142,18 @@ struct PackedArgs {
     int cycle, Kc;            // SpSA: this cycle, entries per cycle
     uint32_t *ring;           // TApSA: [W][alpha][L][n] bit-sliced neighbour counts
     int alpha, slot, filled;  // TApSA: ring length, this cycle's slot, min(c+1, alpha)
+    // VAR (per-p-bit variability profile, plain rule)
+    const float2 *prof;       // [W][32][n] {fl32(lam), fl32(lam * delta)}
+    const double *lam64;      // [W*32][n] exact lam (near-tie path)
+    const double *del64;      // [W*32][n] exact delta
+    const uint32_t *pplanes;  // [W][nplanes][n] bit-sliced clamped periods, or null (all fire)
+    const uint8_t *divs;      // [ndiv] the present periods that divide this sub-step's counter
+    int ndiv, nplanes;
+    int do_cut;               // accumulate pacc (first sub-step of a cycle; always 1 off VAR)
+    float i0f;                // fl32(i0) of this cycle
+    float margin;             // prefilter margin scale (1; huge = every update takes the exact path)
+    double i0;                // i0 of this cycle
+    double *inp_out;          // [W*32][n] i0 * raw of every fired p-bit, or null
 };
 
 // Exact H >= thr for H = mix64(x); thr == ~0 encodes "never" (tanh == -1),
@@ -196,6 +208,31 @@ __device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t yh, ui
     return zh ^ t.y;
 }
 
+// High word zh of the last multiply of the second absorb; the draw's top word
+// is zh ^ (zh >> 31), i.e. within 1 of zh.
+__device__ __forceinline__ uint32_t packed_hash_hi(uint32_t sl, uint32_t sh, uint32_t count) {
+    constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
+    constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
+    uint32_t yl = sl ^ count ^ __funnelshift_r(sl, sh, 30), yh = sh ^ mulhi(sh, 1u << 2);
+    const uint32_t zl = yl * M1L;
+    const uint32_t zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
+    yl = zl ^ __funnelshift_r(zl, zh, 27);
+    yh = zh ^ mulhi(zh, 1u << 5);
+    return mulhi(yl, M2L) + yl * M2H + yh * M2L;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Second absorb (x = s ^ count; count < 2^30 only touches the low word).
 __device__ __forceinline__ uint32_t packed_second_decide(uint32_t sl, uint32_t sh, uint32_t count,
                                                          uint2 t, uint32_t &word) {
@@ -242,10 +279,11 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     // Larger degrees: entries indexed by raw + dmax.  TApSA: 64-entry rows by S.
     constexpr bool TAPSA = ALG == 1;
     constexpr bool SPSA = ALG == 2;
+    constexpr bool VAR = ALG == 3;
     constexpr bool NIB = L <= 4 && !TAPSA;
     uint2 *sthr = reinterpret_cast<uint2 *>(
         (reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
-    const int tab_entries = TAPSA ? (a.dmax + 1) * 64 : NIB ? (a.dmax + 1) * 16 : a.K;
+    const int tab_entries = VAR ? 0 : TAPSA ? (a.dmax + 1) * 64 : NIB ? (a.dmax + 1) * 16 : a.K;
     uint2 *skey = sthr + tab_entries;                     // [warps][32] {F, C}
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -298,6 +336,28 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             if (i >= a.n) continue;
             const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
             const uint32_t own = __ldg(sw + i);
+            // VAR with a timing spread: the trials of this word whose period
+            // divides the counter (_kernels.py:126), from the bit-sliced periods
+            uint32_t fire = 0xffffffffu;
+            if (VAR && a.pplanes) {
+                uint32_t pl[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    pl[k] = k < a.nplanes ? __ldg(a.pplanes + ((size_t)w * a.nplanes + k) * a.n + i) : 0u;
+                fire = 0;
+                for (int dv = 0; dv < a.ndiv; ++dv) {
+                    const uint32_t pv = __ldg(a.divs + dv);
+                    uint32_t m = 0xffffffffu;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        if (k < a.nplanes) m &= ((pv >> k) & 1u) ? pl[k] : ~pl[k];
+                    fire |= m;
+                }
+                if (!fire && !a.do_cut) {  // nothing fires and no cut to take: carry the word
+                    a.snew[(size_t)w * a.n + i] = own;
+                    continue;
+                }
+            }
             // bit-sliced count p = #{J_ik s_k = +1} (local field) over the d neighbours
             uint32_t p[L];
 #pragma unroll
@@ -328,9 +388,65 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     g[r] = (p[r] & own) | (sum & ~own);
                 }
             }
-            dsum += d;
-            vc_add<L, kCutPlanes>(C, g);
-            if (UPDATE && TAPSA) {
+            if (!VAR || a.do_cut) {
+                dsum += d;
+                vc_add<L, kCutPlanes>(C, g);
+            }
+            if (UPDATE && VAR) {
+                // Per-p-bit variability (pbit.py:57-75): act = r + tanh(lam (i0 raw + delta)).
+                // +1 iff u >= t* = (1 - tanh x) / 2 = 1 / (1 + e^{2x}).  The draw's top
+                // word zh (u 2^32 in [zh - 1, zh + 2)) is compared with an fp32
+                // t = rcp(1 + ex2(2 log2e x)), x from fl32 lam and lam*delta:
+                //   |x - x64| <= A 2^-21.9, A = |lam| |i0 raw| + |lam delta|
+                //   |t - t*|  <= A 2^-22 + |x| 2^-24 + 2^-22   (ex2, rcp, 1 + E rounding)
+                // so with diff = zh - t 2^32 (one rounding, <= 2^7; zh -> fp32 <= 2^7)
+                // |u 2^32 - t* 2^32 - diff| < (A + 1) 2^11 + 2^9 < M = (A + 2) 2^11.
+                // |diff| >= M decides; otherwise (probability ~2^-16) the update is
+                // recomputed in fp64 with the libm-exact tanh, as _kernels.py:150-152.
+                const uint32_t ui = (uint32_t)i;
+                const float2 *pr = a.prof + (size_t)w * 32 * a.n + i;
+                const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
+                uint32_t word = own & ~fire, exact = 0;
+                uint32_t f = fire;
+                while (f) {
+                    const int b = __ffs(f) - 1;
+                    f &= f - 1;
+                    int pop = 0;
+#pragma unroll
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                    const int raw = 2 * pop - d;
+                    const float2 lv = __ldg(pr + (size_t)b * a.n);
+                    const float ir = a.i0f * (float)raw;
+                    const float x = fmaf(lv.x, ir, lv.y);
+                    const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
+                    const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
+                    const uint2 kc = key[b];
+                    uint32_t sl, sh;
+                    packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                    const uint32_t zh = packed_hash_hi(sl, sh, count);
+                    const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
+                    if (fabsf(diff) < fmaf(A, mA, m0))
+                        exact |= 1u << b;
+                    else
+                        word |= (uint32_t)(diff > 0.0f) << b;
+                    if (a.inp_out)
+                        a.inp_out[((size_t)w * 32 + b) * a.n + i] = __dmul_rn(a.i0, (double)raw);
+                }
+                while (exact) {  // rare near-tie: the reference's fp64 arithmetic
+                    const int b = __ffs(exact) - 1;
+                    exact &= exact - 1;
+                    int pop = 0;
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                    const size_t idx = ((size_t)w * 32 + b) * a.n + i;
+                    const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
+                    const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                    const double r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+                    const double inp = __dmul_rn(a.i0, (double)(2 * pop - d));
+                    const double xx = __dmul_rn(a.lam64[idx], __dadd_rn(inp, a.del64[idx]));
+                    word |= (uint32_t)(__dadd_rn(r, pb_libm_tanh(xx)) >= 0.0) << b;
+                }
+                a.snew[(size_t)w * a.n + i] = word;
+            } else if (UPDATE && TAPSA) {
                 // S = p of this cycle + the other filled slots of the ring
                 uint32_t S[kTapsaPlanes];
 #pragma unroll

@@ -256,3 +256,57 @@ def test_packed_tapsa_matches_oracle(oracle, bench_graphs, name, alpha, cycles):
                                alpha=alpha)
     for k in ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "cut_trace", "best_cut"):
         assert np.array_equal(got[k], want[k]), k
+
+
+@pytest.mark.parametrize("name,sig,cycles,margin", [
+    ("G81", (0.5, 0.0, 0.0), 120, None), ("G81", (0.0, 0.7, 0.0), 120, None),
+    ("G55", (0.5, 0.5, 0.5), 60, None), ("G22", (1.0, 1.0, 0.0), 80, None),
+    ("G1", (0.3, 0.4, 0.8), 40, None), ("G48", (0.0, 0.0, 1.0), 50, None),
+    ("G55", (0.5, 0.5, 0.5), 30, "1e9"), ("G1", (0.8, 0.3, 0.0), 30, "1e9")])
+def test_packed_variability_matches_oracle(oracle, bench_graphs, monkeypatch, name, sig, cycles,
+                                           margin):
+    """Per-trial variability profiles on the packed path (fp32 sigmoid prefilter
+    with an exact fp64/libm recheck); margin 1e9 sends every update through the
+    exact recheck, so both branches are compared with the oracle."""
+    if margin is not None:
+        monkeypatch.setenv("PBSA_VAR_MARGIN", margin)
+    g = bench_graphs(name)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, cycles, 10)
+    T = 37
+    seeds = [streams.trial_seed(11, k) for k in range(T)]
+    vc = VariabilityConfig(*sig)
+    profs = [sample_variability(vc, g.n, np.random.default_rng(streams.profile_seed(s))) for s in seeds]
+    keys = [streams.run_key(s) for s in seeds]
+    b = _native.Batch(model, sch, keys, profile_rows=profile_rows(profs, model.n), graph=g,
+                      algo_code=Algorithm.PSA.code)
+    plan = _native.Plan(b)
+    assert plan.info()["path"] == "packed"
+    plan.run()
+    got = plan.download()
+    plan.close()
+    want = oracle.anneal_batch(model, sch, "psa", profs, keys, graph=g)
+    for k in ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
+
+
+def test_packed_variability_shared_profile_and_general_agree(bench_graphs, monkeypatch):
+    """One profile shared by all trials (profile_stride 0) and the general path
+    (PBSA_PACKED_VAR=0) give the same bits as the packed variability path."""
+    g = bench_graphs("G22")
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 50, 10)
+    prof = sample_variability(VariabilityConfig(0.6, 0.6, 0.6), g.n, np.random.default_rng(4))
+    keys = [streams.run_key(s) for s in range(70)]
+    outs = []
+    for env in ("1", "0"):
+        monkeypatch.setenv("PBSA_PACKED_VAR", env)
+        b = _native.Batch(model, sch, keys, profile_rows=profile_rows(prof, model.n), graph=g,
+                          algo_code=Algorithm.PSA.code)
+        plan = _native.Plan(b)
+        assert plan.info()["path"] == ("packed" if env == "1" else "general")
+        plan.run()
+        outs.append(plan.download())
+        plan.close()
+    for k in ("spins", "inputs", "hist", "counts", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
