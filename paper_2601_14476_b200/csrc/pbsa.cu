@@ -353,18 +353,23 @@ void set_packed_smem(K kernel, size_t bytes) {
 using PackedKernel = void (*)(pbsa::PackedArgs);
 PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false,
                                bool spsa = false, bool var = false) {
+#define PBSA_VCASE(l)                                                                 \
+    case l:                                                                           \
+        return cached ? pbsa::packed_sweep<l, true, true, 3>                          \
+                      : pbsa::packed_sweep<l, true, false, 3>;
     if (update && var) {
         switch (L) {
-            case 1: return pbsa::packed_sweep<1, true, false, 3>;
-            case 2: return pbsa::packed_sweep<2, true, false, 3>;
-            case 3: return pbsa::packed_sweep<3, true, false, 3>;
-            case 4: return pbsa::packed_sweep<4, true, false, 3>;
-            case 5: return pbsa::packed_sweep<5, true, false, 3>;
-            case 6: return pbsa::packed_sweep<6, true, false, 3>;
-            case 7: return pbsa::packed_sweep<7, true, false, 3>;
+            PBSA_VCASE(1)
+            PBSA_VCASE(2)
+            PBSA_VCASE(3)
+            PBSA_VCASE(4)
+            PBSA_VCASE(5)
+            PBSA_VCASE(6)
+            PBSA_VCASE(7)
             default: fail(PBSA_EINVAL, "packed variability path supports degree <= 127");
         }
     }
+#undef PBSA_VCASE
 #define PBSA_CASE(l)                                                                  \
     case l:                                                                           \
         return update ? (cached ? pbsa::packed_sweep<l, true, true>                   \
@@ -831,8 +836,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         if (const char *env = std::getenv("PBSA_PDL")) P.use_pdl = env[0] != '0';
         if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;
         const size_t cache_entries = (size_t)P.phase_words * ((n + 31) / 32) * 1024;
-        P.use_cache = cache_entries * 8 <= (32ULL << 30) && !P.var_mode;
-        if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1' && !P.var_mode;
+        // (with a timing spread the fired trials of a word are sparse: no cache)
+        P.use_cache = cache_entries * 8 <= (32ULL << 30) && !many_launches;
+        if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1' && !many_launches;
         if (P.use_cache) P.acache.alloc(cache_entries);
         PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
                                               P.var_mode);

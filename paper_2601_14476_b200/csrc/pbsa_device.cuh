@@ -208,17 +208,21 @@ __device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t yh, ui
     return zh ^ t.y;
 }
 
-// High word zh of the last multiply of the second absorb; the draw's top word
-// is zh ^ (zh >> 31), i.e. within 1 of zh.
-__device__ __forceinline__ uint32_t packed_hash_hi(uint32_t sl, uint32_t sh, uint32_t count) {
+// High word zh of the last multiply of the second absorb, from its input
+// y = x ^ (x >> 30); the draw's top word is zh ^ (zh >> 31), within 1 of zh.
+__device__ __forceinline__ uint32_t packed_hash_hi_y(uint32_t yl, uint32_t yh) {
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
-    uint32_t yl = sl ^ count ^ __funnelshift_r(sl, sh, 30), yh = sh ^ mulhi(sh, 1u << 2);
     const uint32_t zl = yl * M1L;
     const uint32_t zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
     yl = zl ^ __funnelshift_r(zl, zh, 27);
     yh = zh ^ mulhi(zh, 1u << 5);
     return mulhi(yl, M2L) + yl * M2H + yh * M2L;
+}
+
+// Same from the first absorb s (x = s ^ count; count < 2^30 only touches the low word).
+__device__ __forceinline__ uint32_t packed_hash_hi(uint32_t sl, uint32_t sh, uint32_t count) {
+    return packed_hash_hi_y(sl ^ count ^ __funnelshift_r(sl, sh, 30), sh ^ mulhi(sh, 1u << 2));
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -405,12 +409,10 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 // recomputed in fp64 with the libm-exact tanh, as _kernels.py:150-152.
                 const uint32_t ui = (uint32_t)i;
                 const float2 *pr = a.prof + (size_t)w * 32 * a.n + i;
+                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
                 const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
                 uint32_t word = own & ~fire, exact = 0;
-                uint32_t f = fire;
-                while (f) {
-                    const int b = __ffs(f) - 1;
-                    f &= f - 1;
+                auto decide = [&](int b) {
                     int pop = 0;
 #pragma unroll
                     for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
@@ -420,10 +422,16 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     const float x = fmaf(lv.x, ir, lv.y);
                     const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
                     const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
-                    const uint2 kc = key[b];
-                    uint32_t sl, sh;
-                    packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
-                    const uint32_t zh = packed_hash_hi(sl, sh, count);
+                    uint32_t zh;
+                    if (CACHED) {
+                        const uint2 v = __ldcs(ctile + b * 32);
+                        zh = packed_hash_hi_y(v.x ^ count, v.y);
+                    } else {
+                        const uint2 kc = key[b];
+                        uint32_t sl, sh;
+                        packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                        zh = packed_hash_hi(sl, sh, count);
+                    }
                     const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
                     if (fabsf(diff) < fmaf(A, mA, m0))
                         exact |= 1u << b;
@@ -431,6 +439,12 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         word |= (uint32_t)(diff > 0.0f) << b;
                     if (a.inp_out)
                         a.inp_out[((size_t)w * 32 + b) * a.n + i] = __dmul_rn(a.i0, (double)raw);
+                };
+                if (fire == 0xffffffffu) {  // every trial fires (no timing spread)
+#pragma unroll
+                    for (int b = 0; b < 32; ++b) decide(b);
+                } else {
+                    for (uint32_t f = fire; f; f &= f - 1) decide(__ffs(f) - 1);
                 }
                 while (exact) {  // rare near-tie: the reference's fp64 arithmetic
                     const int b = __ffs(exact) - 1;
