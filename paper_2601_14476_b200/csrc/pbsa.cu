@@ -831,7 +831,17 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // per word fill one wave with ~2 tasks per warp.  Small batches: one phase.
         // A timing spread multiplies the launches by t_res: one phase, one chain.
         const bool many_launches = P.var_mode && !P.var_uniform;
-        P.phase_words = (P.W > 16 && !g_oneshot && !many_launches) ? 13 : 0;
+        // Only graphs whose 13 words already fill a wave of resident threads
+        // (sms x 1024) are phased, and only batches of four phases or more
+        // (measured: G55 x 4096 and G81 x 1024 run faster unphased).
+        int sm_count = 148;
+        CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
+        const bool big_graph = 13 * n >= (int64_t)sm_count * 1024;
+        P.phase_words = (!g_oneshot && !many_launches && big_graph && P.W >= 4 * 13) ? 13 : 0;
+        if (P.phase_words > 0) {  // equal phases
+            const int64_t nph = (P.W + P.phase_words - 1) / P.phase_words;
+            P.phase_words = (P.W + nph - 1) / nph;
+        }
         if (const char *env = std::getenv("PBSA_PACKED_PHASE_WORDS")) P.phase_words = std::atoi(env);
         if (const char *env = std::getenv("PBSA_PDL")) P.use_pdl = env[0] != '0';
         if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;

@@ -35,9 +35,11 @@ from paper_2601_14476_b200.pbit import VariabilityConfig, VariabilityProfile  # 
 PEAK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
 
 
-def bytes_per_update(g):
+def bytes_per_update(g, varied=False):
+    """SURVEY 8(d) algorithmic bytes per p-bit update; a varied profile adds
+    the 8-byte fp32 (lam, lam*delta) pair every fired update reads."""
     n, nnz = g.n, 2 * g.m
-    return nnz / n + 1 + (2.125 * nnz + 4 * (n + 1)) / (32 * n)
+    return nnz / n + 1 + (2.125 * nnz + 4 * (n + 1)) / (32 * n) + (8.0 if varied else 0.0)
 
 
 def gpu_run(g, kind, sig, T, cycles=1000, alpha=4):
@@ -101,7 +103,7 @@ def main():
         gpu = gpu_run(g, kind, sig, T)
         cpu = cpu_run(g, kind, sig, cpu_T) if cpu_T else None
         d = denom(name)
-        B = bytes_per_update(g)
+        B = bytes_per_update(g, any(sig))
         row = dict(config=cfg, graph=name, n=g.n, m=g.m, algo=kind.value, sigma=list(sig), trials=T,
                    path=gpu["path"], gpu_ms=gpu["ms"], gpu_upd_s=gpu["upd_s"],
                    roofline_frac=gpu["upd_s"] * B / (PEAK * 1e9), bytes_per_update=B,
@@ -122,6 +124,8 @@ def main():
     add("C2", "G1", Algorithm.PSA, (0, 0, 0), 1024, 0, "sigma = 0 reference point")
     add("C3", "G22", Algorithm.PSA, (0.5, 0.5, 0.5), 4096, 16)
     add("C3", "G55", Algorithm.PSA, (0.5, 0.5, 0.5), 4096, 16)
+    add("C3", "G81", Algorithm.PSA, (0.5, 0.5, 0.5), 4096, 8, "full variability at the C4 size")
+    add("C3", "G81", Algorithm.PSA, (0.5, 0.5, 0.0), 4096, 8, "intensity + offset spread, no timing spread")
     add("C4", "G81", Algorithm.PSA, (0, 0, 0), 4096, 16)
     add("C3'", "G1", Algorithm.TAPSA, (0, 0, 0), 1024, 16, "time-averaged rule (alpha=4)")
     add("C3'", "G81", Algorithm.TAPSA, (0, 0, 0), 4096, 16, "time-averaged rule (alpha=4)")
