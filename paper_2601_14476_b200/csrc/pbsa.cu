@@ -1335,6 +1335,11 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
     CK(cudaGetLastError());
 }
 
+void host_constant_outputs(pbsa_plan *P, double *hist, int64_t *counts, double *trace_i0);
+void download_impl(pbsa_plan *P, int8_t *spins, double *inputs, double *hist, int64_t *counts,
+                   double *trace_i0, double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
+                   bool consts_done);
+
 }  // namespace
 
 // =================================================================== C ABI
@@ -1451,6 +1456,43 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                        double *trace_i0, double *trace_energy, int64_t *trace_cut,
                        int64_t *best_cut) {
     return guarded([&] {
+        download_impl(P, spins, inputs, hist, counts, trace_i0, trace_energy, trace_cut, best_cut,
+                      false);
+    });
+}
+
+}  // extern "C"
+
+namespace {
+
+// Outputs that do not depend on the run: the i0 trace, zero histories of the
+// rules that keep none, and update counts fixed by the periods.  The one-shot
+// call writes them on the host while the device anneals.
+void host_constant_outputs(pbsa_plan *P, double *hist, int64_t *counts, double *trace_i0) {
+    const int64_t n = P->n, T = P->T, C = P->cycles;
+    if (trace_i0)
+        for (int64_t t = 0; t < T; ++t) std::memcpy(trace_i0 + t * C, P->i0.data(), C * sizeof(double));
+    if (P->path == PBSA_PATH_PACKED) {
+        if (hist && !P->tapsa_hist_from_raw && !P->tapsa_packed)
+            parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
+        if (counts && P->pcl.empty()) {
+            parallel_fill(counts, (size_t)(T * n), (int64_t)C);  // every p-bit fires once per cycle
+        } else if (counts) {  // timing spread: #{count < C t_res : period | count}
+            const int64_t mc = C * P->t_res;
+            const uint8_t *pc = P->pcl.data();
+            parallel_for(T * n, 1 << 20, [&](int64_t lo, int64_t hi) {
+                for (int64_t k = lo; k < hi; ++k) counts[k] = (mc + pc[k] - 1) / pc[k];
+            });
+        }
+    } else if (hist && P->algo != 1) {
+        parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
+    }
+}
+
+void download_impl(pbsa_plan *P, int8_t *spins, double *inputs, double *hist, int64_t *counts,
+                   double *trace_i0, double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
+                   bool consts_done) {
+    {
         if (!P) fail(PBSA_EINVAL, "null plan");
         if (!P->ran) fail(PBSA_EINVAL, "plan has not been run");
         DeviceGuard dg(P->device);
@@ -1512,17 +1554,7 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
             if (hist && (P->tapsa_hist_from_raw || P->tapsa_packed))
                 CK(cudaMemcpyAsync(hist, dhist.p, T * n * (P->tapsa_packed ? P->alpha : 1) * sizeof(double),
                                    cudaMemcpyDeviceToHost, st));
-            if (hist && !P->tapsa_hist_from_raw && !P->tapsa_packed)
-                parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
-            if (counts && P->pcl.empty()) {
-                parallel_fill(counts, (size_t)(T * n), (int64_t)C);  // every p-bit fires once per cycle
-            } else if (counts) {  // timing spread: #{count < C t_res : period | count}
-                const int64_t mc = C * P->t_res;
-                const uint8_t *pc = P->pcl.data();
-                parallel_for(T * n, 1 << 20, [&](int64_t lo, int64_t hi) {
-                    for (int64_t k = lo; k < hi; ++k) counts[k] = (mc + pc[k] - 1) / pc[k];
-                });
-            }
+            if (!consts_done) host_constant_outputs(P, hist, counts, trace_i0);
             CK(cudaStreamSynchronize(st));
         } else {
             dim3 tb(32, 8);
@@ -1570,7 +1602,6 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
                                                                    (int)P->Tp, (int)T);
                 }
             }
-            if (hist && P->algo != 1) parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
             if (spins) CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
             if (inputs)
                 CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -1579,13 +1610,16 @@ int pbsa_plan_download(pbsa_plan *P, int8_t *spins, double *inputs, double *hist
             if (hist && P->algo == 1)
                 CK(cudaMemcpyAsync(hist, dhist.p, T * n * P->alpha * sizeof(double),
                                    cudaMemcpyDeviceToHost, st));
+            if (!consts_done) host_constant_outputs(P, hist, counts, trace_i0);
             CK(cudaStreamSynchronize(st));
         }
-        if (trace_i0)
-            for (int64_t t = 0; t < T; ++t) std::memcpy(trace_i0 + t * C, P->i0.data(), C * sizeof(double));
         CK(cudaGetLastError());
-    });
+    }
 }
+
+}  // namespace
+
+extern "C" {
 
 int pbsa_plan_bytes(const pbsa_plan *P, int64_t *h2d_bytes, int64_t *d2h_bytes) {
     return guarded([&] {
@@ -1642,10 +1676,20 @@ int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const i
                               cycles, t_res, algo, alpha, p_stall, trials, keys, &P);
     g_oneshot = false;
     if (rc != PBSA_OK) return rc;
-    rc = pbsa_plan_run(P, device_ms);
-    if (rc == PBSA_OK)
-        rc = pbsa_plan_download(P, spins, inputs, hist, counts, trace_i0, trace_energy, trace_cut,
-                                best_cut);
+    // launch, write the run-independent outputs on the host while the device
+    // anneals, then wait and download the rest
+    rc = guarded([&] {
+        DeviceGuard dg(P->device);
+        CK(cudaEventRecord(P->ev_start, P->stream));
+        CK(cudaGraphLaunch(P->graph_exec, P->stream));
+        CK(cudaEventRecord(P->ev_end, P->stream));
+        host_constant_outputs(P, hist, counts, trace_i0);
+        CK(cudaEventSynchronize(P->ev_end));
+        P->ran = true;
+        if (device_ms) CK(cudaEventElapsedTime(device_ms, P->ev_start, P->ev_end));
+        download_impl(P, spins, inputs, hist, counts, trace_i0, trace_energy, trace_cut, best_cut,
+                      true);
+    });
     const std::string err = g_last_error;
     pbsa_plan_destroy(P);
     if (rc != PBSA_OK) g_last_error = err;

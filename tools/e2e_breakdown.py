@@ -23,3 +23,8 @@ for rep in range(3):
     t3 = time.perf_counter(); plan.close(); t4 = time.perf_counter()
     print(f"T={T} create {1e3*(t1-t0):.1f} ms, run {1e3*(t2-t1):.1f} ms (device {ms:.1f}), "
           f"download {1e3*(t3-t2):.1f} ms, destroy {1e3*(t4-t3):.1f} ms, launches {plan.info() if False else ''}")
+for rep in range(3):
+    t0 = time.perf_counter()
+    out, _ = _native.anneal_batch(b, out=pinned)
+    t1 = time.perf_counter()
+    print(f"one-shot anneal_batch {1e3*(t1-t0):.1f} ms")
