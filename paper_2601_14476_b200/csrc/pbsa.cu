@@ -313,6 +313,13 @@ struct pbsa_plan {
     DevBuf<double> a_inputs;                        // [Np], list order
     DevBuf<uint64_t> athr;  // [cycles][Kt] thresholds (lam = 1, delta = 0, plain rule), or empty
     int tshift = 0, rawmin = 0, Kt = 0;
+    // fast active mode (plain rule): folded draw, fp32 profile, flips only
+    bool fast = false;
+    DevBuf<float2> aprof;                 // [Np] list order or [n] shared
+    DevBuf<uint32_t> flips, nflips;       // [max firing] / [launches]
+    int64_t apmax = 1;                    // largest clamped period
+    std::vector<int32_t> apcl;            // [T][n] clamped periods (host counts)
+    std::vector<uint64_t> kr_host;        // [Tp] absorb(key, TAG_R)
     uint32_t tmask = 0;
 
     DevBuf<uint64_t> kspin;
@@ -352,11 +359,12 @@ void set_packed_smem(K kernel, size_t bytes) {
 
 using PackedKernel = void (*)(pbsa::PackedArgs);
 PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false,
-                               bool spsa = false, bool var = false) {
+                               bool spsa = false, int var = 0) {
 #define PBSA_VCASE(l)                                                                 \
     case l:                                                                           \
-        return cached ? pbsa::packed_sweep<l, true, true, 3>                          \
-                      : pbsa::packed_sweep<l, true, false, 3>;
+        return var == 2 ? pbsa::packed_sweep_timing<l>                                \
+                        : cached ? pbsa::packed_sweep<l, true, true, 3>               \
+                                 : pbsa::packed_sweep<l, true, false, 3>;
     if (update && var) {
         switch (L) {
             PBSA_VCASE(1)
@@ -535,6 +543,48 @@ void setup_active(pbsa_plan &P, int64_t n, const int64_t *indptr, const int64_t 
         P.lam.upload(l, st);
         P.delta.upload(d, st);
     }
+    // fast mode for the plain rule: the draw folds like the packed path's
+    // (i, count < 2^30), no per-p-bit state beyond the last inputs
+    const bool plain_state_free = algo == 0 || (algo == 2 && p_stall == 0.0);
+    const char *fenv = std::getenv("PBSA_ACTIVE_FAST");
+    if (plain_state_free && n < (1LL << 30) && maxcount <= (1LL << 30) && !(fenv && fenv[0] == '0')) {
+        P.fast = true;
+        std::vector<uint64_t> krg(P.Tp);
+        std::vector<uint2> kfc(P.Tp);
+        for (int64_t t = 0; t < P.Tp; ++t) {
+            krg[t] = P.kr_host[t] + kGamma;
+            const uint32_t lo = (uint32_t)krg[t], hi = (uint32_t)(krg[t] >> 32);
+            const uint32_t Y = hi ^ (hi >> 30);
+            kfc[t] = make_uint2(lo ^ ((lo >> 30) | (hi << 2)), Y * 0x1CE4E5B9u);
+        }
+        P.krg.upload(krg, st);
+        P.kfc.upload(kfc, st);
+        if (lam && !P.athr.n) {
+            if (pstride) {
+                std::vector<float2> pf(Np);
+                for (size_t li = 0; li < Np; ++li) {
+                    const int64_t i = list[li] >> tshift, t = list[li] & ((1u << tshift) - 1u);
+                    const double l = lam[t * n + i], d = delta[t * n + i];
+                    pf[li] = make_float2((float)l, (float)(l * d));
+                }
+                P.aprof.upload(pf, st);
+            } else {
+                std::vector<float2> pf(n);
+                for (int64_t i = 0; i < n; ++i) pf[i] = make_float2((float)lam[i], (float)(lam[i] * delta[i]));
+                P.aprof.upload(pf, st);
+            }
+        }
+        P.flips.alloc((size_t)std::max<int64_t>(maxtotal, 1));
+        P.nflips.alloc(std::max<size_t>(P.alaunch.size(), 1));
+        P.apcl.assign((size_t)trials * n, 0);
+        for (int64_t t = 0; t < trials; ++t)
+            for (int64_t i = 0; i < n; ++i) {
+                const int64_t pv = per_of(t, i);
+                P.apcl[(size_t)t * n + i] = (int32_t)pv;
+                P.apmax = std::max(P.apmax, pv);
+            }
+        P.a_counts.release();
+    }
     P.inputs.release();
     P.counts.release();
     P.tshift = tshift;
@@ -597,6 +647,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     P.p_stall = p_stall;
     P.nnz = nnz;
     P.has_graph = gm > 0;
+    // prefilter margin scale (tests: huge sends every update to the exact recheck)
+    if (const char *env = std::getenv("PBSA_VAR_MARGIN")) P.var_margin = (float)std::atof(env);
 
     P.i0.resize(cycles);
     {
@@ -640,8 +692,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     // variability profile on the packed path: plain rule, finite lam/delta,
     // clamped periods below 256 (bit-sliced in at most 8 planes)
     const int64_t maxcount = cycles * t_res;
+    // (PBSA_PACKED_VAR=0 sends variability runs to the active-list kernels)
     bool var_ok = lam && !ideal && (algo == 0 || (algo == 2 && p_stall == 0.0));
-    if (const char *env = std::getenv("PBSA_PACKED_VAR")) var_ok = var_ok && env[0] != '0';
+    const char *venv = std::getenv("PBSA_PACKED_VAR");
+    if (venv) var_ok = var_ok && venv[0] != '0';
     int64_t pmax = 0;
     bool var_uniform = true;
     if (var_ok) {
@@ -679,6 +733,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         kst[t] = habsorb(keys[t], 4);
     }
     P.kspin.upload(kspin, st);
+    P.kr_host = kr;
 
     std::vector<uint32_t> rowptr(n + 1);
     for (int64_t i = 0; i <= n; ++i) rowptr[i] = (uint32_t)indptr[i];
@@ -776,7 +831,6 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             P.lam64.upload(l64, st);
             P.del64.upload(d64, st);
             P.inp_var.alloc((size_t)Tp * n);
-            if (const char *env = std::getenv("PBSA_VAR_MARGIN")) P.var_margin = (float)std::atof(env);
             if (!P.var_uniform) {
                 // clamped periods (a period >= cycles * t_res fires only at count 0),
                 // bit-sliced per word: plane k bit b = bit k of trial 32w+b's period
@@ -811,6 +865,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                         for (int64_t pc = 1; pc <= P.pmax; ++pc)
                             if (present[pc] && count % pc == 0) divs.push_back((uint8_t)pc);
                         const int nd = (int)((int64_t)divs.size() - off);
+                        if (nd > pbsa::kMaxDivisors) fail(PBSA_EINVAL, "too many dividing periods");
                         if (s == 0 || nd > 0)
                             P.plaunch.push_back({(uint32_t)count, c, s == 0, nd, off, true,
                                                  count >= maxcount - P.pmax});
@@ -829,7 +884,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // cache (~67 MB for G81) stays L2-resident across its cycles, which keeps
         // HBM (and the 1 kW power cap) out of the loop; 13 words x ~315 warps
         // per word fill one wave with ~2 tasks per warp.  Small batches: one phase.
-        // A timing spread multiplies the launches by t_res: one phase, one chain.
+        // A timing spread multiplies the launches by t_res: one phase, four chains.
         const bool many_launches = P.var_mode && !P.var_uniform;
         // Only graphs whose 13 words already fill a wave of resident threads
         // (sms x 1024) are phased, and only batches of four phases or more
@@ -851,12 +906,13 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1' && !many_launches;
         if (P.use_cache) P.acache.alloc(cache_entries);
         PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
-                                              P.var_mode);
+                                              P.var_mode ? (P.var_uniform ? 1 : 2) : 0);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
-        set_packed_smem(kern, smem);
+        const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
+        set_packed_smem(kern, smem_up);
         set_packed_smem(packed_kernel_for(P.L, false, false), smem);
         int occ = 0, sms = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pbsa::kPackedThreads, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pbsa::kPackedThreads, smem_up));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         occ = std::max(occ, 1);
         P.chunks = (int)((n + 31) / 32);
@@ -872,7 +928,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
         // small batches need many chains to hide launch gaps; large ones only a
         // couple (fewer graph nodes to instantiate)
-        int chains = many_launches ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
+        int chains = many_launches ? 4 : (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
         if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
         chains = (int)std::min<int64_t>(chains, P.W);
         if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
@@ -1040,7 +1096,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
         PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
-                                                 P.var_mode);
+                                                 P.var_mode ? (P.var_uniform ? 1 : 2) : 0);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
@@ -1129,7 +1185,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                         cudaLaunchConfig_t cfg{};
                         cfg.gridDim = dim3((unsigned)blocks);
                         cfg.blockDim = dim3(pbsa::kPackedThreads);
-                        cfg.dynamicSmemBytes = smem;
+                        cfg.dynamicSmemBytes = (pl.update && P.var_mode && !P.var_uniform) ? pbsa::kTimingSmem : smem;
                         cfg.stream = cs;
                         cudaLaunchAttribute attr[1];
                         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1173,6 +1229,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         if (P.counts.n) CK(cudaMemsetAsync(P.counts.p, 0, P.counts.n * sizeof(int32_t), st));
         if (P.a_inputs.n) CK(cudaMemsetAsync(P.a_inputs.p, 0, P.a_inputs.n * sizeof(double), st));
         if (P.a_counts.n) CK(cudaMemsetAsync(P.a_counts.p, 0, P.a_counts.n * sizeof(int32_t), st));
+        if (P.nflips.n) CK(cudaMemsetAsync(P.nflips.p, 0, P.nflips.n * sizeof(uint32_t), st));
         if (P.hist.n) CK(cudaMemsetAsync(P.hist.p, 0, P.hist.n * sizeof(double), st));
         if (P.hist_i.n) CK(cudaMemsetAsync(P.hist_i.p, 0, P.hist_i.n * sizeof(int32_t), st));
         CK(cudaMemsetAsync(P.cut_acc.p, 0, P.cut_acc.n * sizeof(unsigned long long), st));
@@ -1218,10 +1275,45 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                 a.i0 = P.i0[c];
                 a.p_stall = P.p_stall;
                 a.count = L.count;
-                pbsa::general_active<<<grid_for(L.total, TB), TB, 0, st>>>(a);
-                CK(cudaGetLastError());
-                pbsa::general_scatter<<<grid_for(L.total, TB), TB, 0, st>>>(P.g_spins[0].p, P.st_g.p,
-                                                                           P.st_v.p, L.total);
+                if (P.fast) {
+                    pbsa::FastArgs f{};
+                    f.s = P.g_spins[0].p;
+                    f.list = P.alist.p;
+                    f.desc = a.desc;
+                    f.ndesc = L.ndesc;
+                    f.total = L.total;
+                    f.rowptr = P.rowptr.p;
+                    f.col = P.col.p;
+                    f.vali = P.vali.p;
+                    f.hi = a.hi;
+                    f.prof = P.aprof.n ? P.aprof.p : nullptr;
+                    f.lam64 = P.lam.p;
+                    f.del64 = P.delta.p;
+                    f.shared_profile = P.shared_profile;
+                    f.thr = a.thr;
+                    f.rawmin = P.rawmin;
+                    f.kfc = P.kfc.p;
+                    f.krg = P.krg.p;
+                    f.tshift = P.tshift;
+                    f.tmask = P.tmask;
+                    f.Tp = (int)P.Tp;
+                    f.count = L.count;
+                    f.i0 = P.i0[c];
+                    f.i0f = (float)P.i0[c];
+                    f.margin = P.var_margin;
+                    f.inputs = (int64_t)L.count >= P.cycles * P.t_res - P.apmax ? P.a_inputs.p : nullptr;
+                    f.flips = P.flips.p;
+                    f.nflips = P.nflips.p + li;
+                    pbsa::active_fast<<<grid_for(L.total, TB), TB, 0, st>>>(f);
+                    CK(cudaGetLastError());
+                    pbsa::apply_flips<<<grid_for(L.total, TB), TB, 0, st>>>(P.g_spins[0].p, P.flips.p,
+                                                                           P.nflips.p + li);
+                } else {
+                    pbsa::general_active<<<grid_for(L.total, TB), TB, 0, st>>>(a);
+                    CK(cudaGetLastError());
+                    pbsa::general_scatter<<<grid_for(L.total, TB), TB, 0, st>>>(P.g_spins[0].p, P.st_g.p,
+                                                                               P.st_v.p, L.total);
+                }
                 P.launches += 2;
                 ++P.sweep_launches;
                 ++li;
@@ -1484,8 +1576,15 @@ void host_constant_outputs(pbsa_plan *P, double *hist, int64_t *counts, double *
                 for (int64_t k = lo; k < hi; ++k) counts[k] = (mc + pc[k] - 1) / pc[k];
             });
         }
-    } else if (hist && P->algo != 1) {
-        parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
+    } else {
+        if (hist && P->algo != 1) parallel_fill(hist, (size_t)(T * n * P->alpha), 0.0);
+        if (counts && P->fast) {  // fast active mode: #{count < C t_res : period | count}
+            const int64_t mc = C * P->t_res;
+            const int32_t *pc = P->apcl.data();
+            parallel_for(T * n, 1 << 20, [&](int64_t lo, int64_t hi) {
+                for (int64_t k = lo; k < hi; ++k) counts[k] = (mc + pc[k] - 1) / pc[k];
+            });
+        }
     }
 }
 
@@ -1577,7 +1676,7 @@ void download_impl(pbsa_plan *P, int8_t *spins, double *inputs, double *hist, in
                                                                    (int)P->Tp, (int)T);
                 }
             }
-            if (counts) {
+            if (counts && !P->fast) {
                 dcounts64.alloc((size_t)T * n);
                 if (P->active_mode) {
                     pbsa::list_to_trial_major<int32_t, int64_t><<<grid_for(Np, TB), TB, 0, st>>>(
@@ -1605,7 +1704,7 @@ void download_impl(pbsa_plan *P, int8_t *spins, double *inputs, double *hist, in
             if (spins) CK(cudaMemcpyAsync(spins, dspins.p, T * n, cudaMemcpyDeviceToHost, st));
             if (inputs)
                 CK(cudaMemcpyAsync(inputs, dinputs.p, T * n * sizeof(double), cudaMemcpyDeviceToHost, st));
-            if (counts)
+            if (counts && !P->fast)
                 CK(cudaMemcpyAsync(counts, dcounts64.p, T * n * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
             if (hist && P->algo == 1)
                 CK(cudaMemcpyAsync(hist, dhist.p, T * n * P->alpha * sizeof(double),

@@ -273,6 +273,91 @@ constexpr int kWarpCutPlanes = 13;  // after the warp-level add (32 * 255 < 2^13
 // table lookup by (degree, S), exactly like the plain rule.
 constexpr int kTapsaPlanes = 6;
 
+// Bit-sliced count p = #{J_ik s_k = +1} (the local field, raw = 2p - d) of
+// the 32 trials over the neighbours [beg, end) of one node.
+template <int L>
+__device__ __forceinline__ void gather_counts(const uint32_t *__restrict__ adj,
+                                              const uint32_t *__restrict__ sw, uint32_t beg,
+                                              uint32_t end, uint32_t (&p)[L]) {
+#pragma unroll
+    for (int r = 0; r < L; ++r) p[r] = 0;
+    for (uint32_t k = beg; k < end; ++k) {
+        const uint32_t e = __ldg(adj + k);
+        uint32_t cp = __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
+#pragma unroll
+        for (int r = 0; r < L; ++r) {
+            const uint32_t np = p[r] & cp;
+            p[r] ^= cp;
+            cp = np;
+        }
+    }
+}
+
+// Cut count g = #{J_ik s_i s_k = +1} = (s_i = +1) ? p : d - p, bit-sliced:
+// d - p = ~p + (d + 1) mod 2^L (p <= d < 2^L), then a per-trial select.
+template <int L>
+__device__ __forceinline__ void cut_counts(const uint32_t (&p)[L], uint32_t own, int d,
+                                           uint32_t (&g)[L]) {
+    const uint32_t dp1 = (uint32_t)(d + 1);
+    uint32_t carry = 0;
+#pragma unroll
+    for (int r = 0; r < L; ++r) {
+        const uint32_t m = 0u - ((dp1 >> r) & 1u);
+        const uint32_t x = ~p[r];
+        const uint32_t sum = x ^ m ^ carry;
+        carry = (x & m) | (carry & (x ^ m));
+        g[r] = (p[r] & own) | (sum & ~own);
+    }
+}
+
+// Warp-level bit-sliced add of the 32 lanes' cut counters (all lanes of the
+// warp hold the same 32 trials), then lane b adds trial 32w+b's partial.
+__device__ __forceinline__ void warp_cut_flush(const uint32_t (&C)[kCutPlanes], int dsum, int lane,
+                                               unsigned long long *pacc_w) {
+    uint32_t W13[kWarpCutPlanes];
+#pragma unroll
+    for (int r = 0; r < kWarpCutPlanes; ++r) W13[r] = r < kCutPlanes ? C[r] : 0u;
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        uint32_t carry = 0;
+#pragma unroll
+        for (int r = 0; r < kWarpCutPlanes; ++r) {
+            const uint32_t o = __shfl_xor_sync(0xffffffffu, W13[r], off);
+            const uint32_t sum = W13[r] ^ o ^ carry;
+            carry = (W13[r] & o) | (carry & (W13[r] ^ o));
+            W13[r] = sum;
+        }
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, off);
+    }
+    int acc0 = 0;
+#pragma unroll
+    for (int r = 0; r < kWarpCutPlanes; ++r) acc0 |= (int)((W13[r] >> lane) & 1u) << r;
+    const int acc = 2 * acc0 - dsum;
+    if (pacc_w && acc) atomicAdd(pacc_w + lane, (unsigned long long)(long long)acc);
+}
+
+// Variability near-ties: the reference's fp64 arithmetic (_kernels.py:150-152)
+// on the full 64-bit draw, for the trials flagged in `exact`.
+template <int L>
+__device__ __forceinline__ uint32_t var_exact_bits(const PackedArgs &a, uint32_t exact, const uint32_t (&p)[L],
+                                                int d, int w, int i, uint32_t count) {
+    uint32_t word = 0;
+    while (exact) {
+        const int b = __ffs(exact) - 1;
+        exact &= exact - 1;
+        int pop = 0;
+        for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+        const size_t idx = ((size_t)w * 32 + b) * a.n + i;
+        const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)(uint32_t)i;
+        const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+        const double r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+        const double inp = __dmul_rn(a.i0, (double)(2 * pop - d));
+        const double xx = __dmul_rn(a.lam64[idx], __dadd_rn(inp, a.del64[idx]));
+        word |= (uint32_t)(__dadd_rn(r, pb_libm_tanh(xx)) >= 0.0) << b;
+    }
+    return word;
+}
+
 template <int L, bool UPDATE, bool CACHED, int ALG = 0>
 __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed_sweep(PackedArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
@@ -340,62 +425,13 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             if (i >= a.n) continue;
             const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
             const uint32_t own = __ldg(sw + i);
-            // VAR with a timing spread: the trials of this word whose period
-            // divides the counter (_kernels.py:126), from the bit-sliced periods
-            uint32_t fire = 0xffffffffu;
-            if (VAR && a.pplanes) {
-                uint32_t pl[8];
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    pl[k] = k < a.nplanes ? __ldg(a.pplanes + ((size_t)w * a.nplanes + k) * a.n + i) : 0u;
-                fire = 0;
-                for (int dv = 0; dv < a.ndiv; ++dv) {
-                    const uint32_t pv = __ldg(a.divs + dv);
-                    uint32_t m = 0xffffffffu;
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        if (k < a.nplanes) m &= ((pv >> k) & 1u) ? pl[k] : ~pl[k];
-                    fire |= m;
-                }
-                if (!fire && !a.do_cut) {  // nothing fires and no cut to take: carry the word
-                    a.snew[(size_t)w * a.n + i] = own;
-                    continue;
-                }
-            }
-            // bit-sliced count p = #{J_ik s_k = +1} (local field) over the d neighbours
             uint32_t p[L];
-#pragma unroll
-            for (int r = 0; r < L; ++r) p[r] = 0;
-            for (uint32_t k = beg; k < end; ++k) {
-                const uint32_t e = __ldg(a.adj + k);
-                uint32_t cp = __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
-#pragma unroll
-                for (int r = 0; r < L; ++r) {
-                    const uint32_t np = p[r] & cp;
-                    p[r] ^= cp;
-                    cp = np;
-                }
-            }
+            gather_counts<L>(a.adj, sw, beg, end, p);
             const int d = (int)(end - beg);
-            // cut count g = #{J_ik s_i s_k = +1} = (s_i = +1) ? p : d - p, bit-sliced:
-            // d - p = ~p + (d + 1) mod 2^L (p <= d < 2^L), then a per-trial select
             uint32_t g[L];
-            {
-                const uint32_t dp1 = (uint32_t)(d + 1);
-                uint32_t carry = 0;
-#pragma unroll
-                for (int r = 0; r < L; ++r) {
-                    const uint32_t m = 0u - ((dp1 >> r) & 1u);
-                    const uint32_t x = ~p[r];
-                    const uint32_t sum = x ^ m ^ carry;
-                    carry = (x & m) | (carry & (x ^ m));
-                    g[r] = (p[r] & own) | (sum & ~own);
-                }
-            }
-            if (!VAR || a.do_cut) {
-                dsum += d;
-                vc_add<L, kCutPlanes>(C, g);
-            }
+            cut_counts<L>(p, own, d, g);
+            dsum += d;
+            vc_add<L, kCutPlanes>(C, g);
             if (UPDATE && VAR) {
                 // Per-p-bit variability (pbit.py:57-75): act = r + tanh(lam (i0 raw + delta)).
                 // +1 iff u >= t* = (1 - tanh x) / 2 = 1 / (1 + e^{2x}).  The draw's top
@@ -407,17 +443,18 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 // |u 2^32 - t* 2^32 - diff| < (A + 1) 2^11 + 2^9 < M = (A + 2) 2^11.
                 // |diff| >= M decides; otherwise (probability ~2^-16) the update is
                 // recomputed in fp64 with the libm-exact tanh, as _kernels.py:150-152.
+                // (An fp16 profile halves its bytes but sends ~1 % of the updates to
+                // the recheck, which costs more than the bytes saved: measured.)
                 const uint32_t ui = (uint32_t)i;
                 const float2 *pr = a.prof + (size_t)w * 32 * a.n + i;
                 const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
                 const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
-                uint32_t word = own & ~fire, exact = 0;
-                auto decide = [&](int b) {
+                uint32_t word = 0, exact = 0;
+                auto decide = [&](int b, float2 lv) {
                     int pop = 0;
 #pragma unroll
                     for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                     const int raw = 2 * pop - d;
-                    const float2 lv = __ldg(pr + (size_t)b * a.n);
                     const float ir = a.i0f * (float)raw;
                     const float x = fmaf(lv.x, ir, lv.y);
                     const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
@@ -440,25 +477,9 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     if (a.inp_out)
                         a.inp_out[((size_t)w * 32 + b) * a.n + i] = __dmul_rn(a.i0, (double)raw);
                 };
-                if (fire == 0xffffffffu) {  // every trial fires (no timing spread)
 #pragma unroll
-                    for (int b = 0; b < 32; ++b) decide(b);
-                } else {
-                    for (uint32_t f = fire; f; f &= f - 1) decide(__ffs(f) - 1);
-                }
-                while (exact) {  // rare near-tie: the reference's fp64 arithmetic
-                    const int b = __ffs(exact) - 1;
-                    exact &= exact - 1;
-                    int pop = 0;
-                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
-                    const size_t idx = ((size_t)w * 32 + b) * a.n + i;
-                    const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
-                    const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
-                    const double r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
-                    const double inp = __dmul_rn(a.i0, (double)(2 * pop - d));
-                    const double xx = __dmul_rn(a.lam64[idx], __dadd_rn(inp, a.del64[idx]));
-                    word |= (uint32_t)(__dadd_rn(r, pb_libm_tanh(xx)) >= 0.0) << b;
-                }
+                for (int b = 0; b < 32; ++b) decide(b, __ldg(pr + (size_t)b * a.n));
+                if (exact) word |= var_exact_bits<L>(a, exact, p, d, w, i, count);
                 a.snew[(size_t)w * a.n + i] = word;
             } else if (UPDATE && TAPSA) {
                 // S = p of this cycle + the other filled slots of the ring
@@ -667,28 +688,152 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             }
         }
     }
-    // Warp-level bit-sliced add of the 32 lanes' counters (all lanes of the
-    // warp hold the same 32 trials), then lane b unpacks trial 32w+b.
-    uint32_t W13[kWarpCutPlanes];
-#pragma unroll
-    for (int r = 0; r < kWarpCutPlanes; ++r) W13[r] = r < kCutPlanes ? C[r] : 0u;
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-        uint32_t carry = 0;
-#pragma unroll
-        for (int r = 0; r < kWarpCutPlanes; ++r) {
-            const uint32_t o = __shfl_xor_sync(0xffffffffu, W13[r], off);
-            const uint32_t sum = W13[r] ^ o ^ carry;
-            carry = (W13[r] & o) | (carry & (W13[r] ^ o));
-            W13[r] = sum;
-        }
-        dsum += __shfl_xor_sync(0xffffffffu, dsum, off);
+    warp_cut_flush(C, dsum, lane, live ? a.pacc + (size_t)w * 32 : nullptr);
+}
+
+// ------------------------------------------- packed sweep with a timing spread
+// Per-p-bit periods (pbit.py:74) gate each trial: in sub-step `count` only the
+// trials whose period divides it fire (_kernels.py:126), typically ~15 %, and
+// unevenly across the lanes of a warp.  The fire mask of a (word, node) comes
+// from the bit-sliced periods: OR over the present periods dividing `count`
+// (host list) of the AND of the matching plane polarities.  The warp then
+// compacts its fired (lane, trial) pairs into a shared-memory list and deals
+// them round-robin to its 32 lanes, so a launch costs ~max(mean fires, 1)
+// decisions per lane instead of the maximum lane's count; results return
+// through shared-memory bit masks.  Decision and exact recheck as ALG=3.
+constexpr int kMaxDivisors = 256;
+constexpr size_t kTimingSmem = kPackedWarps * 32 * sizeof(uint2) + kMaxDivisors * 8 * 4 +
+                               2 * kPackedWarps * 32 * 4 + kPackedWarps * 1024 * 4;
+
+template <int L>
+__global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
+    packed_sweep_timing(PackedArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;");
+    extern __shared__ unsigned long long smem_u64[];
+    uint2 *skey = reinterpret_cast<uint2 *>(smem_u64);                           // [warps][32]
+    uint32_t *sdivx = reinterpret_cast<uint32_t *>(skey + kPackedWarps * 32);    // [div][8]
+    uint32_t *sres = sdivx + kMaxDivisors * 8;                                   // [warps][32]
+    uint32_t *sexm = sres + kPackedWarps * 32;                                   // [warps][32]
+    uint32_t *sfl = sexm + kPackedWarps * 32;                                    // [warps][1024]
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int gwarp = blockIdx.x * kPackedWarps + wib;
+    const int w = gwarp / a.warps_per_word;
+    const int q = gwarp % a.warps_per_word;
+    const bool live = w < a.W;
+    uint2 *key = skey + wib * 32;
+    key[lane] = live ? a.kfc[(size_t)w * 32 + lane] : make_uint2(0, 0);
+    // per divisor and plane: 0 selects the plane, ~0 its complement (planes
+    // above nplanes are zero, so their complement passes)
+    for (int k = threadIdx.x; k < a.ndiv * 8; k += blockDim.x) {
+        const uint32_t pv = a.divs[k >> 3];
+        const int pl = k & 7;
+        sdivx[k] = (pl < a.nplanes && ((pv >> pl) & 1u)) ? 0u : 0xffffffffu;
     }
-    int acc0 = 0;
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint32_t count = a.count;
+    uint32_t C[kCutPlanes];
 #pragma unroll
-    for (int r = 0; r < kWarpCutPlanes; ++r) acc0 |= (int)((W13[r] >> lane) & 1u) << r;
-    int acc[1] = {2 * acc0 - dsum};
-    if (live && acc[0]) atomicAdd(a.pacc + (size_t)w * 32 + lane, (unsigned long long)(long long)acc[0]);
+    for (int r = 0; r < kCutPlanes; ++r) C[r] = 0;
+    int dsum = 0;
+    uint32_t *fl = sfl + wib * 1024, *res = sres + wib * 32, *exm = sexm + wib * 32;
+    const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
+
+    if (live) {
+        const uint32_t *sw = a.sold + (size_t)w * a.n;
+        for (int ch = q; ch < a.chunks; ch += a.warps_per_word) {
+            const int i = ch * 32 + lane;
+            const bool valid = i < a.n;
+            // (the gather is issued with the period planes: with a timing
+            // spread almost every warp has some firing trial)
+            uint32_t own = 0, fire = 0, beg = 0, end = 0;
+            uint32_t pl[8];
+            if (valid) {
+                beg = __ldg(a.rowptr + i);
+                end = __ldg(a.rowptr + i + 1);
+                own = __ldg(sw + i);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                pl[k] = (valid && k < a.nplanes) ? __ldg(a.pplanes + ((size_t)w * a.nplanes + k) * a.n + i) : 0u;
+            uint32_t p[L];
+            const int d = (int)(end - beg);
+            gather_counts<L>(a.adj, sw, beg, end, p);
+            if (valid) {
+                for (int dv = 0; dv < a.ndiv; ++dv) {
+                    const uint4 x0 = *reinterpret_cast<const uint4 *>(sdivx + dv * 8);
+                    const uint4 x1 = *reinterpret_cast<const uint4 *>(sdivx + dv * 8 + 4);
+                    fire |= (pl[0] ^ x0.x) & (pl[1] ^ x0.y) & (pl[2] ^ x0.z) & (pl[3] ^ x0.w) &
+                            (pl[4] ^ x1.x) & (pl[5] ^ x1.y) & (pl[6] ^ x1.z) & (pl[7] ^ x1.w);
+                }
+            }
+            if (a.do_cut && valid) {
+                uint32_t g[L];
+                cut_counts<L>(p, own, d, g);
+                dsum += d;
+                vc_add<L, kCutPlanes>(C, g);
+            }
+            // compact the warp's fired (lane, trial) pairs with their raw fields
+            const int c = __popc(fire);
+            int off = c;
+#pragma unroll
+            for (int sft = 1; sft < 32; sft <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, off, sft);
+                if (lane >= sft) off += v;
+            }
+            const int F = __shfl_sync(0xffffffffu, off, 31);
+            off -= c;
+            for (uint32_t f = fire; f; f &= f - 1) {
+                const int b = __ffs(f) - 1;
+                int pop = 0;
+#pragma unroll
+                for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                fl[off++] = ((uint32_t)(2 * pop - d + 1024) << 10) | ((uint32_t)lane << 5) | (uint32_t)b;
+            }
+            res[lane] = 0;
+            exm[lane] = 0;
+            __syncwarp();
+            // two list entries per lane and round, their profile loads in flight together
+            auto fire_one = [&](uint32_t e, float2 lv) {
+                const int b = (int)(e & 31u), l = (int)((e >> 5) & 31u), raw = (int)(e >> 10) - 1024;
+                const int ii = ch * 32 + l;
+                const float ir = a.i0f * (float)raw;
+                const float x = fmaf(lv.x, ir, lv.y);
+                const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
+                const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
+                const uint2 kc = key[b];
+                uint32_t sl, sh;
+                packed_first_absorb(kc.x ^ (uint32_t)ii, kc.y, sl, sh);
+                const uint32_t zh = packed_hash_hi(sl, sh, count);
+                const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
+                if (fabsf(diff) < fmaf(A, mA, m0))
+                    atomicOr(exm + l, 1u << b);
+                else if (diff > 0.0f)
+                    atomicOr(res + l, 1u << b);
+                if (a.inp_out) a.inp_out[((size_t)w * 32 + b) * a.n + ii] = __dmul_rn(a.i0, (double)raw);
+            };
+            auto prof_of = [&](uint32_t e) {
+                return __ldg(a.prof + ((size_t)w * 32 + (e & 31u)) * a.n + ch * 32 + ((e >> 5) & 31u));
+            };
+            for (int k = lane; k < F; k += 64) {
+                const uint32_t e0 = fl[k];
+                const bool two = k + 32 < F;
+                const uint32_t e1 = two ? fl[k + 32] : e0;
+                const float2 lv0 = prof_of(e0), lv1 = prof_of(e1);
+                fire_one(e0, lv0);
+                if (two) fire_one(e1, lv1);
+            }
+            __syncwarp();
+            if (valid) {
+                uint32_t word = (own & ~fire) | res[lane];
+                const uint32_t ex = exm[lane];
+                if (ex) word |= var_exact_bits<L>(a, ex, p, d, w, i, count);
+                a.snew[(size_t)w * a.n + i] = word;
+            }
+            __syncwarp();
+        }
+    }
+    warp_cut_flush(C, dsum, lane, live ? a.pacc + (size_t)w * 32 : nullptr);
 }
 
 // Packed spins [W][n] -> int8 [T][n]
@@ -910,6 +1055,122 @@ __global__ void __launch_bounds__(256) general_active(ActiveArgs a) {
     }
     a.st_g[pos] = (uint32_t)g;
     a.st_v[pos] = up ? 1 : -1;
+}
+
+// ---------------------------------------- active lists, plain rule, fast path
+// The plain rule (pSA; SpSA with p = 0) with a timing spread: only the
+// firing p-bits of a sub-step cost work (active lists as above), and the
+// rule keeps no per-p-bit state -- the update count of a firing p-bit is
+// count / period and its input is i0 * raw -- so a launch reads the list,
+// the fp32 profile pair (list order, coalesced) and the int8 neighbour spins,
+// and writes only the flips (compacted per warp) plus, during the last
+// p_max sub-steps, the inputs.  The draw uses the folded per-trial constants
+// of the packed path; the decision is the packed variability kernel's
+// sigmoid prefilter with its exact fp64 recheck, or the exact integer
+// threshold table when lam = 1 and delta = 0.
+struct FastArgs {
+    int8_t *s;                // [n][Tp] spins (read-only in the launch)
+    const uint32_t *list;     // (node << tshift | trial), bucketed by period
+    const int4 *desc;         // [ndesc] {start, cumulative offset, length, 0}
+    int ndesc, total;
+    const uint32_t *rowptr, *col;
+    const int32_t *vali, *hi; // integer couplings (CSR order), integer fields or null
+    const float2 *prof;       // [Np] list order, or [n] shared; null: table mode
+    const double *lam64, *del64;
+    int shared_profile;
+    const uint64_t *thr;      // [K] this cycle's thresholds (table mode) or null
+    int rawmin;
+    const uint2 *kfc;         // [Tp] folded per-trial constants of absorb(key, TAG_R)
+    const uint64_t *krg;      // [Tp] absorb(key, TAG_R) + GAMMA
+    int tshift;
+    uint32_t tmask;
+    int Tp;
+    uint32_t count;
+    double i0;
+    float i0f, margin;
+    double *inputs;           // [Np] list order (last p_max sub-steps) or null
+    uint32_t *flips;          // compacted spin indices to negate
+    uint32_t *nflips;         // this launch's flip counter
+};
+
+__global__ void __launch_bounds__(256) active_fast(FastArgs a) {
+    __shared__ int4 sdesc[kMaxActiveDesc];
+    for (int k = threadIdx.x; k < a.ndesc; k += blockDim.x) sdesc[k] = a.desc[k];
+    __syncthreads();
+    const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+    bool flip = false;
+    uint32_t g = 0;
+    if (pos < a.total) {
+        int lo = 0, hi = a.ndesc - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (sdesc[mid].y <= pos) lo = mid; else hi = mid - 1;
+        }
+        const uint32_t li = (uint32_t)(sdesc[lo].x + (pos - sdesc[lo].y));
+        const uint32_t e = __ldg(a.list + li);
+        const int i = (int)(e >> a.tshift), t = (int)(e & a.tmask);
+        g = (uint32_t)i * (uint32_t)a.Tp + (uint32_t)t;
+        int raw = a.hi ? __ldg(a.hi + i) : 0;
+        const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
+        for (uint32_t k = beg; k < end; ++k)
+            raw += __ldg(a.vali + k) * (int)a.s[(size_t)__ldg(a.col + k) * a.Tp + t];
+        const uint2 kc = __ldg(a.kfc + t);
+        uint32_t sl, sh;
+        packed_first_absorb(kc.x ^ (uint32_t)i, kc.y, sl, sh);
+        bool up, exact = false;
+        if (a.thr) {  // lam = 1, delta = 0: H >= thr exactly
+            const uint64_t thr = __ldg(a.thr + (raw - a.rawmin));
+            const uint32_t zh = packed_hash_hi(sl, sh, a.count);
+            const uint32_t thi = (uint32_t)(thr >> 32);
+            // top words decide unless they (nearly) tie
+            up = zh > thi;
+            exact = zh - thi + 1u <= 2u;  // |zh - thi| <= 1
+        } else {
+            const float2 lv = __ldg(a.prof + (a.shared_profile ? (size_t)i : (size_t)li));
+            const float ir = a.i0f * (float)raw;
+            const float x = fmaf(lv.x, ir, lv.y);
+            const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
+            const float tt = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
+            const uint32_t zh = packed_hash_hi(sl, sh, a.count);
+            const float diff = fmaf(-tt, 4294967296.0f, __uint2float_rn(zh));
+            up = diff > 0.0f;
+            exact = fabsf(diff) < fmaf(A, 2048.0f * a.margin, 4096.0f * a.margin);
+        }
+        if (exact) {  // the reference's arithmetic on the full 64-bit draw
+            const uint64_t x1 = __ldg(a.krg + t) ^ (uint64_t)(uint32_t)i;
+            const uint64_t H = mix64((mix64(x1) + PB_GAMMA) ^ (uint64_t)a.count);
+            if (a.thr) {
+                const uint64_t thr = __ldg(a.thr + (raw - a.rawmin));
+                up = H >= thr && thr != ~0ULL;
+            } else {
+                const size_t pidx = a.shared_profile ? (size_t)i : (size_t)li;
+                const double r = __dsub_rn(__dmul_rn(2.0, u01_of(H)), 1.0);
+                const double xx = __dmul_rn(a.lam64[pidx], __dadd_rn(__dmul_rn(a.i0, (double)raw), a.del64[pidx]));
+                up = __dadd_rn(r, pb_libm_tanh(xx)) >= 0.0;
+            }
+        }
+        if (a.inputs) a.inputs[li] = __dmul_rn(a.i0, (double)raw);
+        flip = up != (a.s[g] > 0);
+    }
+    // warp-aggregated compaction of the flips
+    const unsigned m = __ballot_sync(0xffffffffu, flip);
+    if (m) {
+        const int lane = threadIdx.x & 31;
+        uint32_t base = 0;
+        if (lane == __ffs(m) - 1) base = atomicAdd(a.nflips, (uint32_t)__popc(m));
+        base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+        if (flip) a.flips[base + __popc(m & ((1u << lane) - 1u))] = g;
+    }
+}
+
+// negate the spins flipped by one sub-step (grid sized for the launch's firings)
+__global__ void apply_flips(int8_t *__restrict__ s, const uint32_t *__restrict__ flips,
+                            const uint32_t *__restrict__ nflips) {
+    const uint32_t pos = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos < *nflips) {
+        const uint32_t g = flips[pos];
+        s[g] = (int8_t)-s[g];
+    }
 }
 
 // list-order per-p-bit state -> [trial][node][k] output rows

@@ -258,18 +258,26 @@ def test_packed_tapsa_matches_oracle(oracle, bench_graphs, name, alpha, cycles):
         assert np.array_equal(got[k], want[k]), k
 
 
-@pytest.mark.parametrize("name,sig,cycles,margin", [
-    ("G81", (0.5, 0.0, 0.0), 120, None), ("G81", (0.0, 0.7, 0.0), 120, None),
-    ("G55", (0.5, 0.5, 0.5), 60, None), ("G22", (1.0, 1.0, 0.0), 80, None),
-    ("G1", (0.3, 0.4, 0.8), 40, None), ("G48", (0.0, 0.0, 1.0), 50, None),
-    ("G55", (0.5, 0.5, 0.5), 30, "1e9"), ("G1", (0.8, 0.3, 0.0), 30, "1e9")])
-def test_packed_variability_matches_oracle(oracle, bench_graphs, monkeypatch, name, sig, cycles,
-                                           margin):
-    """Per-trial variability profiles on the packed path (fp32 sigmoid prefilter
-    with an exact fp64/libm recheck); margin 1e9 sends every update through the
-    exact recheck, so both branches are compared with the oracle."""
+@pytest.mark.parametrize("name,sig,cycles,margin,force", [
+    ("G81", (0.5, 0.0, 0.0), 120, None, None), ("G81", (0.0, 0.7, 0.0), 120, None, None),
+    ("G55", (0.5, 0.5, 0.5), 60, None, None), ("G22", (1.0, 1.0, 0.0), 80, None, None),
+    ("G1", (0.3, 0.4, 0.8), 40, None, None), ("G48", (0.0, 0.0, 1.0), 50, None, None),
+    ("G55", (0.5, 0.5, 0.5), 30, "1e9", None), ("G1", (0.8, 0.3, 0.0), 30, "1e9", None),
+    ("G48", (0.0, 0.0, 1.0), 30, "1e9", None),
+    ("G55", (0.5, 0.5, 0.5), 60, None, "0"), ("G1", (0.3, 0.4, 0.8), 30, None, "0"),
+    ("G55", (0.5, 0.5, 0.5), 30, "1e9", "0"), ("G22", (0.7, 0.2, 0.0), 30, None, "0")])
+def test_variability_matches_oracle(oracle, bench_graphs, monkeypatch, name, sig, cycles, margin,
+                                    force):
+    """Per-trial variability profiles on the packed kernel (ALG=3 without a
+    timing spread, ALG=4 with one) or, with PBSA_PACKED_VAR=0, on the
+    active-list fast kernel; all use the fp32 sigmoid prefilter with an exact
+    fp64/libm recheck, and margin 1e9 sends every update through the exact
+    recheck, so both branches meet the oracle."""
     if margin is not None:
         monkeypatch.setenv("PBSA_VAR_MARGIN", margin)
+    if force is not None:
+        monkeypatch.setenv("PBSA_PACKED_VAR", force)
+    want_path = "general" if force == "0" else "packed"
     g = bench_graphs(name)
     model = maxcut_to_ising(g)
     sch = derive_schedule(model, cycles, 10)
@@ -281,7 +289,7 @@ def test_packed_variability_matches_oracle(oracle, bench_graphs, monkeypatch, na
     b = _native.Batch(model, sch, keys, profile_rows=profile_rows(profs, model.n), graph=g,
                       algo_code=Algorithm.PSA.code)
     plan = _native.Plan(b)
-    assert plan.info()["path"] == "packed"
+    assert plan.info()["path"] == want_path
     plan.run()
     got = plan.download()
     plan.close()
@@ -290,23 +298,30 @@ def test_packed_variability_matches_oracle(oracle, bench_graphs, monkeypatch, na
         assert np.array_equal(got[k], want[k]), k
 
 
-def test_packed_variability_shared_profile_and_general_agree(bench_graphs, monkeypatch):
-    """One profile shared by all trials (profile_stride 0) and the general path
-    (PBSA_PACKED_VAR=0) give the same bits as the packed variability path."""
+@pytest.mark.parametrize("sig", [(0.6, 0.6, 0.6), (0.6, 0.6, 0.0), (0.0, 0.0, 0.7)])
+def test_variability_paths_agree_with_shared_profile(bench_graphs, monkeypatch, sig):
+    """One profile shared by all trials (profile_stride 0): the packed
+    variability kernel, the active-list fast kernel and the original
+    active-list kernel give the same bits."""
     g = bench_graphs("G22")
     model = maxcut_to_ising(g)
     sch = derive_schedule(model, 50, 10)
-    prof = sample_variability(VariabilityConfig(0.6, 0.6, 0.6), g.n, np.random.default_rng(4))
+    prof = sample_variability(VariabilityConfig(*sig), g.n, np.random.default_rng(4))
     keys = [streams.run_key(s) for s in range(70)]
     outs = []
-    for env in ("1", "0"):
-        monkeypatch.setenv("PBSA_PACKED_VAR", env)
+    for env in ({"PBSA_PACKED_VAR": "1"}, {"PBSA_PACKED_VAR": "0"},
+                {"PBSA_PACKED_VAR": "0", "PBSA_ACTIVE_FAST": "0"}):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         b = _native.Batch(model, sch, keys, profile_rows=profile_rows(prof, model.n), graph=g,
                           algo_code=Algorithm.PSA.code)
         plan = _native.Plan(b)
-        assert plan.info()["path"] == ("packed" if env == "1" else "general")
+        assert plan.info()["path"] == ("packed" if env["PBSA_PACKED_VAR"] == "1" else "general")
         plan.run()
         outs.append(plan.download())
         plan.close()
-    for k in ("spins", "inputs", "hist", "counts", "energy_trace", "cut_trace", "best_cut"):
-        assert np.array_equal(outs[0][k], outs[1][k]), k
+        for k in env:
+            monkeypatch.delenv(k)
+    for o in outs[1:]:
+        for k in ("spins", "inputs", "hist", "counts", "energy_trace", "cut_trace", "best_cut"):
+            assert np.array_equal(outs[0][k], o[k]), k
