@@ -919,8 +919,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         const int64_t target_warps = (int64_t)sms * occ * pbsa::kPackedWarps;
         int64_t wpw = std::max<int64_t>(1, target_warps / P.phase_words);  // one phase at a time
         wpw = std::min<int64_t>(wpw, P.chunks);
-        // the per-thread bit-sliced cut counter holds sum(degree) < 2^kCutPlanes
-        const int64_t cap = (1LL << pbsa::kCutPlanes) - 1, dm = std::max<int64_t>(dmax, 1);
+        // the per-thread bit-sliced cut counter holds sum(degree) < 2^(L+2)
+        const int64_t cap = (1LL << (P.L + 2)) - 1, dm = std::max<int64_t>(dmax, 1);
         if (dm > cap) fail(PBSA_EINVAL, "degree too large for the packed cut counter");
         const int64_t max_tasks = cap / dm;  // chunks one warp may take
         wpw = std::max<int64_t>(wpw, std::min<int64_t>((P.chunks + max_tasks - 1) / max_tasks, P.chunks));

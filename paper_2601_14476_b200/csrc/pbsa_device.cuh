@@ -257,8 +257,12 @@ __device__ __forceinline__ void vc_add(uint32_t (&C)[CL], const uint32_t (&x)[L]
     }
 }
 
-constexpr int kCutPlanes = 8;       // per-thread cut counter width (host keeps tasks*dmax < 2^8)
-constexpr int kWarpCutPlanes = 13;  // after the warp-level add (32 * 255 < 2^13)
+// Per-thread cut counter width for degree < 2^L: L + 2 planes, so one lane
+// may take up to 4 nodes (the host sizes warps per word accordingly).
+template <int L>
+struct CutPlanes {
+    static constexpr int value = L + 2;
+};
 
 #ifndef PBSA_PACKED_MIN_BLOCKS
 #define PBSA_PACKED_MIN_BLOCKS 4
@@ -312,26 +316,30 @@ __device__ __forceinline__ void cut_counts(const uint32_t (&p)[L], uint32_t own,
 
 // Warp-level bit-sliced add of the 32 lanes' cut counters (all lanes of the
 // warp hold the same 32 trials), then lane b adds trial 32w+b's partial.
-__device__ __forceinline__ void warp_cut_flush(const uint32_t (&C)[kCutPlanes], int dsum, int lane,
+// After butterfly round j the sums of 2^(j+1) lanes need CP + j + 1 planes,
+// so each round adds only the planes that can be non-zero.
+template <int CP>
+__device__ __forceinline__ void warp_cut_flush(const uint32_t (&C)[CP], int dsum, int lane,
                                                unsigned long long *pacc_w) {
-    uint32_t W13[kWarpCutPlanes];
+    uint32_t W[CP + 5];
 #pragma unroll
-    for (int r = 0; r < kWarpCutPlanes; ++r) W13[r] = r < kCutPlanes ? C[r] : 0u;
+    for (int r = 0; r < CP + 5; ++r) W[r] = r < CP ? C[r] : 0u;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
+    for (int j = 0; j < 5; ++j) {
+        const int off = 16 >> j;
         uint32_t carry = 0;
 #pragma unroll
-        for (int r = 0; r < kWarpCutPlanes; ++r) {
-            const uint32_t o = __shfl_xor_sync(0xffffffffu, W13[r], off);
-            const uint32_t sum = W13[r] ^ o ^ carry;
-            carry = (W13[r] & o) | (carry & (W13[r] ^ o));
-            W13[r] = sum;
+        for (int r = 0; r < CP + j + 1; ++r) {
+            const uint32_t o = r < CP + j ? __shfl_xor_sync(0xffffffffu, W[r], off) : 0u;
+            const uint32_t sum = W[r] ^ o ^ carry;
+            carry = (W[r] & o) | (carry & (W[r] ^ o));
+            W[r] = sum;
         }
         dsum += __shfl_xor_sync(0xffffffffu, dsum, off);
     }
     int acc0 = 0;
 #pragma unroll
-    for (int r = 0; r < kWarpCutPlanes; ++r) acc0 |= (int)((W13[r] >> lane) & 1u) << r;
+    for (int r = 0; r < CP + 5; ++r) acc0 |= (int)((W[r] >> lane) & 1u) << r;
     const int acc = 2 * acc0 - dsum;
     if (pacc_w && acc) atomicAdd(pacc_w + lane, (unsigned long long)(long long)acc);
 }
@@ -413,9 +421,10 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     // Per-trial sum over this thread's nodes of q_i = #{k : J_ik s_i s_k = +1},
     // kept bit-sliced; s_i raw_i = 2 q_i - d_i, so the cut partial is
     // 2 * C - dsum (h = 0).
-    uint32_t C[kCutPlanes];
+    constexpr int CP = CutPlanes<L>::value;
+    uint32_t C[CP];
 #pragma unroll
-    for (int r = 0; r < kCutPlanes; ++r) C[r] = 0;
+    for (int r = 0; r < CP; ++r) C[r] = 0;
     int dsum = 0;
 
     if (live) {
@@ -431,7 +440,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             uint32_t g[L];
             cut_counts<L>(p, own, d, g);
             dsum += d;
-            vc_add<L, kCutPlanes>(C, g);
+            vc_add<L, CP>(C, g);
             if (UPDATE && VAR) {
                 // Per-p-bit variability (pbit.py:57-75): act = r + tanh(lam (i0 raw + delta)).
                 // +1 iff u >= t* = (1 - tanh x) / 2 = 1 / (1 + e^{2x}).  The draw's top
@@ -732,9 +741,10 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
     __syncthreads();
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const uint32_t count = a.count;
-    uint32_t C[kCutPlanes];
+    constexpr int CP = CutPlanes<L>::value;
+    uint32_t C[CP];
 #pragma unroll
-    for (int r = 0; r < kCutPlanes; ++r) C[r] = 0;
+    for (int r = 0; r < CP; ++r) C[r] = 0;
     int dsum = 0;
     uint32_t *fl = sfl + wib * 1024, *res = sres + wib * 32, *exm = sexm + wib * 32;
     const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
@@ -771,7 +781,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
                 uint32_t g[L];
                 cut_counts<L>(p, own, d, g);
                 dsum += d;
-                vc_add<L, kCutPlanes>(C, g);
+                vc_add<L, CP>(C, g);
             }
             // compact the warp's fired (lane, trial) pairs with their raw fields
             const int c = __popc(fire);
