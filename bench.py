@@ -212,6 +212,29 @@ def algorithmic_bytes_per_update(graph):
     return nnz / n + 1 + (2.125 * nnz + 4 * (n + 1)) / (32 * n)
 
 
+def alu_ceiling(n, trials, cycles, local, flush):
+    """Measured instruction ceiling of the sweep (SURVEY 8(d) "measure it with
+    an RNG-only kernel"): the same packed kernel, launch shape and schedule on
+    an edgeless graph of the same n and trials, so only the per-update draw,
+    threshold lookup and decision remain.  Returns updates/s."""
+    import torch
+    from paper_2601_14476_b200.annealer import AnnealSchedule
+    from paper_2601_14476_b200.model import IsingModel
+    model = IsingModel.from_edges(n, [], h=np.zeros(n))
+    sch = AnnealSchedule(i0_min=0.05, i0_max=5.0, beta=0.01 ** (1.0 / (cycles - 1)), cycles=cycles,
+                         t_res=10)
+    b = _native.Batch(model, sch, streams.run_keys(streams.trial_seeds(7, trials)))
+    plan = _native.Plan(b, device=local)
+    best = 0.0
+    for _ in range(3):
+        flush.zero_()
+        torch.cuda.synchronize()
+        plan.run()
+        best = max(best, trials * n * cycles / (plan.info()["sweep_ms_mean"] * cycles * 1e-3))
+    plan.close()
+    return best
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -307,6 +330,9 @@ def main():
         return
 
     B = algorithmic_bytes_per_update(graph)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    alu = alu_ceiling(graph.n, hi - lo, min(args.cycles, 200), local, flush)
+    del flush
     upd_per_launch = (hi - lo) * graph.n
     achieved = B * upd_per_launch / (info["sweep_ms_mean"] * 1e-3) / 1e9
     peak, peak_kind = peaks()
@@ -346,7 +372,11 @@ def main():
                      "peak_source": peak_kind,
                      "kernel": info["path"] + "_sweep",
                      "kernel_ms_mean": info["sweep_ms_mean"],
-                     "bytes_per_update": B, "updates_per_launch": upd_per_launch},
+                     "bytes_per_update": B, "updates_per_launch": upd_per_launch,
+                     "alu_ceiling": {"value": alu, "unit": UNIT,
+                                     "frac": (upd_per_launch / (info["sweep_ms_mean"] * 1e-3)) / alu,
+                                     "how": "same packed kernel and launch shape on an edgeless graph "
+                                            "of the same n and trials (draw + threshold + decision only)"}},
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
         "gpu_launches": info["launches"] * args.steps,
