@@ -244,6 +244,33 @@ __device__ __forceinline__ uint32_t packed_second_decide(uint32_t sl, uint32_t s
                            word);
 }
 
+// Plain-rule variant with the table entry t = (lo, hi) of the 33-bit
+// n2 = ~thi + 2: the carry of zh + n2 is zh >= thi - 1 and its low word is
+// D = zh - thi + 1, so D < 3 (zh within 1 of thi, where the draw's low word
+// or the final xorshift's bit 0 matter) is the only case that needs the
+// exact 64-bit test, and every other carry is the exact decision -- also for
+// thi <= 1, which the 33rd bit keeps.  Returns D.
+__device__ __forceinline__ uint32_t packed_decide_n2(uint32_t yl, uint32_t yh, uint2 t,
+                                                     uint32_t &word) {
+    constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
+    constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
+    uint32_t zl = yl * M1L;
+    uint32_t zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
+    yl = zl ^ __funnelshift_r(zl, zh, 27);
+    yh = zh ^ mulhi(zh, 1u << 5);
+    zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
+    uint32_t D;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+        : "=r"(D), "=r"(word) : "r"(zh), "r"(t.x), "r"(word), "r"(word + t.y));
+    return D;
+}
+
+__device__ __forceinline__ uint32_t packed_second_decide_n2(uint32_t sl, uint32_t sh, uint32_t count,
+                                                            uint2 t, uint32_t &word) {
+    return packed_decide_n2(sl ^ count ^ __funnelshift_r(sl, sh, 30), sh ^ mulhi(sh, 1u << 2), t,
+                            word);
+}
+
 // Bit-sliced counter: add the L-bit per-trial numbers x[] into C[] (CL planes).
 template <int L, int CL>
 __device__ __forceinline__ void vc_add(uint32_t (&C)[CL], const uint32_t (&x)[L]) {
@@ -403,7 +430,12 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             }
             thi = ok ? (uint32_t)(a.thr[raw + a.dmax] >> 32) : 0u;
         }
-        sthr[k] = make_uint2(~thi, thi);
+        if (ALG == 0) {  // (lo, hi) of the 33-bit ~thi + 2 (packed_decide_n2)
+            const uint64_t n2 = (uint64_t)(~thi) + 2u;
+            sthr[k] = make_uint2((uint32_t)n2, (uint32_t)(n2 >> 32));
+        } else {
+            sthr[k] = make_uint2(~thi, thi);
+        }
     }
     uint2 *key = skey + wib * 32;
     key[lane] = live ? a.kfc[(size_t)w * 32 + lane] : make_uint2(0, 0);
@@ -668,15 +700,15 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     }
                     if (CACHED) {
                         const uint2 v = __ldcs(ctile + b * 32);
-                        tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
+                        tie = min(tie, packed_decide_n2(v.x ^ count, v.y, t, word));
                     } else {
                         const uint2 kc = key[b];
                         uint32_t sl, sh;
                         packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
-                        tie = min(tie, packed_second_decide(sl, sh, count, t, word));
+                        tie = min(tie, packed_second_decide_n2(sl, sh, count, t, word));
                     }
                 }
-                if (tie < 2) {  // rare: some trial's high words nearly tie -> exact 64-bit test
+                if (tie < 3) {  // rare: some trial's draw is within 1 of its threshold -> exact 64-bit test
                     word = 0;
                     for (int b = 0; b < 32; ++b) {
                         int pop = 0;
