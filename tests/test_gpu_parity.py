@@ -325,3 +325,29 @@ def test_variability_paths_agree_with_shared_profile(bench_graphs, monkeypatch, 
     for o in outs[1:]:
         for k in ("spins", "inputs", "hist", "counts", "energy_trace", "cut_trace", "best_cut"):
             assert np.array_equal(outs[0][k], o[k]), k
+
+
+@pytest.mark.parametrize("t_res,sig_nu,want", [(40, 0.8, "packed"), (64, 3.0, "general"), (1, 0.0, "packed"),
+                                                (3, 2.0, "packed")])
+def test_variability_long_periods_and_many_divisors(oracle, t_res, sig_nu, want):
+    """Long periods need all 8 bit planes and sub-steps with many dividing
+    periods; a period >= 256 (after clamping to cycles * t_res) falls back to
+    the general path. Non-multiple-of-32 node count and trial count."""
+    g = random_graph(333, 21, weights=(-1, 1), p_edge=0.02)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, cycles=12, t_res=t_res)
+    T = 45
+    rng = np.random.default_rng(t_res)
+    vc = VariabilityConfig(0.3, 0.3, sig_nu, t_res=t_res)
+    profs = [sample_variability(vc, g.n, np.random.default_rng(int(rng.integers(1 << 30)))) for _ in range(T)]
+    keys = [streams.run_key(int(rng.integers(1 << 62))) for _ in range(T)]
+    b = _native.Batch(model, sch, keys, profile_rows=profile_rows(profs, model.n), graph=g,
+                      algo_code=Algorithm.PSA.code)
+    plan = _native.Plan(b)
+    assert plan.info()["path"] == want
+    plan.run()
+    got = plan.download()
+    plan.close()
+    want_out = oracle.anneal_batch(model, sch, "psa", profs, keys, graph=g)
+    for k in ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want_out[k]), k
