@@ -351,3 +351,29 @@ def test_variability_long_periods_and_many_divisors(oracle, t_res, sig_nu, want)
     want_out = oracle.anneal_batch(model, sch, "psa", profs, keys, graph=g)
     for k in ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "cut_trace", "best_cut"):
         assert np.array_equal(got[k], want_out[k]), k
+
+
+def test_concurrent_calls_from_threads_are_independent(bench_graphs):
+    """The C ABI is reentrant (ctypes releases the GIL; every call owns its
+    plan, stream and buffers), as the reference kernel is under the engine's
+    thread pool (engine.py:122-123): concurrent calls equal sequential ones."""
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = []
+    for k, (name, sig) in enumerate([("G81", (0, 0, 0)), ("G55", (0.5, 0.5, 0.5)), ("G1", (0.4, 0, 0)),
+                                     ("G22", (0, 0, 0)), ("G81", (0.3, 0.3, 0.3)), ("G48", (0, 0, 0))]):
+        g = bench_graphs(name)
+        model = maxcut_to_ising(g)
+        sch = derive_schedule(model, 40, 10)
+        seeds = [streams.trial_seed(k, j) for j in range(40)]
+        vc = VariabilityConfig(*sig)
+        profs = None if vc.is_ideal else [
+            sample_variability(vc, g.n, np.random.default_rng(streams.profile_seed(s))) for s in seeds]
+        jobs.append(_native.Batch(model, sch, [streams.run_key(s) for s in seeds],
+                                  profile_rows=profile_rows(profs, model.n), graph=g,
+                                  algo_code=Algorithm.PSA.code))
+    seq = [_native.anneal_batch(b)[0] for b in jobs]
+    with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        par = list(ex.map(lambda b: _native.anneal_batch(b)[0], jobs + jobs))
+    for k, out in enumerate(par):
+        for key in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
+            assert np.array_equal(out[key], seq[k % len(jobs)][key]), (k, key)
