@@ -241,7 +241,8 @@ struct pbsa_plan {
     bool tapsa_hist_from_raw = false;  // TAPSA alpha=1 routed to the packed path
     bool tapsa_packed = false;         // TAPSA alpha>=2 on the packed path (bit-sliced ring)
     bool spsa_packed = false;          // SPSA p>0 on the packed path (per-p-bit drive index)
-    DevBuf<uint32_t> sidx, sthi;       // [W][32][n]
+    DevBuf<uint32_t> sidx;             // [W][32][n] drive index per p-bit
+    DevBuf<uint32_t> thr_hi;           // [cycles][K] high words of the thresholds
     DevBuf<uint2> kfs;                 // [Tp] (F, C) of absorb(key, TAG_STALL) + GAMMA
     DevBuf<uint64_t> kstg;             // [Tp] absorb(key, TAG_STALL) + GAMMA
     DevBuf<double> i0_dev;             // [cycles]
@@ -774,7 +775,6 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             const double ps = std::ceil(std::ldexp(p_stall, 53));
             P.p_stall64 = ps >= 0x1p53 ? ~0ULL : ((uint64_t)ps << 11);
             P.sidx.alloc((size_t)P.W * 32 * n);
-            P.sthi.alloc((size_t)P.W * 32 * n);
             P.i0_dev.upload(P.i0, st);
         }
         if (P.tapsa_packed) {
@@ -801,6 +801,11 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                     thr[(size_t)c * P.K + raw + P.dmax] =
                         threshold_h64(pb_libm_tanh(P.i0[c] * (double)raw));
             P.thr.upload(thr, st);
+            if (P.spsa_packed) {
+                std::vector<uint32_t> hi(thr.size());
+                for (size_t k = 0; k < thr.size(); ++k) hi[k] = (uint32_t)(thr[k] >> 32);
+                P.thr_hi.upload(hi, st);
+            }
         }
         for (auto &b : P.p_spins) b.alloc((size_t)P.W * n);
         P.pacc.alloc((size_t)(cycles + 1) * P.Tp);
@@ -892,7 +897,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         int sm_count = 148;
         CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
         const bool big_graph = 13 * n >= (int64_t)sm_count * 1024;
-        P.phase_words = (!g_oneshot && !many_launches && big_graph && P.W >= 4 * 13) ? 13 : 0;
+        // (SpSA streams its per-p-bit drive index, which no phase keeps in L2: unphased)
+        P.phase_words = (!g_oneshot && !many_launches && big_graph && P.W >= 4 * 13 && !P.spsa_packed) ? 13 : 0;
         if (P.phase_words > 0) {  // equal phases
             const int64_t nph = (P.W + P.phase_words - 1) / P.phase_words;
             P.phase_words = (P.W + nph - 1) / nph;
@@ -907,7 +913,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         if (P.use_cache) P.acache.alloc(cache_entries);
         PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
                                               P.var_mode ? (P.var_uniform ? 1 : 2) : 0);
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16;
         const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
         set_packed_smem(kern, smem_up);
         set_packed_smem(packed_kernel_for(P.L, false, false), smem);
@@ -928,7 +934,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
         // small batches need many chains to hide launch gaps; large ones only a
         // couple (fewer graph nodes to instantiate)
-        int chains = many_launches ? 4 : (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
+        int chains = (many_launches || (P.spsa_packed && !g_oneshot && P.W >= 64)) ? 4
+                                                                     : (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
         if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
         chains = (int)std::min<int64_t>(chains, P.W);
         if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
@@ -1098,7 +1105,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
                                                  P.var_mode ? (P.var_uniform ? 1 : 2) : 0);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + pbsa::kPackedWarps * 32 * 8 + 16;
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
         // Word phases run one after another so that a phase's first-absorb
         // cache (PW words x n x 256 B) stays L2-resident across its cycles;
@@ -1165,7 +1172,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     }
                     if (P.spsa_packed) {
                         a.sidx = P.sidx.p + (size_t)w0 * 32 * P.n;
-                        a.sthi = P.sthi.p + (size_t)w0 * 32 * P.n;
+                        a.thr_hi_all = P.thr_hi.p;
                         a.kfs = P.kfs.p + w0 * 32;
                         a.kst = P.kstg.p + w0 * 32;
                         a.thr_all = P.thr.p;

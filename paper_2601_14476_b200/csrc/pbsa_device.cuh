@@ -134,7 +134,7 @@ struct PackedArgs {
     uint32_t count;           // global sub-step counter c * t_res (< 2^30)
     int do_update;            // 0: only accumulate pacc (final cut pass)
     uint32_t *sidx;           // SpSA: [W][32][n] threshold-table index of each p-bit's drive
-    uint32_t *sthi;           // SpSA: [W][32][n] high word of that threshold
+    const uint32_t *thr_hi_all;  // SpSA: [cycles][K] high words of all thresholds
     const uint2 *kfs;         // SpSA: [Tp] per-trial (F, C) of absorb(key, TAG_STALL)
     const uint64_t *kst;      // SpSA: [Tp] absorb(key, TAG_STALL) + GAMMA (exact slow path)
     const uint64_t *thr_all;  // SpSA: [cycles][K] all thresholds
@@ -439,7 +439,10 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     }
     uint2 *key = skey + wib * 32;
     key[lane] = live ? a.kfc[(size_t)w * 32 + lane] : make_uint2(0, 0);
-    uint32_t *scount = reinterpret_cast<uint32_t *>(skey + kPackedWarps * 32);
+    // SpSA: the per-trial constants of the stall stream, likewise per warp
+    uint2 *skeys = skey + kPackedWarps * 32;
+    if (SPSA) skeys[wib * 32 + lane] = live ? a.kfs[(size_t)w * 32 + lane] : make_uint2(0, 0);
+    uint32_t *scount = reinterpret_cast<uint32_t *>(skeys + kPackedWarps * 32);
     if (threadIdx.x == 0) scount[0] = a.count;
     __syncthreads();
     // Programmatic dependent launch: everything above reads only host-written
@@ -603,9 +606,10 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     const uint2 pst = make_uint2(~(uint32_t)(a.p_stall64 >> 32),
                                                  (uint32_t)(a.p_stall64 >> 32));
                     uint32_t gew = 0, ties = 0xffffffffu;
-#pragma unroll 4
+                    const uint2 *keys = skeys + wib * 32;
+#pragma unroll 8
                     for (int b = 31; b >= 0; --b) {
-                        const uint2 ks = a.kfs[(size_t)w * 32 + b];
+                        const uint2 ks = keys[b];
                         uint32_t sl, sh;
                         packed_first_absorb(ks.x ^ ui, ks.y, sl, sh);
                         ties = min(ties, packed_second_decide(sl, sh, count, pst, gew));
@@ -620,33 +624,46 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         }
                     }
                 }
-                // pass 2: drive (stalled: the stored threshold word, an independent
-                // coalesced load; fresh: this cycle's shared-memory table, stored
-                // together with its index), then the activation decision
-                uint32_t *sthi = a.sthi + (size_t)w * 32 * a.n + i;
+                // pass 2: drive (stalled: the stored index, a coalesced load, then
+                // its threshold's high word from the all-cycles table; fresh: this
+                // cycle's shared-memory table, and the index is stored), then the
+                // activation decision.  Eight trials per group: the stalled trials'
+                // loads are issued together before the group's decisions.
                 uint32_t word = 0, tie = 0xffffffffu;
-#pragma unroll 8
-                for (int b = 31; b >= 0; --b) {
-                    int pop = 0;
+                for (int gq = 3; gq >= 0; --gq) {
+                    uint32_t th[8];
 #pragma unroll
-                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
-                    uint2 t;
-                    if ((stallw >> b) & 1u) {
-                        const uint32_t thi = sthi[(size_t)b * a.n];
-                        t = make_uint2(~thi, thi);
-                    } else {
-                        t = NIB ? sthr[d * 16 + pop] : sthr[2 * pop - d + a.dmax];
-                        sidx[(size_t)b * a.n] = (uint32_t)(base + 2 * pop);
-                        sthi[(size_t)b * a.n] = t.y;
+                    for (int j = 7; j >= 0; --j) {
+                        const int b = gq * 8 + j;
+                        th[j] = ((stallw >> b) & 1u) ? sidx[(size_t)b * a.n] : 0u;
                     }
-                    if (CACHED) {
-                        const uint2 v = __ldcs(ctile + b * 32);
-                        tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
-                    } else {
-                        const uint2 kc = key[b];
-                        uint32_t sl, sh;
-                        packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
-                        tie = min(tie, packed_second_decide(sl, sh, count, t, word));
+#pragma unroll
+                    for (int j = 7; j >= 0; --j) {
+                        const int b = gq * 8 + j;
+                        if ((stallw >> b) & 1u) th[j] = __ldg(a.thr_hi_all + th[j]);
+                    }
+#pragma unroll
+                    for (int j = 7; j >= 0; --j) {
+                        const int b = gq * 8 + j;
+                        int pop = 0;
+#pragma unroll
+                        for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                        uint2 t;
+                        if ((stallw >> b) & 1u) {
+                            t = make_uint2(~th[j], th[j]);
+                        } else {
+                            t = NIB ? sthr[d * 16 + pop] : sthr[2 * pop - d + a.dmax];
+                            sidx[(size_t)b * a.n] = (uint32_t)(base + 2 * pop);
+                        }
+                        if (CACHED) {
+                            const uint2 v = __ldcs(ctile + b * 32);
+                            tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
+                        } else {
+                            const uint2 kc = key[b];
+                            uint32_t sl, sh;
+                            packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                            tie = min(tie, packed_second_decide(sl, sh, count, t, word));
+                        }
                     }
                 }
                 if (tie < 2) {  // rare near-tie in an activation draw: exact 64-bit test
