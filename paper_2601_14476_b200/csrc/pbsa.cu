@@ -399,7 +399,9 @@ PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = fal
             PBSA_TCASE(3)
             PBSA_TCASE(4)
             PBSA_TCASE(5)
-            default: fail(PBSA_EINVAL, "packed TApSA supports degree <= 31");
+            PBSA_TCASE(6)
+            PBSA_TCASE(7)
+            default: fail(PBSA_EINVAL, "packed TApSA supports degree <= 127");
         }
     }
     if (update && spsa) {
@@ -687,7 +689,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     // of each absorb into per-trial constants (pbsa_device.cuh)
     const bool small_counters = n <= (1LL << 30) && cycles * t_res <= (1LL << 30);
     // time-averaged rule on the packed path: sum of alpha counts must stay < 64
-    const bool tapsa_packed = algo == 1 && alpha >= 2 && alpha * dmax <= 63 && dmax <= 31;
+    // (the history sum S of alpha counts of at most dmax < 2^L lives in L + 3 planes)
+    int Lbits = 1;
+    while ((1 << Lbits) - 1 < dmax) ++Lbits;
+    const bool tapsa_packed = algo == 1 && alpha >= 2 && dmax <= 127 && alpha * dmax < (1LL << (Lbits + 3));
     // stalled rule on the packed path: per-p-bit threshold index into all cycles' tables
     const bool spsa_packed = algo == 2 && p_stall > 0.0 && cycles * (2 * dmax + 1) < (1LL << 31);
     // variability profile on the packed path: plain rule, finite lam/delta,
@@ -778,18 +783,16 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             P.i0_dev.upload(P.i0, st);
         }
         if (P.tapsa_packed) {
-            // thresholds per (cycle, degree d, S): acc = 2 S - f d, f = min(c+1, alpha),
-            // inp = i0 * (acc / f) exactly as _kernels.py:138 evaluates it
-            P.K = (P.dmax + 1) * 64;
+            // thresholds per (cycle, acc): acc = 2 S - f d in [-f dmax, f dmax],
+            // f = min(c+1, alpha), entry acc + f dmax; inp = i0 * (acc / f) exactly as
+            // _kernels.py:138 evaluates it
+            P.K = (int)(2 * alpha * P.dmax + 1);
             std::vector<uint64_t> thr((size_t)cycles * P.K, ~0ULL);
             for (int64_t c = 0; c < cycles; ++c) {
                 const int64_t f = std::min<int64_t>(c + 1, alpha);
-                for (int d = 0; d <= P.dmax; ++d)
-                    for (int64_t S = 0; S <= f * d && S < 64; ++S) {
-                        const double acc = (double)(2 * S - f * d);
-                        thr[(size_t)c * P.K + d * 64 + S] =
-                            threshold_h64(pb_libm_tanh(P.i0[c] * (acc / (double)f)));
-                    }
+                for (int64_t acc = -f * P.dmax; acc <= f * P.dmax; ++acc)
+                    thr[(size_t)c * P.K + acc + f * P.dmax] =
+                        threshold_h64(pb_libm_tanh(P.i0[c] * ((double)acc / (double)f)));
             }
             P.thr.upload(thr, st);
             P.ring.alloc((size_t)P.W * alpha * P.L * n);
@@ -1648,7 +1651,9 @@ void download_impl(pbsa_plan *P, int8_t *spins, double *inputs, double *hist, in
                     case 2: launch_hist_from_ring<2>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
                     case 3: launch_hist_from_ring<3>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
                     case 4: launch_hist_from_ring<4>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
-                    default: launch_hist_from_ring<5>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
+                    case 5: launch_hist_from_ring<5>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
+                    case 6: launch_hist_from_ring<6>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
+                    default: launch_hist_from_ring<7>(P->ring.p, P->rowptr.p, (int)n, (int)T, (int)P->alpha, written, dhist.p, st); break;
                 }
             }
             // copies first (asynchronous into page-locked buffers), then the

@@ -302,7 +302,6 @@ struct CutPlanes {
 // the drive is i0 * (acc / filled) with acc = 2 S - filled * d and
 // S = sum of p over the filled slots (< 64), so the threshold is a per-cycle
 // table lookup by (degree, S), exactly like the plain rule.
-constexpr int kTapsaPlanes = 6;
 
 // Bit-sliced count p = #{J_ik s_k = +1} (the local field, raw = 2p - d) of
 // the 32 trials over the neighbours [beg, end) of one node.
@@ -407,7 +406,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     constexpr bool NIB = L <= 4 && !TAPSA;
     uint2 *sthr = reinterpret_cast<uint2 *>(
         (reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
-    const int tab_entries = VAR ? 0 : TAPSA ? (a.dmax + 1) * 64 : NIB ? (a.dmax + 1) * 16 : a.K;
+    const int tab_entries = VAR ? 0 : TAPSA ? a.K : NIB ? (a.dmax + 1) * 16 : a.K;
     uint2 *skey = sthr + tab_entries;                     // [warps][32] {F, C}
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -419,7 +418,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     for (int k = threadIdx.x; k < tab_entries; k += blockDim.x) {
         uint32_t thi;
         if (TAPSA) {
-            thi = (uint32_t)(a.thr[k] >> 32);  // host table is already [degree][S]
+            thi = (uint32_t)(a.thr[k] >> 32);  // host table is already [acc + f dmax]
         } else {
             int raw = k - a.dmax;
             bool ok = true;
@@ -526,41 +525,48 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 if (exact) word |= var_exact_bits<L>(a, exact, p, d, w, i, count);
                 a.snew[(size_t)w * a.n + i] = word;
             } else if (UPDATE && TAPSA) {
-                // S = p of this cycle + the other filled slots of the ring
-                uint32_t S[kTapsaPlanes];
+                // S = p of this cycle + the other filled slots of the ring, in
+                // SP = L + 3 planes (the host admits alpha * dmax < 2^SP)
+                constexpr int SP = L + 3;
+                constexpr int SB = SP < 8 ? SP : 8;  // planes carried by the byte transposition
+                uint32_t S[SP];
 #pragma unroll
-                for (int r = 0; r < kTapsaPlanes; ++r) S[r] = r < L ? p[r] : 0u;
+                for (int r = 0; r < SP; ++r) S[r] = r < L ? p[r] : 0u;
                 uint32_t *ring = a.ring + (size_t)w * a.alpha * L * a.n + i;
                 for (int qs = 0; qs < a.filled; ++qs) {
                     if (qs == a.slot) continue;
                     uint32_t x[L];
 #pragma unroll
                     for (int r = 0; r < L; ++r) x[r] = ring[(size_t)(qs * L + r) * a.n];
-                    vc_add<L, kTapsaPlanes>(S, x);
+                    vc_add<L, SP>(S, x);
                 }
 #pragma unroll
                 for (int r = 0; r < L; ++r) ring[(size_t)(a.slot * L + r) * a.n] = p[r];
-                // byte-transpose S: B[k] byte j = S of trial 4k + j (the shifted
-                // copies of a 4-bit group never overlap, so the multiply is a spread)
+                // byte-transpose S: B[k] byte j = S of trial 4k + j (low 8 planes; the
+                // shifted copies of a 4-bit group never overlap, so the multiply is a spread)
                 uint32_t B[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     B[k] = 0;
 #pragma unroll
-                    for (int r = 0; r < kTapsaPlanes; ++r) {
+                    for (int r = 0; r < SB; ++r) {
                         const uint32_t x4 = (S[r] >> (4 * k)) & 0xFu;
                         B[k] |= (x4 * (0x00204081u << r)) & (0x01010101u << r);
                     }
                 }
-                const uint32_t rb = (uint32_t)__cvta_generic_to_shared(sthr) + (uint32_t)d * 512u;
+                // thresholds indexed by acc + f dmax = 2 S + f (dmax - d) (f = filled)
+                const int off = a.filled * (a.dmax - d);
+                const uint32_t rb = (uint32_t)__cvta_generic_to_shared(sthr) + 8u * (uint32_t)off;
                 const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
                 uint32_t word = 0, tie = 0xffffffffu;
                 const uint32_t ui = (uint32_t)i;
 #pragma unroll
                 for (int b = 31; b >= 0; --b) {
                     const int k = b >> 2, j = b & 3;
-                    const uint32_t x = j == 0 ? (B[k] << 3) : (B[k] >> (8 * j - 3));
-                    const uint32_t addr = (x & 0x1F8u) | rb;
+                    uint32_t sv = (B[k] >> (8 * j)) & 0xFFu;
+#pragma unroll
+                    for (int r = 8; r < SP; ++r) sv |= ((S[r] >> b) & 1u) << r;
+                    const uint32_t addr = rb + (sv << 4);
                     uint2 t;
                     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "r"(addr));
                     if (CACHED) {
@@ -577,17 +583,17 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     word = 0;
                     for (int b = 0; b < 32; ++b) {
                         int sb = 0;
-                        for (int r = 0; r < kTapsaPlanes; ++r) sb |= (int)((S[r] >> b) & 1u) << r;
+                        for (int r = 0; r < SP; ++r) sb |= (int)((S[r] >> b) & 1u) << r;
                         const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
                         const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
-                        word |= (uint32_t)hash_ge_exact(x2, a.thr[d * 64 + sb]) << b;
+                        word |= (uint32_t)hash_ge_exact(x2, a.thr[2 * sb + off]) << b;
                     }
                 }
                 a.snew[(size_t)w * a.n + i] = word;
                 if (a.raw_out) {  // last cycle only: acc = sum of the filled raw fields
                     for (int b = 0; b < 32; ++b) {
                         int sb = 0;
-                        for (int r = 0; r < kTapsaPlanes; ++r) sb |= (int)((S[r] >> b) & 1u) << r;
+                        for (int r = 0; r < SP; ++r) sb |= (int)((S[r] >> b) & 1u) << r;
                         a.raw_out[(size_t)i * a.Tp + w * 32 + b] = (int16_t)(2 * sb - a.filled * d);
                     }
                 }

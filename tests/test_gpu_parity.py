@@ -238,7 +238,9 @@ def test_packed_spsa_matches_oracle(oracle, bench_graphs, name, p_stall, cycles)
         assert np.array_equal(got[k], want[k]), k
 
 
-@pytest.mark.parametrize("name,alpha,cycles", [("G81", 4, 200), ("G55", 4, 120), ("G48", 7, 150)])
+@pytest.mark.parametrize("name,alpha,cycles", [("G81", 4, 200), ("G55", 4, 120), ("G48", 7, 150),
+                                               ("G1", 4, 60), ("G22", 4, 80), ("G81", 8, 50),
+                                               ("G1", 2, 40), ("G22", 11, 40)])
 def test_packed_tapsa_matches_oracle(oracle, bench_graphs, name, alpha, cycles):
     """Time-averaged rule on the packed path (bit-sliced history ring)."""
     g = bench_graphs(name)
