@@ -37,6 +37,11 @@ def golden_bench():
 
 
 @pytest.fixture(scope="session")
+def golden_acceptance():
+    return dict(np.load(GOLDEN / "acceptance.npz"))
+
+
+@pytest.fixture(scope="session")
 def golden_streams():
     return json.loads((GOLDEN / "streams.json").read_text())
 

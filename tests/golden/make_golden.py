@@ -20,6 +20,9 @@ Outputs:
   small.npz      14-node differential case of test_annealer.py:271-293:
                  all three rules x {ideal, varied} x seeds {0, 1}, full outputs
   bench.npz      benchmark-sized runs at cycles=1000 (G1/G22/G55/G81 analogs)
+  acceptance.npz per-trial results of the reference's acceptance criteria 4, 5
+                 and 7 (variability runs of all three rules); `make_golden.py
+                 acceptance` regenerates only this file
 """
 
 from __future__ import annotations
@@ -173,8 +176,47 @@ def make_bench() -> None:
     np.savez_compressed(OUT / "bench.npz", **out)
 
 
+def make_acceptance() -> None:
+    """Per-trial results behind the reference's acceptance criteria 4, 5 and 7
+    (/root/reference/pkg/tests/test_acceptance.py:156-230): the variability
+    runs of the plain, time-averaged and stalled rules."""
+    from pbitsa.engine import sweep
+    out = {}
+    g1 = to_graph(analogs.make_analog("G1"))
+    # criterion 4: plain rule, sigma_nu in {0, 1}, 50 trials
+    for sn in (0.0, 1.0):
+        spec = ExperimentSpec(graph="G1", algo=AlgorithmConfig(Algorithm.PSA),
+                              variability=VariabilityConfig(sigma_nu=sn, t_res=10),
+                              cycles=CYCLES, trials=50, base_seed=0, threads=8)
+        s = run_trials(spec, {"G1": g1})
+        out[f"c4_nu{sn:g}_final_cuts"] = np.array([r.final_cut for r in s.results])
+        print("criterion 4", sn, s.mean_cut, flush=True)
+    # criterion 5: time-averaged rule (alpha 4), sweep sigma_delta in {0, 0.5, 1}, 100 trials
+    spec = ExperimentSpec(graph="G1", algo=AlgorithmConfig(Algorithm.TAPSA, alpha=4),
+                          cycles=CYCLES, trials=100, base_seed=0, threads=8)
+    for v, s in zip((0.0, 0.5, 1.0), sweep(spec, "sigma_delta", [0.0, 0.5, 1.0], {"G1": g1})):
+        out[f"c5_delta{v:g}_final_cuts"] = np.array([r.final_cut for r in s.results])
+        print("criterion 5", v, s.mean_cut, flush=True)
+    # criterion 7 specs (120 cycles, 6 trials, seed 2): full cut traces
+    for name, kind, sig in (("G1", Algorithm.PSA, (0.0, 0.0, 0.3)),
+                            ("G47", Algorithm.TAPSA, (0.5, 0.0, 0.0)),
+                            ("G48", Algorithm.SPSA, (0.0, 0.5, 0.0))):
+        g = to_graph(analogs.make_analog(name))
+        spec = ExperimentSpec(graph=name, algo=AlgorithmConfig(kind), cycles=120, trials=6,
+                              base_seed=2, variability=VariabilityConfig(*sig), threads=2)
+        s = run_trials(spec, {name: g})
+        out[f"c7_{name}_{kind.value}_cut_traces"] = np.stack([r.cut_trace for r in s.results])
+        out[f"c7_{name}_{kind.value}_energy_traces"] = np.stack([r.energy_trace for r in s.results])
+        print("criterion 7", name, kind.value, s.mean_cut, flush=True)
+    np.savez_compressed(OUT / "acceptance.npz", **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["acceptance"]:
+        make_acceptance()
+        raise SystemExit
     make_streams()
     make_small()
     make_analogs()
     make_bench()
+    make_acceptance()

@@ -379,3 +379,51 @@ def test_concurrent_calls_from_threads_are_independent(bench_graphs):
     for k, out in enumerate(par):
         for key in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
             assert np.array_equal(out[key], seq[k % len(jobs)][key]), (k, key)
+
+
+def test_acceptance_criterion_4_timing_variability(golden_acceptance, bench_graphs):
+    """/root/reference/pkg/tests/test_acceptance.py:156-172: pSA on G1 with
+    sigma_nu = 1 beats sigma_nu = 0 by > 2 SE over 50 trials -- here every
+    per-trial final cut equals the reference's."""
+    g = bench_graphs("G1")
+    means, ses = {}, {}
+    for sn in (0.0, 1.0):
+        spec = engine.ExperimentSpec(graph="G1", algo=AlgorithmConfig(Algorithm.PSA),
+                                     variability=VariabilityConfig(sigma_nu=sn, t_res=10),
+                                     cycles=1000, trials=50)
+        s = engine.run_trials(spec, {"G1": g})
+        assert np.array_equal([r.final_cut for r in s.results],
+                              golden_acceptance[f"c4_nu{sn:g}_final_cuts"]), sn
+        means[sn], ses[sn] = s.mean_cut, s.std_cut / math.sqrt(50)
+    assert means[1.0] - means[0.0] > 2.0 * math.hypot(ses[1.0], ses[0.0])
+
+
+def test_acceptance_criterion_5_offset_sweep_time_averaged(golden_acceptance, bench_graphs):
+    """test_acceptance.py:173-187: TApSA (alpha 4) on G1 swept over
+    sigma_delta in {0, 0.5, 1} (one device batch), 100 trials each: per-trial
+    final cuts equal the reference's and the normalized means vary < 0.02."""
+    g = bench_graphs("G1")
+    spec = engine.ExperimentSpec(graph="G1", algo=AlgorithmConfig(Algorithm.TAPSA, alpha=4),
+                                 cycles=1000, trials=100)
+    sums = engine.sweep(spec, "sigma_delta", [0.0, 0.5, 1.0], {"G1": g})
+    for v, s in zip((0.0, 0.5, 1.0), sums):
+        assert np.array_equal([r.final_cut for r in s.results],
+                              golden_acceptance[f"c5_delta{v:g}_final_cuts"]), v
+    norms = [s.mean_cut / 11605 for s in sums]
+    assert max(norms) - min(norms) < 0.02
+
+
+@pytest.mark.parametrize("name,kind,sig", [("G1", Algorithm.PSA, (0.0, 0.0, 0.3)),
+                                           ("G47", Algorithm.TAPSA, (0.5, 0.0, 0.0)),
+                                           ("G48", Algorithm.SPSA, (0.0, 0.5, 0.0))])
+def test_acceptance_criterion_7_specs(golden_acceptance, bench_graphs, name, kind, sig):
+    """The three specs of test_acceptance.py:205-230 (120 cycles, 6 trials,
+    seed 2): full cut and energy traces equal the reference's."""
+    g = bench_graphs(name)
+    spec = engine.ExperimentSpec(graph=name, algo=AlgorithmConfig(kind), cycles=120, trials=6,
+                                 base_seed=2, variability=VariabilityConfig(*sig))
+    s = engine.run_trials(spec, {name: g})
+    assert np.array_equal(np.stack([r.cut_trace for r in s.results]),
+                          golden_acceptance[f"c7_{name}_{kind.value}_cut_traces"])
+    assert np.array_equal(np.stack([r.energy_trace for r in s.results]),
+                          golden_acceptance[f"c7_{name}_{kind.value}_energy_traces"])

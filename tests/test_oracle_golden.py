@@ -87,3 +87,25 @@ def test_profile_golden_prefix(golden_bench, bench_graphs):
         assert np.array_equal(profs[0].lam[:3], golden_bench[p + "lam3"])
         assert np.array_equal(profs[0].delta[:3], golden_bench[p + "delta3"])
         assert np.array_equal(profs[0].period[:8], golden_bench[p + "period8"])
+
+
+@pytest.mark.parametrize("name,kind,sig", [("G1", "psa", (0.0, 0.0, 0.3)),
+                                           ("G47", "tapsa", (0.5, 0.0, 0.0)),
+                                           ("G48", "spsa", (0.0, 0.5, 0.0))])
+def test_oracle_acceptance_criterion_7_specs(oracle, golden_acceptance, bench_graphs, name, kind, sig):
+    """Variability runs of all three rules (test_acceptance.py:205-230 specs:
+    120 cycles, 6 trials, seed 2, default alpha 4 / p_stall 0.5)."""
+    from paper_2601_14476_b200 import streams
+    from paper_2601_14476_b200.annealer import derive_schedule
+    from paper_2601_14476_b200.model import maxcut_to_ising
+    from paper_2601_14476_b200.pbit import VariabilityConfig, sample_variability
+    g = bench_graphs(name)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 120, 10)
+    seeds = [streams.trial_seed(2, k) for k in range(6)]
+    profs = [sample_variability(VariabilityConfig(*sig), g.n,
+                                np.random.default_rng(streams.profile_seed(s))) for s in seeds]
+    out = oracle.anneal_batch(model, sch, kind, profs, [streams.run_key(s) for s in seeds], graph=g,
+                              alpha=4, p_stall=0.5)
+    assert np.array_equal(out["cut_trace"], golden_acceptance[f"c7_{name}_{kind}_cut_traces"])
+    assert np.array_equal(out["energy_trace"], golden_acceptance[f"c7_{name}_{kind}_energy_traces"])
