@@ -427,3 +427,24 @@ def test_acceptance_criterion_7_specs(golden_acceptance, bench_graphs, name, kin
                           golden_acceptance[f"c7_{name}_{kind.value}_cut_traces"])
     assert np.array_equal(np.stack([r.energy_trace for r in s.results]),
                           golden_acceptance[f"c7_{name}_{kind.value}_energy_traces"])
+
+
+def test_acceptance_criteria_6_and_8_schedule_endpoints_and_largest_graph(bench_graphs):
+    """test_acceptance.py:189-203 and 233-255: on every benchmark the recorded
+    i0 sequence starts at i0_min, ends at i0_max (1e-9 relative) and increases;
+    G81 TApSA (alpha 4) for one trial is well inside the 600 s budget."""
+    import time
+    from paper_2601_14476_b200 import benchmarks
+    for name in benchmarks.BENCHMARKS:
+        g = bench_graphs(name)
+        model = maxcut_to_ising(g)
+        sch = derive_schedule(model, cycles=1000)
+        t0 = time.perf_counter()
+        res = run_anneal(model, sch, AlgorithmConfig(Algorithm.TAPSA), VariabilityProfile.ideal(model.n),
+                         seed=0, graph=g)
+        elapsed = time.perf_counter() - t0
+        assert res.i0_trace[0] == sch.i0_min, name
+        assert abs(res.i0_trace[-1] - sch.i0_max) / sch.i0_max <= 1e-9, name
+        assert np.all(np.diff(res.i0_trace) > 0), name
+        if name == "G81":
+            assert (g.n, g.m) == (20000, 40000) and elapsed < 600.0
