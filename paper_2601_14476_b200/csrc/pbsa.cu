@@ -285,6 +285,10 @@ struct pbsa_plan {
         bool update, inp;
     };
     std::vector<PLaunch> plaunch;
+    // resident mode: one cluster per word anneals all cycles in one launch
+    bool resident = false;
+    int res_cs = 1, res_threads = 256;
+    size_t res_smem = 0;
 
     // general path
     DevBuf<int8_t> g_spins[2];
@@ -429,6 +433,23 @@ PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = fal
     }
 #undef PBSA_CASE
 #undef PBSA_TCASE
+}
+
+using ResidentKernel = void (*)(pbsa::ResidentArgs);
+ResidentKernel resident_kernel_for(int L, bool cached) {
+    switch (L) {
+#define PBSA_RCASE(l) \
+    case l: return cached ? pbsa::resident_sweep<l, true> : pbsa::resident_sweep<l, false>;
+        PBSA_RCASE(1)
+        PBSA_RCASE(2)
+        PBSA_RCASE(3)
+        PBSA_RCASE(4)
+        PBSA_RCASE(5)
+        PBSA_RCASE(6)
+        PBSA_RCASE(7)
+#undef PBSA_RCASE
+        default: fail(PBSA_EINVAL, "resident sweep supports degree <= 127");
+    }
 }
 
 template <int L>
@@ -951,6 +972,43 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             P.ev_join.push_back(e);
         }
         P.packed_blocks = (int)grid_for(P.W * wpw, pbsa::kPackedWarps);
+        // resident mode (plain rule, ideal profile): a word's double-buffered
+        // state in shared memory; cluster size so that W clusters cover the SMs
+        {
+            const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode;
+            const int tab = (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
+            P.res_smem = 512 + (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;
+            int max_smem = 0;
+            CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+            // measured: small batches (<= 64 words) of small dense graphs (n <= 2500,
+            // mean degree >= 8: G1, G47, G22) run 1.1-2.2x faster resident; sparse
+            // or larger problems are faster with launched sweeps
+            bool want = P.W <= 64 && n <= 2500 && nnz >= 8 * n;
+            if (const char *env = std::getenv("PBSA_RESIDENT")) want = env[0] == '1';
+            int csz = 1;  // (measured: 8 for a handful of words, 4 beats 8 at 32 words)
+            while (csz < (P.W <= 8 ? 8 : 4) && P.W * csz < sms) csz *= 2;
+            if (const char *env = std::getenv("PBSA_RESIDENT_CS")) csz = std::max(1, std::atoi(env));
+            const int64_t per = (n + csz - 1) / csz;
+            int64_t slice = 0;  // largest CTA slice of the adjacency
+            for (int64_t r = 0; r < csz; ++r) {
+                const int64_t lo = std::min<int64_t>(n, r * per), hi = std::min<int64_t>(n, lo + per);
+                slice = std::max<int64_t>(slice, indptr[hi] - indptr[lo]);
+            }
+            P.res_smem += 4 * (size_t)(per + 1 + slice);
+            if (plain && want && P.res_smem <= (size_t)max_smem) {
+                int thr = (int)std::min<int64_t>(1024, ((per + 31) / 32) * 32);
+                // the per-thread cut counter takes up to 32 nodes
+                while ((per + thr - 1) / thr > 32 && thr < 1024) thr *= 2;
+                P.resident = true;
+                P.res_cs = csz;
+                P.res_threads = thr;
+                if (P.use_cache && P.phase_words < P.W) P.acache.alloc((size_t)P.W * P.chunks * 1024);
+                P.phase_words = P.W;
+                ResidentKernel rk = resident_kernel_for(P.L, P.use_cache);
+                CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
+                if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            }
+        }
         P.updates_per_run = (int64_t)n * trials * cycles;
         if (many_launches) {  // sum over p-bits of #{count < cycles t_res : period | count}
             int64_t ups = 0;
@@ -1117,7 +1175,49 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         // the others' blocks.
         const int G = (int)P.chain_streams.size() + 1;
         int cur = 0;
-        for (int64_t p0 = 0; p0 < P.W; p0 += P.phase_words) {
+        if (P.resident) {
+            if (P.use_cache) {
+                pbsa::packed_cache_init<<<grid_for(P.W * P.chunks * 1024, TB), TB, 0, st>>>(
+                    P.acache.p, P.krg.p, (int)P.n, P.chunks, (int)P.W);
+                ++P.launches;
+            }
+            pbsa::ResidentArgs r{};
+            r.s_in = P.p_spins[0].p;
+            r.s_out = P.p_spins[1].p;
+            r.rowptr = P.rowptr.p;
+            r.adj = P.adj.p;
+            r.kfc = P.kfc.p;
+            r.acache = P.use_cache ? P.acache.p : nullptr;
+            r.krg = P.krg.p;
+            r.thr = P.thr.p;
+            r.pacc = P.pacc.p;
+            r.raw_out = P.raw_last.p;
+            r.n = (int)P.n;
+            r.W = (int)P.W;
+            r.Tp = (int)P.Tp;
+            r.K = P.K;
+            r.dmax = P.dmax;
+            r.chunks = P.chunks;
+            r.cycles = (int)P.cycles;
+            r.t_res = (int)P.t_res;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)(P.W * P.res_cs));
+            cfg.blockDim = dim3((unsigned)P.res_threads);
+            cfg.dynamicSmemBytes = P.res_smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)P.res_cs;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&cfg, resident_kernel_for(P.L, P.use_cache), r));
+            ++P.launches;
+            P.sweep_launches = P.cycles;
+            cur = 1;
+        }
+        for (int64_t p0 = 0; p0 < P.W && !P.resident; p0 += P.phase_words) {
             const int64_t p1 = std::min<int64_t>(P.W, p0 + P.phase_words);
             if (P.use_cache) {
                 pbsa::packed_cache_init<<<grid_for((p1 - p0) * P.chunks * 1024, TB), TB, 0, st>>>(

@@ -22,6 +22,7 @@
 // Both paths draw every random number from the same splitmix-style counter
 // hash as streams.py:29-55, regenerated in-kernel from (key, tag, node, count).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -305,22 +306,58 @@ struct CutPlanes {
 
 // Bit-sliced count p = #{J_ik s_k = +1} (the local field, raw = 2p - d) of
 // the 32 trials over the neighbours [beg, end) of one node.
-template <int L>
-__device__ __forceinline__ void gather_counts(const uint32_t *__restrict__ adj,
-                                              const uint32_t *__restrict__ sw, uint32_t beg,
-                                              uint32_t end, uint32_t (&p)[L]) {
+// Carry-save adder: (h, l) = a + b + l as bit-sliced digits (two LOP3s).
+__device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32_t b) {
+    const uint32_t u = l ^ a;
+    h = (l & a) | (u & b);
+    l = u ^ b;
+}
+
+// Bit-sliced count over neighbours [beg, end), the neighbour word of entry k
+// given by nb(k).  Degrees >= 8 go through a Harley-Seal carry-save tree
+// (seven CSAs per eight neighbours, ~2 ops each, plus one ripple of the
+// weight-8 digit) instead of an L-plane ripple per neighbour.
+template <int L, typename NB>
+__device__ __forceinline__ void count_neighbours(uint32_t beg, uint32_t end, NB nb, uint32_t (&p)[L]) {
 #pragma unroll
     for (int r = 0; r < L; ++r) p[r] = 0;
-    for (uint32_t k = beg; k < end; ++k) {
-        const uint32_t e = __ldg(adj + k);
-        uint32_t cp = __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
+    auto ripple = [&](uint32_t cp, int from) {
 #pragma unroll
         for (int r = 0; r < L; ++r) {
+            if (r < from) continue;
             const uint32_t np = p[r] & cp;
             p[r] ^= cp;
             cp = np;
         }
+    };
+    uint32_t k = beg;
+    if (L >= 4) {
+        for (; k + 8 <= end; k += 8) {
+            uint32_t x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = nb(k + j);
+            uint32_t twosA, twosB, foursA, foursB, eights;
+            csa(twosA, p[0], x[0], x[1]);
+            csa(twosB, p[0], x[2], x[3]);
+            csa(foursA, p[1], twosA, twosB);
+            csa(twosA, p[0], x[4], x[5]);
+            csa(twosB, p[0], x[6], x[7]);
+            csa(foursB, p[1], twosA, twosB);
+            csa(eights, p[2], foursA, foursB);
+            ripple(eights, 3);
+        }
     }
+    for (; k < end; ++k) ripple(nb(k), 0);
+}
+
+template <int L>
+__device__ __forceinline__ void gather_counts(const uint32_t *__restrict__ adj,
+                                              const uint32_t *__restrict__ sw, uint32_t beg,
+                                              uint32_t end, uint32_t (&p)[L]) {
+    count_neighbours<L>(beg, end, [&](uint32_t k) {
+        const uint32_t e = __ldg(adj + k);
+        return __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
+    }, p);
 }
 
 // Cut count g = #{J_ik s_i s_k = +1} = (s_i = +1) ? p : d - p, bit-sliced:
@@ -899,6 +936,178 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
         }
     }
     warp_cut_flush(C, dsum, lane, live ? a.pacc + (size_t)w * 32 : nullptr);
+}
+
+// ------------------------------------------------ resident multi-cycle sweep
+// For words whose whole spin state fits shared memory (8 n bytes double
+// buffered, n <= ~25k), one thread-block cluster anneals one trial word for
+// ALL cycles in a single launch: every CTA keeps a full copy of the word's
+// state in shared memory, updates its slice of the nodes (gather from local
+// shared memory, the packed kernel's decision), and writes each new word into
+// its own and every peer CTA's next buffer through distributed shared memory;
+// one cluster barrier per cycle is the synchronous commit of _kernels.py:151-155.
+// No per-cycle launches and no state traffic through L2 -- the lever for
+// small graphs and batches, where per-cycle launch latency dominates.
+struct ResidentArgs {
+    const uint32_t *s_in;       // [W][n] initial words
+    uint32_t *s_out;            // [W][n] final words
+    const uint32_t *rowptr;     // [n+1]
+    const uint32_t *adj;        // [nnz] column | (J < 0) << 31
+    const uint2 *kfc;           // [Tp] folded per-trial constants
+    const uint2 *acache;        // [W][chunks][32][32] first-absorb cache, or null
+    const uint64_t *krg;        // [Tp] absorb(key, TAG_R) + GAMMA
+    const uint64_t *thr;        // [cycles][K] thresholds
+    unsigned long long *pacc;   // [cycles+1][Tp]
+    int16_t *raw_out;           // [n][Tp] raw fields of the last cycle
+    int n, W, Tp, K, dmax, chunks, cycles, t_res;
+};
+
+constexpr int kResidentExtraPlanes = 3;  // cut counters for up to 32 nodes per thread
+
+template <int L, bool CACHED>
+__global__ void __launch_bounds__(1024, 1) resident_sweep(ResidentArgs a) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CS = (int)cluster.num_blocks();
+    const int rank = (int)cluster.block_rank();
+    const int w = (int)(blockIdx.x / CS);
+    constexpr bool NIB = L <= 4;
+    extern __shared__ unsigned long long smem_u64[];
+    uint2 *sthr = reinterpret_cast<uint2 *>((reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
+    const int tab_entries = NIB ? (a.dmax + 1) * 16 : a.K;
+    uint2 *key = sthr + tab_entries;
+    uint32_t *S0 = reinterpret_cast<uint32_t *>(key + 32);
+    uint32_t *S1 = S0 + a.n;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (int k = tid; k < a.n; k += blockDim.x) S0[k] = a.s_in[(size_t)w * a.n + k];
+    if (tid < 32) key[tid] = a.kfc[(size_t)w * 32 + tid];
+    const int per = (a.n + CS - 1) / CS;
+    const int lo = rank * per, hi = min(a.n, lo + per);
+    // this CTA's nodes' CSR rows in shared memory too (a cluster barrier
+    // flushes L1, which would otherwise re-fetch them from L2 every cycle)
+    uint32_t *rowS = S1 + a.n;                  // [hi - lo + 1], relative offsets
+    uint32_t *adjS = rowS + (per + 1);          // [rowptr[hi] - rowptr[lo]]
+    const uint32_t r0 = a.rowptr[lo], r1 = a.rowptr[hi];
+    for (int k = tid; k <= hi - lo; k += blockDim.x) rowS[k] = a.rowptr[lo + k] - r0;
+    for (uint32_t k = tid; k < r1 - r0; k += blockDim.x) adjS[k] = a.adj[r0 + k];
+    uint32_t *cs = S0, *ns = S1;
+    constexpr int CP = L + 2 + kResidentExtraPlanes;
+    cluster.sync();  // every CTA of the cluster runs before any shared-memory exchange
+
+    for (int c = 0; c <= a.cycles; ++c) {
+        const int cc = c < a.cycles ? c : a.cycles - 1;
+        const uint64_t *thr = a.thr + (size_t)cc * a.K;
+        __syncthreads();  // the previous cycle's table readers are done
+        for (int k = tid; k < tab_entries; k += blockDim.x) {
+            int raw = k - a.dmax;
+            bool ok = true;
+            if (NIB) {
+                const int d = k >> 4, pp = k & 15;
+                raw = 2 * pp - d;
+                ok = pp <= d;
+            }
+            const uint32_t thi = ok ? (uint32_t)(thr[raw + a.dmax] >> 32) : 0u;
+            const uint64_t n2 = (uint64_t)(~thi) + 2u;
+            sthr[k] = make_uint2((uint32_t)n2, (uint32_t)(n2 >> 32));
+        }
+        __syncthreads();
+        const uint32_t count = (uint32_t)(c * a.t_res);
+        uint32_t C[CP];
+#pragma unroll
+        for (int r = 0; r < CP; ++r) C[r] = 0;
+        int dsum = 0;
+        for (int base = lo + warp * 32; base < hi; base += nwarps * 32) {
+            const int i = base + lane;
+            if (i >= hi) continue;
+            const uint32_t beg = rowS[i - lo], end = rowS[i - lo + 1];
+            const uint32_t own = cs[i];
+            uint32_t p[L];
+            count_neighbours<L>(beg, end, [&](uint32_t k) {
+                const uint32_t e = adjS[k];
+                return cs[e & 0x7fffffffu] ^ (uint32_t)((int32_t)e >> 31);
+            }, p);
+            const int d = (int)(end - beg);
+            uint32_t g[L];
+            cut_counts<L>(p, own, d, g);
+            dsum += d;
+            vc_add<L, CP>(C, g);
+            if (c == a.cycles) continue;  // final cut pass
+            const uint32_t ui = (uint32_t)i;
+            const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + (i >> 5)) * 1024 + (i & 31) : nullptr;
+            uint32_t word = 0, tie = 0xffffffffu;
+            uint32_t N[4] = {0u, 0u, 0u, 0u};
+            uint32_t rb = 0;
+            if (NIB) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                    for (int r = 0; r < L; ++r) {
+                        uint32_t x = (p[r] >> (8 * k)) & 0xFFu;
+                        x = (x | (x << 12)) & 0x000F000Fu;
+                        x = (x | (x << 6)) & 0x03030303u;
+                        x = (x | (x << 3)) & 0x11111111u;
+                        N[k] |= x << r;
+                    }
+                }
+                rb = (uint32_t)__cvta_generic_to_shared(sthr) + (uint32_t)d * 128u;
+            }
+            const uint2 *tb = sthr + (a.dmax - d);
+#pragma unroll
+            for (int b = 31; b >= 0; --b) {
+                uint2 t;
+                if (NIB) {
+                    const int k = b >> 3, j = b & 7;
+                    const uint32_t x = j == 0 ? (N[k] << 3) : (N[k] >> (4 * j - 3));
+                    const uint32_t addr = (x & 0x78u) | rb;
+                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "r"(addr));
+                } else {
+                    int pop = 0;
+#pragma unroll
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                    t = tb[2 * pop];
+                }
+                if (CACHED) {
+                    const uint2 v = __ldcs(ctile + b * 32);
+                    tie = min(tie, packed_decide_n2(v.x ^ count, v.y, t, word));
+                } else {
+                    const uint2 kc = key[b];
+                    uint32_t sl, sh;
+                    packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                    tie = min(tie, packed_second_decide_n2(sl, sh, count, t, word));
+                }
+            }
+            if (tie < 3) {  // rare: a draw within 1 of its threshold -> exact 64-bit test
+                word = 0;
+                for (int b = 0; b < 32; ++b) {
+                    int pop = 0;
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                    const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
+                    const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                    word |= (uint32_t)hash_ge_exact(x2, thr[2 * pop - d + a.dmax]) << b;
+                }
+            }
+            ns[i] = word;
+            for (int r = 1; r < CS; ++r) {  // the peers' copies of this word
+                const int peer = rank + r < CS ? rank + r : rank + r - CS;
+                *cluster.map_shared_rank(ns + i, peer) = word;
+            }
+            if (a.raw_out && c == a.cycles - 1) {
+                for (int b = 0; b < 32; ++b) {
+                    int pop = 0;
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                    a.raw_out[(size_t)i * a.Tp + w * 32 + b] = (int16_t)(2 * pop - d);
+                }
+            }
+        }
+        warp_cut_flush(C, dsum, lane, a.pacc + (size_t)c * a.Tp + (size_t)w * 32);
+        if (c < a.cycles) {
+            cluster.sync();  // every copy of the next state is complete
+            uint32_t *t = cs;
+            cs = ns;
+            ns = t;
+        }
+    }
+    for (int i = lo + tid; i < hi; i += blockDim.x) a.s_out[(size_t)w * a.n + i] = cs[i];
 }
 
 // Packed spins [W][n] -> int8 [T][n]
