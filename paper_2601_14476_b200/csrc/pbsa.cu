@@ -286,9 +286,10 @@ struct pbsa_plan {
     };
     std::vector<PLaunch> plaunch;
     // resident mode: one cluster per word anneals all cycles in one launch
-    bool resident = false;
+    bool resident = false, res_timing = false;
     int res_cs = 1, res_threads = 256;
     size_t res_smem = 0;
+    DevBuf<pbsa::RLaunch> rlaunch;     // resident timing: the sub-step list
 
     // general path
     DevBuf<int8_t> g_spins[2];
@@ -436,6 +437,20 @@ PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = fal
 }
 
 using ResidentKernel = void (*)(pbsa::ResidentArgs);
+using ResidentTimingKernel = void (*)(pbsa::ResidentTimingArgs);
+ResidentTimingKernel resident_timing_for(int L) {
+    switch (L) {
+        case 1: return pbsa::resident_timing<1>;
+        case 2: return pbsa::resident_timing<2>;
+        case 3: return pbsa::resident_timing<3>;
+        case 4: return pbsa::resident_timing<4>;
+        case 5: return pbsa::resident_timing<5>;
+        case 6: return pbsa::resident_timing<6>;
+        case 7: return pbsa::resident_timing<7>;
+        default: fail(PBSA_EINVAL, "resident sweep supports degree <= 127");
+    }
+}
+
 ResidentKernel resident_kernel_for(int L, bool cached) {
     switch (L) {
 #define PBSA_RCASE(l) \
@@ -976,6 +991,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // state in shared memory; cluster size so that W clusters cover the SMs
         {
             const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode;
+            const bool timing = P.var_mode && !P.var_uniform;
             const int tab = (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
             P.res_smem = 512 + (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;
             int max_smem = 0;
@@ -995,10 +1011,27 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 slice = std::max<int64_t>(slice, indptr[hi] - indptr[lo]);
             }
             P.res_smem += 4 * (size_t)(per + 1 + slice);
-            if (plain && want && P.res_smem <= (size_t)max_smem) {
-                int thr = (int)std::min<int64_t>(1024, ((per + 31) / 32) * 32);
-                // the per-thread cut counter takes up to 32 nodes
-                while ((per + thr - 1) / thr > 32 && thr < 1024) thr *= 2;
+            if (timing) {
+                const int64_t thr = std::min<int64_t>(512, ((per + 31) / 32) * 32);
+                P.res_smem = 32 * 8 + 8 * (size_t)n + (thr / 32) * (256 + 4096) + pbsa::kMaxDivisors * 32 +
+                             4 * (size_t)(P.nplanes * per + per + 1 + slice) + 64;
+            }
+            if (timing && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
+                P.resident = true;
+                P.res_timing = true;
+                P.res_cs = csz;
+                P.res_threads = (int)std::min<int64_t>(512, ((per + 31) / 32) * 32);
+                std::vector<pbsa::RLaunch> rl;
+                for (const pbsa_plan::PLaunch &pl : P.plaunch)
+                    rl.push_back({pl.count, (int)pl.cycle, pl.do_cut, pl.ndiv, (int)pl.div_off, pl.inp ? 1 : 0,
+                                  P.i0[std::min<int64_t>(pl.cycle, cycles - 1)]});
+                P.rlaunch.upload(rl, st);
+                if (!P.i0_dev.n) P.i0_dev.upload(P.i0, st);
+                ResidentTimingKernel rk = resident_timing_for(P.L);
+                CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
+            } else if (plain && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
+                // (the per-thread cut counter takes up to 32 nodes)
+                const int thr = (int)std::min<int64_t>(512, ((per + 31) / 32) * 32);
                 P.resident = true;
                 P.res_cs = csz;
                 P.res_threads = thr;
@@ -1175,7 +1208,47 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         // the others' blocks.
         const int G = (int)P.chain_streams.size() + 1;
         int cur = 0;
-        if (P.resident) {
+        if (P.resident && P.res_timing) {
+            pbsa::ResidentTimingArgs r{};
+            r.s_in = P.p_spins[0].p;
+            r.s_out = P.p_spins[1].p;
+            r.rowptr = P.rowptr.p;
+            r.adj = P.adj.p;
+            r.kfc = P.kfc.p;
+            r.krg = P.krg.p;
+            r.prof = P.prof.p;
+            r.lam64 = P.lam64.p;
+            r.del64 = P.del64.p;
+            r.pplanes = P.pplanes.p;
+            r.divs = P.vdivs.p;
+            r.launches = P.rlaunch.p;
+            r.nlaunch = (int)P.rlaunch.n;
+            r.i0 = P.i0_dev.p;
+            r.pacc = P.pacc.p;
+            r.inp_out = P.inp_var.p;
+            r.n = (int)P.n;
+            r.W = (int)P.W;
+            r.Tp = (int)P.Tp;
+            r.nplanes = P.nplanes;
+            r.cycles = (int)P.cycles;
+            r.margin = P.var_margin;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)(P.W * P.res_cs));
+            cfg.blockDim = dim3((unsigned)P.res_threads);
+            cfg.dynamicSmemBytes = P.res_smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = (unsigned)P.res_cs;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CK(cudaLaunchKernelEx(&cfg, resident_timing_for(P.L), r));
+            ++P.launches;
+            P.sweep_launches = (int64_t)P.rlaunch.n - 1;
+            cur = 1;
+        } else if (P.resident) {
             if (P.use_cache) {
                 pbsa::packed_cache_init<<<grid_for(P.W * P.chunks * 1024, TB), TB, 0, st>>>(
                     P.acache.p, P.krg.p, (int)P.n, P.chunks, (int)P.W);

@@ -965,7 +965,7 @@ struct ResidentArgs {
 constexpr int kResidentExtraPlanes = 3;  // cut counters for up to 32 nodes per thread
 
 template <int L, bool CACHED>
-__global__ void __launch_bounds__(1024, 1) resident_sweep(ResidentArgs a) {
+__global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int CS = (int)cluster.num_blocks();
@@ -1102,6 +1102,223 @@ __global__ void __launch_bounds__(1024, 1) resident_sweep(ResidentArgs a) {
         warp_cut_flush(C, dsum, lane, a.pacc + (size_t)c * a.Tp + (size_t)w * 32);
         if (c < a.cycles) {
             cluster.sync();  // every copy of the next state is complete
+            uint32_t *t = cs;
+            cs = ns;
+            ns = t;
+        }
+    }
+    for (int i = lo + tid; i < hi; i += blockDim.x) a.s_out[(size_t)w * a.n + i] = cs[i];
+}
+
+// Resident variant of the timing-spread kernel (packed_sweep_timing): one
+// cluster per trial word runs every sub-step of the run in one launch, the
+// word's state, CSR slice and bit-sliced periods in shared memory, one
+// cluster barrier per sub-step.  With ten sub-steps per cycle the launched
+// form is bound by launch latency on small graphs; this removes it.
+struct RLaunch {
+    uint32_t count;
+    int cycle, do_cut, ndiv, div_off, inp;
+    double i0;
+};
+
+struct ResidentTimingArgs {
+    const uint32_t *s_in;
+    uint32_t *s_out;
+    const uint32_t *rowptr, *adj;
+    const uint2 *kfc;
+    const uint64_t *krg;
+    const float2 *prof;         // [Tp][n]
+    const double *lam64, *del64;
+    const uint32_t *pplanes;    // [W][nplanes][n]
+    const uint8_t *divs;
+    const RLaunch *launches;
+    int nlaunch;
+    const double *i0;           // [cycles]
+    unsigned long long *pacc;   // [cycles+1][Tp]
+    double *inp_out;            // [Tp][n]
+    int n, W, Tp, nplanes, cycles;
+    float margin;
+};
+
+template <int L>
+__global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CS = (int)cluster.num_blocks();
+    const int rank = (int)cluster.block_rank();
+    const int w = (int)(blockIdx.x / CS);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int per = (a.n + CS - 1) / CS;
+    const int lo = rank * per, hi = min(a.n, lo + per);
+    extern __shared__ unsigned long long smem_u64[];
+    uint2 *key = reinterpret_cast<uint2 *>(smem_u64);        // [32]
+    uint32_t *S0 = reinterpret_cast<uint32_t *>(key + 32);   // [n]
+    uint32_t *S1 = S0 + a.n;                                  // [n]
+    uint32_t *res = S1 + a.n;                                 // [nwarps][32]
+    uint32_t *exm = res + nwarps * 32;                        // [nwarps][32]
+    uint32_t *fl = exm + nwarps * 32;                         // [nwarps][1024]
+    uint32_t *sdivx = fl + nwarps * 1024;                     // [kMaxDivisors][8]
+    uint32_t *plS = sdivx + kMaxDivisors * 8;                 // [nplanes][per]
+    uint32_t *rowS = plS + a.nplanes * per;                   // [per + 1]
+    uint32_t *adjS = rowS + per + 1;
+    for (int k = tid; k < a.n; k += blockDim.x) S0[k] = a.s_in[(size_t)w * a.n + k];
+    if (tid < 32) key[tid] = a.kfc[(size_t)w * 32 + tid];
+    const uint32_t r0 = a.rowptr[lo], r1 = a.rowptr[hi];
+    for (int k = tid; k <= hi - lo; k += blockDim.x) rowS[k] = a.rowptr[lo + k] - r0;
+    for (uint32_t k = tid; k < r1 - r0; k += blockDim.x) adjS[k] = a.adj[r0 + k];
+    for (int k = tid; k < a.nplanes * per; k += blockDim.x) {
+        const int pl = k / per, j = k - pl * per;
+        plS[k] = lo + j < hi ? a.pplanes[((size_t)w * a.nplanes + pl) * a.n + lo + j] : 0u;
+    }
+    uint32_t *cs = S0, *ns = S1;
+    uint32_t *wfl = fl + warp * 1024, *wres = res + warp * 32, *wexm = exm + warp * 32;
+    constexpr int CP = L + 2 + kResidentExtraPlanes;
+    uint32_t C[CP];
+#pragma unroll
+    for (int r = 0; r < CP; ++r) C[r] = 0;
+    int dsum = 0;
+    const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
+    cluster.sync();
+
+    RLaunch Rn = a.launches[0];
+    for (int li = 0; li < a.nlaunch; ++li) {
+        const RLaunch R = Rn;
+        if (li + 1 < a.nlaunch) Rn = a.launches[li + 1];  // in flight during this sub-step
+        const bool update = R.cycle < a.cycles;
+        const double i0 = R.i0;
+        const float i0f = (float)i0;
+        const uint32_t count = R.count;
+        // this sub-step's dividing periods as plane polarity masks (0 selects the
+        // plane, ~0 its complement; absent planes are zero and pass)
+        for (int k = tid; k < R.ndiv * 8; k += blockDim.x) {
+            const uint32_t pv = a.divs[R.div_off + (k >> 3)];
+            const int pl = k & 7;
+            sdivx[k] = (pl < a.nplanes && ((pv >> pl) & 1u)) ? 0u : 0xffffffffu;
+        }
+        __syncthreads();
+        for (int base = lo + warp * 32; base < hi; base += nwarps * 32) {
+            const int i = base + lane;
+            const bool valid = i < hi;
+            uint32_t own = 0, fire = 0, beg = 0, end = 0;
+            if (valid) {
+                own = cs[i];
+                beg = rowS[i - lo];
+                end = rowS[i - lo + 1];
+                if (update) {
+                    uint32_t pl[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) pl[k] = k < a.nplanes ? plS[k * per + (i - lo)] : 0u;
+                    for (int dv = 0; dv < R.ndiv; ++dv) {
+                        const uint4 x0 = *reinterpret_cast<const uint4 *>(sdivx + dv * 8);
+                        const uint4 x1 = *reinterpret_cast<const uint4 *>(sdivx + dv * 8 + 4);
+                        fire |= (pl[0] ^ x0.x) & (pl[1] ^ x0.y) & (pl[2] ^ x0.z) & (pl[3] ^ x0.w) &
+                                (pl[4] ^ x1.x) & (pl[5] ^ x1.y) & (pl[6] ^ x1.z) & (pl[7] ^ x1.w);
+                    }
+                }
+            }
+            const bool any = __any_sync(0xffffffffu, fire != 0);
+            if (!R.do_cut && !any) {  // nothing fires: carry the words
+                if (valid && update) {
+                    ns[i] = own;
+                    for (int r = 1; r < CS; ++r)
+                        *cluster.map_shared_rank(ns + i, rank + r < CS ? rank + r : rank + r - CS) = own;
+                }
+                continue;
+            }
+            uint32_t p[L];
+            count_neighbours<L>(beg, end, [&](uint32_t k) {
+                const uint32_t e = adjS[k];
+                return cs[e & 0x7fffffffu] ^ (uint32_t)((int32_t)e >> 31);
+            }, p);
+            const int d = (int)(end - beg);
+            if (R.do_cut && valid) {
+                uint32_t g[L];
+                cut_counts<L>(p, own, d, g);
+                dsum += d;
+                vc_add<L, CP>(C, g);
+            }
+            if (!update) continue;
+            // warp-balanced fired (lane, trial, raw) list, as packed_sweep_timing
+            const int c = __popc(fire);
+            int off = c;
+#pragma unroll
+            for (int sft = 1; sft < 32; sft <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, off, sft);
+                if (lane >= sft) off += v;
+            }
+            const int F = __shfl_sync(0xffffffffu, off, 31);
+            off -= c;
+            for (uint32_t f = fire; f; f &= f - 1) {
+                const int b = __ffs(f) - 1;
+                int pop = 0;
+#pragma unroll
+                for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                wfl[off++] = ((uint32_t)(2 * pop - d + 1024) << 10) | ((uint32_t)lane << 5) | (uint32_t)b;
+            }
+            wres[lane] = 0;
+            wexm[lane] = 0;
+            __syncwarp();
+            // two list entries per lane and round, their profile loads in flight together
+            auto fire_one = [&](uint32_t e, float2 lv) {
+                const int b = (int)(e & 31u), l = (int)((e >> 5) & 31u), raw = (int)(e >> 10) - 1024;
+                const int ii = base + l;
+                const float ir = i0f * (float)raw;
+                const float x = fmaf(lv.x, ir, lv.y);
+                const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
+                const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
+                const uint2 kc = key[b];
+                uint32_t sl, sh;
+                packed_first_absorb(kc.x ^ (uint32_t)ii, kc.y, sl, sh);
+                const uint32_t zh = packed_hash_hi(sl, sh, count);
+                const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
+                if (fabsf(diff) < fmaf(A, mA, m0))
+                    atomicOr(wexm + l, 1u << b);
+                else if (diff > 0.0f)
+                    atomicOr(wres + l, 1u << b);
+                if (R.inp) a.inp_out[((size_t)w * 32 + b) * a.n + ii] = __dmul_rn(i0, (double)raw);
+            };
+            auto prof_of = [&](uint32_t e) {
+                return __ldg(a.prof + ((size_t)w * 32 + (e & 31u)) * a.n + base + ((e >> 5) & 31u));
+            };
+            for (int k = lane; k < F; k += 64) {
+                const uint32_t e0 = wfl[k];
+                const bool two = k + 32 < F;
+                const uint32_t e1 = two ? wfl[k + 32] : e0;
+                const float2 lv0 = prof_of(e0), lv1 = prof_of(e1);
+                fire_one(e0, lv0);
+                if (two) fire_one(e1, lv1);
+            }
+            __syncwarp();
+            if (valid) {
+                uint32_t word = (own & ~fire) | wres[lane];
+                uint32_t ex = wexm[lane];
+                while (ex) {  // rare near-tie: the reference's fp64 arithmetic
+                    const int b = __ffs(ex) - 1;
+                    ex &= ex - 1;
+                    int pop = 0;
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                    const size_t idx = ((size_t)w * 32 + b) * a.n + i;
+                    const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)(uint32_t)i;
+                    const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                    const double r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+                    const double xx = __dmul_rn(a.lam64[idx], __dadd_rn(__dmul_rn(i0, (double)(2 * pop - d)),
+                                                                       a.del64[idx]));
+                    word |= (uint32_t)(__dadd_rn(r, pb_libm_tanh(xx)) >= 0.0) << b;
+                }
+                ns[i] = word;
+                for (int r = 1; r < CS; ++r)
+                    *cluster.map_shared_rank(ns + i, rank + r < CS ? rank + r : rank + r - CS) = word;
+            }
+            __syncwarp();
+        }
+        if (R.do_cut) {
+            warp_cut_flush(C, dsum, lane, a.pacc + (size_t)R.cycle * a.Tp + (size_t)w * 32);
+#pragma unroll
+            for (int r = 0; r < CP; ++r) C[r] = 0;
+            dsum = 0;
+        }
+        if (update) {
+            cluster.sync();
             uint32_t *t = cs;
             cs = ns;
             ns = t;
