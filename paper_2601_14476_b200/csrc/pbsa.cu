@@ -451,10 +451,12 @@ ResidentTimingKernel resident_timing_for(int L) {
     }
 }
 
-ResidentKernel resident_kernel_for(int L, bool cached) {
+ResidentKernel resident_kernel_for(int L, bool cached, bool varu = false) {
     switch (L) {
-#define PBSA_RCASE(l) \
-    case l: return cached ? pbsa::resident_sweep<l, true> : pbsa::resident_sweep<l, false>;
+#define PBSA_RCASE(l)                                                                          \
+    case l:                                                                                    \
+        return varu ? (cached ? pbsa::resident_sweep<l, true, true> : pbsa::resident_sweep<l, false, true>) \
+                    : (cached ? pbsa::resident_sweep<l, true, false> : pbsa::resident_sweep<l, false, false>);
         PBSA_RCASE(1)
         PBSA_RCASE(2)
         PBSA_RCASE(3)
@@ -992,6 +994,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         {
             const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode;
             const bool timing = P.var_mode && !P.var_uniform;
+            const bool varu = P.var_mode && P.var_uniform;
             const int tab = (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
             P.res_smem = 512 + (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;
             int max_smem = 0;
@@ -999,7 +1002,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             // measured: small batches (<= 64 words) of small dense graphs (n <= 2500,
             // mean degree >= 8: G1, G47, G22) run 1.1-2.2x faster resident; sparse
             // or larger problems are faster with launched sweeps
-            bool want = P.W <= 64 && n <= 2500 && nnz >= 8 * n;
+            bool want = (P.W <= 64 || (P.var_mode && !P.var_uniform && P.W <= 128)) && n <= 2500 &&
+                        nnz >= 8 * n;
             if (const char *env = std::getenv("PBSA_RESIDENT")) want = env[0] == '1';
             int csz = 1;  // (measured: 8 for a handful of words, 4 beats 8 at 32 words)
             while (csz < (P.W <= 8 ? 8 : 4) && P.W * csz < sms) csz *= 2;
@@ -1029,7 +1033,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 if (!P.i0_dev.n) P.i0_dev.upload(P.i0, st);
                 ResidentTimingKernel rk = resident_timing_for(P.L);
                 CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
-            } else if (plain && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
+            } else if ((plain || varu) && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
                 // (the per-thread cut counter takes up to 32 nodes)
                 const int thr = (int)std::min<int64_t>(512, ((per + 31) / 32) * 32);
                 P.resident = true;
@@ -1037,8 +1041,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 P.res_threads = thr;
                 if (P.use_cache && P.phase_words < P.W) P.acache.alloc((size_t)P.W * P.chunks * 1024);
                 P.phase_words = P.W;
-                ResidentKernel rk = resident_kernel_for(P.L, P.use_cache);
+                ResidentKernel rk = resident_kernel_for(P.L, P.use_cache, varu);
                 CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
+                if (varu && !P.i0_dev.n) P.i0_dev.upload(P.i0, st);
                 if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             }
         }
@@ -1273,6 +1278,14 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             r.chunks = P.chunks;
             r.cycles = (int)P.cycles;
             r.t_res = (int)P.t_res;
+            if (P.var_mode) {
+                r.prof = P.prof.p;
+                r.lam64 = P.lam64.p;
+                r.del64 = P.del64.p;
+                r.i0 = P.i0_dev.p;
+                r.inp_out = P.inp_var.p;
+                r.margin = P.var_margin;
+            }
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3((unsigned)(P.W * P.res_cs));
             cfg.blockDim = dim3((unsigned)P.res_threads);
@@ -1285,7 +1298,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&cfg, resident_kernel_for(P.L, P.use_cache), r));
+            CK(cudaLaunchKernelEx(&cfg, resident_kernel_for(P.L, P.use_cache, P.var_mode), r));
             ++P.launches;
             P.sweep_launches = P.cycles;
             cur = 1;

@@ -960,21 +960,27 @@ struct ResidentArgs {
     unsigned long long *pacc;   // [cycles+1][Tp]
     int16_t *raw_out;           // [n][Tp] raw fields of the last cycle
     int n, W, Tp, K, dmax, chunks, cycles, t_res;
+    // VARU: per-p-bit lam/delta without a timing spread (ALG=3 decision)
+    const float2 *prof;         // [Tp][n]
+    const double *lam64, *del64;
+    const double *i0;           // [cycles]
+    double *inp_out;            // [Tp][n] inputs of the last cycle
+    float margin;
 };
 
 constexpr int kResidentExtraPlanes = 3;  // cut counters for up to 32 nodes per thread
 
-template <int L, bool CACHED>
+template <int L, bool CACHED, bool VARU = false>
 __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int CS = (int)cluster.num_blocks();
     const int rank = (int)cluster.block_rank();
     const int w = (int)(blockIdx.x / CS);
-    constexpr bool NIB = L <= 4;
+    constexpr bool NIB = L <= 4 && !VARU;
     extern __shared__ unsigned long long smem_u64[];
     uint2 *sthr = reinterpret_cast<uint2 *>((reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
-    const int tab_entries = NIB ? (a.dmax + 1) * 16 : a.K;
+    const int tab_entries = VARU ? 0 : NIB ? (a.dmax + 1) * 16 : a.K;
     uint2 *key = sthr + tab_entries;
     uint32_t *S0 = reinterpret_cast<uint32_t *>(key + 32);
     uint32_t *S1 = S0 + a.n;
@@ -1034,6 +1040,61 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
             if (c == a.cycles) continue;  // final cut pass
             const uint32_t ui = (uint32_t)i;
             const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + (i >> 5)) * 1024 + (i & 31) : nullptr;
+            if (VARU) {  // the packed ALG=3 decision (sigmoid prefilter, exact recheck)
+                const double i0 = a.i0[cc];
+                const float i0f = (float)i0;
+                const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
+                const float2 *pr = a.prof + (size_t)w * 32 * a.n + i;
+                uint32_t word = 0, exact = 0;
+#pragma unroll
+                for (int b = 0; b < 32; ++b) {
+                    int pop = 0;
+#pragma unroll
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                    const int raw = 2 * pop - d;
+                    const float2 lv = __ldg(pr + (size_t)b * a.n);
+                    const float ir = i0f * (float)raw;
+                    const float x = fmaf(lv.x, ir, lv.y);
+                    const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
+                    const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
+                    uint32_t zh;
+                    if (CACHED) {
+                        const uint2 v = __ldcs(ctile + b * 32);
+                        zh = packed_hash_hi_y(v.x ^ count, v.y);
+                    } else {
+                        const uint2 kc = key[b];
+                        uint32_t sl, sh;
+                        packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                        zh = packed_hash_hi(sl, sh, count);
+                    }
+                    const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
+                    if (fabsf(diff) < fmaf(A, mA, m0))
+                        exact |= 1u << b;
+                    else
+                        word |= (uint32_t)(diff > 0.0f) << b;
+                    if (a.inp_out && c == a.cycles - 1)
+                        a.inp_out[((size_t)w * 32 + b) * a.n + i] = __dmul_rn(i0, (double)raw);
+                }
+                while (exact) {
+                    const int b = __ffs(exact) - 1;
+                    exact &= exact - 1;
+                    int pop = 0;
+                    for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
+                    const size_t idx = ((size_t)w * 32 + b) * a.n + i;
+                    const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
+                    const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                    const double r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+                    const double xx = __dmul_rn(a.lam64[idx], __dadd_rn(__dmul_rn(i0, (double)(2 * pop - d)),
+                                                                       a.del64[idx]));
+                    word |= (uint32_t)(__dadd_rn(r, pb_libm_tanh(xx)) >= 0.0) << b;
+                }
+                ns[i] = word;
+                for (int r = 1; r < CS; ++r) {
+                    const int peer = rank + r < CS ? rank + r : rank + r - CS;
+                    *cluster.map_shared_rank(ns + i, peer) = word;
+                }
+                continue;
+            }
             uint32_t word = 0, tie = 0xffffffffu;
             uint32_t N[4] = {0u, 0u, 0u, 0u};
             uint32_t rb = 0;
