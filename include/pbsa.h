@@ -108,6 +108,23 @@ int pbsa_plan_summary(pbsa_plan *plan, int64_t *final_cut_sum, int64_t *best_cut
 int pbsa_plan_info(const pbsa_plan *plan, int *path, int64_t *launches_per_run,
                    double *sweep_ms_mean, int64_t *sweep_launches, int64_t *words);
 
+/* Which sweep kernel a plan runs (pbsa_plan_kernel). */
+enum {
+    PBSA_KERNEL_PACKED = 1,          /* packed_sweep, one launch per sub-step */
+    PBSA_KERNEL_PACKED_TIMING = 2,   /* packed_sweep_timing (period spread) */
+    PBSA_KERNEL_RESIDENT = 3,        /* resident_sweep, one cluster launch per run */
+    PBSA_KERNEL_RESIDENT_TIMING = 4, /* resident_timing */
+    PBSA_KERNEL_ACTIVE_FAST = 5,     /* general path: active lists, plain rule */
+    PBSA_KERNEL_ACTIVE = 6,          /* general path: active lists, all rules */
+    PBSA_KERNEL_FULL = 7             /* general path: fp64 full pass */
+};
+
+/*
+ * The sweep kernel family of a plan (PBSA_KERNEL_*), and the cluster size of
+ * the resident kernels (1 otherwise).  Diagnostic; results do not depend on it.
+ */
+int pbsa_plan_kernel(const pbsa_plan *plan, int *kernel, int *cluster_size);
+
 /*
  * Bytes one end-to-end call moves: host->device at plan creation (CSR,
  * edges, keys, profiles, schedule tables) and device->host for a full

@@ -41,6 +41,7 @@ _SIGNATURES = [
     ("pbsa_plan_info", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_I64),
                                       ctypes.POINTER(_F64), ctypes.POINTER(_I64),
                                       ctypes.POINTER(_I64)]),
+    ("pbsa_plan_kernel", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("pbsa_plan_bytes", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("pbsa_plan_destroy", ctypes.c_int, [_P]),
     ("pbsa_anneal_loop_batch", ctypes.c_int,
@@ -54,6 +55,10 @@ _SIGNATURES = [
 ]
 
 EXPORTED = [name for name, _, _ in _SIGNATURES]
+
+# pbsa_plan_kernel codes (include/pbsa.h PBSA_KERNEL_*)
+KERNELS = {1: "packed", 2: "packed_timing", 3: "resident", 4: "resident_timing", 5: "active_fast",
+           6: "active", 7: "full"}
 
 
 def load() -> ctypes.CDLL:
@@ -202,7 +207,10 @@ class Plan:
         ms = _F64()
         _check(load().pbsa_plan_info(self._h, ctypes.byref(path), ctypes.byref(launches),
                                      ctypes.byref(ms), ctypes.byref(sweeps), ctypes.byref(words)))
+        kern, cs = ctypes.c_int(), ctypes.c_int()
+        _check(load().pbsa_plan_kernel(self._h, ctypes.byref(kern), ctypes.byref(cs)))
         return dict(path={1: "packed", 2: "general"}.get(path.value, "?"),
+                    kernel=KERNELS.get(kern.value, "?"), cluster_size=cs.value,
                     launches=launches.value, sweep_ms_mean=ms.value,
                     sweep_launches=sweeps.value, words=words.value)
 

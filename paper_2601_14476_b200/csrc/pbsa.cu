@@ -1715,6 +1715,20 @@ int pbsa_plan_info(const pbsa_plan *P, int *path, int64_t *launches_per_run,
     });
 }
 
+int pbsa_plan_kernel(const pbsa_plan *P, int *kernel, int *cluster_size) {
+    return guarded([&] {
+        if (!P) fail(PBSA_EINVAL, "null plan");
+        int k;
+        if (P->path == PBSA_PATH_PACKED)
+            k = P->resident ? (P->res_timing ? PBSA_KERNEL_RESIDENT_TIMING : PBSA_KERNEL_RESIDENT)
+                            : (P->var_mode && !P->var_uniform ? PBSA_KERNEL_PACKED_TIMING : PBSA_KERNEL_PACKED);
+        else
+            k = P->active_mode ? (P->fast ? PBSA_KERNEL_ACTIVE_FAST : PBSA_KERNEL_ACTIVE) : PBSA_KERNEL_FULL;
+        if (kernel) *kernel = k;
+        if (cluster_size) *cluster_size = P->resident ? P->res_cs : 1;
+    });
+}
+
 int pbsa_plan_summary(pbsa_plan *P, int64_t *final_cut_sum, int64_t *best_cut_max,
                       int64_t *updates) {
     return guarded([&] {

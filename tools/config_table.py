@@ -33,6 +33,9 @@ from paper_2601_14476_b200.model import maxcut_to_ising  # noqa: E402
 from paper_2601_14476_b200.pbit import VariabilityConfig, VariabilityProfile  # noqa: E402
 
 PEAK = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"] if (ROOT / "MEASURED_PEAKS.json").exists() else 6650.0
+# shared-memory ceiling for designs whose state is SMEM-resident
+# (148 SMs x 128 B/clk x 1.965 GHz; theoretical)
+SMEM_PEAK = 148 * 128 * 1.965
 
 
 def bytes_per_update(g, varied=False):
@@ -59,7 +62,7 @@ def gpu_run(g, kind, sig, T, cycles=1000, alpha=4):
     cut_sum, best, ups = plan.summary()
     info = plan.info()
     plan.close()
-    return dict(ms=ms, updates=ups, upd_s=ups / ms * 1e3, path=info["path"], mean_cut=cut_sum / T,
+    return dict(ms=ms, updates=ups, upd_s=ups / ms * 1e3, path=info["kernel"], mean_cut=cut_sum / T,
                 best=best, profile_s=t_prof)
 
 
@@ -104,9 +107,12 @@ def main():
         cpu = cpu_run(g, kind, sig, cpu_T) if cpu_T else None
         d = denom(name)
         B = bytes_per_update(g, any(sig))
+        resident = gpu["path"].startswith("resident")
+        peak = SMEM_PEAK if resident else PEAK
         row = dict(config=cfg, graph=name, n=g.n, m=g.m, algo=kind.value, sigma=list(sig), trials=T,
                    path=gpu["path"], gpu_ms=gpu["ms"], gpu_upd_s=gpu["upd_s"],
-                   roofline_frac=gpu["upd_s"] * B / (PEAK * 1e9), bytes_per_update=B,
+                   roofline_frac=gpu["upd_s"] * B / (peak * 1e9), bound="smem" if resident else "hbm",
+                   bytes_per_update=B,
                    cpu_upd_s=cpu["upd_s"] if cpu else None, cpu_threads=threads,
                    cpu_sample_trials=cpu_T, speedup=(gpu["upd_s"] / cpu["upd_s"]) if cpu else None,
                    mean_cut=gpu["mean_cut"], normalized=(gpu["mean_cut"] / d) if d else None,
@@ -136,12 +142,16 @@ def main():
     out = ROOT / "profiles" / f"{args.tag}_configs.json"
     out.write_text(json.dumps(rows, indent=1))
     lines = [f"# {args.tag}: BASELINE configs on one B200 vs the CPU reference port ({threads} threads)", "",
-             "| cfg | graph (n) | rule | sigma | trials | path | GPU ms/run | GPU upd/s | frac of HBM roofline | CPU upd/s | GPU/CPU | mean cut / best-known |",
+             "Kernels: `packed` (one launch per sub-step), `packed_timing`, `resident` / `resident_timing` (one "
+             "cluster launch per run, state in shared memory: their roofline is the SMEM ceiling, "
+             f"{SMEM_PEAK / 1000:.1f} TB/s), `active_fast` / `active` (general path). Bytes per update: "
+             "SURVEY 8(d) B, plus 8 B for a varied profile.", "",
+             "| cfg | graph (n) | rule | sigma | trials | kernel | GPU ms/run | GPU upd/s | frac of roofline (bound) | CPU upd/s | GPU/CPU | mean cut / best-known |",
              "|---|---|---|---|---:|---|---:|---:|---:|---:|---:|---:|"]
     for r in rows:
         lines.append(
             f"| {r['config']} | {r['graph']} ({r['n']}) | {r['algo']} | {tuple(r['sigma'])} | {r['trials']} | "
-            f"{r['path']} | {r['gpu_ms']:.1f} | {r['gpu_upd_s']:.3g} | {r['roofline_frac']:.3f} | "
+            f"{r['path']} | {r['gpu_ms']:.1f} | {r['gpu_upd_s']:.3g} | {r['roofline_frac']:.3f} ({r['bound']}) | "
             f"{(r['cpu_upd_s'] or 0):.3g} | {(r['speedup'] or 0):.0f} | "
             f"{(r['normalized'] if r['normalized'] is not None else float('nan')):.4f} |")
     (ROOT / "profiles" / f"{args.tag}_configs.md").write_text("\n".join(lines) + "\n")
