@@ -54,6 +54,11 @@ def parse():
     ap.add_argument("--cycles", type=int, default=1000)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rng", choices=["replay", "philox"], default="replay",
+                    help="activation stream of the headline run: the reference's counter hash "
+                         "(bit-exact, default) or the native Philox4x32-10 stream")
+    ap.add_argument("--no-philox-leg", action="store_true",
+                    help="skip the extra native-Philox measurement reported under 'philox'")
     ap.add_argument("--cpu-sample-trials", type=int, default=0,
                     help="trials in the CPU baseline sample (default 8 per thread)")
     return ap.parse_args()
@@ -88,7 +93,9 @@ def config_dict(args, graph, real, world):
                     f"(n={graph.n}, m={graph.m}), pSA, sigma=(0,0,0), {args.trials} trials x "
                     f"{args.cycles} cycles x t_res 10, trials sharded over {world} GPU(s)",
         "graph": args.graph, "n": graph.n, "m": graph.m, "trials": args.trials,
-        "cycles": args.cycles, "t_res": 10, "algo": "psa", "rng": "replay (reference counter hash)",
+        "cycles": args.cycles, "t_res": 10, "algo": "psa",
+        "rng": ("replay (reference counter hash)" if args.rng == "replay"
+                else "philox (native Philox4x32-10 stream)"),
         "parallelism": f"trial-shard x{world}", "l2": "flushed (512 MiB write) between steps",
     }
 
@@ -262,7 +269,9 @@ def main():
     graph, real, model, sch = workload(args.graph, args.cycles)
     lo, hi = shard(args.trials, rank, world)
     seeds = streams.trial_seeds(0, hi)[lo:hi]
-    batch = _native.Batch(model, sch, streams.run_keys(seeds), graph=graph)
+    nseed = streams.native_seed(0)
+    batch = _native.Batch(model, sch, streams.run_keys(seeds), graph=graph, rng=args.rng,
+                          rng_seed=nseed, first_trial=lo)
     plan = _native.Plan(batch, device=local)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
 
@@ -272,7 +281,10 @@ def main():
             torch.distributed.barrier()
 
     def reduce_summary():
-        s, b, u = plan.summary()
+        return reduce_summary_of(plan)
+
+    def reduce_summary_of(p):
+        s, b, u = p.summary()
         t = torch.tensor([s, u], dtype=torch.int64, device=f"cuda:{local}")
         m = torch.tensor([b], dtype=torch.int64, device=f"cuda:{local}")
         if world > 1:
@@ -298,6 +310,29 @@ def main():
     info = plan.info()
     h2d, d2h = plan.transfer_bytes()
     plan.close()
+
+    # the other stream on the same workload (same timing rules), reported
+    # beside the headline: the native Philox mode of the same packed sweep
+    other = None
+    if not args.no_philox_leg:
+        alt = "philox" if args.rng == "replay" else "replay"
+        ob = _native.Batch(model, sch, streams.run_keys(seeds), graph=graph, rng=alt,
+                           rng_seed=nseed, first_trial=lo)
+        oplan = _native.Plan(ob, device=local)
+        for _ in range(args.warmup):
+            flush.zero_()
+            oplan.run()
+        barrier()
+        oms = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            oms += oplan.run()
+            ocut, obest, _ = reduce_summary_of(oplan)
+        barrier()
+        oinfo = oplan.info()
+        oplan.close()
+        other = (alt, oms / args.steps, ocut, obest, oinfo)
     del flush
 
     # end-to-end through the public C ABI call with host buffers: inputs are
@@ -318,9 +353,12 @@ def main():
     step_ms = dev_ms / args.steps
     e2e_step_ms = e2e_ms / args.e2e_steps
     if world > 1:
-        v = torch.tensor([step_ms, e2e_step_ms], dtype=torch.float64, device=f"cuda:{local}")
+        v = torch.tensor([step_ms, e2e_step_ms, other[1] if other else 0.0],
+                         dtype=torch.float64, device=f"cuda:{local}")
         torch.distributed.all_reduce(v, op=torch.distributed.ReduceOp.MAX)
         step_ms, e2e_step_ms = float(v[0]), float(v[1])
+        if other:
+            other = (other[0], float(v[2])) + other[2:]
     total_updates = args.trials * graph.n * args.cycles
     assert updates == total_updates, (updates, total_updates)
 
@@ -359,7 +397,8 @@ def main():
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "u64",
-        "data": "synthetic (seeded structure-matched G-set analog; replayed reference RNG)",
+        "data": "synthetic (seeded structure-matched G-set analog; "
+                + ("replayed reference RNG)" if args.rng == "replay" else "native Philox RNG)"),
         "config": config_dict(args, graph, real, world),
         "quality": {"mean_final_cut": cut_sum / args.trials, "best_cut": best,
                     "best_known": bk,
@@ -378,6 +417,13 @@ def main():
                                      "how": "same packed kernel and launch shape on an edgeless graph "
                                             "of the same n and trials (draw + threshold + decision only)"}},
         "cpu_baseline": cpu,
+        other[0] if other else "philox": None if other is None else {
+            "value": total_updates / (other[1] * 1e-3), "unit": UNIT, "ms_per_step": other[1],
+            "kernel_ms_mean": other[4]["sweep_ms_mean"],
+            "stream": ("native Philox4x32-10 (PBSA_RNG_PHILOX), same packed sweep and timing rules"
+                       if other[0] == "philox" else "replayed reference counter hash"),
+            "quality": {"mean_final_cut": other[2] / args.trials, "best_cut": other[3],
+                        "mean_cut_over_best_known": (other[2] / args.trials / bk) if bk else None}},
         "clocks": clk.summary(),
         "gpu_launches": info["launches"] * args.steps,
         "wall_ms_timed_region": wall_ms,

@@ -39,6 +39,14 @@ enum { PBSA_ALGO_PSA = 0, PBSA_ALGO_TAPSA = 1, PBSA_ALGO_SPSA = 2 };
 /* Which device path a plan runs (pbsa_plan_info). */
 enum { PBSA_PATH_PACKED = 1, PBSA_PATH_GENERAL = 2 };
 
+/* Random stream of the activation draws (pbsa_plan_create_ex). */
+enum {
+    PBSA_RNG_REPLAY = 0, /* the reference's counter hash (streams.py:29-55), bit-exact */
+    PBSA_RNG_PHILOX = 1  /* native Philox4x32-10 (philox.cuh): X = philox({i, count,
+                            k >> 2, 3}, rng_seed)[k & 3] for global trial k, and
+                            r = (2X + 1) 2^-32 - 1 */
+};
+
 typedef struct pbsa_plan pbsa_plan;
 
 int pbsa_abi_version(void);
@@ -71,6 +79,27 @@ int pbsa_plan_create(int device, int64_t n, const int64_t *indptr, const int64_t
                      double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
                      int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
                      pbsa_plan **out);
+
+/*
+ * pbsa_plan_create with a choice of random stream.  rng_mode PBSA_RNG_REPLAY
+ * is pbsa_plan_create.  PBSA_RNG_PHILOX draws every activation uniform from
+ * Philox4x32-10 keyed by rng_seed, with the global trial index
+ * first_trial + t in the counter (a multiple of 4, so any sharding of the
+ * trials by multiples of 4 gives identical per-trial results); initial spins
+ * still come from keys[] as in the reference.  Philox mode covers the plain
+ * rule with an ideal profile on +-1 MAX-CUT models (the packed sweep); other
+ * inputs return PBSA_EINVAL.  No reference interface corresponds: the
+ * reference has only its counter hash (streams.py); this is the north_star's
+ * native RNG mode.
+ */
+int pbsa_plan_create_ex(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                        const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                        const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                        const int64_t *ge_j, const int64_t *ge_w, const double *lam,
+                        const double *delta, const int64_t *period, int64_t profile_stride,
+                        double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                        int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                        int rng_mode, uint64_t rng_seed, int64_t first_trial, pbsa_plan **out);
 
 /*
  * Run the whole anneal on the device from the initial spins: `cycles` main
@@ -151,6 +180,20 @@ int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const i
                            double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
                            float *device_ms);
 
+/* pbsa_anneal_loop_batch with a choice of random stream (see pbsa_plan_create_ex). */
+int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                              const double *values, const double *h, int64_t mm,
+                              const int64_t *me_i, const int64_t *me_j, const double *me_w,
+                              int64_t gm, const int64_t *ge_i, const int64_t *ge_j,
+                              const int64_t *ge_w, const double *lam, const double *delta,
+                              const int64_t *period, int64_t profile_stride, double i0_min,
+                              double beta, int64_t cycles, int64_t t_res, int algo, int64_t alpha,
+                              double p_stall, int64_t trials, const uint64_t *keys, int rng_mode,
+                              uint64_t rng_seed, int64_t first_trial, int8_t *spins,
+                              double *inputs, double *hist, int64_t *counts, double *trace_i0,
+                              double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
+                              float *device_ms);
+
 /*
  * Device self-checks (used by the parity tests): evaluate the device
  * counter hash stream_u64(key, tag, a, b) (streams.py:41-45) and the device
@@ -159,6 +202,9 @@ int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const i
 int pbsa_debug_stream_u64(int device, int64_t count, const uint64_t *key, const uint64_t *tag,
                           const uint64_t *a, const uint64_t *b, uint64_t *out);
 int pbsa_debug_tanh(int device, int64_t count, const double *x, double *out);
+/* Philox4x32-10 on the device: ctr[4*count], key[2*count] -> out[4*count]. */
+int pbsa_debug_philox(int device, int64_t count, const uint32_t *ctr, const uint32_t *key,
+                      uint32_t *out);
 
 /* Host builds of device-side pieces (no GPU needed):
  *   pbsa_libm_tanh_host  -- the device tanh (same source, libm_tanh.cuh);
@@ -167,6 +213,12 @@ int pbsa_debug_tanh(int device, int64_t count, const double *x, double *out);
  *     r + t >= 0 with r = 2 u01 - 1 (_kernels.py:149-152); ~0 means never. */
 double pbsa_libm_tanh_host(double x);
 uint64_t pbsa_threshold_host(double t);
+/*   pbsa_threshold_native_host -- the same for the Philox stream: +1 iff the
+ *     32-bit draw X >= threshold (2^32 means never);
+ *   pbsa_philox_host -- Philox4x32-10 of ctr[4] under key[2] (same source as
+ *     the device, philox.cuh). */
+uint64_t pbsa_threshold_native_host(double t);
+void pbsa_philox_host(const uint32_t *ctr, const uint32_t *key, uint32_t *out);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,15 @@ def lib() -> ctypes.CDLL:
         L.orc_u01.argtypes = [u64, u64, u64, u64]
         L.orc_tanh.restype = dbl
         L.orc_tanh.argtypes = [dbl]
+        L.orc_philox4x32_10.restype = None
+        L.orc_philox4x32_10.argtypes = [ptr, ptr, ptr]
+        L.orc_anneal_batch_rng.restype = ctypes.c_int
+        L.orc_anneal_batch_rng.argtypes = (
+            [i64, ctypes.c_int, i64, ptr, ptr, ptr, ptr, i64, ptr, ptr, ptr, i64, ptr, ptr, ptr,
+             ptr, ptr, ptr, i64, dbl, dbl, i64, i64, ctypes.c_int, i64, dbl, ptr,
+             ctypes.c_int, u64, i64]
+            + [ptr] * 8
+        )
         L.orc_anneal_batch.restype = ctypes.c_int
         L.orc_anneal_batch.argtypes = (
             [i64, ctypes.c_int, i64, ptr, ptr, ptr, ptr, i64, ptr, ptr, ptr, i64, ptr, ptr, ptr,
@@ -72,6 +81,15 @@ def stream_u64(key: int, tag: int, a: int = 0, b: int = 0) -> int:
 
 def uniform01(key: int, tag: int, a: int = 0, b: int = 0) -> float:
     return float(lib().orc_u01(key & MASK64, tag & MASK64, a & MASK64, b & MASK64))
+
+
+def philox4x32_10(ctr, key) -> list[int]:
+    """Philox4x32-10 of a 4-word counter under a 2-word key (native RNG mode)."""
+    c = (ctypes.c_uint32 * 4)(*[int(x) & 0xFFFFFFFF for x in ctr])
+    k = (ctypes.c_uint32 * 2)(*[int(x) & 0xFFFFFFFF for x in key])
+    o = (ctypes.c_uint32 * 4)()
+    lib().orc_philox4x32_10(ctypes.addressof(c), ctypes.addressof(k), ctypes.addressof(o))
+    return list(o)
 
 
 def run_key(seed: int) -> int:
@@ -100,13 +118,19 @@ def _p(a) -> int:
 
 
 def anneal_batch(model, schedule, algo: str, profiles, keys, graph=None, alpha: int = 1,
-                 p_stall: float = 0.5, threads: int | None = None) -> dict:
+                 p_stall: float = 0.5, threads: int | None = None, rng: str = "replay",
+                 rng_seed: int = 0, first_trial: int = 0) -> dict:
     """Run len(keys) trials of anneal_loop on the CPU (restated in C).
 
     ``profiles`` is one profile object shared by all trials or a sequence
     with one per trial.  ``alpha`` follows annealer.py:235 (1 unless TAPSA).
     Returns a dict of stacked per-trial arrays in the anneal_loop order.
+    ``rng="philox"`` draws the activation uniforms from the native Philox
+    stream of global trials ``first_trial + t`` under ``rng_seed`` (the CUDA
+    library's PBSA_RNG_PHILOX mode) instead of the reference's counter hash.
     """
+    if rng not in ("replay", "philox"):
+        raise ValueError(f"rng must be 'replay' or 'philox', got {rng!r}")
     keys = np.asarray([int(k) & MASK64 for k in keys], dtype=np.uint64)
     T = int(keys.size)
     n = int(model.n)
@@ -135,12 +159,13 @@ def anneal_batch(model, schedule, algo: str, profiles, keys, graph=None, alpha: 
         i0_trace=np.empty((T, C)), energy_trace=np.empty((T, C)),
         cut_trace=np.empty((T, C), np.int64), best_cut=np.empty(T, np.int64),
     )
-    rc = lib().orc_anneal_batch(
+    rc = lib().orc_anneal_batch_rng(
         T, int(threads or os.cpu_count() or 1), n, _p(indptr), _p(indices), _p(values), _p(h),
         int(me_i.size), _p(me_i), _p(me_j), _p(me_w), int(ge_i.size), _p(ge_i), _p(ge_j),
         _p(ge_w), _p(lam), _p(delta), _p(period), stride, float(schedule.i0_min),
         float(schedule.beta), C, int(schedule.t_res), code, int(alpha), float(p_stall),
-        _p(keys), *(_p(out[k]) for k in ("spins", "inputs", "hist", "counts", "i0_trace",
+        _p(keys), int(rng == "philox"), int(rng_seed) & MASK64, int(first_trial),
+        *(_p(out[k]) for k in ("spins", "inputs", "hist", "counts", "i0_trace",
                                           "energy_trace", "cut_trace", "best_cut")))
     if rc != 0:
         raise RuntimeError(f"oracle anneal failed with status {rc}")

@@ -15,6 +15,9 @@
  *   - counter hash            streams.py:29-55, _kernels.py:44-59
  *   - anneal_loop              _kernels.py:68-175 (all three input rules)
  *   - per-cycle energy / cut   _kernels.py:157-171 (same accumulation order)
+ *   - and, with no reference counterpart, the native Philox4x32-10 activation
+ *     stream of the CUDA library's PBSA_RNG_PHILOX mode (pinned by the
+ *     published Random123 known-answer vectors, not by the reference)
  *
  * Build: gcc -O2 -ffp-contract=off -fPIC -shared (see oracle/Makefile).
  * FMA contraction must stay off so that every fp64 operation rounds exactly
@@ -58,6 +61,47 @@ double orc_u01(uint64_t key, uint64_t tag, uint64_t a, uint64_t b) {
 double orc_tanh(double x) { return tanh(x); }
 
 /*
+ * Native RNG mode (no reference counterpart: the north_star's Philox stream,
+ * include/pbsa.h PBSA_RNG_PHILOX).  Philox4x32-10 as published by Salmon et
+ * al. (SC'11, Random123): per round (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2,
+ * c = (hi1^c1^k0, lo1, hi0^c3^k1, lo0), then k += (W0, W1).  Pinned by the
+ * Random123 known-answer vectors in tests/test_oracle_golden.py.
+ */
+void orc_philox4x32_10(const uint32_t *ctr, const uint32_t *key, uint32_t *out) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* The native activation uniform's r = 2u - 1, u = (X + 1/2) 2^-32, X the
+ * word (k & 3) of Philox(ctr = {i, count, k >> 2, 3}, key = seed). */
+static double orc_native_r(uint64_t seed, uint64_t k, uint64_t i, uint64_t count) {
+    uint32_t ctr[4] = {(uint32_t)i, (uint32_t)count, (uint32_t)(k >> 2), 3u};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)}, o[4];
+    orc_philox4x32_10(ctr, key, o);
+    return (2.0 * (double)o[k & 3] + 1.0) * 0x1p-32 - 1.0;
+}
+
+int orc_anneal_rng(int64_t n, const int64_t *indptr, const int64_t *indices, const double *values,
+                   const double *h, int64_t mm, const int64_t *me_i, const int64_t *me_j,
+                   const double *me_w, int64_t gm, const int64_t *ge_i, const int64_t *ge_j,
+                   const int64_t *ge_w, const double *lam, const double *delta,
+                   const int64_t *period, double i0_min, double beta, int64_t cycles,
+                   int64_t t_res, int algo, int64_t alpha, double p_stall, uint64_t key, int rng,
+                   uint64_t seed, int64_t trial, int8_t *spins, double *inputs, double *hist,
+                   int64_t *counts, double *trace_i0, double *trace_energy, int64_t *trace_cut,
+                   int64_t *best_cut);
+
+/*
  * One trial of the annealing loop (_kernels.py:68-175).
  *
  * Inputs mirror anneal_loop's positional arguments; outputs are caller-owned
@@ -73,6 +117,24 @@ int orc_anneal(int64_t n, const int64_t *indptr, const int64_t *indices, const d
                int algo, int64_t alpha, double p_stall, uint64_t key, int8_t *spins,
                double *inputs, double *hist, int64_t *counts, double *trace_i0,
                double *trace_energy, int64_t *trace_cut, int64_t *best_cut) {
+    return orc_anneal_rng(n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm, ge_i, ge_j,
+                          ge_w, lam, delta, period, i0_min, beta, cycles, t_res, algo, alpha,
+                          p_stall, key, 0, 0, 0, spins, inputs, hist, counts, trace_i0,
+                          trace_energy, trace_cut, best_cut);
+}
+
+/* orc_anneal with a choice of activation stream: rng = 0 the reference's
+ * counter hash, rng = 1 the native Philox draw of global trial `trial`
+ * under `seed` (orc_native_r).  Everything else is identical. */
+int orc_anneal_rng(int64_t n, const int64_t *indptr, const int64_t *indices, const double *values,
+                   const double *h, int64_t mm, const int64_t *me_i, const int64_t *me_j,
+                   const double *me_w, int64_t gm, const int64_t *ge_i, const int64_t *ge_j,
+                   const int64_t *ge_w, const double *lam, const double *delta,
+                   const int64_t *period, double i0_min, double beta, int64_t cycles,
+                   int64_t t_res, int algo, int64_t alpha, double p_stall, uint64_t key, int rng,
+                   uint64_t seed, int64_t trial, int8_t *spins, double *inputs, double *hist,
+                   int64_t *counts, double *trace_i0, double *trace_energy, int64_t *trace_cut,
+                   int64_t *best_cut) {
     int64_t *stage_idx = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
     int8_t *stage_val = (int8_t *)malloc((size_t)(n > 0 ? n : 1));
     if (!stage_idx || !stage_val) {
@@ -124,7 +186,8 @@ int orc_anneal(int64_t n, const int64_t *indptr, const int64_t *indices, const d
                 }
                 inputs[i] = inp;
                 counts[i] += 1;
-                double r = 2.0 * orc_u01(key, ORC_TAG_R, (uint64_t)i, (uint64_t)count) - 1.0;
+                double r = rng ? orc_native_r(seed, (uint64_t)trial, (uint64_t)i, (uint64_t)count)
+                               : 2.0 * orc_u01(key, ORC_TAG_R, (uint64_t)i, (uint64_t)count) - 1.0;
                 double act = r + tanh(lam[i] * (inp + delta[i]));
                 stage_idx[n_active] = i;
                 stage_val[n_active] = act >= 0.0 ? 1 : -1;
@@ -161,6 +224,18 @@ int orc_anneal(int64_t n, const int64_t *indptr, const int64_t *indices, const d
  * (profile_stride = n) or shared (profile_stride = 0).  Outputs are laid out
  * [T][...] contiguously.
  */
+int orc_anneal_batch_rng(int64_t T, int nthreads, int64_t n, const int64_t *indptr,
+                         const int64_t *indices, const double *values, const double *h, int64_t mm,
+                         const int64_t *me_i, const int64_t *me_j, const double *me_w, int64_t gm,
+                         const int64_t *ge_i, const int64_t *ge_j, const int64_t *ge_w,
+                         const double *lam, const double *delta, const int64_t *period,
+                         int64_t profile_stride, double i0_min, double beta, int64_t cycles,
+                         int64_t t_res, int algo, int64_t alpha, double p_stall,
+                         const uint64_t *keys, int rng, uint64_t seed, int64_t first_trial,
+                         int8_t *spins, double *inputs, double *hist, int64_t *counts,
+                         double *trace_i0, double *trace_energy, int64_t *trace_cut,
+                         int64_t *best_cut);
+
 typedef struct {
     int64_t n, mm, gm;
     const int64_t *indptr, *indices, *me_i, *me_j, *ge_i, *ge_j, *ge_w, *period;
@@ -170,6 +245,9 @@ typedef struct {
     int64_t cycles, t_res, alpha;
     int algo;
     const uint64_t *keys;
+    int rng;
+    uint64_t seed;
+    int64_t first_trial;
     int64_t T;
     int8_t *spins;
     double *inputs, *hist, *trace_i0, *trace_energy;
@@ -187,10 +265,11 @@ static void *orc_worker(void *arg) {
         pthread_mutex_unlock(&b->lock);
         if (t >= b->T) break;
         int64_t n = b->n, ps = b->profile_stride, C = b->cycles;
-        int rc = orc_anneal(n, b->indptr, b->indices, b->values, b->h, b->mm, b->me_i, b->me_j,
+        int rc = orc_anneal_rng(n, b->indptr, b->indices, b->values, b->h, b->mm, b->me_i, b->me_j,
                             b->me_w, b->gm, b->ge_i, b->ge_j, b->ge_w, b->lam + t * ps,
                             b->delta + t * ps, b->period + t * ps, b->i0_min, b->beta, C,
-                            b->t_res, b->algo, b->alpha, b->p_stall, b->keys[t],
+                            b->t_res, b->algo, b->alpha, b->p_stall, b->keys[t], b->rng,
+                            b->seed, b->first_trial + t,
                             b->spins + t * n, b->inputs + t * n, b->hist + t * n * b->alpha,
                             b->counts + t * n, b->trace_i0 + t * C, b->trace_energy + t * C,
                             b->trace_cut + t * C, b->best_cut + t);
@@ -209,8 +288,27 @@ int orc_anneal_batch(int64_t T, int nthreads, int64_t n, const int64_t *indptr,
                      const uint64_t *keys, int8_t *spins, double *inputs, double *hist,
                      int64_t *counts, double *trace_i0, double *trace_energy,
                      int64_t *trace_cut, int64_t *best_cut) {
+    return orc_anneal_batch_rng(T, nthreads, n, indptr, indices, values, h, mm, me_i, me_j, me_w,
+                                gm, ge_i, ge_j, ge_w, lam, delta, period, profile_stride, i0_min,
+                                beta, cycles, t_res, algo, alpha, p_stall, keys, 0, 0, 0, spins,
+                                inputs, hist, counts, trace_i0, trace_energy, trace_cut, best_cut);
+}
+
+/* orc_anneal_batch with a choice of stream; trial t is global trial first_trial + t. */
+int orc_anneal_batch_rng(int64_t T, int nthreads, int64_t n, const int64_t *indptr,
+                         const int64_t *indices, const double *values, const double *h, int64_t mm,
+                         const int64_t *me_i, const int64_t *me_j, const double *me_w, int64_t gm,
+                         const int64_t *ge_i, const int64_t *ge_j, const int64_t *ge_w,
+                         const double *lam, const double *delta, const int64_t *period,
+                         int64_t profile_stride, double i0_min, double beta, int64_t cycles,
+                         int64_t t_res, int algo, int64_t alpha, double p_stall,
+                         const uint64_t *keys, int rng, uint64_t seed, int64_t first_trial,
+                         int8_t *spins, double *inputs, double *hist, int64_t *counts,
+                         double *trace_i0, double *trace_energy, int64_t *trace_cut,
+                         int64_t *best_cut) {
     orc_batch_t b;
     memset(&b, 0, sizeof b);
+    b.rng = rng; b.seed = seed; b.first_trial = first_trial;
     b.n = n; b.mm = mm; b.gm = gm;
     b.indptr = indptr; b.indices = indices; b.values = values; b.h = h;
     b.me_i = me_i; b.me_j = me_j; b.me_w = me_w;

@@ -19,6 +19,7 @@ LIB_PATH = Path(os.environ.get("PBSA_LIB") or
 
 PBSA_OK = 0
 PATH_PACKED, PATH_GENERAL = 1, 2
+RNG_MODES = {"replay": 0, "philox": 1}  # include/pbsa.h PBSA_RNG_*
 
 _lib: ctypes.CDLL | None = None
 
@@ -34,6 +35,10 @@ _SIGNATURES = [
     ("pbsa_plan_create", ctypes.c_int,
      [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
       _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.POINTER(_P)]),
+    ("pbsa_plan_create_ex", ctypes.c_int,
+     [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
+      _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.c_int, ctypes.c_uint64,
+      _I64, ctypes.POINTER(_P)]),
     ("pbsa_plan_run", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_float)]),
     ("pbsa_plan_download", ctypes.c_int, [_P] + [_P] * 8),
     ("pbsa_plan_summary", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
@@ -48,10 +53,17 @@ _SIGNATURES = [
      [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
       _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P] + [_P] * 8
      + [ctypes.POINTER(ctypes.c_float)]),
+    ("pbsa_anneal_loop_batch_ex", ctypes.c_int,
+     [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
+      _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.c_int, ctypes.c_uint64,
+      _I64] + [_P] * 8 + [ctypes.POINTER(ctypes.c_float)]),
     ("pbsa_debug_stream_u64", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P, _P, _P]),
     ("pbsa_debug_tanh", ctypes.c_int, [ctypes.c_int, _I64, _P, _P]),
+    ("pbsa_debug_philox", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P]),
     ("pbsa_libm_tanh_host", _F64, [_F64]),
     ("pbsa_threshold_host", ctypes.c_uint64, [_F64]),
+    ("pbsa_threshold_native_host", ctypes.c_uint64, [_F64]),
+    ("pbsa_philox_host", None, [_P, _P, _P]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGNATURES]
@@ -113,7 +125,10 @@ class Batch:
     """Host-side arguments of one batched anneal_loop call (_kernels.py:69-91)."""
 
     def __init__(self, model, schedule, keys, profile_rows=None, graph=None, algo_code=0,
-                 alpha=1, p_stall=0.5):
+                 alpha=1, p_stall=0.5, rng="replay", rng_seed=0, first_trial=0):
+        if rng not in RNG_MODES:
+            raise ValueError(f"rng must be one of {sorted(RNG_MODES)}, got {rng!r}")
+        self.rng, self.rng_seed, self.first_trial = rng, int(rng_seed), int(first_trial)
         self.n = int(model.n)
         self.indptr = _c(model.indptr, np.int64)
         self.indices = _c(model.indices, np.int64)
@@ -148,7 +163,8 @@ class Batch:
                 int(self.ge_i.size), _ptr(self.ge_i), _ptr(self.ge_j), _ptr(self.ge_w),
                 _ptr(self.lam), _ptr(self.delta), _ptr(self.period), self.stride,
                 self.i0_min, self.beta, self.cycles, self.t_res, self.algo, self.alpha,
-                self.p_stall, self.T, _ptr(self.keys))
+                self.p_stall, self.T, _ptr(self.keys), RNG_MODES[self.rng],
+                self.rng_seed & 0xFFFFFFFFFFFFFFFF, self.first_trial)
 
     def alloc_outputs(self) -> dict:
         T, n, C = self.T, self.n, self.cycles
@@ -171,7 +187,7 @@ def anneal_batch(batch: Batch, device: int = 0, out: dict | None = None) -> tupl
     if out is None:
         out = batch.alloc_outputs()
     ms = ctypes.c_float(0.0)
-    _check(lib.pbsa_anneal_loop_batch(device, *batch._args(),
+    _check(lib.pbsa_anneal_loop_batch_ex(device, *batch._args(),
                                       *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))
     return out, float(ms.value)
 
@@ -184,7 +200,7 @@ class Plan:
         require_device(device)
         self.batch, self.device = batch, device
         h = _P()
-        _check(lib.pbsa_plan_create(device, *batch._args(), ctypes.byref(h)))
+        _check(lib.pbsa_plan_create_ex(device, *batch._args(), ctypes.byref(h)))
         self._h = h
 
     def run(self) -> float:
@@ -240,6 +256,27 @@ def debug_stream_u64(keys, tags, a, b, device: int = 0) -> np.ndarray:
     _check(lib.pbsa_debug_stream_u64(device, out.size, *(x.ctypes.data for x in arrs),
                                      out.ctypes.data))
     return out
+
+
+def debug_philox(ctr, key, device: int = 0) -> np.ndarray:
+    """Device Philox4x32-10: ctr [m, 4], key [m, 2] (uint32) -> [m, 4]."""
+    lib = load()
+    require_device(device)
+    c = np.ascontiguousarray(ctr, dtype=np.uint32).reshape(-1, 4)
+    k = np.ascontiguousarray(key, dtype=np.uint32).reshape(-1, 2)
+    out = np.empty_like(c)
+    _check(lib.pbsa_debug_philox(device, c.shape[0], c.ctypes.data, k.ctypes.data,
+                                 out.ctypes.data))
+    return out
+
+
+def philox_host(ctr, key) -> list[int]:
+    """Host build of the device Philox4x32-10 (same source, philox.cuh)."""
+    c = (ctypes.c_uint32 * 4)(*[int(x) & 0xFFFFFFFF for x in ctr])
+    k = (ctypes.c_uint32 * 2)(*[int(x) & 0xFFFFFFFF for x in key])
+    o = (ctypes.c_uint32 * 4)()
+    load().pbsa_philox_host(ctypes.addressof(c), ctypes.addressof(k), ctypes.addressof(o))
+    return list(o)
 
 
 def debug_tanh(x, device: int = 0) -> np.ndarray:

@@ -103,6 +103,15 @@ uint64_t threshold_u53(double t) {
     return (uint64_t)(two52 + q);
 }
 
+// Native mode (philox.cuh): +1 iff (2X + 1) 2^-32 - 1 + t >= 0, i.e.
+// (2X + 1) 2^20 >= U = ceil((1 - t) 2^52); the smallest such 32-bit X,
+// 2^32 meaning "never".
+uint64_t threshold_native(double t) {
+    const uint64_t u = threshold_u53(t);
+    if (u <= (1ULL << 20)) return 0;
+    return (u - (1ULL << 20) + (1ULL << 21) - 1) >> 21;
+}
+
 uint64_t threshold_h64(double t) {
     const uint64_t u = threshold_u53(t);
     if (u >= (1ULL << 53)) return ~0ULL;  // never +1
@@ -240,6 +249,9 @@ struct pbsa_plan {
     bool int_energy = true;
     bool tapsa_hist_from_raw = false;  // TAPSA alpha=1 routed to the packed path
     bool tapsa_packed = false;         // TAPSA alpha>=2 on the packed path (bit-sliced ring)
+    bool native = false;               // PBSA_RNG_PHILOX: Philox draws (philox.cuh)
+    uint64_t nseed = 0;                // Philox key
+    int64_t first_trial = 0;           // global index of trial 0 (Philox trial groups)
     bool spsa_packed = false;          // SPSA p>0 on the packed path (per-p-bit drive index)
     DevBuf<uint32_t> sidx;             // [W][32][n] drive index per p-bit
     DevBuf<uint32_t> thr_hi;           // [cycles][K] high words of the thresholds
@@ -365,7 +377,19 @@ void set_packed_smem(K kernel, size_t bytes) {
 
 using PackedKernel = void (*)(pbsa::PackedArgs);
 PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false,
-                               bool spsa = false, int var = 0) {
+                               bool spsa = false, int var = 0, bool native = false) {
+    if (update && native) {  // Philox draws, plain rule, ideal profile (no first-absorb cache)
+        switch (L) {
+            case 1: return pbsa::packed_sweep<1, true, false, 4>;
+            case 2: return pbsa::packed_sweep<2, true, false, 4>;
+            case 3: return pbsa::packed_sweep<3, true, false, 4>;
+            case 4: return pbsa::packed_sweep<4, true, false, 4>;
+            case 5: return pbsa::packed_sweep<5, true, false, 4>;
+            case 6: return pbsa::packed_sweep<6, true, false, 4>;
+            case 7: return pbsa::packed_sweep<7, true, false, 4>;
+            default: fail(PBSA_EINVAL, "packed path supports degree <= 127");
+        }
+    }
 #define PBSA_VCASE(l)                                                                 \
     case l:                                                                           \
         return var == 2 ? pbsa::packed_sweep_timing<l>                                \
@@ -640,8 +664,14 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                  const int64_t *gei, const int64_t *gej, const int64_t *gew, const double *lam,
                  const double *delta, const int64_t *period, int64_t pstride, double i0_min,
                  double beta, int64_t cycles, int64_t t_res, int algo, int64_t alpha,
-                 double p_stall, int64_t trials, const uint64_t *keys) {
+                 double p_stall, int64_t trials, const uint64_t *keys, int rng_mode,
+                 uint64_t rng_seed, int64_t first_trial) {
     // ------------------------------------------------------- validation
+    if (rng_mode != PBSA_RNG_REPLAY && rng_mode != PBSA_RNG_PHILOX)
+        fail(PBSA_EINVAL, "rng_mode must be 0 (replay) or 1 (philox)");
+    if (rng_mode == PBSA_RNG_PHILOX && (first_trial < 0 || first_trial % 4 != 0 ||
+                                        first_trial + trials + 31 >= (1LL << 33)))
+        fail(PBSA_EINVAL, "philox mode: first_trial must be a multiple of 4 in [0, 2^33)");
     if (n < 1 || n > INT32_MAX / 2) fail(PBSA_EINVAL, "n must be in [1, 2^30), got %lld", (long long)n);
     if (trials < 1 || trials > (1LL << 24)) fail(PBSA_EINVAL, "trials must be in [1, 2^24]");
     if (cycles < 1) fail(PBSA_EINVAL, "cycles must be >= 1");
@@ -753,6 +783,12 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     }
     const bool packed = (((rule_is_psa || tapsa_packed || spsa_packed) && ideal) || var_ok) && unit_J &&
                         zero_h && graph_is_model && dmax <= 127 && small_counters;
+    if (rng_mode == PBSA_RNG_PHILOX && !(packed && ideal && rule_is_psa))
+        fail(PBSA_EINVAL, "rng_mode=philox supports the plain rule (pSA, TApSA alpha=1, SpSA "
+                          "p_stall=0) with an ideal profile on a +-1 MAX-CUT model of degree <= 127");
+    P.native = rng_mode == PBSA_RNG_PHILOX;
+    P.nseed = rng_seed;
+    P.first_trial = first_trial;
     P.var_mode = packed && var_ok;
     P.var_uniform = var_uniform;
     P.pmax = pmax;
@@ -836,11 +872,13 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             P.ring.alloc((size_t)P.W * alpha * P.L * n);
         } else {
             // thresholds per (cycle, raw): inp = i0 * raw; act = r + tanh(inp) (lam = 1, delta = 0)
+            // (native mode: the smallest Philox word X that gives +1, threshold_native)
             std::vector<uint64_t> thr((size_t)cycles * P.K);
             for (int64_t c = 0; c < cycles; ++c)
-                for (int raw = -P.dmax; raw <= P.dmax; ++raw)
-                    thr[(size_t)c * P.K + raw + P.dmax] =
-                        threshold_h64(pb_libm_tanh(P.i0[c] * (double)raw));
+                for (int raw = -P.dmax; raw <= P.dmax; ++raw) {
+                    const double t = pb_libm_tanh(P.i0[c] * (double)raw);
+                    thr[(size_t)c * P.K + raw + P.dmax] = P.native ? threshold_native(t) : threshold_h64(t);
+                }
             P.thr.upload(thr, st);
             if (P.spsa_packed) {
                 std::vector<uint32_t> hi(thr.size());
@@ -939,7 +977,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
         const bool big_graph = 13 * n >= (int64_t)sm_count * 1024;
         // (SpSA streams its per-p-bit drive index, which no phase keeps in L2: unphased)
-        P.phase_words = (!g_oneshot && !many_launches && big_graph && P.W >= 4 * 13 && !P.spsa_packed) ? 13 : 0;
+        // (native Philox draws keep no cache, so nothing gains from phases: measured
+        // G81 x 4096 9.1e11 updates/s unphased vs 7.8e11 in phases of 13)
+        P.phase_words = (!g_oneshot && !many_launches && big_graph && P.W >= 4 * 13 && !P.spsa_packed &&
+                         !P.native) ? 13 : 0;
         if (P.phase_words > 0) {  // equal phases
             const int64_t nph = (P.W + P.phase_words - 1) / P.phase_words;
             P.phase_words = (P.W + nph - 1) / nph;
@@ -951,9 +992,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // (with a timing spread the fired trials of a word are sparse: no cache)
         P.use_cache = cache_entries * 8 <= (32ULL << 30) && !many_launches;
         if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1' && !many_launches;
+        if (P.native) P.use_cache = false;  // Philox draws cache nothing
         if (P.use_cache) P.acache.alloc(cache_entries);
         PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
-                                              P.var_mode ? (P.var_uniform ? 1 : 2) : 0);
+                                              P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16;
         const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
         set_packed_smem(kern, smem_up);
@@ -992,7 +1034,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // resident mode (plain rule, ideal profile): a word's double-buffered
         // state in shared memory; cluster size so that W clusters cover the SMs
         {
-            const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode;
+            // (native mode runs the launched sweep only)
+            const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode && !P.native;
             const bool timing = P.var_mode && !P.var_uniform;
             const bool varu = P.var_mode && P.var_uniform;
             const int tab = (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
@@ -1202,7 +1245,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
         PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
-                                                 P.var_mode ? (P.var_uniform ? 1 : 2) : 0);
+                                                 P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16;
         CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
@@ -1344,6 +1387,12 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     a.chunks = P.chunks;
                     a.count = pl.count;
                     a.do_update = pl.update;
+                    if (P.native) {
+                        a.nk0 = (uint32_t)P.nseed;
+                        a.nk1 = (uint32_t)(P.nseed >> 32);
+                        a.ngroup = (uint32_t)((P.first_trial + w0 * 32) / 4);
+                        pbsa::philox_round_keys(a.nk0, a.nk1, a.rk);
+                    }
                     a.do_cut = pl.do_cut;
                     if (P.var_mode) {
                         const size_t off = (size_t)w0 * 32 * P.n;
@@ -1652,6 +1701,20 @@ int pbsa_plan_create(int device, int64_t n, const int64_t *indptr, const int64_t
                      double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
                      int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
                      pbsa_plan **out) {
+    return pbsa_plan_create_ex(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm,
+                               ge_i, ge_j, ge_w, lam, delta, period, profile_stride, i0_min, beta,
+                               cycles, t_res, algo, alpha, p_stall, trials, keys, PBSA_RNG_REPLAY,
+                               0, 0, out);
+}
+
+int pbsa_plan_create_ex(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                        const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                        const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                        const int64_t *ge_j, const int64_t *ge_w, const double *lam,
+                        const double *delta, const int64_t *period, int64_t profile_stride,
+                        double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                        int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                        int rng_mode, uint64_t rng_seed, int64_t first_trial, pbsa_plan **out) {
     return guarded([&] {
         if (!out) fail(PBSA_EINVAL, "null plan out-pointer");
         *out = nullptr;
@@ -1659,7 +1722,7 @@ int pbsa_plan_create(int device, int64_t n, const int64_t *indptr, const int64_t
         std::unique_ptr<pbsa_plan> P(new pbsa_plan());
         create_plan(*P, device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm, ge_i,
                     ge_j, ge_w, lam, delta, period, profile_stride, i0_min, beta, cycles, t_res,
-                    algo, alpha, p_stall, trials, keys);
+                    algo, alpha, p_stall, trials, keys, rng_mode, rng_seed, first_trial);
         DeviceGuard dg(device);
         // capture the whole anneal into one graph
         CK(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
@@ -1980,11 +2043,31 @@ int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const i
                            double *inputs, double *hist, int64_t *counts, double *trace_i0,
                            double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
                            float *device_ms) {
+    return pbsa_anneal_loop_batch_ex(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w,
+                                     gm, ge_i, ge_j, ge_w, lam, delta, period, profile_stride,
+                                     i0_min, beta, cycles, t_res, algo, alpha, p_stall, trials,
+                                     keys, PBSA_RNG_REPLAY, 0, 0, spins, inputs, hist, counts,
+                                     trace_i0, trace_energy, trace_cut, best_cut, device_ms);
+}
+
+int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                              const double *values, const double *h, int64_t mm,
+                              const int64_t *me_i, const int64_t *me_j, const double *me_w,
+                              int64_t gm, const int64_t *ge_i, const int64_t *ge_j,
+                              const int64_t *ge_w, const double *lam, const double *delta,
+                              const int64_t *period, int64_t profile_stride, double i0_min,
+                              double beta, int64_t cycles, int64_t t_res, int algo, int64_t alpha,
+                              double p_stall, int64_t trials, const uint64_t *keys, int rng_mode,
+                              uint64_t rng_seed, int64_t first_trial, int8_t *spins,
+                              double *inputs, double *hist, int64_t *counts, double *trace_i0,
+                              double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
+                              float *device_ms) {
     pbsa_plan *P = nullptr;
     g_oneshot = true;
-    int rc = pbsa_plan_create(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm,
-                              ge_i, ge_j, ge_w, lam, delta, period, profile_stride, i0_min, beta,
-                              cycles, t_res, algo, alpha, p_stall, trials, keys, &P);
+    int rc = pbsa_plan_create_ex(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm,
+                                 ge_i, ge_j, ge_w, lam, delta, period, profile_stride, i0_min,
+                                 beta, cycles, t_res, algo, alpha, p_stall, trials, keys, rng_mode,
+                                 rng_seed, first_trial, &P);
     g_oneshot = false;
     if (rc != PBSA_OK) return rc;
     // launch, write the run-independent outputs on the host while the device
@@ -2025,6 +2108,22 @@ int pbsa_debug_stream_u64(int device, int64_t count, const uint64_t *key, const 
     });
 }
 
+int pbsa_debug_philox(int device, int64_t count, const uint32_t *ctr, const uint32_t *key,
+                      uint32_t *out) {
+    return guarded([&] {
+        if (count < 0 || (count > 0 && (!ctr || !key || !out))) fail(PBSA_EINVAL, "bad arguments");
+        if (count == 0) return;
+        DeviceGuard dg(device);
+        DevBuf<uint32_t> dc, dk, dout;
+        dc.upload(ctr, 4 * count, 0);
+        dk.upload(key, 2 * count, 0);
+        dout.alloc((size_t)(4 * count));
+        pbsa::debug_philox<<<grid_for(count, 256), 256>>>(count, dc.p, dk.p, dout.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, dout.p, sizeof(uint32_t) * 4 * count, cudaMemcpyDeviceToHost));
+    });
+}
+
 int pbsa_debug_tanh(int device, int64_t count, const double *x, double *out) {
     return guarded([&] {
         if (count < 0) fail(PBSA_EINVAL, "negative count");
@@ -2042,5 +2141,13 @@ int pbsa_debug_tanh(int device, int64_t count, const double *x, double *out) {
 double pbsa_libm_tanh_host(double x) { return pb_libm_tanh(x); }
 
 uint64_t pbsa_threshold_host(double t) { return threshold_h64(t); }
+
+uint64_t pbsa_threshold_native_host(double t) { return threshold_native(t); }
+
+void pbsa_philox_host(const uint32_t *ctr, const uint32_t *key, uint32_t *out) {
+    uint32_t o[4];
+    pbsa::philox4x32_10(ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1], o);
+    for (int k = 0; k < 4; ++k) out[k] = o[k];
+}
 
 }  // extern "C"

@@ -27,6 +27,7 @@
 #include <stdint.h>
 
 #include "libm_tanh.cuh"
+#include "philox.cuh"
 
 #define PB_GAMMA 0x9E3779B97F4A7C15ULL
 #define PB_M1 0xBF58476D1CE4E5B9ULL
@@ -155,6 +156,10 @@ struct PackedArgs {
     float margin;             // prefilter margin scale (1; huge = every update takes the exact path)
     double i0;                // i0 of this cycle
     double *inp_out;          // [W*32][n] i0 * raw of every fired p-bit, or null
+    // NATIVE (ALG=4: Philox4x32-10 draws instead of the replayed hash, philox.cuh)
+    uint32_t nk0, nk1;        // Philox key (native seed)
+    uint32_t rk[20];          // its ten round keys (philox_round_keys)
+    uint32_t ngroup;          // Philox trial-group counter of this launch's word 0: (first trial) / 4
 };
 
 // Exact H >= thr for H = mix64(x); thr == ~0 encodes "never" (tanh == -1),
@@ -440,6 +445,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     constexpr bool TAPSA = ALG == 1;
     constexpr bool SPSA = ALG == 2;
     constexpr bool VAR = ALG == 3;
+    constexpr bool NATIVE = ALG == 4;  // plain rule, Philox draws (philox.cuh)
     constexpr bool NIB = L <= 4 && !TAPSA;
     uint2 *sthr = reinterpret_cast<uint2 *>(
         (reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
@@ -454,6 +460,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
 
     for (int k = threadIdx.x; k < tab_entries; k += blockDim.x) {
         uint32_t thi;
+        uint64_t tfull = 0;  // NATIVE: the 33-bit Philox threshold T
         if (TAPSA) {
             thi = (uint32_t)(a.thr[k] >> 32);  // host table is already [acc + f dmax]
         } else {
@@ -464,9 +471,13 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 raw = 2 * pp - d;
                 ok = pp <= d;
             }
-            thi = ok ? (uint32_t)(a.thr[raw + a.dmax] >> 32) : 0u;
+            tfull = ok ? a.thr[raw + a.dmax] : 0ULL;
+            thi = (uint32_t)(tfull >> 32);
         }
-        if (ALG == 0) {  // (lo, hi) of the 33-bit ~thi + 2 (packed_decide_n2)
+        if (NATIVE) {  // (lo, hi) of the 33-bit 2^32 - T: carry of X + it is X >= T
+            const uint64_t nt = (1ULL << 32) - tfull;
+            sthr[k] = make_uint2((uint32_t)nt, (uint32_t)(nt >> 32));
+        } else if (ALG == 0) {  // (lo, hi) of the 33-bit ~thi + 2 (packed_decide_n2)
             const uint64_t n2 = (uint64_t)(~thi) + 2u;
             sthr[k] = make_uint2((uint32_t)n2, (uint32_t)(n2 >> 32));
         } else {
@@ -726,6 +737,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
                 uint32_t word = 0, tie = 0xffffffffu;
                 const uint32_t ui = (uint32_t)i;
+                uint32_t X[4];  // NATIVE: the current Philox block (trials 4k .. 4k + 3)
                 // NIB: transpose the L count planes into 32 nibbles (N[k] nibble j =
                 // count of trial 8k + j), a few ops per 32 trials instead of 2L per trial
                 uint32_t N[4] = {0u, 0u, 0u, 0u};
@@ -758,7 +770,15 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                         t = tb[2 * pop];
                     }
-                    if (CACHED) {
+                    if (NATIVE) {
+                        // one Philox call per four trials: counter (i, count, group, tag)
+                        if ((b & 3) == 3)
+                            philox4x32_10_rk(ui, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
+                                             kNativeTagR, a.rk, X);
+                        uint32_t dummy;
+                        asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+                            : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
+                    } else if (CACHED) {
                         const uint2 v = __ldcs(ctile + b * 32);
                         tie = min(tie, packed_decide_n2(v.x ^ count, v.y, t, word));
                     } else {
@@ -768,7 +788,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         tie = min(tie, packed_second_decide_n2(sl, sh, count, t, word));
                     }
                 }
-                if (tie < 3) {  // rare: some trial's draw is within 1 of its threshold -> exact 64-bit test
+                if (!NATIVE && tie < 3) {  // rare: some trial's draw is within 1 of its threshold -> exact 64-bit test
                     word = 0;
                     for (int b = 0; b < 32; ++b) {
                         int pop = 0;
@@ -1929,6 +1949,15 @@ __global__ void debug_stream(int64_t cnt, const uint64_t *key, const uint64_t *t
                              const uint64_t *x, const uint64_t *y, uint64_t *out) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g < cnt) out[g] = absorb(absorb(absorb(key[g], tag[g]), x[g]), y[g]);
+}
+
+__global__ void debug_philox(int64_t cnt, const uint32_t *ctr, const uint32_t *key, uint32_t *out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    uint32_t o[4];
+    philox4x32_10(ctr[4 * k], ctr[4 * k + 1], ctr[4 * k + 2], ctr[4 * k + 3], key[2 * k],
+                  key[2 * k + 1], o);
+    for (int j = 0; j < 4; ++j) out[4 * k + j] = o[j];
 }
 
 __global__ void debug_tanh(int64_t cnt, const double *x, double *out) {

@@ -27,10 +27,18 @@ from .engine import ExperimentSpec, run_trial_range
 from .model import MaxCutGraph
 
 
-def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+def shard_range(total: int, rank: int, world: int, align: int = 4) -> tuple[int, int]:
+    """Contiguous trial range of ``rank``.  Interior boundaries are multiples of
+    ``align`` (4: the native Philox stream draws four trials per call, so its
+    results are shard-invariant only for 4-aligned shards; replay results are
+    invariant to any split)."""
     if not 0 <= rank < world:
         raise ValueError(f"rank {rank} outside world of {world}")
-    return total * rank // world, total * (rank + 1) // world
+
+    def edge(r: int) -> int:
+        return total if r >= world else (total * r // world) // align * align
+
+    return edge(rank), edge(rank + 1)
 
 
 @dataclass

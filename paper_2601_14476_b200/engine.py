@@ -39,8 +39,14 @@ class ExperimentSpec:
     base_seed: int = 0
     threads: int = 1
     resample_variability: bool = True
+    # not in the reference: "replay" (default) draws from the reference's
+    # counter hash, bit-exact; "philox" from the native Philox4x32-10 stream
+    # (include/pbsa.h PBSA_RNG_PHILOX; plain rule, ideal profile)
+    rng: str = "replay"
 
     def __post_init__(self) -> None:
+        if self.rng not in ("replay", "philox"):
+            raise ValueError(f"rng must be 'replay' or 'philox', got {self.rng!r}")
         if self.cycles < 2:
             raise ValueError("cycles must be >= 2")
         if self.trials < 1:
@@ -107,7 +113,8 @@ def run_trial_range(spec: ExperimentSpec, graph: MaxCutGraph, start: int, stop: 
     batch = _native.Batch(model, schedule, streams.run_keys(seeds),
                           profile_rows=profile_rows(profs, model.n), graph=graph,
                           algo_code=spec.algo.kind.code, alpha=spec.algo.kernel_alpha,
-                          p_stall=spec.algo.p_stall)
+                          p_stall=spec.algo.p_stall, rng=spec.rng,
+                          rng_seed=streams.native_seed(spec.base_seed), first_trial=start)
     dev = _native.default_device() if device is None else device
     try:
         out, _ = _native.anneal_batch(batch, device=dev)
@@ -169,7 +176,8 @@ def sweep(spec: ExperimentSpec, axis: str, values: Sequence[float],
         keys = np.tile(streams.run_keys(seeds), len(grouped))
         batch = _native.Batch(model, schedule, keys, profile_rows=(lam, delta, period, model.n),
                               graph=graph, algo_code=spec.algo.kind.code,
-                              alpha=spec.algo.kernel_alpha, p_stall=spec.algo.p_stall)
+                              alpha=spec.algo.kernel_alpha, p_stall=spec.algo.p_stall,
+                              rng=spec.rng, rng_seed=streams.native_seed(spec.base_seed))
         res, _ = _native.anneal_batch(batch, device=_native.default_device())
         elapsed = (time.perf_counter() - t0) / len(grouped)
         T = spec.trials

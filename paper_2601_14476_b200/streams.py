@@ -60,6 +60,15 @@ def profile_seed(seed: int) -> int:
     return stream_u64(seed & MASK64, TAG_PROFILE)
 
 
+TAG_NATIVE = 7  # not in the reference: key of the native Philox stream (rng="philox")
+
+
+def native_seed(base_seed: int) -> int:
+    """64-bit Philox key of an experiment's native activation stream (one key
+    per experiment; trials are told apart by their global index in the counter)."""
+    return stream_u64(base_seed & MASK64, TAG_NATIVE)
+
+
 # ------------------------------------------------------- vectorised helpers
 
 def _mix64_vec(z: np.ndarray) -> np.ndarray:

@@ -87,3 +87,48 @@ def test_compute_calls_fail_loudly_without_gpu():
     with pytest.raises(RuntimeError):
         annealer.run_anneal(m, sch, annealer.AlgorithmConfig(annealer.Algorithm.PSA),
                             pbit.VariabilityProfile.ideal(3), seed=0, graph=g)
+
+
+# Random123 known-answer vectors for Philox4x32-10 (kat_vectors, philox4x32_10):
+# (counter, key, output)
+PHILOX_KATS = [
+    ([0, 0, 0, 0], [0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+    ([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+    ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+     [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]),
+]
+
+
+def test_host_philox_matches_random123_kats():
+    for ctr, key, want in PHILOX_KATS:
+        assert _native.philox_host(ctr, key) == want
+
+
+def test_host_philox_equals_oracle_philox(oracle):
+    rng = np.random.default_rng(3)
+    for _ in range(2000):
+        ctr = [int(x) for x in rng.integers(0, 2 ** 32, 4)]
+        key = [int(x) for x in rng.integers(0, 2 ** 32, 2)]
+        assert _native.philox_host(ctr, key) == oracle.philox4x32_10(ctr, key)
+
+
+def _native_decision(t: float, x: int) -> bool:
+    """The oracle's native decision: r = (2X + 1) 2^-32 - 1, +1 iff r + t >= 0."""
+    r = (2.0 * x + 1.0) * 2.0 ** -32 - 1.0
+    return r + t >= 0.0
+
+
+def test_native_threshold_matches_native_decision():
+    lib = _native.load()
+    rng = np.random.default_rng(12)
+    ts = np.concatenate([np.tanh(rng.uniform(-30, 30, 3000)), rng.uniform(-1, 1, 3000),
+                         np.ldexp(rng.uniform(-1, 1, 1000), rng.integers(-60, 0, 1000)),
+                         np.array([-1.0, 1.0, 0.0, -0.0, 2.0 ** -33, -(2.0 ** -33),
+                                   1 - 2.0 ** -53, -1 + 2.0 ** -53])])
+    for t in ts:
+        T = int(lib.pbsa_threshold_native_host(float(t)))
+        assert 0 <= T <= 2 ** 32
+        if T < 2 ** 32:
+            assert _native_decision(float(t), T)
+        if T > 0:
+            assert not _native_decision(float(t), T - 1)

@@ -109,3 +109,39 @@ def test_oracle_acceptance_criterion_7_specs(oracle, golden_acceptance, bench_gr
                               alpha=4, p_stall=0.5)
     assert np.array_equal(out["cut_trace"], golden_acceptance[f"c7_{name}_{kind}_cut_traces"])
     assert np.array_equal(out["energy_trace"], golden_acceptance[f"c7_{name}_{kind}_energy_traces"])
+
+
+def test_oracle_philox_matches_random123_kats(oracle):
+    """The native stream's generator, pinned by the published Random123
+    known-answer vectors (the reference has no Philox; see include/pbsa.h)."""
+    kats = [
+        ([0, 0, 0, 0], [0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+        ([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+        ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+         [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]),
+    ]
+    for ctr, key, want in kats:
+        assert oracle.philox4x32_10(ctr, key) == want
+
+
+def test_oracle_philox_mode_is_a_different_stream_with_the_same_schedule(oracle):
+    """rng="philox" changes only the activation draws: same i0 trace, same
+    initial spins, same update counts; different trajectories."""
+    from paper_2601_14476_b200.annealer import derive_schedule
+    from paper_2601_14476_b200.model import maxcut_to_ising
+    from paper_2601_14476_b200.pbit import VariabilityProfile
+    from cases import random_graph
+    g = random_graph(40, 3, p_edge=0.15)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 30, 10)
+    keys = [oracle.run_key(oracle.trial_seed(0, k)) for k in range(8)]
+    prof = VariabilityProfile.ideal(model.n)
+    a = oracle.anneal_batch(model, sch, "psa", prof, keys, graph=g)
+    b = oracle.anneal_batch(model, sch, "psa", prof, keys, graph=g, rng="philox", rng_seed=99)
+    c = oracle.anneal_batch(model, sch, "psa", prof, keys[4:], graph=g, rng="philox",
+                            rng_seed=99, first_trial=4)
+    assert np.array_equal(a["i0_trace"], b["i0_trace"])
+    assert np.array_equal(a["counts"], b["counts"])
+    assert not np.array_equal(a["cut_trace"], b["cut_trace"])
+    for k in ("spins", "cut_trace", "energy_trace", "inputs"):
+        assert np.array_equal(b[k][4:], c[k])
