@@ -87,8 +87,8 @@ int pbsa_plan_create(int device, int64_t n, const int64_t *indptr, const int64_t
  * first_trial + t in the counter (a multiple of 4, so any sharding of the
  * trials by multiples of 4 gives identical per-trial results); initial spins
  * still come from keys[] as in the reference.  Philox mode covers the plain
- * rule with an ideal profile on +-1 MAX-CUT models (the packed sweep); other
- * inputs return PBSA_EINVAL.  No reference interface corresponds: the
+ * rule (ideal, or with a lam/delta/period variability profile) on +-1
+ * MAX-CUT models (the packed sweeps); other inputs return PBSA_EINVAL.  No reference interface corresponds: the
  * reference has only its counter hash (streams.py); this is the north_star's
  * native RNG mode.
  */

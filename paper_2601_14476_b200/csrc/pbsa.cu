@@ -378,6 +378,22 @@ void set_packed_smem(K kernel, size_t bytes) {
 using PackedKernel = void (*)(pbsa::PackedArgs);
 PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false,
                                bool spsa = false, int var = 0, bool native = false) {
+    if (update && native && var) {  // Philox draws, per-p-bit profile (no first-absorb cache)
+        switch (L) {
+#define PBSA_NVCASE(l)                                                                \
+    case l:                                                                           \
+        return var == 2 ? pbsa::packed_sweep_timing<l, true> : pbsa::packed_sweep<l, true, false, 5>;
+            PBSA_NVCASE(1)
+            PBSA_NVCASE(2)
+            PBSA_NVCASE(3)
+            PBSA_NVCASE(4)
+            PBSA_NVCASE(5)
+            PBSA_NVCASE(6)
+            PBSA_NVCASE(7)
+#undef PBSA_NVCASE
+            default: fail(PBSA_EINVAL, "packed variability path supports degree <= 127");
+        }
+    }
     if (update && native) {  // Philox draws, plain rule, ideal profile (no first-absorb cache)
         switch (L) {
             case 1: return pbsa::packed_sweep<1, true, false, 4>;
@@ -783,9 +799,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     }
     const bool packed = (((rule_is_psa || tapsa_packed || spsa_packed) && ideal) || var_ok) && unit_J &&
                         zero_h && graph_is_model && dmax <= 127 && small_counters;
-    if (rng_mode == PBSA_RNG_PHILOX && !(packed && ideal && rule_is_psa))
+    if (rng_mode == PBSA_RNG_PHILOX && !(packed && ((ideal && rule_is_psa) || var_ok)))
         fail(PBSA_EINVAL, "rng_mode=philox supports the plain rule (pSA, TApSA alpha=1, SpSA "
-                          "p_stall=0) with an ideal profile on a +-1 MAX-CUT model of degree <= 127");
+                          "p_stall=0), ideal or with a variability profile, on a +-1 MAX-CUT model "
+                          "of degree <= 127");
     P.native = rng_mode == PBSA_RNG_PHILOX;
     P.nseed = rng_seed;
     P.first_trial = first_trial;
@@ -1036,8 +1053,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         {
             // (native mode runs the launched sweep only)
             const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode && !P.native;
-            const bool timing = P.var_mode && !P.var_uniform;
-            const bool varu = P.var_mode && P.var_uniform;
+            const bool timing = P.var_mode && !P.var_uniform && !P.native;
+            const bool varu = P.var_mode && P.var_uniform && !P.native;
             const int tab = (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
             P.res_smem = 512 + (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;
             int max_smem = 0;

@@ -414,7 +414,8 @@ __device__ __forceinline__ void warp_cut_flush(const uint32_t (&C)[CP], int dsum
 
 // Variability near-ties: the reference's fp64 arithmetic (_kernels.py:150-152)
 // on the full 64-bit draw, for the trials flagged in `exact`.
-template <int L>
+// NATIVE: the same on the Philox draw, r = (2X + 1) 2^-32 - 1 (philox.cuh).
+template <int L, bool NATIVE = false>
 __device__ __forceinline__ uint32_t var_exact_bits(const PackedArgs &a, uint32_t exact, const uint32_t (&p)[L],
                                                 int d, int w, int i, uint32_t count) {
     uint32_t word = 0;
@@ -424,9 +425,18 @@ __device__ __forceinline__ uint32_t var_exact_bits(const PackedArgs &a, uint32_t
         int pop = 0;
         for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
         const size_t idx = ((size_t)w * 32 + b) * a.n + i;
-        const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)(uint32_t)i;
-        const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
-        const double r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+        double r;
+        if (NATIVE) {
+            uint32_t o[4];
+            philox4x32_10_rk((uint32_t)i, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
+                             kNativeTagR, a.rk, o);
+            const uint32_t x = (b & 2) ? ((b & 1) ? o[3] : o[2]) : ((b & 1) ? o[1] : o[0]);
+            r = __dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(2.0, (double)x), 1.0), 0x1p-32), 1.0);
+        } else {
+            const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)(uint32_t)i;
+            const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+            r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+        }
         const double inp = __dmul_rn(a.i0, (double)(2 * pop - d));
         const double xx = __dmul_rn(a.lam64[idx], __dadd_rn(inp, a.del64[idx]));
         word |= (uint32_t)(__dadd_rn(r, pb_libm_tanh(xx)) >= 0.0) << b;
@@ -444,8 +454,8 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     // Larger degrees: entries indexed by raw + dmax.  TApSA: 64-entry rows by S.
     constexpr bool TAPSA = ALG == 1;
     constexpr bool SPSA = ALG == 2;
-    constexpr bool VAR = ALG == 3;
-    constexpr bool NATIVE = ALG == 4;  // plain rule, Philox draws (philox.cuh)
+    constexpr bool VAR = ALG == 3 || ALG == 5;
+    constexpr bool NATIVE = ALG == 4 || ALG == 5;  // Philox draws (philox.cuh): 4 ideal, 5 varied
     constexpr bool NIB = L <= 4 && !TAPSA;
     uint2 *sthr = reinterpret_cast<uint2 *>(
         (reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
@@ -474,7 +484,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             tfull = ok ? a.thr[raw + a.dmax] : 0ULL;
             thi = (uint32_t)(tfull >> 32);
         }
-        if (NATIVE) {  // (lo, hi) of the 33-bit 2^32 - T: carry of X + it is X >= T
+        if (ALG == 4) {  // (lo, hi) of the 33-bit 2^32 - T: carry of X + it is X >= T
             const uint64_t nt = (1ULL << 32) - tfull;
             sthr[k] = make_uint2((uint32_t)nt, (uint32_t)(nt >> 32));
         } else if (ALG == 0) {  // (lo, hi) of the 33-bit ~thi + 2 (packed_decide_n2)
@@ -541,6 +551,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
                 const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
                 uint32_t word = 0, exact = 0;
+                uint32_t X[4];  // NATIVE: the current Philox block (trials 4k .. 4k + 3)
                 auto decide = [&](int b, float2 lv) {
                     int pop = 0;
 #pragma unroll
@@ -551,7 +562,12 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
                     const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
                     uint32_t zh;
-                    if (CACHED) {
+                    if (NATIVE) {  // u 2^32 = X + 1/2: the replay margin covers it
+                        if ((b & 3) == 0)
+                            philox4x32_10_rk(ui, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
+                                             kNativeTagR, a.rk, X);
+                        zh = X[b & 3];
+                    } else if (CACHED) {
                         const uint2 v = __ldcs(ctile + b * 32);
                         zh = packed_hash_hi_y(v.x ^ count, v.y);
                     } else {
@@ -570,7 +586,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 };
 #pragma unroll
                 for (int b = 0; b < 32; ++b) decide(b, __ldg(pr + (size_t)b * a.n));
-                if (exact) word |= var_exact_bits<L>(a, exact, p, d, w, i, count);
+                if (exact) word |= var_exact_bits<L, NATIVE>(a, exact, p, d, w, i, count);
                 a.snew[(size_t)w * a.n + i] = word;
             } else if (UPDATE && TAPSA) {
                 // S = p of this cycle + the other filled slots of the ring, in
@@ -826,7 +842,7 @@ constexpr int kMaxDivisors = 256;
 constexpr size_t kTimingSmem = kPackedWarps * 32 * sizeof(uint2) + kMaxDivisors * 8 * 4 +
                                2 * kPackedWarps * 32 * 4 + kPackedWarps * 1024 * 4;
 
-template <int L>
+template <int L, bool NATIVE = false>
 __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
     packed_sweep_timing(PackedArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
@@ -923,10 +939,18 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
                 const float x = fmaf(lv.x, ir, lv.y);
                 const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
                 const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
-                const uint2 kc = key[b];
-                uint32_t sl, sh;
-                packed_first_absorb(kc.x ^ (uint32_t)ii, kc.y, sl, sh);
-                const uint32_t zh = packed_hash_hi(sl, sh, count);
+                uint32_t zh;
+                if (NATIVE) {  // one Philox block per fired trial (fired trials are sparse)
+                    uint32_t o[4];
+                    philox4x32_10_rk((uint32_t)ii, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
+                                     kNativeTagR, a.rk, o);
+                    zh = (b & 2) ? ((b & 1) ? o[3] : o[2]) : ((b & 1) ? o[1] : o[0]);
+                } else {
+                    const uint2 kc = key[b];
+                    uint32_t sl, sh;
+                    packed_first_absorb(kc.x ^ (uint32_t)ii, kc.y, sl, sh);
+                    zh = packed_hash_hi(sl, sh, count);
+                }
                 const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
                 if (fabsf(diff) < fmaf(A, mA, m0))
                     atomicOr(exm + l, 1u << b);
@@ -949,7 +973,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
             if (valid) {
                 uint32_t word = (own & ~fire) | res[lane];
                 const uint32_t ex = exm[lane];
-                if (ex) word |= var_exact_bits<L>(a, ex, p, d, w, i, count);
+                if (ex) word |= var_exact_bits<L, NATIVE>(a, ex, p, d, w, i, count);
                 a.snew[(size_t)w * a.n + i] = word;
             }
             __syncwarp();

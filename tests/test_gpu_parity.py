@@ -468,13 +468,34 @@ def test_device_philox_matches_random123_kats_and_host():
 
 
 def _native_run(graph, trials, cycles, seed=0x1234_5678_9ABC_DEF0, first_trial=0, algo=0,
-                alpha=1, p_stall=0.5):
+                alpha=1, p_stall=0.5, profs=None):
     model = maxcut_to_ising(graph)
     sch = derive_schedule(model, cycles, 10)
     keys = [streams.run_key(streams.trial_seed(0, first_trial + k)) for k in range(trials)]
     b = _native.Batch(model, sch, keys, graph=graph, algo_code=algo, alpha=alpha,
-                      p_stall=p_stall, rng="philox", rng_seed=seed, first_trial=first_trial)
+                      p_stall=p_stall, rng="philox", rng_seed=seed, first_trial=first_trial,
+                      profile_rows=profile_rows(profs, model.n))
     return model, sch, keys, _native.anneal_batch(b)[0]
+
+
+@pytest.mark.parametrize("name,sig,trials,cycles", [
+    ("G81", (0.5, 0.5, 0.5), 64, 30), ("G55", (0.5, 0.5, 0.0), 64, 40),
+    ("G1", (0.0, 0.0, 0.5), 40, 60), ("G22", (0.5, 0.5, 0.5), 36, 40)])
+def test_philox_mode_with_variability_matches_oracle(oracle, bench_graphs, name, sig, trials,
+                                                     cycles):
+    """Varied profiles under the native stream: the sigmoid prefilter and the
+    exact fp64 recheck on the Philox draw (packed_sweep ALG=5 and
+    packed_sweep_timing<L, NATIVE>) against the oracle's Philox mode."""
+    graph = bench_graphs(name)
+    n = graph.n
+    profs = [sample_variability(VariabilityConfig(*sig), n, np.random.default_rng(500 + k))
+             for k in range(trials)]
+    seed = 0xFEED_F00D_1234
+    model, sch, keys, got = _native_run(graph, trials, cycles, seed, profs=profs)
+    want = oracle.anneal_batch(model, sch, "psa", profs, keys, graph=graph, rng="philox",
+                               rng_seed=seed)
+    for k in ("spins", "inputs", "counts", "i0_trace", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
 
 
 @pytest.mark.parametrize("name,trials,cycles", [("G81", 96, 40), ("G55", 64, 60),
@@ -507,8 +528,32 @@ def test_philox_mode_rejects_unsupported_inputs(bench_graphs):
     graph = bench_graphs("G1")
     with pytest.raises(ValueError, match="philox"):
         _native_run(graph, 8, 10, algo=1, alpha=3)
+    with pytest.raises(ValueError, match="philox"):
+        _native_run(graph, 8, 10, algo=2, p_stall=0.3)
     with pytest.raises(ValueError, match="multiple of 4"):
         _native_run(graph, 8, 10, first_trial=2)
+
+
+@pytest.mark.parametrize("name,sig,trials", [("G1", (0.0, 0.0, 0.5), 128),
+                                             ("G81", (0.5, 0.5, 0.5), 256),
+                                             ("G55", (1.0, 0.0, 0.0), 256)])
+def test_philox_cut_statistics_match_reference_with_variability(bench_graphs, golden_analogs,
+                                                                name, sig, trials):
+    """The north_star statistical bar where pSA actually anneals (the
+    variability study, normalized cuts 0.4-0.999): mean final cut and mean
+    per-trial best cut of the native stream within 0.5 % of the best-known cut
+    of the replayed reference stream (which is bit-exact to the reference)."""
+    graph = bench_graphs(name)
+    best_known = golden_analogs[name]["best_known_analog"]
+    spec = engine.ExperimentSpec(graph=name, algo=AlgorithmConfig(Algorithm.PSA),
+                                 variability=VariabilityConfig(*sig), cycles=1000, trials=trials)
+    rep = engine.run_trials(spec, {name: graph})
+    nat = engine.run_trials(dataclasses.replace(spec, rng="philox"), {name: graph})
+    assert abs(nat.mean_cut - rep.mean_cut) <= 0.005 * best_known, (nat.mean_cut, rep.mean_cut)
+    b_rep = np.mean([r.best_cut for r in rep.results])
+    b_nat = np.mean([r.best_cut for r in nat.results])
+    assert abs(b_nat - b_rep) <= 0.005 * best_known, (b_nat, b_rep)
+    assert nat.mean_cut > 0.3 * best_known  # a run that anneals, not the sigma = 0 degenerate case
 
 
 def test_philox_cut_statistics_match_reference_stream(bench_graphs, golden_analogs):
