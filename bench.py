@@ -70,8 +70,10 @@ def dist_env():
 
 
 def shard(total, rank, world):
-    lo = total * rank // world
-    return lo, total * (rank + 1) // world
+    # contiguous, 4-aligned interior boundaries (the native Philox stream draws
+    # four trials per call; distributed.shard_range)
+    from paper_2601_14476_b200.distributed import shard_range
+    return shard_range(total, rank, world)
 
 
 def workload(name, cycles):

@@ -250,6 +250,7 @@ struct pbsa_plan {
     bool tapsa_hist_from_raw = false;  // TAPSA alpha=1 routed to the packed path
     bool tapsa_packed = false;         // TAPSA alpha>=2 on the packed path (bit-sliced ring)
     bool native = false;               // PBSA_RNG_PHILOX: Philox draws (philox.cuh)
+    bool reg4 = false;                 // packed path: every degree is 4 (gather_counts_reg4)
     uint64_t nseed = 0;                // Philox key
     int64_t first_trial = 0;           // global index of trial 0 (Philox trial groups)
     bool spsa_packed = false;          // SPSA p>0 on the packed path (per-p-bit drive index)
@@ -845,6 +846,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         std::vector<uint32_t> adjv(nnz);
         for (int64_t k = 0; k < nnz; ++k)
             adjv[k] = (uint32_t)indices[k] | (values[k] < 0 ? 0x80000000u : 0u);
+        // degree-4 regular graph (tori): rows at 4i, gathered with one 16-byte load
+        P.reg4 = nnz == 4 * n;
+        for (int64_t i = 0; i < n && P.reg4; ++i) P.reg4 = indptr[i] == 4 * i;
+        if (const char *env = std::getenv("PBSA_REG4")) P.reg4 = P.reg4 && env[0] != '0';
         P.adj.upload(adjv, st);
         std::vector<uint64_t> krg(P.Tp);
         std::vector<uint2> kfc(P.Tp);
@@ -1404,6 +1409,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     a.chunks = P.chunks;
                     a.count = pl.count;
                     a.do_update = pl.update;
+                    a.reg4 = P.reg4 ? 1 : 0;
                     if (P.native) {
                         a.nk0 = (uint32_t)P.nseed;
                         a.nk1 = (uint32_t)(P.nseed >> 32);

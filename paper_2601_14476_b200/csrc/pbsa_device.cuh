@@ -160,6 +160,7 @@ struct PackedArgs {
     uint32_t nk0, nk1;        // Philox key (native seed)
     uint32_t rk[20];          // its ten round keys (philox_round_keys)
     uint32_t ngroup;          // Philox trial-group counter of this launch's word 0: (first trial) / 4
+    int reg4;                 // every degree is 4 (rowptr[i] = 4i): gather_counts_reg4
 };
 
 // Exact H >= thr for H = mix64(x); thr == ~0 encodes "never" (tanh == -1),
@@ -365,6 +366,27 @@ __device__ __forceinline__ void gather_counts(const uint32_t *__restrict__ adj,
     }, p);
 }
 
+// Degree-4 regular graphs (the G-set tori): node i's entries sit at 4i, so the
+// row needs no rowptr load and its four entries come in one 16-byte load --
+// one dependent global load fewer in front of the neighbour gather.
+template <int L>
+__device__ __forceinline__ void gather_counts_reg4(const uint32_t *__restrict__ adj,
+                                                   const uint32_t *__restrict__ sw, int i,
+                                                   uint32_t (&p)[L]) {
+    const uint4 e = __ldg(reinterpret_cast<const uint4 *>(adj) + i);
+    const uint32_t x0 = __ldg(sw + (e.x & 0x7fffffffu)) ^ (uint32_t)((int32_t)e.x >> 31);
+    const uint32_t x1 = __ldg(sw + (e.y & 0x7fffffffu)) ^ (uint32_t)((int32_t)e.y >> 31);
+    const uint32_t x2 = __ldg(sw + (e.z & 0x7fffffffu)) ^ (uint32_t)((int32_t)e.z >> 31);
+    const uint32_t x3 = __ldg(sw + (e.w & 0x7fffffffu)) ^ (uint32_t)((int32_t)e.w >> 31);
+    // bit-sliced x0 + x1 + x2 + x3 (<= 4 < 2^L, L >= 3 since dmax = 4)
+    const uint32_t s01 = x0 ^ x1, c01 = x0 & x1, s23 = x2 ^ x3, c23 = x2 & x3;
+    const uint32_t s = s01 ^ s23, cs = s01 & s23;     // weight-1 digit and its carry
+    const uint32_t t = c01 ^ c23 ^ cs;                 // weight-2 digit
+    const uint32_t f = (c01 & c23) | (cs & (c01 ^ c23));  // weight-4 digit
+#pragma unroll
+    for (int r = 0; r < L; ++r) p[r] = r == 0 ? s : r == 1 ? t : r == 2 ? f : 0u;
+}
+
 // Cut count g = #{J_ik s_i s_k = +1} = (s_i = +1) ? p : d - p, bit-sliced:
 // d - p = ~p + (d + 1) mod 2^L (p <= d < 2^L), then a per-trial select.
 template <int L>
@@ -524,11 +546,19 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
         for (int ch = q; ch < a.chunks; ch += a.warps_per_word) {
             const int i = ch * 32 + lane;
             if (i >= a.n) continue;
-            const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
-            const uint32_t own = __ldg(sw + i);
             uint32_t p[L];
-            gather_counts<L>(a.adj, sw, beg, end, p);
-            const int d = (int)(end - beg);
+            int d;
+            uint32_t own;
+            if (L >= 3 && a.reg4) {
+                own = __ldg(sw + i);
+                gather_counts_reg4<L>(a.adj, sw, i, p);
+                d = 4;
+            } else {
+                const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
+                own = __ldg(sw + i);
+                gather_counts<L>(a.adj, sw, beg, end, p);
+                d = (int)(end - beg);
+            }
             uint32_t g[L];
             cut_counts<L>(p, own, d, g);
             dsum += d;
@@ -886,17 +916,30 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
             // spread almost every warp has some firing trial)
             uint32_t own = 0, fire = 0, beg = 0, end = 0;
             uint32_t pl[8];
+            const bool reg4 = L >= 3 && a.reg4;
             if (valid) {
-                beg = __ldg(a.rowptr + i);
-                end = __ldg(a.rowptr + i + 1);
+                if (!reg4) {
+                    beg = __ldg(a.rowptr + i);
+                    end = __ldg(a.rowptr + i + 1);
+                }
                 own = __ldg(sw + i);
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k)
                 pl[k] = (valid && k < a.nplanes) ? __ldg(a.pplanes + ((size_t)w * a.nplanes + k) * a.n + i) : 0u;
             uint32_t p[L];
-            const int d = (int)(end - beg);
-            gather_counts<L>(a.adj, sw, beg, end, p);
+            int d = (int)(end - beg);
+            if (reg4) {
+                if (valid) {
+                    gather_counts_reg4<L>(a.adj, sw, i, p);
+                    d = 4;
+                } else {
+#pragma unroll
+                    for (int r = 0; r < L; ++r) p[r] = 0;
+                }
+            } else {
+                gather_counts<L>(a.adj, sw, beg, end, p);
+            }
             if (valid) {
                 for (int dv = 0; dv < a.ndiv; ++dv) {
                     const uint4 x0 = *reinterpret_cast<const uint4 *>(sdivx + dv * 8);

@@ -45,7 +45,7 @@ def bytes_per_update(g, varied=False):
     return nnz / n + 1 + (2.125 * nnz + 4 * (n + 1)) / (32 * n) + (8.0 if varied else 0.0)
 
 
-def gpu_run(g, kind, sig, T, cycles=1000, alpha=4):
+def gpu_run(g, kind, sig, T, cycles=1000, alpha=4, rng="replay"):
     m = maxcut_to_ising(g)
     sch = derive_schedule(m, cycles, 10)
     spec = ExperimentSpec(graph="x", algo=AlgorithmConfig(kind, alpha=alpha),
@@ -55,7 +55,8 @@ def gpu_run(g, kind, sig, T, cycles=1000, alpha=4):
     profs = trial_profiles(spec, m.n, seeds)
     t_prof = time.perf_counter() - t0
     b = _native.Batch(m, sch, streams.run_keys(seeds), profile_rows=profile_rows(profs, m.n), graph=g,
-                      algo_code=kind.code, alpha=spec.algo.kernel_alpha, p_stall=0.5)
+                      algo_code=kind.code, alpha=spec.algo.kernel_alpha, p_stall=0.5, rng=rng,
+                      rng_seed=streams.native_seed(0))
     plan = _native.Plan(b)
     plan.run()
     ms = plan.run()
@@ -104,6 +105,7 @@ def main():
     def add(cfg, name, kind, sig, T, cpu_T, note=""):
         g, _ = benchmarks.load(name)
         gpu = gpu_run(g, kind, sig, T)
+        nat = gpu_run(g, kind, sig, T, rng="philox") if kind == Algorithm.PSA else None
         cpu = cpu_run(g, kind, sig, cpu_T) if cpu_T else None
         d = denom(name)
         B = bytes_per_update(g, any(sig))
@@ -116,7 +118,11 @@ def main():
                    cpu_upd_s=cpu["upd_s"] if cpu else None, cpu_threads=threads,
                    cpu_sample_trials=cpu_T, speedup=(gpu["upd_s"] / cpu["upd_s"]) if cpu else None,
                    mean_cut=gpu["mean_cut"], normalized=(gpu["mean_cut"] / d) if d else None,
-                   profile_sampling_s=gpu["profile_s"], note=note)
+                   profile_sampling_s=gpu["profile_s"], note=note,
+                   philox_path=nat["path"] if nat else None,
+                   philox_gpu_ms=nat["ms"] if nat else None,
+                   philox_upd_s=nat["upd_s"] if nat else None,
+                   philox_normalized=(nat["mean_cut"] / d) if (nat and d) else None)
         rows.append(row)
         print(json.dumps(row), flush=True)
 
@@ -146,14 +152,19 @@ def main():
              "cluster launch per run, state in shared memory: their roofline is the SMEM ceiling, "
              f"{SMEM_PEAK / 1000:.1f} TB/s), `active_fast` / `active` (general path). Bytes per update: "
              "SURVEY 8(d) B, plus 8 B for a varied profile.", "",
-             "| cfg | graph (n) | rule | sigma | trials | kernel | GPU ms/run | GPU upd/s | frac of roofline (bound) | CPU upd/s | GPU/CPU | mean cut / best-known |",
-             "|---|---|---|---|---:|---|---:|---:|---:|---:|---:|---:|"]
+             "Philox columns: the same run with the native Philox4x32-10 stream (`rng=\"philox\"`; "
+             "plain rule only; always the launched packed kernels).", "",
+             "| cfg | graph (n) | rule | sigma | trials | kernel | GPU ms/run | GPU upd/s | frac of roofline (bound) | CPU upd/s | GPU/CPU | mean cut / best-known | Philox kernel | Philox ms | Philox upd/s | Philox mean cut / best-known |",
+             "|---|---|---|---|---:|---|---:|---:|---:|---:|---:|---:|---|---:|---:|---:|"]
     for r in rows:
         lines.append(
             f"| {r['config']} | {r['graph']} ({r['n']}) | {r['algo']} | {tuple(r['sigma'])} | {r['trials']} | "
             f"{r['path']} | {r['gpu_ms']:.1f} | {r['gpu_upd_s']:.3g} | {r['roofline_frac']:.3f} ({r['bound']}) | "
             f"{(r['cpu_upd_s'] or 0):.3g} | {(r['speedup'] or 0):.0f} | "
-            f"{(r['normalized'] if r['normalized'] is not None else float('nan')):.4f} |")
+            f"{(r['normalized'] if r['normalized'] is not None else float('nan')):.4f} | "
+            + (f"{r['philox_path']} | {r['philox_gpu_ms']:.1f} | {r['philox_upd_s']:.3g} | "
+               f"{(r['philox_normalized'] if r['philox_normalized'] is not None else float('nan')):.4f} |"
+               if r['philox_path'] else "- | - | - | - |"))
     (ROOT / "profiles" / f"{args.tag}_configs.md").write_text("\n".join(lines) + "\n")
 
 
