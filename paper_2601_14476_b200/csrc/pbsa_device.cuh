@@ -370,10 +370,8 @@ __device__ __forceinline__ void gather_counts(const uint32_t *__restrict__ adj,
 // row needs no rowptr load and its four entries come in one 16-byte load --
 // one dependent global load fewer in front of the neighbour gather.
 template <int L>
-__device__ __forceinline__ void gather_counts_reg4(const uint32_t *__restrict__ adj,
-                                                   const uint32_t *__restrict__ sw, int i,
+__device__ __forceinline__ void gather_counts_row4(const uint4 e, const uint32_t *__restrict__ sw,
                                                    uint32_t (&p)[L]) {
-    const uint4 e = __ldg(reinterpret_cast<const uint4 *>(adj) + i);
     const uint32_t x0 = __ldg(sw + (e.x & 0x7fffffffu)) ^ (uint32_t)((int32_t)e.x >> 31);
     const uint32_t x1 = __ldg(sw + (e.y & 0x7fffffffu)) ^ (uint32_t)((int32_t)e.y >> 31);
     const uint32_t x2 = __ldg(sw + (e.z & 0x7fffffffu)) ^ (uint32_t)((int32_t)e.z >> 31);
@@ -385,6 +383,13 @@ __device__ __forceinline__ void gather_counts_reg4(const uint32_t *__restrict__ 
     const uint32_t f = (c01 & c23) | (cs & (c01 ^ c23));  // weight-4 digit
 #pragma unroll
     for (int r = 0; r < L; ++r) p[r] = r == 0 ? s : r == 1 ? t : r == 2 ? f : 0u;
+}
+
+template <int L>
+__device__ __forceinline__ void gather_counts_reg4(const uint32_t *__restrict__ adj,
+                                                   const uint32_t *__restrict__ sw, int i,
+                                                   uint32_t (&p)[L]) {
+    gather_counts_row4<L>(__ldg(reinterpret_cast<const uint4 *>(adj) + i), sw, p);
 }
 
 // Cut count g = #{J_ik s_i s_k = +1} = (s_i = +1) ? p : d - p, bit-sliced:
@@ -543,15 +548,32 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
 
     if (live) {
         const uint32_t *sw = a.sold + (size_t)w * a.n;
+        // degree-4 rows: the next chunk's row (one 16-byte load) and own word are
+        // fetched one iteration ahead, so only the neighbour loads precede the counts
+        // (only the last chunk has lanes past n, and it has no successor)
+        const bool R4 = L >= 3 && a.reg4;
+        const uint4 *adj4 = reinterpret_cast<const uint4 *>(a.adj);
+        uint4 e_nx = make_uint4(0u, 0u, 0u, 0u);
+        uint32_t own_nx = 0;
+        if (R4 && q < a.chunks && q * 32 + lane < a.n) {
+            e_nx = __ldg(adj4 + q * 32 + lane);
+            own_nx = __ldg(sw + q * 32 + lane);
+        }
         for (int ch = q; ch < a.chunks; ch += a.warps_per_word) {
             const int i = ch * 32 + lane;
             if (i >= a.n) continue;
             uint32_t p[L];
             int d;
             uint32_t own;
-            if (L >= 3 && a.reg4) {
-                own = __ldg(sw + i);
-                gather_counts_reg4<L>(a.adj, sw, i, p);
+            if (R4) {
+                const uint4 e = e_nx;
+                own = own_nx;
+                const int ni = i + 32 * a.warps_per_word;
+                if (ni < a.n) {
+                    e_nx = __ldg(adj4 + ni);
+                    own_nx = __ldg(sw + ni);
+                }
+                gather_counts_row4<L>(e, sw, p);
                 d = 4;
             } else {
                 const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
