@@ -479,24 +479,29 @@ PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = fal
 
 using ResidentKernel = void (*)(pbsa::ResidentArgs);
 using ResidentTimingKernel = void (*)(pbsa::ResidentTimingArgs);
-ResidentTimingKernel resident_timing_for(int L) {
+ResidentTimingKernel resident_timing_for(int L, bool native = false) {
     switch (L) {
-        case 1: return pbsa::resident_timing<1>;
-        case 2: return pbsa::resident_timing<2>;
-        case 3: return pbsa::resident_timing<3>;
-        case 4: return pbsa::resident_timing<4>;
-        case 5: return pbsa::resident_timing<5>;
-        case 6: return pbsa::resident_timing<6>;
-        case 7: return pbsa::resident_timing<7>;
+#define PBSA_RTCASE(l) \
+    case l: return native ? pbsa::resident_timing<l, true> : pbsa::resident_timing<l, false>;
+        PBSA_RTCASE(1)
+        PBSA_RTCASE(2)
+        PBSA_RTCASE(3)
+        PBSA_RTCASE(4)
+        PBSA_RTCASE(5)
+        PBSA_RTCASE(6)
+        PBSA_RTCASE(7)
+#undef PBSA_RTCASE
         default: fail(PBSA_EINVAL, "resident sweep supports degree <= 127");
     }
 }
 
-ResidentKernel resident_kernel_for(int L, bool cached, bool varu = false) {
+ResidentKernel resident_kernel_for(int L, bool cached, bool varu = false, bool native = false) {
     switch (L) {
 #define PBSA_RCASE(l)                                                                          \
     case l:                                                                                    \
-        return varu ? (cached ? pbsa::resident_sweep<l, true, true> : pbsa::resident_sweep<l, false, true>) \
+        return native ? (varu ? pbsa::resident_sweep<l, false, true, true>                     \
+                              : pbsa::resident_sweep<l, false, false, true>)                   \
+               : varu ? (cached ? pbsa::resident_sweep<l, true, true> : pbsa::resident_sweep<l, false, true>) \
                     : (cached ? pbsa::resident_sweep<l, true, false> : pbsa::resident_sweep<l, false, false>);
         PBSA_RCASE(1)
         PBSA_RCASE(2)
@@ -1056,10 +1061,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // resident mode (plain rule, ideal profile): a word's double-buffered
         // state in shared memory; cluster size so that W clusters cover the SMs
         {
-            // (native mode runs the launched sweep only)
-            const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode && !P.native;
-            const bool timing = P.var_mode && !P.var_uniform && !P.native;
-            const bool varu = P.var_mode && P.var_uniform && !P.native;
+            const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode;
+            const bool timing = P.var_mode && !P.var_uniform;
+            const bool varu = P.var_mode && P.var_uniform;
             const int tab = (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
             P.res_smem = 512 + (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;
             int max_smem = 0;
@@ -1096,7 +1100,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                                   P.i0[std::min<int64_t>(pl.cycle, cycles - 1)]});
                 P.rlaunch.upload(rl, st);
                 if (!P.i0_dev.n) P.i0_dev.upload(P.i0, st);
-                ResidentTimingKernel rk = resident_timing_for(P.L);
+                ResidentTimingKernel rk = resident_timing_for(P.L, P.native);
                 CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
             } else if ((plain || varu) && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
                 // (the per-thread cut counter takes up to 32 nodes)
@@ -1106,7 +1110,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 P.res_threads = thr;
                 if (P.use_cache && P.phase_words < P.W) P.acache.alloc((size_t)P.W * P.chunks * 1024);
                 P.phase_words = P.W;
-                ResidentKernel rk = resident_kernel_for(P.L, P.use_cache, varu);
+                ResidentKernel rk = resident_kernel_for(P.L, P.use_cache, varu, P.native);
                 CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
                 if (varu && !P.i0_dev.n) P.i0_dev.upload(P.i0, st);
                 if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -1302,6 +1306,10 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             r.nplanes = P.nplanes;
             r.cycles = (int)P.cycles;
             r.margin = P.var_margin;
+            if (P.native) {
+                pbsa::philox_round_keys((uint32_t)P.nseed, (uint32_t)(P.nseed >> 32), r.rk);
+                r.ngroup = (uint32_t)(P.first_trial / 4);
+            }
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3((unsigned)(P.W * P.res_cs));
             cfg.blockDim = dim3((unsigned)P.res_threads);
@@ -1314,7 +1322,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&cfg, resident_timing_for(P.L), r));
+            CK(cudaLaunchKernelEx(&cfg, resident_timing_for(P.L, P.native), r));
             ++P.launches;
             P.sweep_launches = (int64_t)P.rlaunch.n - 1;
             cur = 1;
@@ -1351,6 +1359,10 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                 r.inp_out = P.inp_var.p;
                 r.margin = P.var_margin;
             }
+            if (P.native) {
+                pbsa::philox_round_keys((uint32_t)P.nseed, (uint32_t)(P.nseed >> 32), r.rk);
+                r.ngroup = (uint32_t)(P.first_trial / 4);
+            }
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3((unsigned)(P.W * P.res_cs));
             cfg.blockDim = dim3((unsigned)P.res_threads);
@@ -1363,7 +1375,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&cfg, resident_kernel_for(P.L, P.use_cache, P.var_mode), r));
+            CK(cudaLaunchKernelEx(&cfg, resident_kernel_for(P.L, P.use_cache, P.var_mode, P.native), r));
             ++P.launches;
             P.sweep_launches = P.cycles;
             cur = 1;

@@ -1075,11 +1075,14 @@ struct ResidentArgs {
     const double *i0;           // [cycles]
     double *inp_out;            // [Tp][n] inputs of the last cycle
     float margin;
+    // NATIVE: Philox draws (philox.cuh); thr then holds the 32-bit thresholds
+    uint32_t rk[20];            // round keys of the native seed
+    uint32_t ngroup;            // Philox trial group of word 0: (first trial) / 4
 };
 
 constexpr int kResidentExtraPlanes = 3;  // cut counters for up to 32 nodes per thread
 
-template <int L, bool CACHED, bool VARU = false>
+template <int L, bool CACHED, bool VARU = false, bool NATIVE = false>
 __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -1121,12 +1124,15 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                 raw = 2 * pp - d;
                 ok = pp <= d;
             }
-            const uint32_t thi = ok ? (uint32_t)(thr[raw + a.dmax] >> 32) : 0u;
-            const uint64_t n2 = (uint64_t)(~thi) + 2u;
+            const uint64_t tfull = ok ? thr[raw + a.dmax] : 0ULL;
+            const uint32_t thi = (uint32_t)(tfull >> 32);
+            // replay: the 33-bit ~thi + 2 (packed_decide_n2); native: 2^32 - T
+            const uint64_t n2 = NATIVE ? (1ULL << 32) - tfull : (uint64_t)(~thi) + 2u;
             sthr[k] = make_uint2((uint32_t)n2, (uint32_t)(n2 >> 32));
         }
         __syncthreads();
         const uint32_t count = (uint32_t)(c * a.t_res);
+        const uint32_t grp = a.ngroup + 8u * (uint32_t)w;  // NATIVE: Philox group of trial 0
         uint32_t C[CP];
 #pragma unroll
         for (int r = 0; r < CP; ++r) C[r] = 0;
@@ -1155,6 +1161,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                 const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
                 const float2 *pr = a.prof + (size_t)w * 32 * a.n + i;
                 uint32_t word = 0, exact = 0;
+                uint32_t X[4];
 #pragma unroll
                 for (int b = 0; b < 32; ++b) {
                     int pop = 0;
@@ -1167,7 +1174,11 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                     const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
                     const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
                     uint32_t zh;
-                    if (CACHED) {
+                    if (NATIVE) {
+                        if ((b & 3) == 0)
+                            philox4x32_10_rk(ui, count, grp + (uint32_t)(b >> 2), kNativeTagR, a.rk, X);
+                        zh = X[b & 3];
+                    } else if (CACHED) {
                         const uint2 v = __ldcs(ctile + b * 32);
                         zh = packed_hash_hi_y(v.x ^ count, v.y);
                     } else {
@@ -1190,9 +1201,17 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                     int pop = 0;
                     for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                     const size_t idx = ((size_t)w * 32 + b) * a.n + i;
-                    const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
-                    const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
-                    const double r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+                    double r;
+                    if (NATIVE) {
+                        uint32_t o[4];
+                        philox4x32_10_rk(ui, count, grp + (uint32_t)(b >> 2), kNativeTagR, a.rk, o);
+                        const uint32_t x = (b & 2) ? ((b & 1) ? o[3] : o[2]) : ((b & 1) ? o[1] : o[0]);
+                        r = __dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(2.0, (double)x), 1.0), 0x1p-32), 1.0);
+                    } else {
+                        const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
+                        const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                        r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+                    }
                     const double xx = __dmul_rn(a.lam64[idx], __dadd_rn(__dmul_rn(i0, (double)(2 * pop - d)),
                                                                        a.del64[idx]));
                     word |= (uint32_t)(__dadd_rn(r, pb_libm_tanh(xx)) >= 0.0) << b;
@@ -1222,6 +1241,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                 rb = (uint32_t)__cvta_generic_to_shared(sthr) + (uint32_t)d * 128u;
             }
             const uint2 *tb = sthr + (a.dmax - d);
+            uint32_t X[4];
 #pragma unroll
             for (int b = 31; b >= 0; --b) {
                 uint2 t;
@@ -1236,7 +1256,13 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                     for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                     t = tb[2 * pop];
                 }
-                if (CACHED) {
+                if (NATIVE) {
+                    if ((b & 3) == 3)
+                        philox4x32_10_rk(ui, count, grp + (uint32_t)(b >> 2), kNativeTagR, a.rk, X);
+                    uint32_t dummy;
+                    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+                        : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
+                } else if (CACHED) {
                     const uint2 v = __ldcs(ctile + b * 32);
                     tie = min(tie, packed_decide_n2(v.x ^ count, v.y, t, word));
                 } else {
@@ -1246,7 +1272,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                     tie = min(tie, packed_second_decide_n2(sl, sh, count, t, word));
                 }
             }
-            if (tie < 3) {  // rare: a draw within 1 of its threshold -> exact 64-bit test
+            if (!NATIVE && tie < 3) {  // rare: a draw within 1 of its threshold -> exact 64-bit test
                 word = 0;
                 for (int b = 0; b < 32; ++b) {
                     int pop = 0;
@@ -1308,9 +1334,11 @@ struct ResidentTimingArgs {
     double *inp_out;            // [Tp][n]
     int n, W, Tp, nplanes, cycles;
     float margin;
+    uint32_t rk[20];            // NATIVE: Philox round keys
+    uint32_t ngroup;            // NATIVE: Philox trial group of word 0
 };
 
-template <int L>
+template <int L, bool NATIVE = false>
 __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -1436,10 +1464,18 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
                 const float x = fmaf(lv.x, ir, lv.y);
                 const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
                 const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
-                const uint2 kc = key[b];
-                uint32_t sl, sh;
-                packed_first_absorb(kc.x ^ (uint32_t)ii, kc.y, sl, sh);
-                const uint32_t zh = packed_hash_hi(sl, sh, count);
+                uint32_t zh;
+                if (NATIVE) {
+                    uint32_t o[4];
+                    philox4x32_10_rk((uint32_t)ii, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
+                                     kNativeTagR, a.rk, o);
+                    zh = (b & 2) ? ((b & 1) ? o[3] : o[2]) : ((b & 1) ? o[1] : o[0]);
+                } else {
+                    const uint2 kc = key[b];
+                    uint32_t sl, sh;
+                    packed_first_absorb(kc.x ^ (uint32_t)ii, kc.y, sl, sh);
+                    zh = packed_hash_hi(sl, sh, count);
+                }
                 const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
                 if (fabsf(diff) < fmaf(A, mA, m0))
                     atomicOr(wexm + l, 1u << b);
@@ -1468,9 +1504,18 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
                     int pop = 0;
                     for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                     const size_t idx = ((size_t)w * 32 + b) * a.n + i;
-                    const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)(uint32_t)i;
-                    const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
-                    const double r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+                    double r;
+                    if (NATIVE) {
+                        uint32_t o[4];
+                        philox4x32_10_rk((uint32_t)i, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
+                                         kNativeTagR, a.rk, o);
+                        const uint32_t x = (b & 2) ? ((b & 1) ? o[3] : o[2]) : ((b & 1) ? o[1] : o[0]);
+                        r = __dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(2.0, (double)x), 1.0), 0x1p-32), 1.0);
+                    } else {
+                        const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)(uint32_t)i;
+                        const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                        r = __dsub_rn(__dmul_rn(2.0, u01_of(mix64(x2))), 1.0);
+                    }
                     const double xx = __dmul_rn(a.lam64[idx], __dadd_rn(__dmul_rn(i0, (double)(2 * pop - d)),
                                                                        a.del64[idx]));
                     word |= (uint32_t)(__dadd_rn(r, pb_libm_tanh(xx)) >= 0.0) << b;

@@ -480,12 +480,14 @@ def _native_run(graph, trials, cycles, seed=0x1234_5678_9ABC_DEF0, first_trial=0
 
 @pytest.mark.parametrize("name,sig,trials,cycles", [
     ("G81", (0.5, 0.5, 0.5), 64, 30), ("G55", (0.5, 0.5, 0.0), 64, 40),
-    ("G1", (0.0, 0.0, 0.5), 40, 60), ("G22", (0.5, 0.5, 0.5), 36, 40)])
+    ("G1", (0.0, 0.0, 0.5), 40, 60), ("G22", (0.5, 0.5, 0.5), 36, 40),
+    ("G1", (0.5, 0.5, 0.0), 40, 60)])
 def test_philox_mode_with_variability_matches_oracle(oracle, bench_graphs, name, sig, trials,
                                                      cycles):
     """Varied profiles under the native stream: the sigmoid prefilter and the
-    exact fp64 recheck on the Philox draw (packed_sweep ALG=5 and
-    packed_sweep_timing<L, NATIVE>) against the oracle's Philox mode."""
+    exact fp64 recheck on the Philox draw (packed_sweep ALG=5,
+    packed_sweep_timing<L, NATIVE>, and the resident cluster kernels for the
+    small G1 batches) against the oracle's Philox mode."""
     graph = bench_graphs(name)
     n = graph.n
     profs = [sample_variability(VariabilityConfig(*sig), n, np.random.default_rng(500 + k))
