@@ -925,17 +925,23 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                                      c == cycles - 1});
         }
         if (P.var_mode) {
-            // per-p-bit profile, trial-major [Tp][n] (padding trials: ideal)
+            // per-p-bit profile, trial-major [Tp][n] (padding trials: ideal).  The
+            // fp32 pair of the timing kernels is [W][n][32] instead: their fired
+            // p-bits are a sparse random ~15 % of each (word, node), so keeping a
+            // node's 32 trials in 256 contiguous bytes lets nearby fires share
+            // DRAM bursts that the [W][32][n] layout spreads over 32 rows
             const int64_t Tp = P.Tp;
+            const bool node_major = !P.var_uniform;
             std::vector<float2> pf((size_t)Tp * n, make_float2(1.0f, 0.0f));
             std::vector<double> l64((size_t)Tp * n, 1.0), d64((size_t)Tp * n, 0.0);
             parallel_for(trials, 16, [&](int64_t t0, int64_t t1) {
                 for (int64_t t = t0; t < t1; ++t)
                     for (int64_t i = 0; i < n; ++i) {
                         const size_t src = (size_t)(pstride ? t * n : 0) + i, dst = (size_t)t * n + i;
+                        const size_t pdst = node_major ? ((size_t)(t >> 5) * n + i) * 32 + (t & 31) : dst;
                         l64[dst] = lam[src];
                         d64[dst] = delta[src];
-                        pf[dst] = make_float2((float)lam[src], (float)(lam[src] * delta[src]));
+                        pf[pdst] = make_float2((float)lam[src], (float)(lam[src] * delta[src]));
                     }
             });
             P.prof.upload(pf, st);

@@ -145,7 +145,7 @@ struct PackedArgs {
     uint32_t *ring;           // TApSA: [W][alpha][L][n] bit-sliced neighbour counts
     int alpha, slot, filled;  // TApSA: ring length, this cycle's slot, min(c+1, alpha)
     // VAR (per-p-bit variability profile, plain rule)
-    const float2 *prof;       // [W][32][n] {fl32(lam), fl32(lam * delta)}
+    const float2 *prof;       // {fl32(lam), fl32(lam * delta)}: [W][32][n], or [W][n][32] (timing kernels)
     const double *lam64;      // [W*32][n] exact lam (near-tie path)
     const double *del64;      // [W*32][n] exact delta
     const uint32_t *pplanes;  // [W][nplanes][n] bit-sliced clamped periods, or null (all fire)
@@ -1024,7 +1024,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
                 if (a.inp_out) a.inp_out[((size_t)w * 32 + b) * a.n + ii] = __dmul_rn(a.i0, (double)raw);
             };
             auto prof_of = [&](uint32_t e) {
-                return __ldg(a.prof + ((size_t)w * 32 + (e & 31u)) * a.n + ch * 32 + ((e >> 5) & 31u));
+                return __ldg(a.prof + ((size_t)w * a.n + ch * 32 + ((e >> 5) & 31u)) * 32 + (e & 31u));
             };
             for (int k = lane; k < F; k += 64) {
                 const uint32_t e0 = fl[k];
@@ -1323,7 +1323,7 @@ struct ResidentTimingArgs {
     const uint32_t *rowptr, *adj;
     const uint2 *kfc;
     const uint64_t *krg;
-    const float2 *prof;         // [Tp][n]
+    const float2 *prof;         // [W][n][32] (node-major: a node's 32 trials contiguous)
     const double *lam64, *del64;
     const uint32_t *pplanes;    // [W][nplanes][n]
     const uint8_t *divs;
@@ -1484,7 +1484,7 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
                 if (R.inp) a.inp_out[((size_t)w * 32 + b) * a.n + ii] = __dmul_rn(i0, (double)raw);
             };
             auto prof_of = [&](uint32_t e) {
-                return __ldg(a.prof + ((size_t)w * 32 + (e & 31u)) * a.n + base + ((e >> 5) & 31u));
+                return __ldg(a.prof + ((size_t)w * a.n + base + ((e >> 5) & 31u)) * 32 + (e & 31u));
             };
             for (int k = lane; k < F; k += 64) {
                 const uint32_t e0 = wfl[k];
