@@ -202,6 +202,10 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
 int pbsa_debug_stream_u64(int device, int64_t count, const uint64_t *key, const uint64_t *tag,
                           const uint64_t *a, const uint64_t *b, uint64_t *out);
 int pbsa_debug_tanh(int device, int64_t count, const double *x, double *out);
+/* The varied-profile prefilter on given (lam, delta, i0, raw, zh): out bit 1 =
+ * undecided (exact fp64 recheck), bit 0 = the decision otherwise. */
+int pbsa_debug_var_prefilter(int device, int64_t count, const double *lam, const double *delta,
+                             const double *i0, const int *raw, const uint32_t *zh, uint32_t *out);
 /* Philox4x32-10 on the device: ctr[4*count], key[2*count] -> out[4*count]. */
 int pbsa_debug_philox(int device, int64_t count, const uint32_t *ctr, const uint32_t *key,
                       uint32_t *out);

@@ -60,6 +60,7 @@ _SIGNATURES = [
     ("pbsa_debug_stream_u64", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P, _P, _P]),
     ("pbsa_debug_tanh", ctypes.c_int, [ctypes.c_int, _I64, _P, _P]),
     ("pbsa_debug_philox", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P]),
+    ("pbsa_debug_var_prefilter", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P, _P, _P, _P]),
     ("pbsa_libm_tanh_host", _F64, [_F64]),
     ("pbsa_threshold_host", ctypes.c_uint64, [_F64]),
     ("pbsa_threshold_native_host", ctypes.c_uint64, [_F64]),
@@ -267,6 +268,19 @@ def debug_philox(ctr, key, device: int = 0) -> np.ndarray:
     out = np.empty_like(c)
     _check(lib.pbsa_debug_philox(device, c.shape[0], c.ctypes.data, k.ctypes.data,
                                  out.ctypes.data))
+    return out
+
+
+def debug_var_prefilter(lam, delta, i0, raw, zh, device: int = 0) -> np.ndarray:
+    """Device variability prefilter codes (bit 1 undecided, bit 0 decision)."""
+    lib = load()
+    require_device(device)
+    a = [np.ascontiguousarray(x, dtype=np.float64) for x in (lam, delta, i0)]
+    r = np.ascontiguousarray(raw, dtype=np.int32)
+    z = np.ascontiguousarray(zh, dtype=np.uint32)
+    out = np.empty(z.size, np.uint32)
+    _check(lib.pbsa_debug_var_prefilter(device, z.size, *(x.ctypes.data for x in a), r.ctypes.data,
+                                        z.ctypes.data, out.ctypes.data))
     return out
 
 

@@ -280,7 +280,8 @@ struct pbsa_plan {
     DevBuf<int16_t> raw_last;         // [n][Tp]
     // packed VAR mode: per-p-bit variability profile under the plain rule
     bool var_mode = false, var_uniform = true;
-    DevBuf<float2> prof;               // [Tp][n] {fl32(lam), fl32(lam * delta)}
+    DevBuf<float2> prof;               // [Tp][n] {fl32(lam), fl32(lam * delta)} (no timing spread)
+    DevBuf<__half2> prof16;            // [W][n][32] {fl16(lam), fl16(lam * delta)} (timing spread)
     DevBuf<double> lam64, del64;       // [Tp][n]
     DevBuf<double> inp_var;            // [Tp][n] last i0 * raw of every p-bit
     DevBuf<uint32_t> pplanes;          // [W][nplanes][n]
@@ -932,7 +933,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             // DRAM bursts that the [W][32][n] layout spreads over 32 rows
             const int64_t Tp = P.Tp;
             const bool node_major = !P.var_uniform;
-            std::vector<float2> pf((size_t)Tp * n, make_float2(1.0f, 0.0f));
+            std::vector<float2> pf(node_major ? 0 : (size_t)Tp * n, make_float2(1.0f, 0.0f));
+            std::vector<__half2> pf16(node_major ? (size_t)Tp * n : 0, __floats2half2_rn(1.0f, 0.0f));
             std::vector<double> l64((size_t)Tp * n, 1.0), d64((size_t)Tp * n, 0.0);
             parallel_for(trials, 16, [&](int64_t t0, int64_t t1) {
                 for (int64_t t = t0; t < t1; ++t)
@@ -941,10 +943,14 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                         const size_t pdst = node_major ? ((size_t)(t >> 5) * n + i) * 32 + (t & 31) : dst;
                         l64[dst] = lam[src];
                         d64[dst] = delta[src];
-                        pf[pdst] = make_float2((float)lam[src], (float)(lam[src] * delta[src]));
+                        // timing kernels: fp16 pair (overflow -> inf -> the exact recheck)
+                        if (node_major)
+                            pf16[pdst] = __floats2half2_rn((float)lam[src], (float)(lam[src] * delta[src]));
+                        else
+                            pf[pdst] = make_float2((float)lam[src], (float)(lam[src] * delta[src]));
                     }
             });
-            P.prof.upload(pf, st);
+            if (node_major) P.prof16.upload(pf16, st); else P.prof.upload(pf, st);
             P.lam64.upload(l64, st);
             P.del64.upload(d64, st);
             P.inp_var.alloc((size_t)Tp * n);
@@ -1296,7 +1302,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             r.adj = P.adj.p;
             r.kfc = P.kfc.p;
             r.krg = P.krg.p;
-            r.prof = P.prof.p;
+            r.prof = P.prof16.p;
             r.lam64 = P.lam64.p;
             r.del64 = P.del64.p;
             r.pplanes = P.pplanes.p;
@@ -1437,7 +1443,8 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     a.do_cut = pl.do_cut;
                     if (P.var_mode) {
                         const size_t off = (size_t)w0 * 32 * P.n;
-                        a.prof = P.prof.p + off;
+                        a.prof = P.var_uniform ? P.prof.p + off : nullptr;
+                        a.prof16 = P.var_uniform ? nullptr : P.prof16.p + off;
                         a.lam64 = P.lam64.p + off;
                         a.del64 = P.del64.p + off;
                         a.pplanes = P.var_uniform ? nullptr : P.pplanes.p + (size_t)w0 * P.nplanes * P.n;
@@ -2162,6 +2169,28 @@ int pbsa_debug_philox(int device, int64_t count, const uint32_t *ctr, const uint
         pbsa::debug_philox<<<grid_for(count, 256), 256>>>(count, dc.p, dk.p, dout.p);
         CK(cudaGetLastError());
         CK(cudaMemcpy(out, dout.p, sizeof(uint32_t) * 4 * count, cudaMemcpyDeviceToHost));
+    });
+}
+
+int pbsa_debug_var_prefilter(int device, int64_t count, const double *lam, const double *delta,
+                             const double *i0, const int *raw, const uint32_t *zh, uint32_t *out) {
+    return guarded([&] {
+        if (count < 0 || (count > 0 && (!lam || !delta || !i0 || !raw || !zh || !out)))
+            fail(PBSA_EINVAL, "bad arguments");
+        if (count == 0) return;
+        DeviceGuard dg(device);
+        DevBuf<double> dl, dd, di;
+        DevBuf<int> dr;
+        DevBuf<uint32_t> dz, dout;
+        dl.upload(lam, count, 0);
+        dd.upload(delta, count, 0);
+        di.upload(i0, count, 0);
+        dr.upload(raw, count, 0);
+        dz.upload(zh, count, 0);
+        dout.alloc(count);
+        pbsa::debug_var_prefilter<<<grid_for(count, 256), 256>>>(count, dl.p, dd.p, di.p, dr.p, dz.p, dout.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, dout.p, sizeof(uint32_t) * count, cudaMemcpyDeviceToHost));
     });
 }
 

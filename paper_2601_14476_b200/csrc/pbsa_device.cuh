@@ -23,6 +23,7 @@
 // hash as streams.py:29-55, regenerated in-kernel from (key, tag, node, count).
 #pragma once
 #include <cooperative_groups.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -145,7 +146,8 @@ struct PackedArgs {
     uint32_t *ring;           // TApSA: [W][alpha][L][n] bit-sliced neighbour counts
     int alpha, slot, filled;  // TApSA: ring length, this cycle's slot, min(c+1, alpha)
     // VAR (per-p-bit variability profile, plain rule)
-    const float2 *prof;       // {fl32(lam), fl32(lam * delta)}: [W][32][n], or [W][n][32] (timing kernels)
+    const float2 *prof;       // [W][32][n] {fl32(lam), fl32(lam * delta)} (no timing spread)
+    const __half2 *prof16;    // [W][n][32] {fl16(lam), fl16(lam * delta)} (timing spread)
     const double *lam64;      // [W*32][n] exact lam (near-tie path)
     const double *del64;      // [W*32][n] exact delta
     const uint32_t *pplanes;  // [W][nplanes][n] bit-sliced clamped periods, or null (all fire)
@@ -242,6 +244,43 @@ __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// Variability prefilter on the fp16 profile pair (fl16(lam), fl16(lam delta)).
+// The computed x = fl16(lam) ir + fl16(lam delta) is within
+//   dx <= A 2^-10.9 + 2^-22,   A = |lam| |i0 raw| + |lam delta|,
+// of the reference's fp64 x (fp16 rounding 2^-11 each, ir and fma in fp32).  On
+// [x - dx, x + dx] the slope of t*(x) = 1/(1 + e^{2x}) is at most
+// 2 q e^{2 dx}, q = t(1 - t) at x (cosh(x + dx) >= cosh(x) e^{-dx}), so with
+// A <= 256 (e^{2 dx} <= 1.35) the threshold moves by at most
+// q (5.93e6 A + 2765) units of 2^-32; the fp32 evaluation of t and of
+// zh - t 2^32 adds at most (A + 1) 2^11 + 2^9 (the fp32-profile analysis).
+// Hence |zh - t 2^32| >= M = A 2^11 + 5120 + 6.3e6 q A decides exactly;
+// otherwise (and for A > 256, or a non-finite pair) the update takes the exact
+// fp64 recheck.  Returns diff > 0 in bit 0 and "undecided" in bit 1.
+// The same on the fp32 pair (fl32(lam), fl32(lam delta)) -- the kernels without
+// a timing spread, whose profile reads are coalesced: |x - x64| <= A 2^-21.9,
+// so M = (A + 2) 2^11 (module comment of packed_sweep) and only ~2^-16 of the
+// updates take the recheck.
+__device__ __forceinline__ uint32_t var_prefilter(float2 lv, float ir, uint32_t zh, float ms) {
+    const float x = fmaf(lv.x, ir, lv.y);
+    const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
+    const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
+    const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
+    const bool undecided = !(fabsf(diff) >= ms * fmaf(A, 2048.0f, 4096.0f));
+    return (undecided ? 2u : 0u) | (diff > 0.0f ? 1u : 0u);
+}
+
+__device__ __forceinline__ uint32_t var_prefilter(__half2 h, float ir, uint32_t zh, float ms) {
+    const float2 lv = __half22float2(h);
+    const float x = fmaf(lv.x, ir, lv.y);
+    const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
+    const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
+    const float q = fmaf(-t, t, t);
+    const float M = ms * fmaf(6.3e6f * q, A, fmaf(A, 2048.0f, 5120.0f));
+    const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
+    const bool undecided = !(fabsf(diff) >= M) || !(A <= 256.0f);
+    return (undecided ? 2u : 0u) | (diff > 0.0f ? 1u : 0u);
 }
 
 // Second absorb (x = s ^ count; count < 2^30 only touches the low word).
@@ -596,12 +635,12 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 // |u 2^32 - t* 2^32 - diff| < (A + 1) 2^11 + 2^9 < M = (A + 2) 2^11.
                 // |diff| >= M decides; otherwise (probability ~2^-16) the update is
                 // recomputed in fp64 with the libm-exact tanh, as _kernels.py:150-152.
-                // (An fp16 profile halves its bytes but sends ~1 % of the updates to
-                // the recheck, which costs more than the bytes saved: measured.)
+                // (An fp16 profile halves these coalesced bytes but its wider margin
+                // sends ~5e-4 of the updates to the divergent recheck: measured 10 %
+                // slower here; the timing kernels, whose reads are scattered, use it.)
                 const uint32_t ui = (uint32_t)i;
                 const float2 *pr = a.prof + (size_t)w * 32 * a.n + i;
                 const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
-                const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
                 uint32_t word = 0, exact = 0;
                 uint32_t X[4];  // NATIVE: the current Philox block (trials 4k .. 4k + 3)
                 auto decide = [&](int b, float2 lv) {
@@ -610,9 +649,6 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                     const int raw = 2 * pop - d;
                     const float ir = a.i0f * (float)raw;
-                    const float x = fmaf(lv.x, ir, lv.y);
-                    const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
-                    const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
                     uint32_t zh;
                     if (NATIVE) {  // u 2^32 = X + 1/2: the replay margin covers it
                         if ((b & 3) == 0)
@@ -628,11 +664,11 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
                         zh = packed_hash_hi(sl, sh, count);
                     }
-                    const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
-                    if (fabsf(diff) < fmaf(A, mA, m0))
+                    const uint32_t v = var_prefilter(lv, ir, zh, a.margin);
+                    if (v & 2u)
                         exact |= 1u << b;
                     else
-                        word |= (uint32_t)(diff > 0.0f) << b;
+                        word |= (v & 1u) << b;
                     if (a.inp_out)
                         a.inp_out[((size_t)w * 32 + b) * a.n + i] = __dmul_rn(a.i0, (double)raw);
                 };
@@ -927,7 +963,6 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
     for (int r = 0; r < CP; ++r) C[r] = 0;
     int dsum = 0;
     uint32_t *fl = sfl + wib * 1024, *res = sres + wib * 32, *exm = sexm + wib * 32;
-    const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
 
     if (live) {
         const uint32_t *sw = a.sold + (size_t)w * a.n;
@@ -997,13 +1032,10 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
             exm[lane] = 0;
             __syncwarp();
             // two list entries per lane and round, their profile loads in flight together
-            auto fire_one = [&](uint32_t e, float2 lv) {
+            auto fire_one = [&](uint32_t e, __half2 lv) {
                 const int b = (int)(e & 31u), l = (int)((e >> 5) & 31u), raw = (int)(e >> 10) - 1024;
                 const int ii = ch * 32 + l;
                 const float ir = a.i0f * (float)raw;
-                const float x = fmaf(lv.x, ir, lv.y);
-                const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
-                const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
                 uint32_t zh;
                 if (NATIVE) {  // one Philox block per fired trial (fired trials are sparse)
                     uint32_t o[4];
@@ -1016,21 +1048,21 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
                     packed_first_absorb(kc.x ^ (uint32_t)ii, kc.y, sl, sh);
                     zh = packed_hash_hi(sl, sh, count);
                 }
-                const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
-                if (fabsf(diff) < fmaf(A, mA, m0))
+                const uint32_t v = var_prefilter(lv, ir, zh, a.margin);
+                if (v & 2u)
                     atomicOr(exm + l, 1u << b);
-                else if (diff > 0.0f)
+                else if (v & 1u)
                     atomicOr(res + l, 1u << b);
                 if (a.inp_out) a.inp_out[((size_t)w * 32 + b) * a.n + ii] = __dmul_rn(a.i0, (double)raw);
             };
             auto prof_of = [&](uint32_t e) {
-                return __ldg(a.prof + ((size_t)w * a.n + ch * 32 + ((e >> 5) & 31u)) * 32 + (e & 31u));
+                return __ldg(a.prof16 + ((size_t)w * a.n + ch * 32 + ((e >> 5) & 31u)) * 32 + (e & 31u));
             };
             for (int k = lane; k < F; k += 64) {
                 const uint32_t e0 = fl[k];
                 const bool two = k + 32 < F;
                 const uint32_t e1 = two ? fl[k + 32] : e0;
-                const float2 lv0 = prof_of(e0), lv1 = prof_of(e1);
+                const __half2 lv0 = prof_of(e0), lv1 = prof_of(e1);
                 fire_one(e0, lv0);
                 if (two) fire_one(e1, lv1);
             }
@@ -1070,7 +1102,7 @@ struct ResidentArgs {
     int16_t *raw_out;           // [n][Tp] raw fields of the last cycle
     int n, W, Tp, K, dmax, chunks, cycles, t_res;
     // VARU: per-p-bit lam/delta without a timing spread (ALG=3 decision)
-    const float2 *prof;         // [Tp][n]
+    const float2 *prof;         // [Tp][n] {fl32(lam), fl32(lam * delta)}
     const double *lam64, *del64;
     const double *i0;           // [cycles]
     double *inp_out;            // [Tp][n] inputs of the last cycle
@@ -1158,7 +1190,6 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
             if (VARU) {  // the packed ALG=3 decision (sigmoid prefilter, exact recheck)
                 const double i0 = a.i0[cc];
                 const float i0f = (float)i0;
-                const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
                 const float2 *pr = a.prof + (size_t)w * 32 * a.n + i;
                 uint32_t word = 0, exact = 0;
                 uint32_t X[4];
@@ -1170,9 +1201,6 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                     const int raw = 2 * pop - d;
                     const float2 lv = __ldg(pr + (size_t)b * a.n);
                     const float ir = i0f * (float)raw;
-                    const float x = fmaf(lv.x, ir, lv.y);
-                    const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
-                    const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
                     uint32_t zh;
                     if (NATIVE) {
                         if ((b & 3) == 0)
@@ -1187,11 +1215,11 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                         packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
                         zh = packed_hash_hi(sl, sh, count);
                     }
-                    const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
-                    if (fabsf(diff) < fmaf(A, mA, m0))
+                    const uint32_t v = var_prefilter(lv, ir, zh, a.margin);
+                    if (v & 2u)
                         exact |= 1u << b;
                     else
-                        word |= (uint32_t)(diff > 0.0f) << b;
+                        word |= (v & 1u) << b;
                     if (a.inp_out && c == a.cycles - 1)
                         a.inp_out[((size_t)w * 32 + b) * a.n + i] = __dmul_rn(i0, (double)raw);
                 }
@@ -1323,7 +1351,7 @@ struct ResidentTimingArgs {
     const uint32_t *rowptr, *adj;
     const uint2 *kfc;
     const uint64_t *krg;
-    const float2 *prof;         // [W][n][32] (node-major: a node's 32 trials contiguous)
+    const __half2 *prof;        // [W][n][32] fp16 pairs (node-major: a node's 32 trials contiguous)
     const double *lam64, *del64;
     const uint32_t *pplanes;    // [W][nplanes][n]
     const uint8_t *divs;
@@ -1375,7 +1403,6 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
 #pragma unroll
     for (int r = 0; r < CP; ++r) C[r] = 0;
     int dsum = 0;
-    const float mA = 2048.0f * a.margin, m0 = 4096.0f * a.margin;
     cluster.sync();
 
     RLaunch Rn = a.launches[0];
@@ -1457,13 +1484,10 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
             wexm[lane] = 0;
             __syncwarp();
             // two list entries per lane and round, their profile loads in flight together
-            auto fire_one = [&](uint32_t e, float2 lv) {
+            auto fire_one = [&](uint32_t e, __half2 lv) {
                 const int b = (int)(e & 31u), l = (int)((e >> 5) & 31u), raw = (int)(e >> 10) - 1024;
                 const int ii = base + l;
                 const float ir = i0f * (float)raw;
-                const float x = fmaf(lv.x, ir, lv.y);
-                const float A = fmaf(fabsf(lv.x), fabsf(ir), fabsf(lv.y));
-                const float t = rcp_approx(1.0f + ex2_approx(x * 2.88539008f));
                 uint32_t zh;
                 if (NATIVE) {
                     uint32_t o[4];
@@ -1476,10 +1500,10 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
                     packed_first_absorb(kc.x ^ (uint32_t)ii, kc.y, sl, sh);
                     zh = packed_hash_hi(sl, sh, count);
                 }
-                const float diff = fmaf(-t, 4294967296.0f, __uint2float_rn(zh));
-                if (fabsf(diff) < fmaf(A, mA, m0))
+                const uint32_t v = var_prefilter(lv, ir, zh, a.margin);
+                if (v & 2u)
                     atomicOr(wexm + l, 1u << b);
-                else if (diff > 0.0f)
+                else if (v & 1u)
                     atomicOr(wres + l, 1u << b);
                 if (R.inp) a.inp_out[((size_t)w * 32 + b) * a.n + ii] = __dmul_rn(i0, (double)raw);
             };
@@ -1490,7 +1514,7 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
                 const uint32_t e0 = wfl[k];
                 const bool two = k + 32 < F;
                 const uint32_t e1 = two ? wfl[k + 32] : e0;
-                const float2 lv0 = prof_of(e0), lv1 = prof_of(e1);
+                const __half2 lv0 = prof_of(e0), lv1 = prof_of(e1);
                 fire_one(e0, lv0);
                 if (two) fire_one(e1, lv1);
             }
@@ -2092,6 +2116,18 @@ __global__ void debug_philox(int64_t cnt, const uint32_t *ctr, const uint32_t *k
     philox4x32_10(ctr[4 * k], ctr[4 * k + 1], ctr[4 * k + 2], ctr[4 * k + 3], key[2 * k],
                   key[2 * k + 1], o);
     for (int j = 0; j < 4; ++j) out[4 * k + j] = o[j];
+}
+
+// The variability prefilter on given inputs (profile pair rounded exactly as
+// the host rounds it): out = var_prefilter code (bit 1: undecided, bit 0: +1).
+__global__ void debug_var_prefilter(int64_t cnt, const double *lam, const double *delta,
+                                    const double *i0, const int *raw, const uint32_t *zh,
+                                    uint32_t *out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= cnt) return;
+    const __half2 h = __floats2half2_rn((float)lam[k], (float)(lam[k] * delta[k]));
+    const float ir = (float)i0[k] * (float)raw[k];
+    out[k] = var_prefilter(h, ir, zh[k], 1.0f);
 }
 
 __global__ void debug_tanh(int64_t cnt, const double *x, double *out) {

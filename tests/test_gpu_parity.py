@@ -576,3 +576,40 @@ def test_philox_cut_statistics_match_reference_stream(bench_graphs, golden_analo
         best_nat = np.mean([r.best_cut for r in nat.results])
         assert abs(nat.mean_cut - rep.mean_cut) <= 0.005 * best_known, (name, nat.mean_cut, rep.mean_cut)
         assert abs(best_nat - best_rep) <= 0.005 * best_known, (name, best_nat, best_rep)
+
+
+def test_variability_prefilter_is_exact_where_it_decides():
+    """The fp16-profile prefilter of the timing kernels (var_prefilter) may only decide an update
+    when every draw u 2^32 in [zh - 1, zh + 2) gives the reference's fp64
+    decision r + tanh(lam (i0 raw + delta)) >= 0 (_kernels.py:149-152).
+    Probed on 2M random and near-threshold inputs, including large |x|."""
+    rng = np.random.default_rng(21)
+    m = 2_000_000
+    lam = 1.0 + rng.choice([0.1, 0.5, 1.0, 3.0], m) * rng.standard_normal(m)
+    delta = rng.choice([0.0, 0.1, 0.5, 2.0], m) * rng.standard_normal(m)
+    i0 = np.exp(rng.uniform(np.log(0.01), np.log(10.0), m))
+    raw = rng.integers(-40, 41, m)
+    x = lam * (i0 * raw + delta)
+    tt = np.tanh(x)
+    ustar = (1.0 - tt) / 2.0                  # +1 iff u >= u* (up to fp64 rounding)
+    near = np.floor(ustar * 2.0 ** 32) + rng.integers(-3_000_000, 3_000_000, m)
+    uni = rng.integers(0, 2 ** 32, m).astype(np.float64)
+    is_uni = rng.random(m) < 0.3
+    zh = np.where(is_uni, uni, near)
+    zh = np.clip(zh, 1, 2 ** 32 - 3).astype(np.uint64).astype(np.uint32)
+    code = _native.debug_var_prefilter(lam, delta, i0, raw, zh)
+    decided = (code & 2) == 0
+    # exact reference decision at both ends of the draw's interval (monotone in u)
+    inp = i0 * raw
+    for off in (-1.0, 1.999999):
+        u = (zh.astype(np.float64) + off) * 2.0 ** -32
+        r = 2.0 * u - 1.0
+        ref = (r + np.tanh(lam * (inp + delta))) >= 0.0
+        bad = decided & (ref != ((code & 1) == 1))
+        assert not bad.any(), np.flatnonzero(bad)[:5]
+    # random draws rarely need the recheck (here A reaches ~10^3, beyond the
+    # benchmark range, and A > 256 always rechecks); the near-threshold probe
+    # straddles the margin
+    moderate = np.abs(lam) * np.abs(inp) + np.abs(lam * delta) < 64
+    assert decided[is_uni & moderate].mean() > 0.99
+    assert 0.05 < decided[~is_uni].mean() < 0.99
