@@ -613,3 +613,45 @@ def test_variability_prefilter_is_exact_where_it_decides():
     moderate = np.abs(lam) * np.abs(inp) + np.abs(lam * delta) < 64
     assert decided[is_uni & moderate].mean() > 0.99
     assert 0.05 < decided[~is_uni].mean() < 0.99
+
+
+# ------------------------------------------------ engine invariances (test_engine.py)
+
+@pytest.mark.parametrize("name,kind,sig", [("G81", Algorithm.PSA, (0, 0, 0)),
+                                           ("G1", Algorithm.PSA, (0, 0, 0.5)),
+                                           ("G55", Algorithm.TAPSA, (0, 0, 0)),
+                                           ("G22", Algorithm.SPSA, (0.5, 0.5, 0.0))])
+def test_rerun_identical_and_more_trials_never_perturb_earlier_ones(bench_graphs, name, kind, sig):
+    """/root/reference/pkg/tests/test_engine.py:34-41 (rerun identical) and
+    :57-62 (adding trials never perturbs the earlier ones) on the device paths:
+    word padding, word phases and chains must not leak between trials."""
+    graph = bench_graphs(name)
+    base = engine.ExperimentSpec(graph=name, algo=AlgorithmConfig(kind, alpha=3, p_stall=0.4),
+                                 variability=VariabilityConfig(*sig), cycles=40, trials=37)
+    a = engine.run_trials(base, {name: graph})
+    b = engine.run_trials(base, {name: graph})
+    c = engine.run_trials(dataclasses.replace(base, trials=100), {name: graph})
+    for ra, rb, rc in zip(a.results, b.results, c.results[:37]):
+        assert np.array_equal(ra.final_state.spins, rb.final_state.spins)
+        assert np.array_equal(ra.final_state.spins, rc.final_state.spins)
+        assert np.array_equal(ra.cut_trace, rc.cut_trace)
+        assert np.array_equal(ra.final_state.inputs, rc.final_state.inputs)
+        assert np.array_equal(ra.update_counts, rc.update_counts)
+
+
+def test_with_and_without_graph_same_dynamics(bench_graphs):
+    """/root/reference/pkg/tests/test_annealer.py:216-230: the graph only adds
+    the cut trace; spins, inputs and energies are the same without it."""
+    g = bench_graphs("G22")
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 50, 10)
+    for cfg in (AlgorithmConfig(Algorithm.PSA), AlgorithmConfig(Algorithm.TAPSA, alpha=4)):
+        for prof in (VariabilityProfile.ideal(model.n),
+                     sample_variability(VariabilityConfig(0.5, 0.5, 0.5), model.n,
+                                        np.random.default_rng(4))):
+            with_g = run_anneal(model, sch, cfg, prof, seed=11, graph=g)
+            without = run_anneal(model, sch, cfg, prof, seed=11)
+            assert np.array_equal(with_g.final_state.spins, without.final_state.spins)
+            assert np.array_equal(with_g.energy_trace, without.energy_trace)
+            assert np.array_equal(with_g.final_state.inputs, without.final_state.inputs)
+            assert without.cut_trace is None and with_g.cut_trace is not None
