@@ -86,9 +86,11 @@ int pbsa_plan_create(int device, int64_t n, const int64_t *indptr, const int64_t
  * Philox4x32-10 keyed by rng_seed, with the global trial index
  * first_trial + t in the counter (a multiple of 4, so any sharding of the
  * trials by multiples of 4 gives identical per-trial results); initial spins
- * still come from keys[] as in the reference.  Philox mode covers the plain
- * rule (ideal, or with a lam/delta/period variability profile) on +-1
- * MAX-CUT models (the packed sweeps); other inputs return PBSA_EINVAL.  No reference interface corresponds: the
+ * still come from keys[] as in the reference; the SpSA stall draw is the same
+ * Philox word with tag 4.  Philox mode covers every input of the packed path
+ * (+-1 MAX-CUT models of degree <= 127: all three rules on an ideal profile,
+ * the plain rule with a lam/delta/period profile); other inputs return
+ * PBSA_EINVAL.  No reference interface corresponds: the
  * reference has only its counter hash (streams.py); this is the north_star's
  * native RNG mode.
  */

@@ -82,13 +82,19 @@ void orc_philox4x32_10(const uint32_t *ctr, const uint32_t *key, uint32_t *out) 
     out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-/* The native activation uniform's r = 2u - 1, u = (X + 1/2) 2^-32, X the
- * word (k & 3) of Philox(ctr = {i, count, k >> 2, 3}, key = seed). */
-static double orc_native_r(uint64_t seed, uint64_t k, uint64_t i, uint64_t count) {
-    uint32_t ctr[4] = {(uint32_t)i, (uint32_t)count, (uint32_t)(k >> 2), 3u};
+/* The native stream's word X of global trial k: word (k & 3) of
+ * Philox(ctr = {i, count, k >> 2, tag}, key = seed); tag 3 = activation,
+ * 4 = SpSA stall. */
+static uint32_t orc_native_x(uint64_t seed, uint64_t k, uint64_t i, uint64_t count, uint32_t tag) {
+    uint32_t ctr[4] = {(uint32_t)i, (uint32_t)count, (uint32_t)(k >> 2), tag};
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)}, o[4];
     orc_philox4x32_10(ctr, key, o);
-    return (2.0 * (double)o[k & 3] + 1.0) * 0x1p-32 - 1.0;
+    return o[k & 3];
+}
+
+/* Native activation: r = 2u - 1 with u = (X + 1/2) 2^-32, i.e. (2X + 1) 2^-32 - 1. */
+static double orc_native_r(uint64_t seed, uint64_t k, uint64_t i, uint64_t count) {
+    return (2.0 * (double)orc_native_x(seed, k, i, count, 3u) + 1.0) * 0x1p-32 - 1.0;
 }
 
 int orc_anneal_rng(int64_t n, const int64_t *indptr, const int64_t *indices, const double *values,
@@ -178,7 +184,9 @@ int orc_anneal_rng(int64_t n, const int64_t *indptr, const int64_t *indices, con
                     if (counts[i] == 0) {
                         inp = i0 * raw;
                     } else {
-                        double u = orc_u01(key, ORC_TAG_STALL, (uint64_t)i, (uint64_t)count);
+                        double u = rng ? ((double)orc_native_x(seed, (uint64_t)trial, (uint64_t)i,
+                                                                (uint64_t)count, 4u) + 0.5) * 0x1p-32
+                                       : orc_u01(key, ORC_TAG_STALL, (uint64_t)i, (uint64_t)count);
                         inp = u < p_stall ? inputs[i] : i0 * raw;
                     }
                 } else {

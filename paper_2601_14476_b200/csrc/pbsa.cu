@@ -396,6 +396,22 @@ PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = fal
             default: fail(PBSA_EINVAL, "packed variability path supports degree <= 127");
         }
     }
+    if (update && native && (tapsa || spsa)) {  // Philox draws, TApSA / SpSA, ideal profile
+        switch (L) {
+#define PBSA_NRCASE(l)                                                                \
+    case l:                                                                           \
+        return tapsa ? pbsa::packed_sweep<l, true, false, 6> : pbsa::packed_sweep<l, true, false, 7>;
+            PBSA_NRCASE(1)
+            PBSA_NRCASE(2)
+            PBSA_NRCASE(3)
+            PBSA_NRCASE(4)
+            PBSA_NRCASE(5)
+            PBSA_NRCASE(6)
+            PBSA_NRCASE(7)
+#undef PBSA_NRCASE
+            default: fail(PBSA_EINVAL, "packed TApSA/SpSA support degree <= 127");
+        }
+    }
     if (update && native) {  // Philox draws, plain rule, ideal profile (no first-absorb cache)
         switch (L) {
             case 1: return pbsa::packed_sweep<1, true, false, 4>;
@@ -806,10 +822,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     }
     const bool packed = (((rule_is_psa || tapsa_packed || spsa_packed) && ideal) || var_ok) && unit_J &&
                         zero_h && graph_is_model && dmax <= 127 && small_counters;
-    if (rng_mode == PBSA_RNG_PHILOX && !(packed && ((ideal && rule_is_psa) || var_ok)))
-        fail(PBSA_EINVAL, "rng_mode=philox supports the plain rule (pSA, TApSA alpha=1, SpSA "
-                          "p_stall=0), ideal or with a variability profile, on a +-1 MAX-CUT model "
-                          "of degree <= 127");
+    if (rng_mode == PBSA_RNG_PHILOX && !packed)
+        fail(PBSA_EINVAL, "rng_mode=philox runs on the packed path only: a +-1 MAX-CUT model of "
+                          "degree <= 127 with pSA/TApSA/SpSA on an ideal profile, or the plain rule "
+                          "with a variability profile");
     P.native = rng_mode == PBSA_RNG_PHILOX;
     P.nseed = rng_seed;
     P.first_trial = first_trial;
@@ -881,6 +897,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             // u = (H >> 11) 2^-53 < p  <=>  H < ceil(p 2^53) << 11   (p * 2^53 is exact)
             const double ps = std::ceil(std::ldexp(p_stall, 53));
             P.p_stall64 = ps >= 0x1p53 ? ~0ULL : ((uint64_t)ps << 11);
+            // native: (X + 1/2) 2^-32 < p  <=>  X < S = ceil(p 2^32 - 1/2)   (exact in fp64)
+            if (P.native) P.p_stall64 = (uint64_t)std::ceil(std::ldexp(p_stall, 32) - 0.5);
             P.sidx.alloc((size_t)P.W * 32 * n);
             P.i0_dev.upload(P.i0, st);
         }
@@ -892,9 +910,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             std::vector<uint64_t> thr((size_t)cycles * P.K, ~0ULL);
             for (int64_t c = 0; c < cycles; ++c) {
                 const int64_t f = std::min<int64_t>(c + 1, alpha);
-                for (int64_t acc = -f * P.dmax; acc <= f * P.dmax; ++acc)
-                    thr[(size_t)c * P.K + acc + f * P.dmax] =
-                        threshold_h64(pb_libm_tanh(P.i0[c] * ((double)acc / (double)f)));
+                for (int64_t acc = -f * P.dmax; acc <= f * P.dmax; ++acc) {
+                    const double t = pb_libm_tanh(P.i0[c] * ((double)acc / (double)f));
+                    thr[(size_t)c * P.K + acc + f * P.dmax] = P.native ? threshold_native(t) : threshold_h64(t);
+                }
             }
             P.thr.upload(thr, st);
             P.ring.alloc((size_t)P.W * alpha * P.L * n);

@@ -317,6 +317,14 @@ __device__ __forceinline__ uint32_t packed_second_decide_n2(uint32_t sl, uint32_
                             word);
 }
 
+// Native decision: shift (X >= T) into `word` as the carry of X + (2^32 - T),
+// t = (lo, hi) of the 33-bit 2^32 - T (T = 2^32 never fires, T = 0 always).
+__device__ __forceinline__ void native_decide(uint32_t X, uint2 t, uint32_t &word) {
+    uint32_t dummy;
+    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
+        : "=r"(dummy), "=r"(word) : "r"(X), "r"(t.x), "r"(word), "r"(word + t.y));
+}
+
 // Bit-sliced counter: add the L-bit per-trial numbers x[] into C[] (CL planes).
 template <int L, int CL>
 __device__ __forceinline__ void vc_add(uint32_t (&C)[CL], const uint32_t (&x)[L]) {
@@ -518,10 +526,12 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     // per degree d indexed by the neighbour count p (raw = 2p - d), so a
     // trial's entry address is (p * 8) | row base, formed with one LOP3.
     // Larger degrees: entries indexed by raw + dmax.  TApSA: 64-entry rows by S.
-    constexpr bool TAPSA = ALG == 1;
-    constexpr bool SPSA = ALG == 2;
+    // ALG: 0 plain, 1 TApSA, 2 SpSA, 3 varied profile (replayed hash);
+    // 4 plain, 5 varied, 6 TApSA, 7 SpSA with Philox draws (philox.cuh)
+    constexpr bool TAPSA = ALG == 1 || ALG == 6;
+    constexpr bool SPSA = ALG == 2 || ALG == 7;
     constexpr bool VAR = ALG == 3 || ALG == 5;
-    constexpr bool NATIVE = ALG == 4 || ALG == 5;  // Philox draws (philox.cuh): 4 ideal, 5 varied
+    constexpr bool NATIVE = ALG >= 4;
     constexpr bool NIB = L <= 4 && !TAPSA;
     uint2 *sthr = reinterpret_cast<uint2 *>(
         (reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
@@ -538,7 +548,8 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
         uint32_t thi;
         uint64_t tfull = 0;  // NATIVE: the 33-bit Philox threshold T
         if (TAPSA) {
-            thi = (uint32_t)(a.thr[k] >> 32);  // host table is already [acc + f dmax]
+            tfull = a.thr[k];  // host table is already [acc + f dmax]
+            thi = (uint32_t)(tfull >> 32);
         } else {
             int raw = k - a.dmax;
             bool ok = true;
@@ -550,7 +561,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             tfull = ok ? a.thr[raw + a.dmax] : 0ULL;
             thi = (uint32_t)(tfull >> 32);
         }
-        if (ALG == 4) {  // (lo, hi) of the 33-bit 2^32 - T: carry of X + it is X >= T
+        if (NATIVE && !VAR) {  // (lo, hi) of the 33-bit 2^32 - T: carry of X + it is X >= T
             const uint64_t nt = (1ULL << 32) - tfull;
             sthr[k] = make_uint2((uint32_t)nt, (uint32_t)(nt >> 32));
         } else if (ALG == 0) {  // (lo, hi) of the 33-bit ~thi + 2 (packed_decide_n2)
@@ -712,6 +723,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
                 uint32_t word = 0, tie = 0xffffffffu;
                 const uint32_t ui = (uint32_t)i;
+                uint32_t X[4];  // NATIVE: the current Philox block
 #pragma unroll
                 for (int b = 31; b >= 0; --b) {
                     const int k = b >> 2, j = b & 3;
@@ -721,7 +733,12 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                     const uint32_t addr = rb + (sv << 4);
                     uint2 t;
                     asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "r"(addr));
-                    if (CACHED) {
+                    if (NATIVE) {
+                        if ((b & 3) == 3)
+                            philox4x32_10_rk(ui, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
+                                             kNativeTagR, a.rk, X);
+                        native_decide(X[b & 3], t, word);
+                    } else if (CACHED) {
                         const uint2 v = __ldcs(ctile + b * 32);
                         tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
                     } else {
@@ -731,7 +748,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         tie = min(tie, packed_second_decide(sl, sh, count, t, word));
                     }
                 }
-                if (tie < 2) {  // rare near-tie: exact 64-bit test
+                if (!NATIVE && tie < 2) {  // rare near-tie: exact 64-bit test
                     word = 0;
                     for (int b = 0; b < 32; ++b) {
                         int sb = 0;
@@ -760,7 +777,20 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 const uint32_t ui = (uint32_t)i;
                 // pass 1: stall bits of the 32 trials (exactly, before any index is replaced)
                 uint32_t stallw = 0;
-                if (a.cycle > 0) {
+                if (NATIVE && a.cycle > 0) {
+                    // stall iff X_stall < S (p_stall64 = S = ceil(p 2^32 - 1/2), u = (X + 1/2) 2^-32)
+                    const uint64_t ns = (1ULL << 32) - a.p_stall64;
+                    const uint2 pst = make_uint2((uint32_t)ns, (uint32_t)(ns >> 32));
+                    uint32_t gew = 0, Xs[4];
+#pragma unroll
+                    for (int b = 31; b >= 0; --b) {
+                        if ((b & 3) == 3)
+                            philox4x32_10_rk(ui, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
+                                             kNativeTagStall, a.rk, Xs);
+                        native_decide(Xs[b & 3], pst, gew);
+                    }
+                    stallw = ~gew;
+                } else if (a.cycle > 0) {
                     const uint2 pst = make_uint2(~(uint32_t)(a.p_stall64 >> 32),
                                                  (uint32_t)(a.p_stall64 >> 32));
                     uint32_t gew = 0, ties = 0xffffffffu;
@@ -788,6 +818,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 // activation decision.  Eight trials per group: the stalled trials'
                 // loads are issued together before the group's decisions.
                 uint32_t word = 0, tie = 0xffffffffu;
+                uint32_t X[4];  // NATIVE: the current Philox block of the activation draws
                 for (int gq = 3; gq >= 0; --gq) {
                     uint32_t th[8];
 #pragma unroll
@@ -795,10 +826,19 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         const int b = gq * 8 + j;
                         th[j] = ((stallw >> b) & 1u) ? sidx[(size_t)b * a.n] : 0u;
                     }
+                    uint32_t tlo[8];  // NATIVE: low words of 2^32 - T of the stalled drives
 #pragma unroll
                     for (int j = 7; j >= 0; --j) {
                         const int b = gq * 8 + j;
-                        if ((stallw >> b) & 1u) th[j] = __ldg(a.thr_hi_all + th[j]);
+                        if ((stallw >> b) & 1u) {
+                            if (NATIVE) {
+                                const uint64_t nt = (1ULL << 32) - __ldg(a.thr_all + th[j]);
+                                tlo[j] = (uint32_t)nt;
+                                th[j] = (uint32_t)(nt >> 32);
+                            } else {
+                                th[j] = __ldg(a.thr_hi_all + th[j]);
+                            }
+                        }
                     }
 #pragma unroll
                     for (int j = 7; j >= 0; --j) {
@@ -808,12 +848,17 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                         uint2 t;
                         if ((stallw >> b) & 1u) {
-                            t = make_uint2(~th[j], th[j]);
+                            t = NATIVE ? make_uint2(tlo[j], th[j]) : make_uint2(~th[j], th[j]);
                         } else {
                             t = NIB ? sthr[d * 16 + pop] : sthr[2 * pop - d + a.dmax];
                             sidx[(size_t)b * a.n] = (uint32_t)(base + 2 * pop);
                         }
-                        if (CACHED) {
+                        if (NATIVE) {
+                            if ((b & 3) == 3)
+                                philox4x32_10_rk(ui, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
+                                                 kNativeTagR, a.rk, X);
+                            native_decide(X[b & 3], t, word);
+                        } else if (CACHED) {
                             const uint2 v = __ldcs(ctile + b * 32);
                             tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
                         } else {
@@ -824,7 +869,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         }
                     }
                 }
-                if (tie < 2) {  // rare near-tie in an activation draw: exact 64-bit test
+                if (!NATIVE && tie < 2) {  // rare near-tie in an activation draw: exact 64-bit test
                     word = 0;
                     for (int b = 0; b < 32; ++b) {
                         const uint32_t idx = sidx[(size_t)b * a.n];

@@ -13,7 +13,8 @@
 // Native-mode draw of trial k (global index), node i, sub-step counter c:
 //   X = philox4x32_10(ctr = {i, c, k >> 2, tag}, key = native seed)[k & 3]
 //   u = (X + 1/2) 2^-32,  r = 2u - 1 = (2X + 1) 2^-32 - 1   (exact in fp64)
-// so four trials of a word share one Philox call.
+// so four trials of a word share one Philox call.  The SpSA stall draw is the
+// same with tag 4: stall iff (X + 1/2) 2^-32 < p_stall.
 #pragma once
 #include <stdint.h>
 
@@ -27,7 +28,8 @@ namespace pbsa {
 
 constexpr uint32_t kPhiloxM0 = 0xD2511F53u, kPhiloxM1 = 0xCD9E8D57u;
 constexpr uint32_t kPhiloxW0 = 0x9E3779B9u, kPhiloxW1 = 0xBB67AE85u;
-constexpr uint32_t kNativeTagR = 3u;  // activation draw (same tag number as streams.TAG_R)
+constexpr uint32_t kNativeTagR = 3u;      // activation draw (same tag number as streams.TAG_R)
+constexpr uint32_t kNativeTagStall = 4u;  // SpSA stall draw (streams.TAG_STALL)
 
 PB_HD uint32_t philox_mulhi(uint32_t a, uint32_t b) {
 #ifdef __CUDA_ARCH__

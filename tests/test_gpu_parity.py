@@ -528,26 +528,50 @@ def test_philox_mode_plain_rule_equivalents_and_shards(oracle, bench_graphs):
 
 def test_philox_mode_rejects_unsupported_inputs(bench_graphs):
     graph = bench_graphs("G1")
+    prof = [sample_variability(VariabilityConfig(0.5, 0.5, 0.5), graph.n,
+                               np.random.default_rng(k)) for k in range(8)]
+    with pytest.raises(ValueError, match="philox"):   # TApSA with a varied profile: general path
+        _native_run(graph, 8, 10, algo=1, alpha=3, profs=prof)
+    g2 = random_graph(30, 5, (-2, -1, 1, 2), 0.3)     # |J| = 2: general path
     with pytest.raises(ValueError, match="philox"):
-        _native_run(graph, 8, 10, algo=1, alpha=3)
-    with pytest.raises(ValueError, match="philox"):
-        _native_run(graph, 8, 10, algo=2, p_stall=0.3)
+        _native_run(g2, 8, 10)
     with pytest.raises(ValueError, match="multiple of 4"):
         _native_run(graph, 8, 10, first_trial=2)
 
 
-@pytest.mark.parametrize("name,sig,trials", [("G1", (0.0, 0.0, 0.5), 128),
-                                             ("G81", (0.5, 0.5, 0.5), 256),
-                                             ("G55", (1.0, 0.0, 0.0), 256)])
+@pytest.mark.parametrize("name,algo,alpha,p_stall,trials,cycles", [
+    ("G81", 1, 4, 0.5, 64, 30), ("G81", 2, 1, 0.4, 64, 30), ("G1", 1, 3, 0.5, 40, 60),
+    ("G1", 2, 1, 0.5, 40, 60), ("G55", 1, 8, 0.5, 36, 40), ("G22", 2, 1, 1.0, 36, 40)])
+def test_philox_mode_time_averaged_and_stalled_rules_match_oracle(oracle, bench_graphs, name, algo,
+                                                                  alpha, p_stall, trials, cycles):
+    """Native stream for the paper's TApSA and SpSA rules (packed_sweep ALG=6/7;
+    SpSA's stall draw uses tag 4) against the oracle's Philox mode."""
+    graph = bench_graphs(name)
+    seed = 0xABCD_0123_4567
+    model, sch, keys, got = _native_run(graph, trials, cycles, seed, algo=algo, alpha=alpha,
+                                        p_stall=p_stall)
+    want = oracle.anneal_batch(model, sch, ["psa", "tapsa", "spsa"][algo],
+                               VariabilityProfile.ideal(model.n), keys, graph=graph, alpha=alpha,
+                               p_stall=p_stall, rng="philox", rng_seed=seed)
+    for k in ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "cut_trace",
+              "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
+
+
+@pytest.mark.parametrize("name,sig,trials,kind", [("G1", (0.0, 0.0, 0.5), 128, Algorithm.PSA),
+                                                  ("G81", (0.5, 0.5, 0.5), 256, Algorithm.PSA),
+                                                  ("G55", (1.0, 0.0, 0.0), 256, Algorithm.PSA),
+                                                  ("G1", (0, 0, 0), 128, Algorithm.TAPSA),
+                                                  ("G1", (0, 0, 0), 128, Algorithm.SPSA)])
 def test_philox_cut_statistics_match_reference_with_variability(bench_graphs, golden_analogs,
-                                                                name, sig, trials):
-    """The north_star statistical bar where pSA actually anneals (the
-    variability study, normalized cuts 0.4-0.999): mean final cut and mean
+                                                                name, sig, trials, kind):
+    """The north_star statistical bar where the anneal works (the variability
+    study, TApSA and SpSA; normalized cuts 0.4-0.999): mean final cut and mean
     per-trial best cut of the native stream within 0.5 % of the best-known cut
     of the replayed reference stream (which is bit-exact to the reference)."""
     graph = bench_graphs(name)
     best_known = golden_analogs[name]["best_known_analog"]
-    spec = engine.ExperimentSpec(graph=name, algo=AlgorithmConfig(Algorithm.PSA),
+    spec = engine.ExperimentSpec(graph=name, algo=AlgorithmConfig(kind, alpha=4, p_stall=0.5),
                                  variability=VariabilityConfig(*sig), cycles=1000, trials=trials)
     rep = engine.run_trials(spec, {name: graph})
     nat = engine.run_trials(dataclasses.replace(spec, rng="philox"), {name: graph})
