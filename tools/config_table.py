@@ -105,7 +105,7 @@ def main():
     def add(cfg, name, kind, sig, T, cpu_T, note=""):
         g, _ = benchmarks.load(name)
         gpu = gpu_run(g, kind, sig, T)
-        nat = gpu_run(g, kind, sig, T, rng="philox") if kind == Algorithm.PSA else None
+        nat = gpu_run(g, kind, sig, T, rng="philox")
         cpu = cpu_run(g, kind, sig, cpu_T) if cpu_T else None
         d = denom(name)
         B = bytes_per_update(g, any(sig))
@@ -153,7 +153,7 @@ def main():
              f"{SMEM_PEAK / 1000:.1f} TB/s), `active_fast` / `active` (general path). Bytes per update: "
              "SURVEY 8(d) B, plus 8 B for a varied profile.", "",
              "Philox columns: the same run with the native Philox4x32-10 stream (`rng=\"philox\"`; "
-             "plain rule only; always the launched packed kernels).", "",
+             "every rule on the packed path).", "",
              "| cfg | graph (n) | rule | sigma | trials | kernel | GPU ms/run | GPU upd/s | frac of roofline (bound) | CPU upd/s | GPU/CPU | mean cut / best-known | Philox kernel | Philox ms | Philox upd/s | Philox mean cut / best-known |",
              "|---|---|---|---|---:|---|---:|---:|---:|---:|---:|---:|---|---:|---:|---:|"]
     for r in rows:
