@@ -300,7 +300,7 @@ struct pbsa_plan {
     };
     std::vector<PLaunch> plaunch;
     // resident mode: one cluster per word anneals all cycles in one launch
-    bool resident = false, res_timing = false;
+    bool resident = false, res_timing = false, res_prof_smem = false;
     int res_cs = 1, res_threads = 256;
     size_t res_smem = 0;
     DevBuf<pbsa::RLaunch> rlaunch;     // resident timing: the sub-step list
@@ -1119,6 +1119,11 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 const int64_t thr = std::min<int64_t>(512, ((per + 31) / 32) * 32);
                 P.res_smem = 32 * 8 + 8 * (size_t)n + (thr / 32) * (256 + 4096) + pbsa::kMaxDivisors * 32 +
                              4 * (size_t)(P.nplanes * per + per + 1 + slice) + 64;
+                // stage the CTA's fp16 profile slice too when it fits (PBSA_RES_PROF=0 disables)
+                const size_t prof_bytes = 4 * (size_t)per * 32;
+                const char *penv = std::getenv("PBSA_RES_PROF");
+                P.res_prof_smem = (!penv || penv[0] != '0') && P.res_smem + prof_bytes <= (size_t)max_smem;
+                if (P.res_prof_smem) P.res_smem += prof_bytes;
             }
             if (timing && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
                 P.resident = true;
@@ -1337,6 +1342,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             r.nplanes = P.nplanes;
             r.cycles = (int)P.cycles;
             r.margin = P.var_margin;
+            r.prof_smem = P.res_prof_smem ? 1 : 0;
             if (P.native) {
                 pbsa::philox_round_keys((uint32_t)P.nseed, (uint32_t)(P.nseed >> 32), r.rk);
                 r.ngroup = (uint32_t)(P.first_trial / 4);

@@ -1409,6 +1409,7 @@ struct ResidentTimingArgs {
     float margin;
     uint32_t rk[20];            // NATIVE: Philox round keys
     uint32_t ngroup;            // NATIVE: Philox trial group of word 0
+    int prof_smem;              // the CTA's profile slice is staged in shared memory
 };
 
 template <int L, bool NATIVE = false>
@@ -1430,7 +1431,10 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
     uint32_t *fl = exm + nwarps * 32;                         // [nwarps][1024]
     uint32_t *sdivx = fl + nwarps * 1024;                     // [kMaxDivisors][8]
     uint32_t *plS = sdivx + kMaxDivisors * 8;                 // [nplanes][per]
-    uint32_t *rowS = plS + a.nplanes * per;                   // [per + 1]
+    // the CTA's slice of the fp16 profile ([per][32], node-major) when it fits:
+    // fired p-bits then read it at shared-memory latency instead of L2's
+    __half2 *profS = reinterpret_cast<__half2 *>(plS + a.nplanes * per);
+    uint32_t *rowS = reinterpret_cast<uint32_t *>(profS + (a.prof_smem ? per * 32 : 0));  // [per + 1]
     uint32_t *adjS = rowS + per + 1;
     for (int k = tid; k < a.n; k += blockDim.x) S0[k] = a.s_in[(size_t)w * a.n + k];
     if (tid < 32) key[tid] = a.kfc[(size_t)w * 32 + tid];
@@ -1440,6 +1444,10 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
     for (int k = tid; k < a.nplanes * per; k += blockDim.x) {
         const int pl = k / per, j = k - pl * per;
         plS[k] = lo + j < hi ? a.pplanes[((size_t)w * a.nplanes + pl) * a.n + lo + j] : 0u;
+    }
+    if (a.prof_smem) {
+        const __half2 *src = a.prof + ((size_t)w * a.n + lo) * 32;
+        for (int k = tid; k < (hi - lo) * 32; k += blockDim.x) profS[k] = src[k];
     }
     uint32_t *cs = S0, *ns = S1;
     uint32_t *wfl = fl + warp * 1024, *wres = res + warp * 32, *wexm = exm + warp * 32;
@@ -1553,7 +1561,9 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
                 if (R.inp) a.inp_out[((size_t)w * 32 + b) * a.n + ii] = __dmul_rn(i0, (double)raw);
             };
             auto prof_of = [&](uint32_t e) {
-                return __ldg(a.prof + ((size_t)w * a.n + base + ((e >> 5) & 31u)) * 32 + (e & 31u));
+                const int j = base + (int)((e >> 5) & 31u);
+                return a.prof_smem ? profS[(j - lo) * 32 + (int)(e & 31u)]
+                                   : __ldg(a.prof + ((size_t)w * a.n + j) * 32 + (e & 31u));
             };
             for (int k = lane; k < F; k += 64) {
                 const uint32_t e0 = wfl[k];
