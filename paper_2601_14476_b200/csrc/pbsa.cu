@@ -300,7 +300,7 @@ struct pbsa_plan {
     };
     std::vector<PLaunch> plaunch;
     // resident mode: one cluster per word anneals all cycles in one launch
-    bool resident = false, res_timing = false, res_prof_smem = false;
+    bool resident = false, res_timing = false, res_prof_smem = false, res_split = false;
     int res_cs = 1, res_threads = 256;
     size_t res_smem = 0;
     DevBuf<pbsa::RLaunch> rlaunch;     // resident timing: the sub-step list
@@ -1116,7 +1116,11 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             }
             P.res_smem += 4 * (size_t)(per + 1 + slice);
             if (timing) {
-                const int64_t thr = std::min<int64_t>(512, ((per + 31) / 32) * 32);
+                // two lanes per node when a CTA's slice still takes one pass of <= 16 warps
+                // (measured: G1 C2 sigma_nu 1.0 70 -> 63 ms; a second pass costs more: G22)
+                P.res_split = (per + 15) / 16 <= 16;
+                if (const char *env = std::getenv("PBSA_RES_SPLIT")) P.res_split = env[0] == '1';
+                const int64_t thr = std::min<int64_t>(512, P.res_split ? ((per + 15) / 16) * 32 : ((per + 31) / 32) * 32);
                 P.res_smem = 32 * 8 + 8 * (size_t)n + (thr / 32) * (256 + 4096) + pbsa::kMaxDivisors * 32 +
                              4 * (size_t)(P.nplanes * per + per + 1 + slice) + 64;
                 // stage the CTA's fp16 profile slice too when it fits (PBSA_RES_PROF=0 disables)
@@ -1125,11 +1129,12 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 P.res_prof_smem = (!penv || penv[0] != '0') && P.res_smem + prof_bytes <= (size_t)max_smem;
                 if (P.res_prof_smem) P.res_smem += prof_bytes;
             }
-            if (timing && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
+            // (per-thread cut counters take up to 32 nodes: 16 warps x 16 nodes x 32)
+            if (timing && want && P.res_smem <= (size_t)max_smem && per <= 16 * 16 * 32) {
                 P.resident = true;
                 P.res_timing = true;
                 P.res_cs = csz;
-                P.res_threads = (int)std::min<int64_t>(512, ((per + 31) / 32) * 32);
+                P.res_threads = (int)std::min<int64_t>(512, P.res_split ? ((per + 15) / 16) * 32 : ((per + 31) / 32) * 32);
                 std::vector<pbsa::RLaunch> rl;
                 for (const pbsa_plan::PLaunch &pl : P.plaunch)
                     rl.push_back({pl.count, (int)pl.cycle, pl.do_cut, pl.ndiv, (int)pl.div_off, pl.inp ? 1 : 0,
@@ -1343,6 +1348,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             r.cycles = (int)P.cycles;
             r.margin = P.var_margin;
             r.prof_smem = P.res_prof_smem ? 1 : 0;
+            r.split = P.res_split ? 1 : 0;
             if (P.native) {
                 pbsa::philox_round_keys((uint32_t)P.nseed, (uint32_t)(P.nseed >> 32), r.rk);
                 r.ngroup = (uint32_t)(P.first_trial / 4);

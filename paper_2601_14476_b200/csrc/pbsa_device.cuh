@@ -1410,6 +1410,7 @@ struct ResidentTimingArgs {
     uint32_t rk[20];            // NATIVE: Philox round keys
     uint32_t ngroup;            // NATIVE: Philox trial group of word 0
     int prof_smem;              // the CTA's profile slice is staged in shared memory
+    int split;                  // 16 nodes per warp, two lanes per node
 };
 
 template <int L, bool NATIVE = false>
@@ -1474,8 +1475,14 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
             sdivx[k] = (pl < a.nplanes && ((pv >> pl) & 1u)) ? 0u : 0xffffffffu;
         }
         __syncthreads();
-        for (int base = lo + warp * 32; base < hi; base += nwarps * 32) {
-            const int i = base + lane;
+        // split mode (a.split): a warp takes 16 nodes, lanes l and l + 16 share
+        // node base + l and split its neighbour list and its fired trials (half
+        // the per-warp critical path of a 32-node chunk; the sub-step is
+        // latency-bound at ~2 warps per scheduler).  Otherwise lane = node.
+        const int cw = a.split ? 16 : 32;
+        for (int base = lo + warp * cw; base < hi; base += nwarps * cw) {
+            const int hl = a.split ? lane & 15 : lane, half = a.split ? lane >> 4 : 0;
+            const int i = base + hl;
             const bool valid = i < hi;
             uint32_t own = 0, fire = 0, beg = 0, end = 0;
             if (valid) {
@@ -1496,7 +1503,7 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
             }
             const bool any = __any_sync(0xffffffffu, fire != 0);
             if (!R.do_cut && !any) {  // nothing fires: carry the words
-                if (valid && update) {
+                if (valid && update && half == 0) {
                     ns[i] = own;
                     for (int r = 1; r < CS; ++r)
                         *cluster.map_shared_rank(ns + i, rank + r < CS ? rank + r : rank + r - CS) = own;
@@ -1504,12 +1511,23 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
                 continue;
             }
             uint32_t p[L];
-            count_neighbours<L>(beg, end, [&](uint32_t k) {
+            const uint32_t mid = a.split ? beg + ((end - beg + 1) >> 1) : end;
+            count_neighbours<L>(half ? mid : beg, half ? end : mid, [&](uint32_t k) {
                 const uint32_t e = adjS[k];
                 return cs[e & 0x7fffffffu] ^ (uint32_t)((int32_t)e >> 31);
             }, p);
+            if (a.split) {   // the two halves' partial counts, added bit-sliced (the sum is <= d < 2^L)
+                uint32_t carry = 0;
+#pragma unroll
+                for (int r = 0; r < L; ++r) {
+                    const uint32_t q = __shfl_xor_sync(0xffffffffu, p[r], 16);
+                    const uint32_t sm = p[r] ^ q ^ carry;
+                    carry = (p[r] & q) | (carry & (p[r] ^ q));
+                    p[r] = sm;
+                }
+            }
             const int d = (int)(end - beg);
-            if (R.do_cut && valid) {
+            if (R.do_cut && valid && half == 0) {
                 uint32_t g[L];
                 cut_counts<L>(p, own, d, g);
                 dsum += d;
@@ -1517,7 +1535,8 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
             }
             if (!update) continue;
             // warp-balanced fired (lane, trial, raw) list, as packed_sweep_timing
-            const int c = __popc(fire);
+            const uint32_t myfire = a.split ? fire & (half ? 0xffff0000u : 0x0000ffffu) : fire;
+            const int c = __popc(myfire);
             int off = c;
 #pragma unroll
             for (int sft = 1; sft < 32; sft <<= 1) {
@@ -1526,15 +1545,17 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
             }
             const int F = __shfl_sync(0xffffffffu, off, 31);
             off -= c;
-            for (uint32_t f = fire; f; f &= f - 1) {
+            for (uint32_t f = myfire; f; f &= f - 1) {
                 const int b = __ffs(f) - 1;
                 int pop = 0;
 #pragma unroll
                 for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
-                wfl[off++] = ((uint32_t)(2 * pop - d + 1024) << 10) | ((uint32_t)lane << 5) | (uint32_t)b;
+                wfl[off++] = ((uint32_t)(2 * pop - d + 1024) << 10) | ((uint32_t)hl << 5) | (uint32_t)b;
             }
-            wres[lane] = 0;
-            wexm[lane] = 0;
+            if (lane < cw) {
+                wres[lane] = 0;
+                wexm[lane] = 0;
+            }
             __syncwarp();
             // two list entries per lane and round, their profile loads in flight together
             auto fire_one = [&](uint32_t e, __half2 lv) {
@@ -1574,9 +1595,9 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
                 if (two) fire_one(e1, lv1);
             }
             __syncwarp();
-            if (valid) {
-                uint32_t word = (own & ~fire) | wres[lane];
-                uint32_t ex = wexm[lane];
+            if (valid && half == 0) {
+                uint32_t word = (own & ~fire) | wres[hl];
+                uint32_t ex = wexm[hl];
                 while (ex) {  // rare near-tie: the reference's fp64 arithmetic
                     const int b = __ffs(ex) - 1;
                     ex &= ex - 1;
