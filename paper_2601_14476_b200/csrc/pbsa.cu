@@ -227,6 +227,12 @@ struct StreamHolder {
     }
 };
 
+struct PbsaHostOut {  // caller's output buffers of a pipelined one-shot call
+    int8_t *spins;
+    double *inputs, *trace_energy;
+    int64_t *trace_cut, *best;
+};
+
 struct pbsa_plan {
     // declared first so it is destroyed last, after every buffer has been
     // released onto it
@@ -249,6 +255,16 @@ struct pbsa_plan {
     bool int_energy = true;
     bool tapsa_hist_from_raw = false;  // TAPSA alpha=1 routed to the packed path
     bool tapsa_packed = false;         // TAPSA alpha>=2 on the packed path (bit-sliced ring)
+    // one-shot pipelined mode: the run is not captured into a graph; word
+    // phases run one after another and each phase's outputs are formatted and
+    // copied to the caller's host buffers on out_stream while the next computes
+    bool pipelined = false;
+    cudaStream_t out_stream = nullptr;
+    std::vector<cudaEvent_t> ev_phase;
+    PbsaHostOut hout{};
+    int64_t mm_ = 0, gm_ = 0;          // model / graph edge counts (direct enqueue)
+    DevBuf<int8_t> o_spins;
+    DevBuf<double> o_inputs;
     bool native = false;               // PBSA_RNG_PHILOX: Philox draws (philox.cuh)
     bool reg4 = false;                 // packed path: every degree is 4 (gather_counts_reg4)
     uint64_t nseed = 0;                // Philox key
@@ -353,6 +369,8 @@ struct pbsa_plan {
         for (cudaEvent_t e : {ev_start, ev_sweep0, ev_sweep1, ev_end, ev_fork})
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
+        for (cudaEvent_t e : ev_phase) cudaEventDestroy(e);
+        if (out_stream) cudaStreamDestroy(out_stream);
         for (cudaStream_t cs : chain_streams) cudaStreamDestroy(cs);
     }
 };
@@ -1043,6 +1061,14 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             const int64_t nph = (P.W + P.phase_words - 1) / P.phase_words;
             P.phase_words = (P.W + nph - 1) / nph;
         }
+        // one-shot calls of the plain rule on the launched path run pipelined
+        // (PBSA_PIPELINE=0 disables): four word phases, each phase's outputs
+        // copied back while the next anneals (decided again below once the
+        // resident choice is known)
+        P.pipelined = g_oneshot && !many_launches && !P.var_mode && !P.tapsa_packed && !P.spsa_packed &&
+                      !P.tapsa_hist_from_raw && P.W >= 16;
+        if (const char *env = std::getenv("PBSA_PIPELINE")) P.pipelined = P.pipelined && env[0] != '0';
+        if (P.pipelined) P.phase_words = (P.W + 3) / 4;
         if (const char *env = std::getenv("PBSA_PACKED_PHASE_WORDS")) P.phase_words = std::atoi(env);
         if (const char *env = std::getenv("PBSA_PDL")) P.use_pdl = env[0] != '0';
         if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;
@@ -1077,6 +1103,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // couple (fewer graph nodes to instantiate)
         int chains = (many_launches || (P.spsa_packed && !g_oneshot && P.W >= 64)) ? 4
                                                                      : (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
+        if (P.pipelined) chains = 2;  // launched directly: keep the launch count low
         if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
         chains = (int)std::min<int64_t>(chains, P.W);
         if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
@@ -1157,6 +1184,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             }
         }
+        if (P.resident) P.pipelined = false;
         P.updates_per_run = (int64_t)n * trials * cycles;
         if (many_launches) {  // sum over p-bits of #{count < cycles t_res : period | count}
             int64_t ups = 0;
@@ -1301,6 +1329,60 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     (void)mm;
 }
 
+// The sweep-interval events are external event nodes inside a captured graph;
+// a directly launched (pipelined) run records them normally.
+cudaError_t record_sweep_event(const pbsa_plan &P, cudaEvent_t ev, cudaStream_t st) {
+    return P.pipelined ? cudaEventRecord(ev, st) : cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+}
+
+// Pipelined one-shot: once the words [w0, w1) have finished their last cut
+// pass, format their trials' outputs (traces, spins, inputs) and copy them to
+// the caller's host buffers on out_stream, while the main stream anneals the
+// next phase.  Outputs of the plain rule on the packed path only.
+void enqueue_phase_outputs(pbsa_plan &P, int64_t w0, int64_t w1, int parity, int k) {
+    const int TB = 256;
+    cudaStream_t os = P.out_stream;
+    CK(cudaEventRecord(P.ev_phase[k], P.stream));
+    CK(cudaStreamWaitEvent(os, P.ev_phase[k], 0));
+    const int64_t n = P.n, C = P.cycles;
+    const int64_t t0 = w0 * 32, t1 = std::min<int64_t>(P.T, w1 * 32);
+    if (t1 <= t0) return;
+    const int64_t Tr = t1 - t0;
+    pbsa::FinalArgs f{};
+    f.pacc = P.pacc.p + t0;
+    f.total_w = P.total_w;
+    f.mode = 0;
+    f.has_graph = P.has_graph;
+    f.C = (int)C;
+    f.Tp = (int)P.Tp;
+    f.T = (int)Tr;
+    f.trace_cut = P.trace_cut.p + t0 * C;
+    f.trace_energy = P.trace_energy.p + t0 * C;
+    f.best = P.best.p + t0;
+    pbsa::finalize_traces<<<grid_for(Tr, TB), TB, 0, os>>>(f);
+    ++P.launches;
+    const PbsaHostOut &h = P.hout;
+    if (h.trace_cut)
+        CK(cudaMemcpyAsync(h.trace_cut + t0 * C, f.trace_cut, Tr * C * sizeof(int64_t), cudaMemcpyDeviceToHost, os));
+    if (h.trace_energy)
+        CK(cudaMemcpyAsync(h.trace_energy + t0 * C, f.trace_energy, Tr * C * sizeof(double),
+                           cudaMemcpyDeviceToHost, os));
+    if (h.best) CK(cudaMemcpyAsync(h.best + t0, f.best, Tr * sizeof(int64_t), cudaMemcpyDeviceToHost, os));
+    if (h.spins) {
+        pbsa::unpack_spins<<<grid_for(n * Tr, TB), TB, 0, os>>>(P.p_spins[parity].p + w0 * n, P.o_spins.p + t0 * n,
+                                                                 (int)n, (int)(w1 - w0), (int)Tr);
+        CK(cudaMemcpyAsync(h.spins + t0 * n, P.o_spins.p + t0 * n, Tr * n, cudaMemcpyDeviceToHost, os));
+        ++P.launches;
+    }
+    if (h.inputs) {
+        pbsa::inputs_from_raw<<<grid_for(n * Tr, TB), TB, 0, os>>>(P.raw_last.p + t0, P.o_inputs.p + t0 * n,
+                                                                   P.i0[C - 1], (int)n, (int)P.Tp, (int)Tr, 1.0);
+        CK(cudaMemcpyAsync(h.inputs + t0 * n, P.o_inputs.p + t0 * n, Tr * n * sizeof(double),
+                           cudaMemcpyDeviceToHost, os));
+        ++P.launches;
+    }
+}
+
 void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
     cudaStream_t st = P.stream;
     const int TB = 256;
@@ -1315,7 +1397,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                                  P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16;
-        CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
+        CK(record_sweep_event(P, P.ev_sweep0, st));
         // Word phases run one after another so that a phase's first-absorb
         // cache (PW words x n x 256 B) stays L2-resident across its cycles;
         // inside a phase, independent word groups run as concurrent chains
@@ -1530,22 +1612,25 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     CK(cudaStreamWaitEvent(st, P.ev_join[g - 1], 0));
                 }
             }
+            if (P.pipelined) enqueue_phase_outputs(P, p0, p1, cur, (int)(p0 / P.phase_words));
         }
-        CK(cudaEventRecordWithFlags(P.ev_sweep1, st, cudaEventRecordExternal));
+        CK(record_sweep_event(P, P.ev_sweep1, st));
         P.final_parity = cur;
-        pbsa::FinalArgs f{};
-        f.pacc = P.pacc.p;
-        f.total_w = P.total_w;
-        f.mode = 0;
-        f.has_graph = P.has_graph;
-        f.C = (int)P.cycles;
-        f.Tp = (int)P.Tp;
-        f.T = (int)P.T;
-        f.trace_cut = P.trace_cut.p;
-        f.trace_energy = P.trace_energy.p;
-        f.best = P.best.p;
-        pbsa::finalize_traces<<<grid_for(P.T, TB), TB, 0, st>>>(f);
-        ++P.launches;
+        if (!P.pipelined) {
+            pbsa::FinalArgs f{};
+            f.pacc = P.pacc.p;
+            f.total_w = P.total_w;
+            f.mode = 0;
+            f.has_graph = P.has_graph;
+            f.C = (int)P.cycles;
+            f.Tp = (int)P.Tp;
+            f.T = (int)P.T;
+            f.trace_cut = P.trace_cut.p;
+            f.trace_energy = P.trace_energy.p;
+            f.best = P.best.p;
+            pbsa::finalize_traces<<<grid_for(P.T, TB), TB, 0, st>>>(f);
+            ++P.launches;
+        }
     } else {
         pbsa::init_general<<<grid_for(P.n * P.Tp, TB), TB, 0, st>>>(P.g_spins[0].p, P.kspin.p,
                                                                     (int)P.n, (int)P.Tp);
@@ -1560,7 +1645,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         if (P.e_acc.n) CK(cudaMemsetAsync(P.e_acc.p, 0, P.e_acc.n * sizeof(unsigned long long), st));
         if (P.dj_acc.n) CK(cudaMemsetAsync(P.dj_acc.p, 0, P.dj_acc.n * sizeof(unsigned long long), st));
         P.launches += 1;
-        CK(cudaEventRecordWithFlags(P.ev_sweep0, st, cudaEventRecordExternal));
+        CK(record_sweep_event(P, P.ev_sweep0, st));
         int cur = 0;
         size_t ai = 0, li = 0;
         const int sm_chunks = std::max<int64_t>(1, std::min<int64_t>(64, (std::max(mm, gm) + 255) / 256));
@@ -1728,7 +1813,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                 ++P.launches;
             }
         }
-        CK(cudaEventRecordWithFlags(P.ev_sweep1, st, cudaEventRecordExternal));
+        CK(record_sweep_event(P, P.ev_sweep1, st));
         P.final_parity = cur;
         pbsa::FinalArgs f{};
         f.cut_acc = P.cut_acc.p;
@@ -1803,6 +1888,12 @@ int pbsa_plan_create_ex(int device, int64_t n, const int64_t *indptr, const int6
                     ge_j, ge_w, lam, delta, period, profile_stride, i0_min, beta, cycles, t_res,
                     algo, alpha, p_stall, trials, keys, rng_mode, rng_seed, first_trial);
         DeviceGuard dg(device);
+        P->mm_ = mm;
+        P->gm_ = gm;
+        if (P->pipelined) {  // one-shot pipelined: launched directly by the call
+            *out = P.release();
+            return;
+        }
         // capture the whole anneal into one graph
         CK(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
         try {
@@ -2149,6 +2240,38 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
                                  rng_seed, first_trial, &P);
     g_oneshot = false;
     if (rc != PBSA_OK) return rc;
+    if (P->pipelined) {
+        // launch the phases directly; each phase's outputs stream back on
+        // out_stream while the next anneals; the run-independent outputs are
+        // written on the host meanwhile
+        rc = guarded([&] {
+            DeviceGuard dg(P->device);
+            AllocStream as(P->stream);
+            P->hout = PbsaHostOut{spins, inputs, trace_energy, trace_cut, best_cut};
+            if (spins) P->o_spins.alloc((size_t)P->T * P->n);
+            if (inputs) P->o_inputs.alloc((size_t)P->T * P->n);
+            CK(cudaStreamCreateWithFlags(&P->out_stream, cudaStreamNonBlocking));
+            const int64_t nph = (P->W + P->phase_words - 1) / P->phase_words;
+            for (int64_t k = 0; k < nph; ++k) {
+                cudaEvent_t e;
+                CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                P->ev_phase.push_back(e);
+            }
+            CK(cudaEventRecord(P->ev_start, P->stream));
+            enqueue_run(*P, P->mm_, P->gm_);
+            CK(cudaEventRecord(P->ev_end, P->stream));
+            host_constant_outputs(P, hist, counts, trace_i0);
+            CK(cudaEventSynchronize(P->ev_end));
+            P->ran = true;
+            if (device_ms) CK(cudaEventElapsedTime(device_ms, P->ev_start, P->ev_end));
+            CK(cudaStreamSynchronize(P->out_stream));
+            CK(cudaGetLastError());
+        });
+        const std::string err = g_last_error;
+        pbsa_plan_destroy(P);
+        if (rc != PBSA_OK) g_last_error = err;
+        return rc;
+    }
     // launch, write the run-independent outputs on the host while the device
     // anneals, then wait and download the rest
     rc = guarded([&] {

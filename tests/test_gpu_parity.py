@@ -679,3 +679,21 @@ def test_with_and_without_graph_same_dynamics(bench_graphs):
             assert np.array_equal(with_g.energy_trace, without.energy_trace)
             assert np.array_equal(with_g.final_state.inputs, without.final_state.inputs)
             assert without.cut_trace is None and with_g.cut_trace is not None
+
+
+@pytest.mark.parametrize("trials", [600, 1000])
+def test_pipelined_one_shot_equals_graph_run(bench_graphs, monkeypatch, trials):
+    """The one-shot call of the plain rule runs pipelined (word phases launched
+    directly, each phase's outputs copied back while the next anneals); its
+    eight outputs equal the captured-graph run of the same batch, including a
+    ragged last word (600 = 18.75 words)."""
+    g = bench_graphs("G81")
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 40, 10)
+    keys = [streams.run_key(streams.trial_seed(0, k)) for k in range(trials)]
+    b = _native.Batch(model, sch, keys, graph=g)
+    piped, _ = _native.anneal_batch(b)
+    monkeypatch.setenv("PBSA_PIPELINE", "0")
+    plain, _ = _native.anneal_batch(b)
+    for k in _native.OUT_ORDER:
+        assert np.array_equal(piped[k], plain[k]), k
