@@ -819,17 +819,19 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 // loads are issued together before the group's decisions.
                 uint32_t word = 0, tie = 0xffffffffu;
                 uint32_t X[4];  // NATIVE: the current Philox block of the activation draws
-                for (int gq = 3; gq >= 0; --gq) {
-                    uint32_t th[8];
+                // groups of GS trials (native: 4, its stalled drives need both threshold words)
+                constexpr int GS = NATIVE ? 4 : 8;
+                for (int gq = 32 / GS - 1; gq >= 0; --gq) {
+                    uint32_t th[GS];
 #pragma unroll
-                    for (int j = 7; j >= 0; --j) {
-                        const int b = gq * 8 + j;
+                    for (int j = GS - 1; j >= 0; --j) {
+                        const int b = gq * GS + j;
                         th[j] = ((stallw >> b) & 1u) ? sidx[(size_t)b * a.n] : 0u;
                     }
-                    uint32_t tlo[8];  // NATIVE: low words of 2^32 - T of the stalled drives
+                    uint32_t tlo[GS];  // NATIVE: low words of 2^32 - T of the stalled drives
 #pragma unroll
-                    for (int j = 7; j >= 0; --j) {
-                        const int b = gq * 8 + j;
+                    for (int j = GS - 1; j >= 0; --j) {
+                        const int b = gq * GS + j;
                         if ((stallw >> b) & 1u) {
                             if (NATIVE) {
                                 const uint64_t nt = (1ULL << 32) - __ldg(a.thr_all + th[j]);
@@ -841,8 +843,8 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         }
                     }
 #pragma unroll
-                    for (int j = 7; j >= 0; --j) {
-                        const int b = gq * 8 + j;
+                    for (int j = GS - 1; j >= 0; --j) {
+                        const int b = gq * GS + j;
                         int pop = 0;
 #pragma unroll
                         for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
