@@ -1105,13 +1105,17 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
             auto prof_of = [&](uint32_t e) {
                 return __ldg(a.prof16 + ((size_t)w * a.n + ch * 32 + ((e >> 5) & 31u)) * 32 + (e & 31u));
             };
-            for (int k = lane; k < F; k += 64) {
-                const uint32_t e0 = fl[k];
-                const bool two = k + 32 < F;
-                const uint32_t e1 = two ? fl[k + 32] : e0;
-                const __half2 lv0 = prof_of(e0), lv1 = prof_of(e1);
-                fire_one(e0, lv0);
-                if (two) fire_one(e1, lv1);
+            // four list entries per lane and round, their profile loads in flight together
+            for (int k = lane; k < F; k += 128) {
+                uint32_t e[4];
+                __half2 lv[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) e[j] = k + 32 * j < F ? fl[k + 32 * j] : fl[k];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) lv[j] = prof_of(e[j]);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (k + 32 * j < F) fire_one(e[j], lv[j]);
             }
             __syncwarp();
             if (valid) {
