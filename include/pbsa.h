@@ -212,6 +212,18 @@ int pbsa_debug_var_prefilter(int device, int64_t count, const double *lam, const
 int pbsa_debug_philox(int device, int64_t count, const uint32_t *ctr, const uint32_t *key,
                       uint32_t *out);
 
+/*
+ * Text of the reference CLI's trace CSV rows (cli.py:163-168, no header) for
+ * T trials x C cycles: "t,c,<i0 text c>,<energy>.0,<cut>\n" with the caller's
+ * repr() strings of the (shared) i0 trace in i0_text[i0_off[c] .. i0_off[c+1]),
+ * integral energies energy[T*C] (|E| < 1e16, so repr is the digits + ".0")
+ * and cut[T*C] (NULL: empty column).  *out_len receives the byte count;
+ * PBSA_EINVAL if out_cap is too small.  Host threads, no GPU.
+ */
+int pbsa_format_trace_csv(int64_t T, int64_t C, const char *i0_text, const int64_t *i0_off,
+                          const int64_t *energy, const int64_t *cut, char *out, int64_t out_cap,
+                          int64_t *out_len);
+
 /* Host builds of device-side pieces (no GPU needed):
  *   pbsa_libm_tanh_host  -- the device tanh (same source, libm_tanh.cuh);
  *   pbsa_threshold_host  -- the packed path's activation threshold for a

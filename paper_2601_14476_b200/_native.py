@@ -61,6 +61,8 @@ _SIGNATURES = [
     ("pbsa_debug_tanh", ctypes.c_int, [ctypes.c_int, _I64, _P, _P]),
     ("pbsa_debug_philox", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P]),
     ("pbsa_debug_var_prefilter", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P, _P, _P, _P]),
+    ("pbsa_format_trace_csv", ctypes.c_int, [_I64, _I64, _P, _P, _P, _P, _P, _I64,
+                                              ctypes.POINTER(_I64)]),
     ("pbsa_libm_tanh_host", _F64, [_F64]),
     ("pbsa_threshold_host", ctypes.c_uint64, [_F64]),
     ("pbsa_threshold_native_host", ctypes.c_uint64, [_F64]),
@@ -309,3 +311,24 @@ def default_device() -> int:
         if v is not None and v.strip():
             return int(v)
     return 0
+
+
+def format_trace_rows(i0_strs: list[bytes], energy_int: np.ndarray, cut: np.ndarray | None) -> bytes:
+    """Trace CSV rows (no header) by the library's host formatter
+    (pbsa_format_trace_csv): energy_int [T][C] integral energies, cut [T][C]
+    or None, i0_strs the repr() bytes of the shared i0 trace."""
+    lib = load()
+    T, C = energy_int.shape
+    text = b"".join(i0_strs)
+    off = np.zeros(C + 1, np.int64)
+    np.cumsum([len(x) for x in i0_strs], out=off[1:])
+    e = np.ascontiguousarray(energy_int, dtype=np.int64)
+    c = None if cut is None else np.ascontiguousarray(cut, dtype=np.int64)
+    cap = T * (C * 96 + int(off[-1])) + 64  # 4 integers <= 21 chars, ".0", 4 separators
+    out = np.empty(cap, np.uint8)
+    n = _I64(0)
+    tb = ctypes.create_string_buffer(text, len(text) + 1)
+    _check(lib.pbsa_format_trace_csv(T, C, ctypes.addressof(tb), off.ctypes.data, e.ctypes.data,
+                                     0 if c is None else c.ctypes.data, out.ctypes.data, cap,
+                                     ctypes.byref(n)))
+    return out[:n.value].tobytes()

@@ -2362,6 +2362,76 @@ int pbsa_debug_tanh(int device, int64_t count, const double *x, double *out) {
     });
 }
 
+// ------------------------------------------------------- trace CSV text
+// Host-side formatter behind paper_2601_14476_b200.traces:
+// the rows "trial,cycle,i0,energy,cut\n" of the reference CLI's trace file
+// (cli.py:163-168), for integral energies, written by all host threads.
+namespace {
+inline int dec_len(uint64_t x) {
+    int n = 1;
+    while (x >= 10) { x /= 10; ++n; }
+    return n;
+}
+inline int int_len(int64_t v) {
+    return v < 0 ? 1 + dec_len((uint64_t)0 - (uint64_t)v) : dec_len((uint64_t)v);
+}
+inline char *put_int(char *p, int64_t v) {
+    uint64_t x = (uint64_t)v;
+    if (v < 0) { *p++ = '-'; x = (uint64_t)0 - x; }
+    char tmp[24];
+    int n = 0;
+    do { tmp[n++] = (char)('0' + x % 10); x /= 10; } while (x);
+    while (n) *p++ = tmp[--n];
+    return p;
+}
+}  // namespace
+
+int pbsa_format_trace_csv(int64_t T, int64_t C, const char *i0_text, const int64_t *i0_off,
+                          const int64_t *energy, const int64_t *cut, char *out, int64_t out_cap,
+                          int64_t *out_len) {
+    return guarded([&] {
+        if (T < 0 || C < 0 || (T * C > 0 && (!i0_text || !i0_off || !energy || !out)) || !out_len)
+            fail(PBSA_EINVAL, "bad arguments");
+        std::vector<int64_t> tlen(T + 1, 0);
+        parallel_for(T, 16, [&](int64_t t0, int64_t t1) {
+            for (int64_t t = t0; t < t1; ++t) {
+                int64_t len = 0;
+                const int tl = int_len(t);
+                for (int64_t c = 0; c < C; ++c) {
+                    // "t,c,i0,E.0,cut\n": four commas, ".0" and the newline
+                    len += tl + int_len(c) + (i0_off[c + 1] - i0_off[c]) + int_len(energy[t * C + c]) +
+                           (cut ? int_len(cut[t * C + c]) : 0) + 7;
+                }
+                tlen[t + 1] = len;
+            }
+        });
+        for (int64_t t = 0; t < T; ++t) tlen[t + 1] += tlen[t];
+        *out_len = tlen[T];
+        if (tlen[T] > out_cap) fail(PBSA_EINVAL, "output buffer too small (%lld bytes needed)", (long long)tlen[T]);
+        parallel_for(T, 16, [&](int64_t t0, int64_t t1) {
+            for (int64_t t = t0; t < t1; ++t) {
+                char *p = out + tlen[t];
+                for (int64_t c = 0; c < C; ++c) {
+                    p = put_int(p, t);
+                    *p++ = ',';
+                    p = put_int(p, c);
+                    *p++ = ',';
+                    const int64_t a = i0_off[c], b = i0_off[c + 1];
+                    std::memcpy(p, i0_text + a, (size_t)(b - a));
+                    p += b - a;
+                    *p++ = ',';
+                    p = put_int(p, energy[t * C + c]);
+                    *p++ = '.';
+                    *p++ = '0';
+                    *p++ = ',';
+                    if (cut) p = put_int(p, cut[t * C + c]);
+                    *p++ = '\n';
+                }
+            }
+        });
+    });
+}
+
 double pbsa_libm_tanh_host(double x) { return pb_libm_tanh(x); }
 
 uint64_t pbsa_threshold_host(double t) { return threshold_h64(t); }
