@@ -118,3 +118,41 @@ def run_trials_sharded(spec: ExperimentSpec, graphs: Mapping[str, MaxCutGraph],
                         mean_final_energy=(e2 / 2) / n,
                         normalized_mean_cut=(mean / bk) if bk else None,
                         anneal_seconds=float(wall.item()), final_cuts=all_cuts)
+
+
+def run_trials_devices(spec: ExperimentSpec, graphs: Mapping[str, MaxCutGraph],
+                       registry: Mapping[str, int] | None = None, devices=None, *,
+                       runner: Callable | None = None):
+    """``run_trials`` over several GPUs from ONE process: the device-ordinal
+    list of the batched entry.  Trial shards
+    ``shard_range(T, r, len(devices))`` run concurrently, one host thread per
+    device (the C-ABI call releases the GIL; each call owns its plan and
+    stream), and the per-trial results are concatenated in trial order, so
+    the summary is identical to the single-device ``run_trials``.  The
+    anneal seconds are the wall time of the whole fan-out.
+
+    ``runner(spec, graph, lo, hi, device) -> (results, seconds)`` defaults to
+    ``engine.run_trial_range`` (tests inject a CPU runner)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import _native
+    from .engine import summarize
+
+    try:
+        graph = graphs[spec.graph]
+    except KeyError:
+        raise KeyError(f"unknown graph {spec.graph!r}; have {sorted(graphs)}") from None
+    if devices is None:
+        devices = list(range(max(1, _native.device_count())))
+    devices = list(devices)
+    if not devices:
+        raise ValueError("need at least one device")
+    run = runner or (lambda s, g, lo, hi, d: run_trial_range(s, g, lo, hi, device=d))
+    spans = [shard_range(spec.trials, r, len(devices)) for r in range(len(devices))]
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(len(devices)) as ex:
+        parts = list(ex.map(lambda a: run(spec, graph, a[0][0], a[0][1], a[1]) if a[0][1] > a[0][0]
+                            else ([], 0.0), zip(spans, devices)))
+    results = [r for part, _ in parts for r in part]
+    best_known = registry.get(spec.graph) if registry is not None else None
+    return summarize(results, best_known, time.perf_counter() - t0)

@@ -103,3 +103,36 @@ def test_two_rank_gloo_sharding_matches_single_process(oracle):
         assert mean == ref.mean_cut and std == ref.std_cut
         assert me == ref.mean_final_energy and norm == ref.normalized_mean_cut
         assert best == int(bests.max())
+
+
+def test_device_list_fan_out_is_trial_ordered_and_exact(oracle):
+    """run_trials_devices: shards on several devices (here a CPU runner with
+    the oracle) concatenate to the single-device trial order and summary."""
+    from paper_2601_14476_b200.distributed import run_trials_devices
+    from paper_2601_14476_b200.engine import summarize
+    spec, graphs = _spec_and_graphs()
+    seen = []
+
+    def runner(s, g, lo, hi, device):
+        seen.append((lo, hi, device))
+        cuts, bests, energies, secs = oracle_runner(s, g, lo, hi)
+
+        class R:
+            def __init__(self, k, c, e):
+                self.trial, self.final_cut, self.final_energy = k, int(c), float(e)
+        return [R(lo + k, c, e) for k, (c, e) in enumerate(zip(cuts, energies))], secs
+
+    out = run_trials_devices(spec, graphs, {"G1": 11605}, devices=[0, 1, 2], runner=runner)
+    spans = sorted((lo, hi) for lo, hi, _ in seen)
+    assert spans[0][0] == 0 and spans[-1][1] == spec.trials
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert len({d for _, _, d in seen}) == len(seen)  # one shard per device
+    assert [r.trial for r in out.results] == list(range(spec.trials))
+    cuts, _, energies, _ = oracle_runner(spec, graphs["G1"], 0, spec.trials)
+
+    class R:
+        def __init__(self, c, e):
+            self.final_cut, self.final_energy = int(c), float(e)
+    ref = summarize([R(c, e) for c, e in zip(cuts, energies)], 11605)
+    assert out.mean_cut == ref.mean_cut and out.std_cut == ref.std_cut
+    assert out.normalized_mean_cut == ref.normalized_mean_cut

@@ -697,3 +697,20 @@ def test_pipelined_one_shot_equals_graph_run(bench_graphs, monkeypatch, trials):
     plain, _ = _native.anneal_batch(b)
     for k in _native.OUT_ORDER:
         assert np.array_equal(piped[k], plain[k]), k
+
+
+def test_device_list_fan_out_equals_single_call(bench_graphs):
+    """distributed.run_trials_devices (one process, a device-ordinal list; here
+    the one visible B200 listed twice, two concurrent plans) gives the
+    single-call run_trials results trial by trial."""
+    from paper_2601_14476_b200.distributed import run_trials_devices
+    g = bench_graphs("G81")
+    spec = engine.ExperimentSpec(graph="G81", algo=AlgorithmConfig(Algorithm.PSA), cycles=40,
+                                 trials=300)
+    one = engine.run_trials(spec, {"G81": g}, {"G81": 14004})
+    two = run_trials_devices(spec, {"G81": g}, {"G81": 14004}, devices=[0, 0])
+    assert len(two.results) == spec.trials
+    for a, b in zip(one.results, two.results):
+        assert np.array_equal(a.final_state.spins, b.final_state.spins)
+        assert np.array_equal(a.cut_trace, b.cut_trace)
+    assert one.mean_cut == two.mean_cut and one.std_cut == two.std_cut
