@@ -317,6 +317,7 @@ struct pbsa_plan {
     std::vector<PLaunch> plaunch;
     // resident mode: one cluster per word anneals all cycles in one launch
     bool resident = false, res_timing = false, res_prof_smem = false, res_split = false;
+    bool res_tapsa = false;
     int res_cs = 1, res_threads = 256;
     size_t res_smem = 0;
     DevBuf<pbsa::RLaunch> rlaunch;     // resident timing: the sub-step list
@@ -530,10 +531,15 @@ ResidentTimingKernel resident_timing_for(int L, bool native = false) {
     }
 }
 
-ResidentKernel resident_kernel_for(int L, bool cached, bool varu = false, bool native = false) {
+ResidentKernel resident_kernel_for(int L, bool cached, bool varu = false, bool native = false,
+                                   bool tapsa = false) {
     switch (L) {
 #define PBSA_RCASE(l)                                                                          \
     case l:                                                                                    \
+        if (tapsa)                                                                             \
+            return native ? pbsa::resident_sweep<l, false, false, true, true>                  \
+                          : (cached ? pbsa::resident_sweep<l, true, false, false, true>        \
+                                    : pbsa::resident_sweep<l, false, false, false, true>);     \
         return native ? (varu ? pbsa::resident_sweep<l, false, true, true>                     \
                               : pbsa::resident_sweep<l, false, false, true>)                   \
                : varu ? (cached ? pbsa::resident_sweep<l, true, true> : pbsa::resident_sweep<l, false, true>) \
@@ -1122,7 +1128,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode;
             const bool timing = P.var_mode && !P.var_uniform;
             const bool varu = P.var_mode && P.var_uniform;
-            const int tab = (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
+            const bool tap = P.tapsa_packed && !P.var_mode;
+            const int tab = tap ? P.K : (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
             P.res_smem = 512 + (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;
             int max_smem = 0;
             CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
@@ -1142,6 +1149,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 slice = std::max<int64_t>(slice, indptr[hi] - indptr[lo]);
             }
             P.res_smem += 4 * (size_t)(per + 1 + slice);
+            if (tap) P.res_smem += 4 * (size_t)alpha * P.L * per;  // the ring slice
             if (timing) {
                 // two lanes per node when a CTA's slice still takes one pass of <= 16 warps
                 // (measured: G1 C2 sigma_nu 1.0 70 -> 63 ms; a second pass costs more: G22)
@@ -1170,7 +1178,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 if (!P.i0_dev.n) P.i0_dev.upload(P.i0, st);
                 ResidentTimingKernel rk = resident_timing_for(P.L, P.native);
                 CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
-            } else if ((plain || varu) && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
+            } else if ((plain || varu || tap) && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
                 // (the per-thread cut counter takes up to 32 nodes)
                 const int thr = (int)std::min<int64_t>(512, ((per + 31) / 32) * 32);
                 P.resident = true;
@@ -1178,7 +1186,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 P.res_threads = thr;
                 if (P.use_cache && P.phase_words < P.W) P.acache.alloc((size_t)P.W * P.chunks * 1024);
                 P.phase_words = P.W;
-                ResidentKernel rk = resident_kernel_for(P.L, P.use_cache, varu, P.native);
+                P.res_tapsa = tap;
+                ResidentKernel rk = resident_kernel_for(P.L, P.use_cache, varu, P.native, tap);
                 CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
                 if (varu && !P.i0_dev.n) P.i0_dev.upload(P.i0, st);
                 if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -1500,7 +1509,11 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            CK(cudaLaunchKernelEx(&cfg, resident_kernel_for(P.L, P.use_cache, P.var_mode, P.native), r));
+            if (P.res_tapsa) {
+                r.ring = P.ring.p;
+                r.alpha = (int)P.alpha;
+            }
+            CK(cudaLaunchKernelEx(&cfg, resident_kernel_for(P.L, P.use_cache, P.var_mode, P.native, P.res_tapsa), r));
             ++P.launches;
             P.sweep_launches = P.cycles;
             cur = 1;

@@ -1161,21 +1161,25 @@ struct ResidentArgs {
     // NATIVE: Philox draws (philox.cuh); thr then holds the 32-bit thresholds
     uint32_t rk[20];            // round keys of the native seed
     uint32_t ngroup;            // Philox trial group of word 0: (first trial) / 4
+    // TAPSA: the time-averaged rule; the CTA's slice of the bit-sliced ring
+    // lives in shared memory and is written back to ring at the end
+    uint32_t *ring;             // [W][alpha][L][n]
+    int alpha;
 };
 
 constexpr int kResidentExtraPlanes = 3;  // cut counters for up to 32 nodes per thread
 
-template <int L, bool CACHED, bool VARU = false, bool NATIVE = false>
+template <int L, bool CACHED, bool VARU = false, bool NATIVE = false, bool TAPSA = false>
 __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
     const int CS = (int)cluster.num_blocks();
     const int rank = (int)cluster.block_rank();
     const int w = (int)(blockIdx.x / CS);
-    constexpr bool NIB = L <= 4 && !VARU;
+    constexpr bool NIB = L <= 4 && !VARU && !TAPSA;
     extern __shared__ unsigned long long smem_u64[];
     uint2 *sthr = reinterpret_cast<uint2 *>((reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
-    const int tab_entries = VARU ? 0 : NIB ? (a.dmax + 1) * 16 : a.K;
+    const int tab_entries = VARU ? 0 : (NIB && !TAPSA) ? (a.dmax + 1) * 16 : a.K;
     uint2 *key = sthr + tab_entries;
     uint32_t *S0 = reinterpret_cast<uint32_t *>(key + 32);
     uint32_t *S1 = S0 + a.n;
@@ -1186,7 +1190,8 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
     const int lo = rank * per, hi = min(a.n, lo + per);
     // this CTA's nodes' CSR rows in shared memory too (a cluster barrier
     // flushes L1, which would otherwise re-fetch them from L2 every cycle)
-    uint32_t *rowS = S1 + a.n;                  // [hi - lo + 1], relative offsets
+    uint32_t *ringS = S1 + a.n;                 // TAPSA: [alpha][L][per] bit-sliced counts
+    uint32_t *rowS = ringS + (TAPSA ? a.alpha * L * per : 0);  // [hi - lo + 1], relative offsets
     uint32_t *adjS = rowS + (per + 1);          // [rowptr[hi] - rowptr[lo]]
     const uint32_t r0 = a.rowptr[lo], r1 = a.rowptr[hi];
     for (int k = tid; k <= hi - lo; k += blockDim.x) rowS[k] = a.rowptr[lo + k] - r0;
@@ -1200,6 +1205,13 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
         const uint64_t *thr = a.thr + (size_t)cc * a.K;
         __syncthreads();  // the previous cycle's table readers are done
         for (int k = tid; k < tab_entries; k += blockDim.x) {
+            if (TAPSA) {  // [acc + f dmax]: replay (~thi, thi) (packed_decide_y); native 2^32 - T
+                const uint64_t tfull = thr[k];
+                const uint32_t thi = (uint32_t)(tfull >> 32);
+                const uint64_t nt = (1ULL << 32) - tfull;
+                sthr[k] = NATIVE ? make_uint2((uint32_t)nt, (uint32_t)(nt >> 32)) : make_uint2(~thi, thi);
+                continue;
+            }
             int raw = k - a.dmax;
             bool ok = true;
             if (NIB) {
@@ -1302,6 +1314,87 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                 }
                 continue;
             }
+            if (TAPSA) {
+                // time-averaged rule (_kernels.py:131-138), as packed_sweep ALG=1:
+                // S = this cycle's count + the other filled ring slots (SP planes),
+                // thresholds indexed by acc + f dmax = 2 S + f (dmax - d)
+                constexpr int SP = L + 3;
+                constexpr int SB = SP < 8 ? SP : 8;
+                const int filled = min(c + 1, a.alpha), slot = c % a.alpha;
+                uint32_t S[SP];
+#pragma unroll
+                for (int r = 0; r < SP; ++r) S[r] = r < L ? p[r] : 0u;
+                uint32_t *rg = ringS + (i - lo);
+                for (int qs = 0; qs < filled; ++qs) {
+                    if (qs == slot) continue;
+                    uint32_t x[L];
+#pragma unroll
+                    for (int r = 0; r < L; ++r) x[r] = rg[(qs * L + r) * per];
+                    vc_add<L, SP>(S, x);
+                }
+#pragma unroll
+                for (int r = 0; r < L; ++r) rg[(slot * L + r) * per] = p[r];
+                uint32_t B[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    B[k] = 0;
+#pragma unroll
+                    for (int r = 0; r < SB; ++r) {
+                        const uint32_t x4 = (S[r] >> (4 * k)) & 0xFu;
+                        B[k] |= (x4 * (0x00204081u << r)) & (0x01010101u << r);
+                    }
+                }
+                const int off = filled * (a.dmax - d);
+                const uint32_t rb = (uint32_t)__cvta_generic_to_shared(sthr) + 8u * (uint32_t)off;
+                uint32_t word = 0, tie = 0xffffffffu;
+                uint32_t X[4];
+#pragma unroll
+                for (int b = 31; b >= 0; --b) {
+                    const int k = b >> 2, j = b & 3;
+                    uint32_t sv = (B[k] >> (8 * j)) & 0xFFu;
+#pragma unroll
+                    for (int r = 8; r < SP; ++r) sv |= ((S[r] >> b) & 1u) << r;
+                    const uint32_t addr = rb + (sv << 4);
+                    uint2 t;
+                    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "r"(addr));
+                    if (NATIVE) {
+                        if ((b & 3) == 3)
+                            philox4x32_10_rk(ui, count, grp + (uint32_t)(b >> 2), kNativeTagR, a.rk, X);
+                        native_decide(X[b & 3], t, word);
+                    } else if (CACHED) {
+                        const uint2 v = __ldcs(ctile + b * 32);
+                        tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
+                    } else {
+                        const uint2 kc = key[b];
+                        uint32_t sl, sh;
+                        packed_first_absorb(kc.x ^ ui, kc.y, sl, sh);
+                        tie = min(tie, packed_second_decide(sl, sh, count, t, word));
+                    }
+                }
+                if (!NATIVE && tie < 2) {  // rare near-tie: exact 64-bit test
+                    word = 0;
+                    for (int b = 0; b < 32; ++b) {
+                        int sb = 0;
+                        for (int r = 0; r < SP; ++r) sb |= (int)((S[r] >> b) & 1u) << r;
+                        const uint64_t x1 = (a.krg[(size_t)w * 32 + b]) ^ (uint64_t)ui;
+                        const uint64_t x2 = (mix64(x1) + PB_GAMMA) ^ (uint64_t)count;
+                        word |= (uint32_t)hash_ge_exact(x2, thr[2 * sb + off]) << b;
+                    }
+                }
+                ns[i] = word;
+                for (int r = 1; r < CS; ++r) {
+                    const int peer = rank + r < CS ? rank + r : rank + r - CS;
+                    *cluster.map_shared_rank(ns + i, peer) = word;
+                }
+                if (a.raw_out && c == a.cycles - 1) {  // acc = sum of the filled raw fields
+                    for (int b = 0; b < 32; ++b) {
+                        int sb = 0;
+                        for (int r = 0; r < SP; ++r) sb |= (int)((S[r] >> b) & 1u) << r;
+                        a.raw_out[(size_t)i * a.Tp + w * 32 + b] = (int16_t)(2 * sb - filled * d);
+                    }
+                }
+                continue;
+            }
             uint32_t word = 0, tie = 0xffffffffu;
             uint32_t N[4] = {0u, 0u, 0u, 0u};
             uint32_t rb = 0;
@@ -1380,6 +1473,13 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
             uint32_t *t = cs;
             cs = ns;
             ns = t;
+        }
+    }
+    if (TAPSA) {  // the ring slots written in the run, for the history output
+        const int slots = min(a.cycles, a.alpha);
+        for (int k = tid; k < slots * L * (hi - lo); k += blockDim.x) {
+            const int j = k % (hi - lo), qr = k / (hi - lo);
+            a.ring[((size_t)w * a.alpha * L + qr) * a.n + lo + j] = ringS[qr * per + j];
         }
     }
     for (int i = lo + tid; i < hi; i += blockDim.x) a.s_out[(size_t)w * a.n + i] = cs[i];

@@ -261,6 +261,39 @@ def test_packed_tapsa_matches_oracle(oracle, bench_graphs, name, alpha, cycles):
         assert np.array_equal(got[k], want[k]), k
 
 
+@pytest.mark.parametrize("name,alpha,trials,cycles,rng", [
+    ("G1", 4, 100, 80, "replay"), ("G22", 11, 40, 40, "replay"), ("G47", 2, 64, 50, "replay"),
+    ("G1", 8, 36, 60, "replay"), ("G1", 3, 40, 60, "philox"), ("G22", 4, 100, 40, "philox"),
+    ("G1", 4, 8, 3, "replay")])
+@pytest.mark.parametrize("resident", ["1", "0"])
+def test_tapsa_resident_cluster_kernel_matches_oracle(oracle, bench_graphs, monkeypatch, name,
+                                                      alpha, trials, cycles, rng, resident):
+    """TApSA on the resident cluster kernel (resident_sweep<TAPSA>: the CTA's
+    slice of the bit-sliced ring held in shared memory for the whole run,
+    written back for the history output) and, forced off, on the launched
+    packed sweep: both bit-identical to the oracle (cycles < alpha included)."""
+    monkeypatch.setenv("PBSA_RESIDENT", resident)
+    graph = bench_graphs(name)
+    model = maxcut_to_ising(graph)
+    sch = derive_schedule(model, cycles, 10)
+    seed = 0x5EED_0000_7777
+    keys = [streams.run_key(streams.trial_seed(0, k)) for k in range(trials)]
+    b = _native.Batch(model, sch, keys, graph=graph, algo_code=1, alpha=alpha,
+                      rng=rng, rng_seed=seed)
+    plan = _native.Plan(b)
+    info = plan.info()
+    assert info["kernel"] == ("resident" if resident == "1" else "packed"), info
+    plan.run()
+    got = plan.download()
+    plan.close()
+    extra = dict(rng="philox", rng_seed=seed) if rng == "philox" else {}
+    want = oracle.anneal_batch(model, sch, "tapsa", VariabilityProfile.ideal(model.n), keys,
+                               graph=graph, alpha=alpha, **extra)
+    for k in ("spins", "inputs", "hist", "counts", "i0_trace", "energy_trace", "cut_trace",
+              "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
+
+
 @pytest.mark.parametrize("name,sig,cycles,margin,force", [
     ("G81", (0.5, 0.0, 0.0), 120, None, None), ("G81", (0.0, 0.7, 0.0), 120, None, None),
     ("G55", (0.5, 0.5, 0.5), 60, None, None), ("G22", (1.0, 1.0, 0.0), 80, None, None),
