@@ -1136,8 +1136,10 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             // measured: small batches (<= 64 words) of small dense graphs (n <= 2500,
             // mean degree >= 8: G1, G47, G22) run 1.1-2.2x faster resident; sparse
             // or larger problems are faster with launched sweeps
-            bool want = (P.W <= 64 || (P.var_mode && !P.var_uniform && P.W <= 128)) && n <= 2500 &&
-                        nnz >= 8 * n;
+            // (TApSA: the launched sweep re-reads the ring every cycle; resident wins to
+            // 128 words: G1 x 4096 alpha 4 27.2 -> 20.5 ms, G47 18.2 -> 16.5, G22 even)
+            bool want = (P.W <= 64 || (P.var_mode && !P.var_uniform && P.W <= 128) ||
+                         (P.tapsa_packed && !P.var_mode && P.W <= 128)) && n <= 2500 && nnz >= 8 * n;
             if (const char *env = std::getenv("PBSA_RESIDENT")) want = env[0] == '1';
             int csz = 1;  // (measured: 8 for a handful of words, 4 beats 8 at 32 words)
             while (csz < (P.W <= 8 ? 8 : 4) && P.W * csz < sms) csz *= 2;
@@ -1178,6 +1180,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 if (!P.i0_dev.n) P.i0_dev.upload(P.i0, st);
                 ResidentTimingKernel rk = resident_timing_for(P.L, P.native);
                 CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
+                if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             } else if ((plain || varu || tap) && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
                 // (the per-thread cut counter takes up to 32 nodes)
                 const int thr = (int)std::min<int64_t>(512, ((per + 31) / 32) * 32);
@@ -2191,7 +2194,7 @@ int pbsa_plan_bytes(const pbsa_plan *P, int64_t *h2d_bytes, int64_t *d2h_bytes) 
                           P->del64.bytes_up + P->pplanes.bytes_up + P->vdivs.bytes_up +
                           P->kfs.bytes_up + P->kstg.bytes_up + P->vali.bytes_up + P->hi32.bytes_up +
                           P->alist.bytes_up + P->adesc.bytes_up + P->athr.bytes_up + P->i0_dev.bytes_up +
-                          P->ge_w32.bytes_up + P->me_w32.bytes_up;
+                          P->ge_w32.bytes_up + P->me_w32.bytes_up + P->prof16.bytes_up;
         const int64_t T = P->T, n = P->n, C = P->cycles;
         int64_t down = T * n + T * n * 8 + 2 * T * C * 8 + T * 8;  // spins, inputs, traces, best
         if (P->path == PBSA_PATH_GENERAL) {

@@ -261,6 +261,38 @@ def test_packed_tapsa_matches_oracle(oracle, bench_graphs, name, alpha, cycles):
         assert np.array_equal(got[k], want[k]), k
 
 
+@pytest.mark.parametrize("name,sig,trials,cycles,rng", [
+    ("G81", (1.0, 1.0, 1.0), 128, 50, "replay"), ("G55", (0.5, 0.5, 0.5), 96, 60, "replay"),
+    ("G60", (0.8, 0.2, 0.6), 64, 40, "replay"), ("G81", (0.5, 0.5, 0.5), 64, 40, "philox"),
+    ("G48", (0.0, 2.0, 0.5), 64, 40, "replay"), ("G81", (0.0, 0.0, 0.5), 64, 40, "replay")])
+def test_timing_kernel_wide_spreads_match_oracle(oracle, bench_graphs, name, sig, trials, cycles,
+                                                 rng):
+    """The launched timing-spread kernel (packed_sweep_timing, fp16 profile
+    pair with the slope-scaled prefilter margin) at wide spreads, replay and
+    Philox: bit-identical to the oracle."""
+    graph = bench_graphs(name)
+    model = maxcut_to_ising(graph)
+    sch = derive_schedule(model, cycles, 10)
+    seeds = [streams.trial_seed(21, k) for k in range(trials)]
+    profs = [sample_variability(VariabilityConfig(*sig), graph.n,
+                                np.random.default_rng(streams.profile_seed(s))) for s in seeds]
+    keys = [streams.run_key(s) for s in seeds]
+    seed = 0x0DDB_A11_5EED
+    b = _native.Batch(model, sch, keys, profile_rows=profile_rows(profs, model.n), graph=graph,
+                      rng=rng, rng_seed=seed)
+    plan = _native.Plan(b)
+    assert plan.info()["kernel"] == "packed_timing", plan.info()
+    up, _ = plan.transfer_bytes()
+    plan.run()
+    got = plan.download()
+    plan.close()
+    assert up >= trials * graph.n * 4   # the fp16 pairs are counted in the upload
+    extra = dict(rng="philox", rng_seed=seed) if rng == "philox" else {}
+    want = oracle.anneal_batch(model, sch, "psa", profs, keys, graph=graph, **extra)
+    for k in ("spins", "inputs", "counts", "i0_trace", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
+
+
 @pytest.mark.parametrize("name,alpha,trials,cycles,rng", [
     ("G1", 4, 100, 80, "replay"), ("G22", 11, 40, 40, "replay"), ("G47", 2, 64, 50, "replay"),
     ("G1", 8, 36, 60, "replay"), ("G1", 3, 40, 60, "philox"), ("G22", 4, 100, 40, "philox"),
