@@ -271,6 +271,7 @@ struct pbsa_plan {
     int64_t first_trial = 0;           // global index of trial 0 (Philox trial groups)
     bool spsa_packed = false;          // SPSA p>0 on the packed path (per-p-bit drive index)
     DevBuf<uint32_t> sidx;             // [W][32][n] drive index per p-bit
+    bool sidx_full = true;             // store every index (PBSA_SIDX_FULL=0: fresh ones only)
     DevBuf<uint32_t> thr_hi;           // [cycles][K] high words of the thresholds
     DevBuf<uint2> kfs;                 // [Tp] (F, C) of absorb(key, TAG_STALL) + GAMMA
     DevBuf<uint64_t> kstg;             // [Tp] absorb(key, TAG_STALL) + GAMMA
@@ -924,6 +925,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             // native: (X + 1/2) 2^-32 < p  <=>  X < S = ceil(p 2^32 - 1/2)   (exact in fp64)
             if (P.native) P.p_stall64 = (uint64_t)std::ceil(std::ldexp(p_stall, 32) - 0.5);
             P.sidx.alloc((size_t)P.W * 32 * n);
+            if (const char *env = std::getenv("PBSA_SIDX_FULL")) P.sidx_full = env[0] != '0';
             P.i0_dev.upload(P.i0, st);
         }
         if (P.tapsa_packed) {
@@ -1594,6 +1596,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                         a.p_stall64 = P.p_stall64;
                         a.cycle = (int)cc;
                         a.Kc = P.K;
+                        a.sidx_full = P.sidx_full ? 1 : 0;
                     }
                     if (P.tapsa_packed) {
                         a.ring = P.ring.p + (size_t)w0 * P.alpha * P.L * P.n;

@@ -143,6 +143,7 @@ struct PackedArgs {
     const uint64_t *thr_all;  // SpSA: [cycles][K] all thresholds
     uint64_t p_stall64;       // SpSA: stall iff H_stall < p_stall64 (~0: always)
     int cycle, Kc;            // SpSA: this cycle, entries per cycle
+    int sidx_full;            // SpSA: store every drive index (full sectors), not only fresh ones
     uint32_t *ring;           // TApSA: [W][alpha][L][n] bit-sliced neighbour counts
     int alpha, slot, filled;  // TApSA: ring length, this cycle's slot, min(c+1, alpha)
     // VAR (per-p-bit variability profile, plain rule)
@@ -822,11 +823,12 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 // groups of GS trials (native: 4, its stalled drives need both threshold words)
                 constexpr int GS = NATIVE ? 4 : 8;
                 for (int gq = 32 / GS - 1; gq >= 0; --gq) {
-                    uint32_t th[GS];
+                    uint32_t th[GS], keep[GS];
 #pragma unroll
                     for (int j = GS - 1; j >= 0; --j) {
                         const int b = gq * GS + j;
                         th[j] = ((stallw >> b) & 1u) ? sidx[(size_t)b * a.n] : 0u;
+                        keep[j] = th[j];
                     }
                     uint32_t tlo[GS];  // NATIVE: low words of 2^32 - T of the stalled drives
 #pragma unroll
@@ -849,12 +851,17 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
 #pragma unroll
                         for (int r = 0; r < L; ++r) pop |= (int)((p[r] >> b) & 1u) << r;
                         uint2 t;
+                        uint32_t nidx = keep[j];
                         if ((stallw >> b) & 1u) {
                             t = NATIVE ? make_uint2(tlo[j], th[j]) : make_uint2(~th[j], th[j]);
                         } else {
                             t = NIB ? sthr[d * 16 + pop] : sthr[2 * pop - d + a.dmax];
-                            sidx[(size_t)b * a.n] = (uint32_t)(base + 2 * pop);
+                            nidx = (uint32_t)(base + 2 * pop);
                         }
+                        // every lane stores (stalled p-bits their unchanged index): whole
+                        // sectors, no partial-sector read-modify-write in L2 / HBM
+                        if (a.sidx_full) sidx[(size_t)b * a.n] = nidx;
+                        else if (!((stallw >> b) & 1u)) sidx[(size_t)b * a.n] = nidx;
                         if (NATIVE) {
                             if ((b & 3) == 3)
                                 philox4x32_10_rk(ui, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
