@@ -1132,7 +1132,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             const bool varu = P.var_mode && P.var_uniform;
             const bool tap = P.tapsa_packed && !P.var_mode;
             const int tab = tap ? P.K : (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
-            P.res_smem = 512 + (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;
+            P.res_smem = 512 + 2 * (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;  // two tables
             int max_smem = 0;
             CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
             // measured: small batches (<= 64 words) of small dense graphs (n <= 2500,

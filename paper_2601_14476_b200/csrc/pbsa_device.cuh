@@ -1185,9 +1185,14 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
     const int w = (int)(blockIdx.x / CS);
     constexpr bool NIB = L <= 4 && !VARU && !TAPSA;
     extern __shared__ unsigned long long smem_u64[];
-    uint2 *sthr = reinterpret_cast<uint2 *>((reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
+    uint2 *sthrA = reinterpret_cast<uint2 *>((reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
     const int tab_entries = VARU ? 0 : (NIB && !TAPSA) ? (a.dmax + 1) * 16 : a.K;
-    uint2 *key = sthr + tab_entries;
+    // two threshold tables: cycle c reads one while cycle c + 1's entries, loaded
+    // at the start of cycle c, are written into the other (the table load's L2
+    // latency leaves the per-cycle critical path; (dmax + 1) 16 entries keep
+    // the second table 128-byte aligned for the NIB address trick)
+    uint2 *sthrB = sthrA + tab_entries;
+    uint2 *key = sthrB + tab_entries;
     uint32_t *S0 = reinterpret_cast<uint32_t *>(key + 32);
     uint32_t *S1 = S0 + a.n;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -1205,34 +1210,48 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
     for (uint32_t k = tid; k < r1 - r0; k += blockDim.x) adjS[k] = a.adj[r0 + k];
     uint32_t *cs = S0, *ns = S1;
     constexpr int CP = L + 2 + kResidentExtraPlanes;
+    // table entry k of a cycle: its source in the cycle's threshold row (-1: unused)
+    // and its shared-memory form
+    auto tab_src = [&](int k) -> int {
+        if (TAPSA) return k;  // [acc + f dmax]
+        if (NIB) {
+            const int d = k >> 4, pp = k & 15;
+            return pp <= d ? 2 * pp - d + a.dmax : -1;
+        }
+        return k;
+    };
+    auto tab_entry = [&](uint64_t tfull) -> uint2 {
+        const uint32_t thi = (uint32_t)(tfull >> 32);
+        if (TAPSA) {  // replay (~thi, thi) (packed_decide_y); native 2^32 - T
+            const uint64_t nt = (1ULL << 32) - tfull;
+            return NATIVE ? make_uint2((uint32_t)nt, (uint32_t)(nt >> 32)) : make_uint2(~thi, thi);
+        }
+        // replay: the 33-bit ~thi + 2 (packed_decide_n2); native: 2^32 - T
+        const uint64_t n2 = NATIVE ? (1ULL << 32) - tfull : (uint64_t)(~thi) + 2u;
+        return make_uint2((uint32_t)n2, (uint32_t)(n2 >> 32));
+    };
+    for (int k = tid; k < tab_entries; k += blockDim.x) {
+        const int sidx = tab_src(k);
+        sthrA[k] = tab_entry(sidx >= 0 ? a.thr[sidx] : 0ULL);
+    }
     cluster.sync();  // every CTA of the cluster runs before any shared-memory exchange
 
+    // next-cycle entries held in registers per thread (the rest load at the cycle's
+    // end; measured: the replayed plain rule is 4 % faster without the registers)
+    constexpr int kPre = VARU ? 0 : TAPSA ? 4 : NATIVE ? 2 : 0;
     for (int c = 0; c <= a.cycles; ++c) {
         const int cc = c < a.cycles ? c : a.cycles - 1;
         const uint64_t *thr = a.thr + (size_t)cc * a.K;
-        __syncthreads();  // the previous cycle's table readers are done
-        for (int k = tid; k < tab_entries; k += blockDim.x) {
-            if (TAPSA) {  // [acc + f dmax]: replay (~thi, thi) (packed_decide_y); native 2^32 - T
-                const uint64_t tfull = thr[k];
-                const uint32_t thi = (uint32_t)(tfull >> 32);
-                const uint64_t nt = (1ULL << 32) - tfull;
-                sthr[k] = NATIVE ? make_uint2((uint32_t)nt, (uint32_t)(nt >> 32)) : make_uint2(~thi, thi);
-                continue;
-            }
-            int raw = k - a.dmax;
-            bool ok = true;
-            if (NIB) {
-                const int d = k >> 4, pp = k & 15;
-                raw = 2 * pp - d;
-                ok = pp <= d;
-            }
-            const uint64_t tfull = ok ? thr[raw + a.dmax] : 0ULL;
-            const uint32_t thi = (uint32_t)(tfull >> 32);
-            // replay: the 33-bit ~thi + 2 (packed_decide_n2); native: 2^32 - T
-            const uint64_t n2 = NATIVE ? (1ULL << 32) - tfull : (uint64_t)(~thi) + 2u;
-            sthr[k] = make_uint2((uint32_t)n2, (uint32_t)(n2 >> 32));
+        uint2 *sthr = (c & 1) ? sthrB : sthrA;
+        uint2 *sthr_next = (c & 1) ? sthrA : sthrB;
+        const bool pre = c + 1 < a.cycles;
+        uint64_t pv[kPre > 0 ? kPre : 1];
+#pragma unroll
+        for (int j = 0; j < kPre; ++j) {
+            const int k = tid + j * (int)blockDim.x;
+            const int sidx = k < tab_entries ? tab_src(k) : -1;
+            pv[j] = (pre && sidx >= 0) ? __ldg(thr + a.K + sidx) : 0ULL;
         }
-        __syncthreads();
         const uint32_t count = (uint32_t)(c * a.t_res);
         const uint32_t grp = a.ngroup + 8u * (uint32_t)w;  // NATIVE: Philox group of trial 0
         uint32_t C[CP];
@@ -1475,8 +1494,19 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
             }
         }
         warp_cut_flush(C, dsum, lane, a.pacc + (size_t)c * a.Tp + (size_t)w * 32);
+        if (pre) {  // next cycle's table (its readers, cycle c - 1, passed the last barrier)
+#pragma unroll
+            for (int j = 0; j < kPre; ++j) {
+                const int k = tid + j * (int)blockDim.x;
+                if (k < tab_entries) sthr_next[k] = tab_entry(pv[j]);
+            }
+            for (int k = tid + kPre * (int)blockDim.x; k < tab_entries; k += blockDim.x) {
+                const int sidx = tab_src(k);
+                sthr_next[k] = tab_entry(sidx >= 0 ? thr[a.K + sidx] : 0ULL);
+            }
+        }
         if (c < a.cycles) {
-            cluster.sync();  // every copy of the next state is complete
+            cluster.sync();  // every copy of the next state (and table) is complete
             uint32_t *t = cs;
             cs = ns;
             ns = t;
