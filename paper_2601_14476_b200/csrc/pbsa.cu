@@ -1076,7 +1076,12 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.pipelined = g_oneshot && !many_launches && !P.var_mode && !P.tapsa_packed && !P.spsa_packed &&
                       !P.tapsa_hist_from_raw && P.W >= 16;
         if (const char *env = std::getenv("PBSA_PIPELINE")) P.pipelined = P.pipelined && env[0] != '0';
-        if (P.pipelined) P.phase_words = (P.W + 3) / 4;
+        // (up to four phases, but each phase at least two waves of word-warps:
+        // measured G81 x 512 one-shot, four phases of 4 words 36.6 ms)
+        if (P.pipelined) {
+            const int64_t fill = (2LL * sm_count * 32 + (n + 31) / 32 - 1) / ((n + 31) / 32);
+            P.phase_words = std::min<int64_t>(P.W, std::max<int64_t>((P.W + 3) / 4, fill));
+        }
         if (const char *env = std::getenv("PBSA_PACKED_PHASE_WORDS")) P.phase_words = std::atoi(env);
         if (const char *env = std::getenv("PBSA_PDL")) P.use_pdl = env[0] != '0';
         if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;
