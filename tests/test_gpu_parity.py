@@ -746,13 +746,14 @@ def test_with_and_without_graph_same_dynamics(bench_graphs):
             assert without.cut_trace is None and with_g.cut_trace is not None
 
 
-@pytest.mark.parametrize("trials", [600, 1000])
-def test_pipelined_one_shot_equals_graph_run(bench_graphs, monkeypatch, trials):
+@pytest.mark.parametrize("name,trials", [("G81", 600), ("G81", 1000), ("G81", 2600), ("G55", 3000)])
+def test_pipelined_one_shot_equals_graph_run(bench_graphs, monkeypatch, name, trials):
     """The one-shot call of the plain rule runs pipelined (word phases launched
     directly, each phase's outputs copied back while the next anneals); its
     eight outputs equal the captured-graph run of the same batch, including a
-    ragged last word (600 = 18.75 words)."""
-    g = bench_graphs("G81")
+    ragged last word (600 = 18.75 words) and ragged last phases (phases are at
+    least two waves of word-warps: G81 16 words, G55 61 words; at most four)."""
+    g = bench_graphs(name)
     model = maxcut_to_ising(g)
     sch = derive_schedule(model, 40, 10)
     keys = [streams.run_key(streams.trial_seed(0, k)) for k in range(trials)]
