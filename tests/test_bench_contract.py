@@ -39,3 +39,23 @@ def test_algorithmic_bytes_per_update_matches_survey():
     for name, want in (("G1", 52.25), ("G22", 22.44), ("G55", 6.46), ("G81", 5.39)):
         g = benchmarks.load(name)[0]
         assert bench.algorithmic_bytes_per_update(g) == pytest.approx(want, abs=0.01)
+
+
+def test_reference_arm_under_torchrun_prints_once_from_rank_zero(oracle):
+    """Under torchrun (N > 1) rank 0 alone runs the CPU reference and prints its
+    line; the other ranks exit 0 without work."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+         "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--cycles", "20",
+         "--cpu-sample-trials", "2"],
+        capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
