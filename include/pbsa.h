@@ -147,7 +147,8 @@ enum {
     PBSA_KERNEL_RESIDENT_TIMING = 4, /* resident_timing */
     PBSA_KERNEL_ACTIVE_FAST = 5,     /* general path: active lists, plain rule */
     PBSA_KERNEL_ACTIVE = 6,          /* general path: active lists, all rules */
-    PBSA_KERNEL_FULL = 7             /* general path: fp64 full pass */
+    PBSA_KERNEL_FULL = 7,            /* general path: fp64 full pass */
+    PBSA_KERNEL_PACKED_BUCKET = 8    /* packed_sweep_bucket (period spread, period-sorted slots) */
 };
 
 /*
@@ -155,6 +156,16 @@ enum {
  * the resident kernels (1 otherwise).  Diagnostic; results do not depend on it.
  */
 int pbsa_plan_kernel(const pbsa_plan *plan, int *kernel, int *cluster_size);
+
+/*
+ * Launch shape of a launched (non-resident) packed plan: word-phase width in
+ * words (phases run one after another; = words when unphased), concurrent
+ * word-group chains per phase, warps per trial word, and whether the
+ * per-(trial, node) first-absorb hash cache is used.  Diagnostic: the parity
+ * tests assert that they exercise the shape the benchmark times.
+ */
+int pbsa_plan_layout(const pbsa_plan *plan, int64_t *phase_words, int *chains,
+                     int *warps_per_word, int *hash_cache);
 
 /*
  * Bytes one end-to-end call moves: host->device at plan creation (CSR,

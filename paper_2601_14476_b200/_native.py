@@ -47,6 +47,8 @@ _SIGNATURES = [
                                       ctypes.POINTER(_F64), ctypes.POINTER(_I64),
                                       ctypes.POINTER(_I64)]),
     ("pbsa_plan_kernel", ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    ("pbsa_plan_layout", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(ctypes.c_int),
+                                        ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     ("pbsa_plan_bytes", ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("pbsa_plan_destroy", ctypes.c_int, [_P]),
     ("pbsa_anneal_loop_batch", ctypes.c_int,
@@ -73,18 +75,21 @@ EXPORTED = [name for name, _, _ in _SIGNATURES]
 
 # pbsa_plan_kernel codes (include/pbsa.h PBSA_KERNEL_*)
 KERNELS = {1: "packed", 2: "packed_timing", 3: "resident", 4: "resident_timing", 5: "active_fast",
-           6: "active", 7: "full"}
+           6: "active", 7: "full", 8: "packed_bucket"}
 
 
 def load() -> ctypes.CDLL:
     """Load libpbsa.so; raises RuntimeError (never falls back) if it is absent."""
     global _lib
     if _lib is None:
-        if not LIB_PATH.exists():
+        # PBSA_LIB: an alternative in-tree build of the same library (A/B
+        # experiments of compile-time variants, tools/); default the product build
+        path = Path(os.environ.get("PBSA_LIB") or LIB_PATH)
+        if not path.exists():
             raise RuntimeError(
-                f"CUDA library {LIB_PATH} is not built; run __graft_entry__.build() "
+                f"CUDA library {path} is not built; run __graft_entry__.build() "
                 "(there is no CPU fallback for the annealing sweep)")
-        lib = ctypes.CDLL(str(LIB_PATH))
+        lib = ctypes.CDLL(str(path))
         for name, res, args in _SIGNATURES:
             fn = getattr(lib, name)
             fn.restype = res
@@ -232,6 +237,14 @@ class Plan:
                     kernel=KERNELS.get(kern.value, "?"), cluster_size=cs.value,
                     launches=launches.value, sweep_ms_mean=ms.value,
                     sweep_launches=sweeps.value, words=words.value)
+
+    def layout(self) -> dict:
+        """Launch shape of a launched packed plan (pbsa_plan_layout)."""
+        pw, ch, wpw, cache = _I64(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _check(load().pbsa_plan_layout(self._h, ctypes.byref(pw), ctypes.byref(ch), ctypes.byref(wpw),
+                                       ctypes.byref(cache)))
+        return dict(phase_words=pw.value, chains=ch.value, warps_per_word=wpw.value,
+                    hash_cache=bool(cache.value))
 
     def transfer_bytes(self) -> tuple[int, int]:
         """(host->device bytes at creation, device->host bytes of a full download)."""

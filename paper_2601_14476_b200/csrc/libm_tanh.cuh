@@ -15,9 +15,11 @@
 //     Its fused multiply-adds were read off the shipped libm.so.6 and are
 //     reproduced with explicit fma(); every other operation is a single
 //     IEEE-rounded add/sub/mul/div with contraction disabled.
-// Parity: tests/test_libm_tanh.py compares pbsa_libm_tanh_host() (this code,
+// Parity: tests/test_native_abi.py::test_host_tanh_port_equals_libm compares
+// pbsa_libm_tanh_host() (this code,
 // compiled for the host) with the system tanh on millions of inputs, and the
-// GPU tests compare the device build against the same host values.
+// GPU tests (test_gpu_parity.py::test_device_tanh_matches_host_libm) compare
+// the device build against the same host values.
 #pragma once
 #include <stdint.h>
 #include <string.h>

@@ -24,7 +24,8 @@
 #include <vector>
 
 #include "../../include/pbsa.h"
-#include "pbsa_device.cuh"
+#include "aux_kernels.cuh"
+#include "dispatch.h"
 
 namespace {
 
@@ -154,10 +155,13 @@ struct DevBuf {
     }
     void upload(const std::vector<T> &v, cudaStream_t s) { upload(v.data(), v.size(), s); }
     void release() {
+        drop();
+        bytes_up = 0;
+    }
+    void drop() {  // free the memory early; keep the upload byte count for pbsa_plan_bytes
         if (p) cudaFreeAsync(p, st);
         p = nullptr;
         n = 0;
-        bytes_up = 0;
     }
     ~DevBuf() { release(); }
 };
@@ -307,6 +311,15 @@ struct pbsa_plan {
     int64_t pmax = 0;
     float var_margin = 1.0f;
     std::vector<uint8_t> pcl;          // [T][n] clamped periods (timing spread only)
+    // timing spread on the launched path: period buckets (packed_sweep_bucket)
+    bool bucket = false;
+    int nclass = 0;                    // distinct clamped periods present
+    int max_ndiv = 0;                  // most classes firing in one sub-step
+    DevBuf<uint8_t> bdivs;             // like vdivs, as class indices
+    DevBuf<uint2> brec;                // [W][chunks][kBucketTile] slot records (slot, fp16 profile pair)
+    DevBuf<uint16_t> boff;             // [W][chunks][nclass + 1] class starts
+    DevBuf<uint8_t> blut;              // [256] clamped period -> class
+    DevBuf<uint8_t> bcper;             // [nclass] class -> clamped period
     // packed launch sequence (one entry per sweep launch, the last one cut-only)
     struct PLaunch {
         uint32_t count;
@@ -367,6 +380,12 @@ struct pbsa_plan {
     int final_parity = 0;  // which spin buffer holds the final state
 
     ~pbsa_plan() {
+        // drain every stream first: after an error in a pipelined one-shot call
+        // the output stream may still be formatting and copying phase outputs
+        // into the caller's host buffers, reading buffers released below
+        if (out_stream) cudaStreamSynchronize(out_stream);
+        for (cudaStream_t cs : chain_streams) cudaStreamSynchronize(cs);
+        if (stream) cudaStreamSynchronize(stream);
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         for (cudaEvent_t e : {ev_start, ev_sweep0, ev_sweep1, ev_end, ev_fork})
             if (e) cudaEventDestroy(e);
@@ -397,164 +416,67 @@ void set_packed_smem(K kernel, size_t bytes) {
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-using PackedKernel = void (*)(pbsa::PackedArgs);
+using pbsa_dispatch::PackedKernel;
+using pbsa_dispatch::ResidentKernel;
+using pbsa_dispatch::ResidentTimingKernel;
+
+// The sweep kernels live in the per-L translation units (dispatch.h).
 PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false,
                                bool spsa = false, int var = 0, bool native = false) {
-    if (update && native && var) {  // Philox draws, per-p-bit profile (no first-absorb cache)
-        switch (L) {
-#define PBSA_NVCASE(l)                                                                \
-    case l:                                                                           \
-        return var == 2 ? pbsa::packed_sweep_timing<l, true> : pbsa::packed_sweep<l, true, false, 5>;
-            PBSA_NVCASE(1)
-            PBSA_NVCASE(2)
-            PBSA_NVCASE(3)
-            PBSA_NVCASE(4)
-            PBSA_NVCASE(5)
-            PBSA_NVCASE(6)
-            PBSA_NVCASE(7)
-#undef PBSA_NVCASE
-            default: fail(PBSA_EINVAL, "packed variability path supports degree <= 127");
-        }
-    }
-    if (update && native && (tapsa || spsa)) {  // Philox draws, TApSA / SpSA, ideal profile
-        switch (L) {
-#define PBSA_NRCASE(l)                                                                \
-    case l:                                                                           \
-        return tapsa ? pbsa::packed_sweep<l, true, false, 6> : pbsa::packed_sweep<l, true, false, 7>;
-            PBSA_NRCASE(1)
-            PBSA_NRCASE(2)
-            PBSA_NRCASE(3)
-            PBSA_NRCASE(4)
-            PBSA_NRCASE(5)
-            PBSA_NRCASE(6)
-            PBSA_NRCASE(7)
-#undef PBSA_NRCASE
-            default: fail(PBSA_EINVAL, "packed TApSA/SpSA support degree <= 127");
-        }
-    }
-    if (update && native) {  // Philox draws, plain rule, ideal profile (no first-absorb cache)
-        switch (L) {
-            case 1: return pbsa::packed_sweep<1, true, false, 4>;
-            case 2: return pbsa::packed_sweep<2, true, false, 4>;
-            case 3: return pbsa::packed_sweep<3, true, false, 4>;
-            case 4: return pbsa::packed_sweep<4, true, false, 4>;
-            case 5: return pbsa::packed_sweep<5, true, false, 4>;
-            case 6: return pbsa::packed_sweep<6, true, false, 4>;
-            case 7: return pbsa::packed_sweep<7, true, false, 4>;
-            default: fail(PBSA_EINVAL, "packed path supports degree <= 127");
-        }
-    }
-#define PBSA_VCASE(l)                                                                 \
-    case l:                                                                           \
-        return var == 2 ? pbsa::packed_sweep_timing<l>                                \
-                        : cached ? pbsa::packed_sweep<l, true, true, 3>               \
-                                 : pbsa::packed_sweep<l, true, false, 3>;
-    if (update && var) {
-        switch (L) {
-            PBSA_VCASE(1)
-            PBSA_VCASE(2)
-            PBSA_VCASE(3)
-            PBSA_VCASE(4)
-            PBSA_VCASE(5)
-            PBSA_VCASE(6)
-            PBSA_VCASE(7)
-            default: fail(PBSA_EINVAL, "packed variability path supports degree <= 127");
-        }
-    }
-#undef PBSA_VCASE
-#define PBSA_CASE(l)                                                                  \
-    case l:                                                                           \
-        return update ? (cached ? pbsa::packed_sweep<l, true, true>                   \
-                                : pbsa::packed_sweep<l, true, false>)                 \
-                      : pbsa::packed_sweep<l, false, false>;
-#define PBSA_TCASE(l)                                                                 \
-    case l:                                                                           \
-        return cached ? pbsa::packed_sweep<l, true, true, 1>                          \
-                      : pbsa::packed_sweep<l, true, false, 1>;
-#define PBSA_SCASE(l)                                                                 \
-    case l:                                                                           \
-        return cached ? pbsa::packed_sweep<l, true, true, 2>                          \
-                      : pbsa::packed_sweep<l, true, false, 2>;
-    if (update && tapsa) {
-        switch (L) {
-            PBSA_TCASE(1)
-            PBSA_TCASE(2)
-            PBSA_TCASE(3)
-            PBSA_TCASE(4)
-            PBSA_TCASE(5)
-            PBSA_TCASE(6)
-            PBSA_TCASE(7)
-            default: fail(PBSA_EINVAL, "packed TApSA supports degree <= 127");
-        }
-    }
-    if (update && spsa) {
-        switch (L) {
-            PBSA_SCASE(1)
-            PBSA_SCASE(2)
-            PBSA_SCASE(3)
-            PBSA_SCASE(4)
-            PBSA_SCASE(5)
-            PBSA_SCASE(6)
-            PBSA_SCASE(7)
-            default: fail(PBSA_EINVAL, "packed SpSA supports degree <= 127");
-        }
-    }
-#undef PBSA_SCASE
+#define PBSA_PK(l) packed_kernel<l>(update, cached, tapsa, spsa, var, native)
     switch (L) {
-        PBSA_CASE(1)
-        PBSA_CASE(2)
-        PBSA_CASE(3)
-        PBSA_CASE(4)
-        PBSA_CASE(5)
-        PBSA_CASE(6)
-        PBSA_CASE(7)
+        case 1: return pbsa_dispatch::PBSA_PK(1);
+        case 2: return pbsa_dispatch::PBSA_PK(2);
+        case 3: return pbsa_dispatch::PBSA_PK(3);
+        case 4: return pbsa_dispatch::PBSA_PK(4);
+        case 5: return pbsa_dispatch::PBSA_PK(5);
+        case 6: return pbsa_dispatch::PBSA_PK(6);
+        case 7: return pbsa_dispatch::PBSA_PK(7);
         default: fail(PBSA_EINVAL, "packed path supports degree <= 127");
     }
-#undef PBSA_CASE
-#undef PBSA_TCASE
+#undef PBSA_PK
 }
 
-using ResidentKernel = void (*)(pbsa::ResidentArgs);
-using ResidentTimingKernel = void (*)(pbsa::ResidentTimingArgs);
+PackedKernel bucket_kernel_for(int L, bool native) {
+    switch (L) {
+        case 1: return pbsa_dispatch::bucket_kernel<1>(native);
+        case 2: return pbsa_dispatch::bucket_kernel<2>(native);
+        case 3: return pbsa_dispatch::bucket_kernel<3>(native);
+        case 4: return pbsa_dispatch::bucket_kernel<4>(native);
+        case 5: return pbsa_dispatch::bucket_kernel<5>(native);
+        case 6: return pbsa_dispatch::bucket_kernel<6>(native);
+        case 7: return pbsa_dispatch::bucket_kernel<7>(native);
+        default: fail(PBSA_EINVAL, "packed variability path supports degree <= 127");
+    }
+}
+
 ResidentTimingKernel resident_timing_for(int L, bool native = false) {
     switch (L) {
-#define PBSA_RTCASE(l) \
-    case l: return native ? pbsa::resident_timing<l, true> : pbsa::resident_timing<l, false>;
-        PBSA_RTCASE(1)
-        PBSA_RTCASE(2)
-        PBSA_RTCASE(3)
-        PBSA_RTCASE(4)
-        PBSA_RTCASE(5)
-        PBSA_RTCASE(6)
-        PBSA_RTCASE(7)
-#undef PBSA_RTCASE
+        case 1: return pbsa_dispatch::resident_timing_kernel<1>(native);
+        case 2: return pbsa_dispatch::resident_timing_kernel<2>(native);
+        case 3: return pbsa_dispatch::resident_timing_kernel<3>(native);
+        case 4: return pbsa_dispatch::resident_timing_kernel<4>(native);
+        case 5: return pbsa_dispatch::resident_timing_kernel<5>(native);
+        case 6: return pbsa_dispatch::resident_timing_kernel<6>(native);
+        case 7: return pbsa_dispatch::resident_timing_kernel<7>(native);
         default: fail(PBSA_EINVAL, "resident sweep supports degree <= 127");
     }
 }
 
 ResidentKernel resident_kernel_for(int L, bool cached, bool varu = false, bool native = false,
                                    bool tapsa = false) {
+#define PBSA_RK(l) resident_kernel<l>(cached, varu, native, tapsa)
     switch (L) {
-#define PBSA_RCASE(l)                                                                          \
-    case l:                                                                                    \
-        if (tapsa)                                                                             \
-            return native ? pbsa::resident_sweep<l, false, false, true, true>                  \
-                          : (cached ? pbsa::resident_sweep<l, true, false, false, true>        \
-                                    : pbsa::resident_sweep<l, false, false, false, true>);     \
-        return native ? (varu ? pbsa::resident_sweep<l, false, true, true>                     \
-                              : pbsa::resident_sweep<l, false, false, true>)                   \
-               : varu ? (cached ? pbsa::resident_sweep<l, true, true> : pbsa::resident_sweep<l, false, true>) \
-                    : (cached ? pbsa::resident_sweep<l, true, false> : pbsa::resident_sweep<l, false, false>);
-        PBSA_RCASE(1)
-        PBSA_RCASE(2)
-        PBSA_RCASE(3)
-        PBSA_RCASE(4)
-        PBSA_RCASE(5)
-        PBSA_RCASE(6)
-        PBSA_RCASE(7)
-#undef PBSA_RCASE
+        case 1: return pbsa_dispatch::PBSA_RK(1);
+        case 2: return pbsa_dispatch::PBSA_RK(2);
+        case 3: return pbsa_dispatch::PBSA_RK(3);
+        case 4: return pbsa_dispatch::PBSA_RK(4);
+        case 5: return pbsa_dispatch::PBSA_RK(5);
+        case 6: return pbsa_dispatch::PBSA_RK(6);
+        case 7: return pbsa_dispatch::PBSA_RK(7);
         default: fail(PBSA_EINVAL, "resident sweep supports degree <= 127");
     }
+#undef PBSA_RK
 }
 
 template <int L>
@@ -1024,6 +946,14 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 P.pplanes.upload(planes, st);
                 std::vector<char> present(256, 0);
                 for (uint8_t pc : P.pcl) present[pc] = 1;  // (padding trials never matter)
+                std::vector<uint8_t> lut(256, 0), cdivs, cper;
+                for (int pc = 1; pc < 256; ++pc)
+                    if (present[pc]) {
+                        lut[pc] = (uint8_t)P.nclass++;
+                        cper.push_back((uint8_t)pc);
+                    }
+                P.blut.upload(lut, st);
+                P.bcper.upload(cper, st);
                 // ... or, with a timing spread, every sub-step some present period
                 // divides (the first sub-step of each cycle always runs: it takes the cut)
                 for (int64_t c = 0; c < cycles; ++c)
@@ -1031,15 +961,23 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                         const int64_t count = c * t_res + s;
                         const int64_t off = (int64_t)divs.size();
                         for (int64_t pc = 1; pc <= P.pmax; ++pc)
-                            if (present[pc] && count % pc == 0) divs.push_back((uint8_t)pc);
+                            if (present[pc] && count % pc == 0) {
+                                divs.push_back((uint8_t)pc);
+                                cdivs.push_back(lut[pc]);
+                            }
                         const int nd = (int)((int64_t)divs.size() - off);
                         if (nd > pbsa::kMaxDivisors) fail(PBSA_EINVAL, "too many dividing periods");
+                        P.max_ndiv = std::max(P.max_ndiv, nd);
                         if (s == 0 || nd > 0)
                             P.plaunch.push_back({(uint32_t)count, c, s == 0, nd, off, true,
                                                  count >= maxcount - P.pmax});
                     }
-                if (divs.empty()) divs.push_back(0);
+                if (divs.empty()) {
+                    divs.push_back(0);
+                    cdivs.push_back(0);
+                }
                 P.vdivs.upload(divs, st);
+                P.bdivs.upload(cdivs, st);
             }
         }
         P.plaunch.push_back({(uint32_t)(cycles * t_res), cycles, 1, 0, 0, false, false});
@@ -1204,6 +1142,29 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             }
         }
         if (P.resident) P.pipelined = false;
+        // timing spread on the launched path: sort every tile's slots into
+        // period buckets once (PBSA_BUCKET=0 keeps packed_sweep_timing)
+        if (many_launches && !P.resident && P.max_ndiv <= pbsa::kBucketMaxDiv) {
+            const char *benv = std::getenv("PBSA_BUCKET");
+            P.bucket = !benv || benv[0] != '0';
+        }
+        if (P.bucket) {
+            const size_t tiles = (size_t)P.W * P.chunks;
+            P.brec.alloc(tiles * pbsa::kBucketTile);
+            P.boff.alloc(tiles * (P.nclass + 1));
+            pbsa::bucket_build<<<grid_for((int64_t)tiles, 8), 256, 0, st>>>(
+                P.pplanes.p, P.nplanes, P.blut.p, P.prof16.p, (int)n, P.chunks, (int)P.W, P.nclass,
+                P.brec.p, P.boff.p);
+            CK(cudaGetLastError());
+            P.prof16.drop();   // (the slot-ordered copy replaces them)
+            P.pplanes.drop();
+            const PackedKernel bk = bucket_kernel_for(P.L, P.native);
+            set_packed_smem(bk, pbsa::bucket_smem_bytes(P.L));
+            int bocc = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bk, pbsa::kPackedThreads,
+                                                             pbsa::bucket_smem_bytes(P.L)));
+            (void)bocc;
+        }
         P.updates_per_run = (int64_t)n * trials * cycles;
         if (many_launches) {  // sum over p-bits of #{count < cycles t_res : period | count}
             int64_t ups = 0;
@@ -1412,8 +1373,9 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                                                    (int)P.n, (int)P.W);
         CK(cudaMemsetAsync(P.pacc.p, 0, P.pacc.n * sizeof(unsigned long long), st));
         P.launches += 1;
-        PackedKernel kern_up = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
-                                                 P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
+        PackedKernel kern_up = P.bucket ? bucket_kernel_for(P.L, P.native)
+                                        : packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
+                                                            P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16;
         CK(record_sweep_event(P, P.ev_sweep0, st));
@@ -1584,7 +1546,15 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                         a.lam64 = P.lam64.p + off;
                         a.del64 = P.del64.p + off;
                         a.pplanes = P.var_uniform ? nullptr : P.pplanes.p + (size_t)w0 * P.nplanes * P.n;
-                        a.divs = P.var_uniform ? nullptr : P.vdivs.p + pl.div_off;
+                        a.divs = P.var_uniform ? nullptr : (P.bucket ? P.bdivs.p : P.vdivs.p) + pl.div_off;
+                        if (P.bucket) {
+                            const size_t toff = (size_t)w0 * P.chunks;
+                            a.brec = P.brec.p + toff * pbsa::kBucketTile;
+                            a.boff = P.boff.p + toff * (P.nclass + 1);
+                            a.nclass = P.nclass;
+                            a.cper = P.bcper.p;
+                            a.maxcount = (uint32_t)(P.cycles * P.t_res);
+                        }
                         a.ndiv = pl.ndiv;
                         a.nplanes = P.nplanes;
                         a.i0 = P.i0[cc];
@@ -1615,7 +1585,9 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                         cudaLaunchConfig_t cfg{};
                         cfg.gridDim = dim3((unsigned)blocks);
                         cfg.blockDim = dim3(pbsa::kPackedThreads);
-                        cfg.dynamicSmemBytes = (pl.update && P.var_mode && !P.var_uniform) ? pbsa::kTimingSmem : smem;
+                        cfg.dynamicSmemBytes = (pl.update && P.var_mode && !P.var_uniform)
+                                                   ? (P.bucket ? pbsa::bucket_smem_bytes(P.L) : pbsa::kTimingSmem)
+                                                   : smem;
                         cfg.stream = cs;
                         cudaLaunchAttribute attr[1];
                         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1978,7 +1950,8 @@ int pbsa_plan_kernel(const pbsa_plan *P, int *kernel, int *cluster_size) {
         int k;
         if (P->path == PBSA_PATH_PACKED)
             k = P->resident ? (P->res_timing ? PBSA_KERNEL_RESIDENT_TIMING : PBSA_KERNEL_RESIDENT)
-                            : (P->var_mode && !P->var_uniform ? PBSA_KERNEL_PACKED_TIMING : PBSA_KERNEL_PACKED);
+                            : (P->var_mode && !P->var_uniform ? (P->bucket ? PBSA_KERNEL_PACKED_BUCKET : PBSA_KERNEL_PACKED_TIMING)
+                                                                : PBSA_KERNEL_PACKED);
         else
             k = P->active_mode ? (P->fast ? PBSA_KERNEL_ACTIVE_FAST : PBSA_KERNEL_ACTIVE) : PBSA_KERNEL_FULL;
         if (kernel) *kernel = k;
@@ -2188,6 +2161,17 @@ void download_impl(pbsa_plan *P, int8_t *spins, double *inputs, double *hist, in
 }  // namespace
 
 extern "C" {
+
+int pbsa_plan_layout(const pbsa_plan *P, int64_t *phase_words, int *chains, int *warps_per_word,
+                     int *hash_cache) {
+    return guarded([&] {
+        if (!P) fail(PBSA_EINVAL, "null plan");
+        if (phase_words) *phase_words = P->phase_words;
+        if (chains) *chains = (int)P->chain_streams.size() + 1;
+        if (warps_per_word) *warps_per_word = P->warps_per_word;
+        if (hash_cache) *hash_cache = P->use_cache ? 1 : 0;
+    });
+}
 
 int pbsa_plan_bytes(const pbsa_plan *P, int64_t *h2d_bytes, int64_t *d2h_bytes) {
     return guarded([&] {

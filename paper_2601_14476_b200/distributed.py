@@ -80,10 +80,20 @@ def run_trials_sharded(spec: ExperimentSpec, graphs: Mapping[str, MaxCutGraph],
     lo, hi = shard_range(spec.trials, rank, world)
     run = runner or default_runner
     t0 = time.perf_counter()
-    cuts, bests, energies, _ = run(spec, graph, lo, hi)
+    if hi > lo:
+        cuts, bests, energies, _ = run(spec, graph, lo, hi)
+    else:  # an empty shard (T < 4 W with 4-aligned edges) still joins the collectives
+        cuts, bests, energies = np.empty(0, np.int64), np.empty(0, np.int64), np.empty(0)
     secs = time.perf_counter() - t0
     if device is None:
-        device = "cuda" if dist.is_initialized() and dist.get_backend() == "nccl" else "cpu"
+        # NCCL: this rank's own GPU (the library's device ordinal, LOCAL_RANK
+        # under torchrun), not whatever torch's current device happens to be
+        if dist.is_initialized() and dist.get_backend() == "nccl":
+            from . import _native
+            device = f"cuda:{_native.default_device()}"
+            torch.cuda.set_device(device)
+        else:
+            device = "cpu"
 
     # integer sums are exact; energies are integers for MAX-CUT models, so the
     # doubled energy sum is exact in int64 as well

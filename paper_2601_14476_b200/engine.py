@@ -157,8 +157,11 @@ def sweep(spec: ExperimentSpec, axis: str, values: Sequence[float],
     # of len(points) * trials trials (same seeds per point, so the sweep stays
     # paired exactly as in the reference).  The ideal point, if any, runs alone
     # on the packed path.
+    # (replay stream only: the native Philox stream is indexed by global trial,
+    # so batching would give point j the counters of trials j*T.., breaking the
+    # pairing; Philox points run one by one)
     grouped = [k for k, s in enumerate(specs)
-               if not s.variability.is_ideal and s.resample_variability]
+               if not s.variability.is_ideal and s.resample_variability and s.rng == "replay"]
     for k, s in enumerate(specs):
         if k not in grouped:
             out[k] = run_trials(s, graphs, registry)

@@ -35,12 +35,17 @@ def _fill(cfg, n, seeds, lam, delta, period, lo, hi):
         lam[k], delta[k], period[k] = p.lam, p.delta, p.period
 
 
-_SHARED = {}
+_CHILD = {}  # set in each forked worker by _init; the parent never touches it
+
+
+def _init(state):
+    _CHILD.clear()
+    _CHILD.update(state)
 
 
 def _worker(args):
     lo, hi = args
-    s = _SHARED
+    s = _CHILD
     _fill(s["cfg"], s["n"], s["seeds"], s["lam"], s["delta"], s["period"], lo, hi)
     return hi - lo
 
@@ -61,15 +66,15 @@ def sample_profiles(cfg: VariabilityConfig, n: int, seeds, workers: int | None =
     lam = np.frombuffer(bufs[0], dtype=np.float64).reshape(T, n)
     delta = np.frombuffer(bufs[1], dtype=np.float64).reshape(T, n)
     period = np.frombuffer(bufs[2], dtype=np.int64).reshape(T, n)
-    _SHARED.update(cfg=cfg, n=n, seeds=list(seeds), lam=lam, delta=delta, period=period)
-    try:
-        step = (T + workers * 4 - 1) // (workers * 4)
-        chunks = [(lo, min(T, lo + step)) for lo in range(0, T, step)]
-        with mp.get_context("fork").Pool(workers) as pool:
-            done = sum(pool.map(_worker, chunks))
-        if done != T:
-            raise RuntimeError("profile workers did not cover every trial")
-        # the arrays keep their mappings alive (np.frombuffer holds a reference)
-        return lam, delta, period
-    finally:
-        _SHARED.clear()
+    # each call hands its own buffers to its own pool through the initializer
+    # (forked children inherit the arguments; nothing module-global is shared
+    # between concurrent calls, e.g. run_trials_devices' per-device threads)
+    state = dict(cfg=cfg, n=n, seeds=list(seeds), lam=lam, delta=delta, period=period)
+    step = (T + workers * 4 - 1) // (workers * 4)
+    chunks = [(lo, min(T, lo + step)) for lo in range(0, T, step)]
+    with mp.get_context("fork").Pool(workers, initializer=_init, initargs=(state,)) as pool:
+        done = sum(pool.map(_worker, chunks))
+    if done != T:
+        raise RuntimeError("profile workers did not cover every trial")
+    # the arrays keep their mappings alive (np.frombuffer holds a reference)
+    return lam, delta, period

@@ -68,3 +68,9 @@ def bench_graphs():
             cache[name] = benchmarks.load(name)[0]
         return cache[name]
     return get
+
+
+@pytest.fixture(scope="session")
+def golden_full():
+    """Per-trial digests of whole benchmark batches (make_fullbatch.py, oracle)."""
+    return dict(np.load(GOLDEN / "fullbatch.npz"))

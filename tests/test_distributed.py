@@ -28,6 +28,9 @@ def _free_port() -> int:
 
 
 def oracle_runner(spec, graph, lo, hi):
+    # an empty shard must not reach the runner (the C ABI rejects 0 trials);
+    # with 7 trials over 2 ranks rank 0's 4-aligned shard is empty
+    assert hi > lo, (lo, hi)
     from oracle import oracle as orc
     from paper_2601_14476_b200 import streams
     from paper_2601_14476_b200.annealer import derive_schedule

@@ -218,6 +218,22 @@ def test_batched_sweep_is_paired_with_single_runs():
         assert s.normalized_mean_cut == alone.normalized_mean_cut
 
 
+def test_philox_sweep_is_paired_with_single_runs(bench_graphs):
+    """A native-stream sweep: every point equals its standalone run_trials (the
+    Philox stream is indexed by global trial, so points are not batched)."""
+    g = bench_graphs("G22")
+    spec = engine.ExperimentSpec(graph="G22", algo=AlgorithmConfig(Algorithm.PSA), cycles=60,
+                                 trials=40, rng="philox")
+    values = [0.3, 0.6]
+    sums = engine.sweep(spec, "sigma_nu", values, {"G22": g})
+    for v, s in zip(values, sums):
+        alone = engine.run_trials(dataclasses.replace(
+            spec, variability=VariabilityConfig(sigma_nu=v)), {"G22": g})
+        for a, b in zip(s.results, alone.results):
+            assert np.array_equal(a.final_state.spins, b.final_state.spins)
+            assert np.array_equal(a.cut_trace, b.cut_trace)
+
+
 @pytest.mark.parametrize("name,p_stall,cycles", [("G81", 0.5, 150), ("G55", 0.3, 120),
                                                   ("G48", 1.0, 60), ("G22", 0.7, 80)])
 def test_packed_spsa_matches_oracle(oracle, bench_graphs, name, p_stall, cycles):
@@ -261,15 +277,21 @@ def test_packed_tapsa_matches_oracle(oracle, bench_graphs, name, alpha, cycles):
         assert np.array_equal(got[k], want[k]), k
 
 
+@pytest.mark.parametrize("bucket", ["1", "0"])
 @pytest.mark.parametrize("name,sig,trials,cycles,rng", [
     ("G81", (1.0, 1.0, 1.0), 128, 50, "replay"), ("G55", (0.5, 0.5, 0.5), 96, 60, "replay"),
     ("G60", (0.8, 0.2, 0.6), 64, 40, "replay"), ("G81", (0.5, 0.5, 0.5), 64, 40, "philox"),
-    ("G48", (0.0, 2.0, 0.5), 64, 40, "replay"), ("G81", (0.0, 0.0, 0.5), 64, 40, "replay")])
-def test_timing_kernel_wide_spreads_match_oracle(oracle, bench_graphs, name, sig, trials, cycles,
-                                                 rng):
-    """The launched timing-spread kernel (packed_sweep_timing, fp16 profile
-    pair with the slope-scaled prefilter margin) at wide spreads, replay and
-    Philox: bit-identical to the oracle."""
+    ("G48", (0.0, 2.0, 0.5), 64, 40, "replay"), ("G81", (0.0, 0.0, 0.5), 64, 40, "replay"),
+    ("G1", (0.0, 0.0, 3.0), 45, 30, "replay"), ("G22", (0.5, 0.5, 2.0), 100, 30, "philox")])
+def test_timing_kernel_wide_spreads_match_oracle(oracle, bench_graphs, monkeypatch, name, sig, trials,
+                                                 cycles, rng, bucket):
+    """The launched timing-spread kernels at wide spreads, replay and Philox:
+    packed_sweep_bucket (period-sorted slots, the default) and, with
+    PBSA_BUCKET=0, packed_sweep_timing (bit-sliced periods), both with the fp16
+    profile pair and the slope-scaled prefilter margin; bit-identical to the
+    oracle (sigma_nu 2-3: dozens of period classes, many dividing per sub-step)."""
+    monkeypatch.setenv("PBSA_BUCKET", bucket)
+    monkeypatch.setenv("PBSA_RESIDENT", "0")
     graph = bench_graphs(name)
     model = maxcut_to_ising(graph)
     sch = derive_schedule(model, cycles, 10)
@@ -281,7 +303,7 @@ def test_timing_kernel_wide_spreads_match_oracle(oracle, bench_graphs, name, sig
     b = _native.Batch(model, sch, keys, profile_rows=profile_rows(profs, model.n), graph=graph,
                       rng=rng, rng_seed=seed)
     plan = _native.Plan(b)
-    assert plan.info()["kernel"] == "packed_timing", plan.info()
+    assert plan.info()["kernel"] == ("packed_bucket" if bucket == "1" else "packed_timing"), plan.info()
     up, _ = plan.transfer_bytes()
     plan.run()
     got = plan.download()
@@ -780,3 +802,114 @@ def test_device_list_fan_out_equals_single_call(bench_graphs):
         assert np.array_equal(a.final_state.spins, b.final_state.spins)
         assert np.array_equal(a.cut_trace, b.cut_trace)
     assert one.mean_cut == two.mean_cut and one.std_cut == two.std_cut
+
+
+# ------------------------------------ whole batches at the configured launch shapes
+
+def _digest(spins, inputs, cut_trace, counts, best):
+    import zlib
+    T = spins.shape[0]
+    return {"final_cut": cut_trace[:, -1].astype(np.int64),
+            "best": np.asarray(best, np.int64),
+            "cut_sum": cut_trace.sum(axis=1).astype(np.int64),
+            "counts_sum": counts.sum(axis=1).astype(np.int64),
+            "spins_crc": np.array([zlib.crc32(np.ascontiguousarray(spins[t]).tobytes())
+                                   for t in range(T)], np.uint32),
+            "inputs_crc": np.array([zlib.crc32(np.ascontiguousarray(inputs[t]).tobytes())
+                                    for t in range(T)], np.uint32)}
+
+
+def _check_digest(golden_full, tag, got):
+    for k, v in got.items():
+        want = golden_full[f"{tag}_{k}"]
+        bad = np.flatnonzero(v != want)
+        assert bad.size == 0, (tag, k, bad[:8])
+
+
+def test_full_batch_bench_plan_matches_oracle(bench_graphs, golden_full, golden_bench):
+    """The exact plan bench.py times (BASELINE C4: G81 x 4096 x 1000, replayed
+    stream): word phases of 13 words in concurrent chains with the per-phase
+    first-absorb cache, replayed as one CUDA graph.  Every trial's final cut,
+    best cut, cut-trace sum, update count, final spins and inputs equal the
+    oracle's (tests/golden/fullbatch.npz); the recorded reference trials match
+    the reference's own outputs; the aggregate is the bench's quality line."""
+    from paper_2601_14476_b200 import streams as st
+    g = bench_graphs("G81")
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 1000, 10)
+    b = _native.Batch(model, sch, st.run_keys(st.trial_seeds(0, 4096)), graph=g)
+    plan = _native.Plan(b)
+    lay = plan.layout()
+    assert plan.info()["kernel"] == "packed"
+    assert 0 < lay["phase_words"] < 128 and lay["chains"] > 1 and lay["hash_cache"], lay
+    plan.run()
+    cut_sum, best, updates = plan.summary()
+    out = plan.download()
+    plan.close()
+    assert (cut_sum, best, updates) == (598190, 2164, 4096 * 20000 * 1000)
+    _check_digest(golden_full, "c4_g81", _digest(out["spins"], out["inputs"], out["cut_trace"],
+                                                  out["counts"], out["best_cut"]))
+    for k in (0, 1, 2047, 4095):
+        assert np.array_equal(out["spins"][k], golden_bench[f"g81_psa_s0_{k}_spins"])
+        assert np.array_equal(out["cut_trace"][k], golden_bench[f"g81_psa_s0_{k}_cut"])
+
+
+def test_full_batch_one_shot_call_matches_oracle(bench_graphs, golden_full):
+    """The same batch through the one-shot C-ABI call (what run_trials and the
+    bench's e2e leg use: pipelined word phases, outputs copied per phase)."""
+    from paper_2601_14476_b200 import streams as st
+    g = bench_graphs("G81")
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 1000, 10)
+    b = _native.Batch(model, sch, st.run_keys(st.trial_seeds(0, 4096)), graph=g)
+    out, _ = _native.anneal_batch(b)
+    _check_digest(golden_full, "c4_g81", _digest(out["spins"], out["inputs"], out["cut_trace"],
+                                                  out["counts"], out["best_cut"]))
+
+
+@pytest.mark.parametrize("tag,name,sig,trials,env,kernel", [
+    ("c3_g22", "G22", (0.5, 0.5, 0.5), 4096, {}, "resident_timing"),
+    ("c3_g22", "G22", (0.5, 0.5, 0.5), 4096, {"PBSA_RESIDENT": "0"}, "packed_bucket"),
+    ("c3_g55", "G55", (0.5, 0.5, 0.5), 4096, {}, "packed_bucket"),
+    ("c3_g55", "G55", (0.5, 0.5, 0.5), 4096, {"PBSA_BUCKET": "0"}, "packed_timing"),
+    ("c2_g1_nu1", "G1", (0.0, 0.0, 1.0), 1024, {}, "resident_timing"),
+    ("c2_g1_nu1", "G1", (0.0, 0.0, 1.0), 1024, {"PBSA_RESIDENT": "0"}, "packed_bucket")])
+def test_full_batch_variability_configs_match_oracle(bench_graphs, golden_full, golden_bench,
+                                                     monkeypatch, tag, name, sig, trials, env,
+                                                     kernel):
+    """BASELINE C3 (G22 / G55 x 4096, sigma = 0.5^3) and C2's sigma_nu = 1 row
+    (G1 x 1024) through engine.run_trials -- the reference's own entry point,
+    per-trial seeds and profiles as /root/reference/pkg/src/pbitsa/engine.py:101-116
+    -- on the kernel each config runs by default and on the alternative one:
+    every trial equals the oracle's, and the trials the reference recorded
+    (1024, 4095) equal the reference's outputs."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = bench_graphs(name)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 1000, 10)
+    cfg = VariabilityConfig(*sig)
+    from paper_2601_14476_b200 import streams as st
+    seeds = st.trial_seeds(0, trials)
+    from paper_2601_14476_b200.profiles import sample_profiles
+    lam, delta, period = sample_profiles(cfg, model.n, seeds)
+    b = _native.Batch(model, sch, st.run_keys(seeds), profile_rows=(lam, delta, period, model.n),
+                      graph=g)
+    plan = _native.Plan(b)
+    assert plan.info()["kernel"] == kernel, plan.info()
+    plan.close()
+    spec = engine.ExperimentSpec(graph=name, algo=AlgorithmConfig(Algorithm.PSA),
+                                 variability=cfg, cycles=1000, trials=trials)
+    s = engine.run_trials(spec, {name: g})
+    rs = s.results
+    _check_digest(golden_full, tag, _digest(
+        np.stack([r.final_state.spins for r in rs]), np.stack([r.final_state.inputs for r in rs]),
+        np.stack([r.cut_trace for r in rs]), np.stack([r.update_counts for r in rs]),
+        [r.best_cut for r in rs]))
+    bench_tag = {"c3_g22": "g22_psa_s5", "c3_g55": "g55_psa_s5"}.get(tag)
+    if bench_tag:
+        for k in (1024, 4095):
+            p = f"{bench_tag}_{k}_"
+            assert np.array_equal(rs[k].final_state.spins, golden_bench[p + "spins"]), p
+            assert np.array_equal(rs[k].cut_trace, golden_bench[p + "cut"]), p
+            assert np.array_equal(rs[k].final_state.inputs, golden_bench[p + "inputs"]), p

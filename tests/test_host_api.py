@@ -219,3 +219,25 @@ def test_spec_summary_and_sweep_validation():
         pb.sweep(spec, "cycles", [1.0], {})
     with pytest.raises(KeyError, match="unknown graph"):
         pb.run_trials(spec, {})
+
+
+def test_parallel_profile_sampling_is_reentrant():
+    """Concurrent sample_profiles calls (run_trials_devices runs one per device
+    thread) each fill their own buffers: identical to sequential calls and to
+    the reference's one-trial-at-a-time draws (engine.py:107-112)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2601_14476_b200 import streams
+    from paper_2601_14476_b200.pbit import VariabilityConfig, sample_variability
+    from paper_2601_14476_b200.profiles import sample_profiles
+    cfg = VariabilityConfig(0.5, 0.5, 0.5)
+    seed_sets = [streams.trial_seeds(b, 900) for b in (0, 5, 9)]
+    seq = [sample_profiles(cfg, 5000, s) for s in seed_sets]
+    with ThreadPoolExecutor(3) as ex:
+        par = list(ex.map(lambda s: sample_profiles(cfg, 5000, s), seed_sets))
+    for a, b in zip(seq, par):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+    for k in (0, 899):
+        p = sample_variability(cfg, 5000, np.random.default_rng(streams.profile_seed(seed_sets[1][k])))
+        assert np.array_equal(par[1][0][k], p.lam) and np.array_equal(par[1][2][k], p.period)
