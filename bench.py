@@ -5,17 +5,24 @@ plain pSA, ideal devices (sigma = 0), 4096 trials x 1000 cycles x t_res 10,
 trials sharded over the N ranks (one process per GPU).  One "step" is one
 whole anneal of the batch (init + 1000 sweep launches + the final cut pass +
 trace finalisation, replayed as one CUDA graph) followed by the end-of-run
-NCCL reduce of the final-cut sum and best cut.
+NCCL all_reduce of the final-cut sum, update count and best cut -- the step
+is timed with CUDA events on the launching stream around both.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...
+
+`--gpus N` (N > 1) outside torchrun re-launches itself under
+torch.distributed.run with N ranks (it fails if fewer than N GPUs are
+visible); under torchrun WORLD_SIZE must equal N.
 
 Prints ONE JSON line on rank 0.  `value` is measured with inputs resident in
-HBM (CUDA events around each step on the plan stream, L2 flushed between
-steps, max over ranks); `e2e` times the public C-ABI call
-pbsa_anneal_loop_batch with host buffers (uploads, run, full download of all
-eight outputs).  `--impl reference` times the reference algorithm on the
-host cores instead (the C restatement in oracle/, all threads).
+HBM (L2 flushed between steps, max over ranks); `e2e` times the public C-ABI
+call pbsa_anneal_loop_batch with host buffers (uploads, run, full download of
+all eight outputs).  Extra legs on the same line: `philox` (the native stream
+on the same workload) and `variability` (BASELINE C3: G55 x 4096, sigma =
+0.5^3, replayed stream, the period-bucket kernel) with its own roofline.
+`--impl reference` times the reference algorithm on the host cores instead
+(the C restatement in oracle/, all threads); `cpu_baseline` additionally
+carries the reference package itself (numba, baseline/_ref) when installed.
 """
 
 from __future__ import annotations
@@ -61,6 +68,10 @@ def parse():
                     help="skip the extra native-Philox measurement reported under 'philox'")
     ap.add_argument("--cpu-sample-trials", type=int, default=0,
                     help="trials in the CPU baseline sample (default 8 per thread)")
+    ap.add_argument("--no-var-leg", action="store_true",
+                    help="skip the BASELINE C3 variability leg (G55 x 4096, sigma = 0.5^3)")
+    ap.add_argument("--no-ref-numba", action="store_true",
+                    help="skip timing the reference package itself (numba) in cpu_baseline")
     return ap.parse_args()
 
 
@@ -176,6 +187,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    world = max(world, args.gpus)
     graph, real, model, sch = workload(args.graph, args.cycles)
     threads = cpu_threads()
     sample = args.cpu_sample_trials or threads
@@ -221,29 +233,6 @@ def algorithmic_bytes_per_update(graph):
     return nnz / n + 1 + (2.125 * nnz + 4 * (n + 1)) / (32 * n)
 
 
-def alu_ceiling(n, trials, cycles, local, flush):
-    """Measured instruction ceiling of the sweep (SURVEY 8(d) "measure it with
-    an RNG-only kernel"): the same packed kernel, launch shape and schedule on
-    an edgeless graph of the same n and trials, so only the per-update draw,
-    threshold lookup and decision remain.  Returns updates/s."""
-    import torch
-    from paper_2601_14476_b200.annealer import AnnealSchedule
-    from paper_2601_14476_b200.model import IsingModel
-    model = IsingModel.from_edges(n, [], h=np.zeros(n))
-    sch = AnnealSchedule(i0_min=0.05, i0_max=5.0, beta=0.01 ** (1.0 / (cycles - 1)), cycles=cycles,
-                         t_res=10)
-    b = _native.Batch(model, sch, streams.run_keys(streams.trial_seeds(7, trials)))
-    plan = _native.Plan(b, device=local)
-    best = 0.0
-    for _ in range(3):
-        flush.zero_()
-        torch.cuda.synchronize()
-        plan.run()
-        best = max(best, trials * n * cycles / (plan.info()["sweep_ms_mean"] * cycles * 1e-3))
-    plan.close()
-    return best
-
-
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -252,21 +241,153 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def issue_model():
+    """Warp instructions per update of the headline sweep kernel, measured by
+    ncu (profiles/sweep_issue.json, written by tools/profile_r02.sh)."""
+    p = ROOT / "profiles" / "sweep_issue.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except (ValueError, OSError):
+            return None
+    return None
+
+
+def reference_numba_sample(name, cycles, trials, threads):
+    """The reference package itself (pbitsa, numba, installed into
+    baseline/_ref): engine.run_trials with `threads` threads on the first
+    `trials` trials (same seeds as the GPU batch).  Returns (updates/s,
+    seconds) or None when the package is not installed."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "pbitsa").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/pbsa_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.append(str(ref))
+    try:
+        from pbitsa import engine as reng
+        from pbitsa.model import MaxCutGraph as RGraph
+        from pbitsa.annealer import AlgorithmConfig as RAlgo, Algorithm as RKind
+    except Exception:
+        return None
+    g = benchmarks.load(name)[0]
+    rg = RGraph(n=g.n, edge_i=np.asarray(g.edge_i), edge_j=np.asarray(g.edge_j),
+                edge_w=np.asarray(g.edge_w))
+    spec = reng.ExperimentSpec(graph=name, algo=RAlgo(RKind.PSA), cycles=cycles, trials=trials,
+                               threads=threads)
+    reng.run_trials(reng.ExperimentSpec(graph=name, algo=RAlgo(RKind.PSA), cycles=2, trials=1),
+                    {name: rg})  # JIT warm-up (numba compile), untimed
+    s = reng.run_trials(spec, {name: rg})
+    updates = sum(int(np.asarray(r.update_counts).sum()) for r in s.results)
+    return updates / s.anneal_seconds, s.anneal_seconds
+
+
+def relaunch_under_torchrun(args):
+    """--gpus N (N > 1) without a torchrun environment: one rank per GPU."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+              file=sys.stderr)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve())] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def variability_leg(args, local, world, rank, flush, barrier):
+    """BASELINE C3's variability workload on the same ranks: G55 x 4096
+    trials x 1000 cycles, sigma = (0.5, 0.5, 0.5), replayed stream (the
+    period-bucket kernel).  Device time per run (events on the plan stream),
+    max over ranks; updates = sum of the update counts."""
+    import torch
+
+    from paper_2601_14476_b200.annealer import profile_rows
+    from paper_2601_14476_b200.engine import ExperimentSpec, trial_profiles
+    from paper_2601_14476_b200.annealer import Algorithm, AlgorithmConfig
+    from paper_2601_14476_b200.pbit import VariabilityConfig
+    name, trials, sig = "G55", 4096, (0.5, 0.5, 0.5)
+    graph, real, model, sch = workload(name, args.cycles)
+    lo, hi = shard(trials, rank, world)
+    seeds = streams.trial_seeds(0, hi)[lo:hi]
+    spec = ExperimentSpec(graph=name, algo=AlgorithmConfig(Algorithm.PSA),
+                          variability=VariabilityConfig(*sig), cycles=args.cycles, trials=trials)
+    profs = trial_profiles(spec, model.n, seeds)
+    b = _native.Batch(model, sch, streams.run_keys(seeds), profile_rows=profile_rows(profs, model.n),
+                      graph=graph, first_trial=lo)
+    plan = _native.Plan(b, device=local)
+    for _ in range(args.warmup):
+        flush.zero_()
+        plan.run()
+    barrier()
+    ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ms += plan.run()
+    barrier()
+    cut_sum, best, updates = plan.summary()
+    info = plan.info()
+    launch_ms = info["sweep_ms_mean"]
+    sweeps = info["sweep_launches"]
+    plan.close()
+    step_ms = ms / args.steps
+    v = torch.tensor([step_ms, cut_sum, best, updates], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        mx = v[:1].clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        sm = v[1:2].clone()
+        torch.distributed.all_reduce(sm)
+        bm = v[2:3].clone()
+        torch.distributed.all_reduce(bm, op=torch.distributed.ReduceOp.MAX)
+        up = v[3:4].clone()
+        torch.distributed.all_reduce(up)
+        step_ms, cut_sum, best, updates = float(mx), float(sm), float(bm), float(up)
+    B = algorithmic_bytes_per_update(graph) + 4.0   # + the fired p-bit's fp16 (lam, lam delta)
+    # average sweep launch: updates of a run / launches, over the mean launch time
+    local_updates = updates / world
+    achieved = B * (local_updates / max(1, sweeps)) / (launch_ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    bk = best_known(name, real)
+    return {
+        "value": updates / (step_ms * 1e-3), "unit": UNIT, "ms_per_step": step_ms,
+        "workload": f"{name} structure-matched analog (n={graph.n}, m={graph.m}), pSA, "
+                    f"sigma=(0.5,0.5,0.5), {trials} trials x {args.cycles} cycles x t_res 10, "
+                    "replayed reference stream (BASELINE C3)",
+        "kernel": info["kernel"], "updates_per_step": int(updates),
+        "quality": {"mean_final_cut": cut_sum / trials, "best_cut": int(best),
+                    "mean_cut_over_best_known": (cut_sum / trials / bk) if bk else None},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_kind,
+                     "bytes_per_update": B, "kernel_ms_mean": launch_ms,
+                     "launches_per_run": sweeps,
+                     "model": "SURVEY 8(d) bytes per fired update (d + 1 + CSR) + 4 B fp16 profile pair; "
+                              "mean over the run's sub-step launches"},
+    }
+
+
 def main():
     args = parse()
+    rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args)
         return
-    rank, world, local = dist_env()
-    torch = None
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    import torch
+    torch.cuda.set_device(local)
     if world > 1:
-        import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        import torch
-        torch.cuda.set_device(local)
 
     graph, real, model, sch = workload(args.graph, args.cycles)
     lo, hi = shard(args.trials, rank, world)
@@ -276,42 +397,58 @@ def main():
                           rng_seed=nseed, first_trial=lo)
     plan = _native.Plan(batch, device=local)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    dev = f"cuda:{local}"
 
     def barrier():
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
 
-    def reduce_summary():
-        return reduce_summary_of(plan)
-
-    def reduce_summary_of(p):
+    def step_of(p):
+        """One step: the whole anneal, then the end-of-run reduction (SUM of
+        final-cut sum and update count, MAX of best cut) -- NCCL for N > 1."""
+        p.run()
         s, b, u = p.summary()
-        t = torch.tensor([s, u], dtype=torch.int64, device=f"cuda:{local}")
-        m = torch.tensor([b], dtype=torch.int64, device=f"cuda:{local}")
+        t = torch.tensor([s, u], dtype=torch.int64, device=dev)
+        m = torch.tensor([b], dtype=torch.int64, device=dev)
         if world > 1:
             torch.distributed.all_reduce(t)
             torch.distributed.all_reduce(m, op=torch.distributed.ReduceOp.MAX)
-        return int(t[0]), int(m[0]), int(t[1])
+        return t, m
 
     for _ in range(args.warmup):
         flush.zero_()
-        plan.run()
-        reduce_summary()
+        step_of(plan)
     barrier()
-    dev_ms = 0.0
+    step_ms_list, anneal_ms = [], 0.0
     t_wall = time.perf_counter()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
-            dev_ms += plan.run()
-            cut_sum, best, updates = reduce_summary()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            t, m = step_of(plan)
+            e1.record()
+            e1.synchronize()
+            step_ms_list.append(e0.elapsed_time(e1))
     barrier()
     wall_ms = 1e3 * (time.perf_counter() - t_wall)
+    cut_sum, updates, best = int(t[0]), int(t[1]), int(m[0])
     info = plan.info()
+    lay = plan.layout()
     h2d, d2h = plan.transfer_bytes()
     plan.close()
+    # the reduction alone (same tensors, events on torch's stream), for the record
+    red_ms = 0.0
+    if world > 1:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.distributed.all_reduce(t)
+        torch.distributed.all_reduce(m, op=torch.distributed.ReduceOp.MAX)
+        e1.record()
+        e1.synchronize()
+        red_ms = e0.elapsed_time(e1)
 
     # the other stream on the same workload (same timing rules), reported
     # beside the headline: the native Philox mode of the same packed sweep
@@ -329,12 +466,17 @@ def main():
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
-            oms += oplan.run()
-            ocut, obest, _ = reduce_summary_of(oplan)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            ot, om = step_of(oplan)
+            e1.record()
+            e1.synchronize()
+            oms += e0.elapsed_time(e1)
         barrier()
         oinfo = oplan.info()
         oplan.close()
-        other = (alt, oms / args.steps, ocut, obest, oinfo)
+        other = (alt, oms / args.steps, int(ot[0]), int(om[0]), oinfo)
+    var = None if args.no_var_leg else variability_leg(args, local, world, rank, flush, barrier)
     del flush
 
     # end-to-end through the public C ABI call with host buffers: inputs are
@@ -348,15 +490,15 @@ def main():
     for _ in range(args.e2e_steps):
         t0 = time.perf_counter()
         out, _ = _native.anneal_batch(batch, device=local, out=pinned)
-        s_local = int(out["cut_trace"][:, -1].sum())
+        int(out["cut_trace"][:, -1].sum())  # the caller reads a result
         e2e_ms += 1e3 * (time.perf_counter() - t0)
     barrier()
 
-    step_ms = dev_ms / args.steps
+    step_ms = sum(step_ms_list) / len(step_ms_list)  # mean over steps; max over ranks below
     e2e_step_ms = e2e_ms / args.e2e_steps
     if world > 1:
         v = torch.tensor([step_ms, e2e_step_ms, other[1] if other else 0.0],
-                         dtype=torch.float64, device=f"cuda:{local}")
+                         dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(v, op=torch.distributed.ReduceOp.MAX)
         step_ms, e2e_step_ms = float(v[0]), float(v[1])
         if other:
@@ -370,13 +512,24 @@ def main():
         return
 
     B = algorithmic_bytes_per_update(graph)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{local}")
-    alu = alu_ceiling(graph.n, hi - lo, min(args.cycles, 200), local, flush)
-    del flush
     upd_per_launch = (hi - lo) * graph.n
-    achieved = B * upd_per_launch / (info["sweep_ms_mean"] * 1e-3) / 1e9
+    launch_s = info["sweep_ms_mean"] * 1e-3
+    achieved = B * upd_per_launch / launch_s / 1e9
     peak, peak_kind = peaks()
     traffic = load_profile_traffic()
+    clocks = clk.summary()
+    issue = None
+    im = issue_model()
+    if im and clocks.get("sm_mhz"):
+        sms = torch.cuda.get_device_properties(local).multi_processor_count
+        ceiling = sms * 4 * clocks["sm_mhz"] * 1e6 / im["warp_inst_per_update"]
+        issue = {"warp_inst_per_update": im["warp_inst_per_update"],
+                 "ceiling": ceiling, "unit": UNIT,
+                 "frac": (upd_per_launch / launch_s) / ceiling,
+                 "how": f"{sms} SMs x 4 warp schedulers x 1 instruction/clk x median SM clock under "
+                        "load / ncu warp instructions per update of the sweep kernel "
+                        "(profiles/sweep_issue.json)",
+                 "source": im.get("source")}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         threads = cpu_threads()
@@ -386,6 +539,19 @@ def main():
                "sample": f"first {sample} of {args.trials} trials (same seeds), {args.cycles} "
                          f"cycles, {secs:.1f} s; C restatement of _kernels.anneal_loop "
                          "(oracle/psa_oracle.c), one trial per pthread"}
+        if not args.no_ref_numba:
+            refs = []
+            for th, n_tr in ((threads, 2 * threads), (1, 2)):
+                r = reference_numba_sample(args.graph, args.cycles, min(n_tr, args.trials), th)
+                if r is None:
+                    break
+                refs.append({"value": r[0], "unit": UNIT, "cores": th, "kind": "reference",
+                             "sample": f"first {min(n_tr, args.trials)} trials, {args.cycles} cycles, "
+                                       f"{r[1]:.1f} s; the reference package itself "
+                                       "(pbitsa.engine.run_trials, numba, threads="
+                                       f"{th}; baseline/_ref)"})
+            if refs:
+                cpu["reference_package"] = refs
     bk = best_known(args.graph, real)
     line = {
         "metric": METRIC,
@@ -405,6 +571,10 @@ def main():
         "quality": {"mean_final_cut": cut_sum / args.trials, "best_cut": best,
                     "best_known": bk,
                     "mean_cut_over_best_known": (cut_sum / args.trials / bk) if bk else None},
+        "collective": {"backend": "nccl" if world > 1 else None, "ranks": world,
+                       "ops": "all_reduce SUM(final-cut sum, updates) + all_reduce MAX(best cut), "
+                              "inside every timed step",
+                       "ms": red_ms if world > 1 else 0.0},
         "e2e": {"value": total_updates / (e2e_step_ms * 1e-3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "pbsa_anneal_loop_batch (host buffers)", "ms_per_step": e2e_step_ms},
@@ -414,10 +584,7 @@ def main():
                      "kernel": info["path"] + "_sweep",
                      "kernel_ms_mean": info["sweep_ms_mean"],
                      "bytes_per_update": B, "updates_per_launch": upd_per_launch,
-                     "alu_ceiling": {"value": alu, "unit": UNIT,
-                                     "frac": (upd_per_launch / (info["sweep_ms_mean"] * 1e-3)) / alu,
-                                     "how": "same packed kernel and launch shape on an edgeless graph "
-                                            "of the same n and trials (draw + threshold + decision only)"}},
+                     "launch_shape": lay, "issue": issue},
         "cpu_baseline": cpu,
         other[0] if other else "philox": None if other is None else {
             "value": total_updates / (other[1] * 1e-3), "unit": UNIT, "ms_per_step": other[1],
@@ -426,7 +593,8 @@ def main():
                        if other[0] == "philox" else "replayed reference counter hash"),
             "quality": {"mean_final_cut": other[2] / args.trials, "best_cut": other[3],
                         "mean_cut_over_best_known": (other[2] / args.trials / bk) if bk else None}},
-        "clocks": clk.summary(),
+        "variability": var,
+        "clocks": clocks,
         "gpu_launches": info["launches"] * args.steps,
         "wall_ms_timed_region": wall_ms,
     }

@@ -59,3 +59,29 @@ def test_reference_arm_under_torchrun_prints_once_from_rank_zero(oracle):
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def test_reference_arm_gpus_flag_without_torchrun_reports_the_job_size(oracle):
+    """`bench.py --impl reference --gpus 2` outside torchrun: the reference arm
+    is the host-core CPU path, run once, reported for the 2-GPU job."""
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2",
+         "--steps", "1", "--warmup", "0", "--cycles", "20", "--cpu-sample-trials", "2"],
+        capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2
+
+
+def test_gpu_arm_fails_loudly_without_enough_gpus():
+    """`bench.py --gpus 2` re-launches itself under torch.distributed.run with
+    one rank per GPU; with fewer visible GPUs (none here) it exits nonzero
+    with a clear message instead of reporting a 1-GPU job."""
+    out = subprocess.run(
+        [sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "0"],
+        capture_output=True, text=True, timeout=300, cwd=str(ROOT),
+        env={**__import__("os").environ, "CUDA_VISIBLE_DEVICES": ""})
+    assert out.returncode == 2
+    assert "needs 2 visible GPUs" in out.stderr
+    assert not [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
