@@ -138,7 +138,10 @@ __device__ __forceinline__ bool hash_ge_exact(uint64_t x, uint64_t thr) {
     return mix64(x) >= thr && thr != ~0ULL;
 }
 
-constexpr int kPackedThreads = 256;
+#ifndef PBSA_PACKED_THREADS
+#define PBSA_PACKED_THREADS 128
+#endif
+constexpr int kPackedThreads = PBSA_PACKED_THREADS;
 constexpr int kPackedWarps = kPackedThreads / 32;
 
 __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
@@ -313,10 +316,10 @@ struct CutPlanes {
 };
 
 #ifndef PBSA_BUCKET_MIN_BLOCKS
-#define PBSA_BUCKET_MIN_BLOCKS 4
+#define PBSA_BUCKET_MIN_BLOCKS 8
 #endif
 #ifndef PBSA_PACKED_MIN_BLOCKS
-#define PBSA_PACKED_MIN_BLOCKS 4
+#define PBSA_PACKED_MIN_BLOCKS 8
 #endif
 
 // TApSA (time-averaged rule, _kernels.py:131-138) on the packed path: every
