@@ -208,6 +208,30 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
                               float *device_ms);
 
 /*
+ * pbsa_anneal_loop_batch_ex over a device-ordinal list (the
+ * reference's engine.run_trials fan-out, engine.py:119-123): the trials are
+ * split into ndev contiguous shards (interior edges multiples of 4, so the
+ * Philox stream's four-trial groups never straddle a shard), shard r runs on
+ * devices[r] from its own host thread with its own plan and stream, and every
+ * output lands at its trial's row of the caller's buffers -- identical to the
+ * single-device call.  A device may be listed more than once.  *device_ms is
+ * the largest shard's device time; the first failing shard's code is returned.
+ */
+int pbsa_anneal_loop_batch_devices(const int *devices, int ndev, int64_t n, const int64_t *indptr,
+                                   const int64_t *indices, const double *values, const double *h,
+                                   int64_t mm, const int64_t *me_i, const int64_t *me_j,
+                                   const double *me_w, int64_t gm, const int64_t *ge_i,
+                                   const int64_t *ge_j, const int64_t *ge_w, const double *lam,
+                                   const double *delta, const int64_t *period,
+                                   int64_t profile_stride, double i0_min, double beta,
+                                   int64_t cycles, int64_t t_res, int algo, int64_t alpha,
+                                   double p_stall, int64_t trials, const uint64_t *keys,
+                                   int rng_mode, uint64_t rng_seed, int64_t first_trial,
+                                   int8_t *spins, double *inputs, double *hist, int64_t *counts,
+                                   double *trace_i0, double *trace_energy, int64_t *trace_cut,
+                                   int64_t *best_cut, float *device_ms);
+
+/*
  * Device self-checks (used by the parity tests): evaluate the device
  * counter hash stream_u64(key, tag, a, b) (streams.py:41-45) and the device
  * tanh on `count` host inputs.

@@ -59,6 +59,10 @@ _SIGNATURES = [
      [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
       _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.c_int, ctypes.c_uint64,
       _I64] + [_P] * 8 + [ctypes.POINTER(ctypes.c_float)]),
+    ("pbsa_anneal_loop_batch_devices", ctypes.c_int,
+     [_P, ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
+      _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.c_int, ctypes.c_uint64,
+      _I64] + [_P] * 8 + [ctypes.POINTER(ctypes.c_float)]),
     ("pbsa_debug_stream_u64", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P, _P, _P]),
     ("pbsa_debug_tanh", ctypes.c_int, [ctypes.c_int, _I64, _P, _P]),
     ("pbsa_debug_philox", ctypes.c_int, [ctypes.c_int, _I64, _P, _P, _P]),
@@ -198,6 +202,34 @@ def anneal_batch(batch: Batch, device: int = 0, out: dict | None = None) -> tupl
     _check(lib.pbsa_anneal_loop_batch_ex(device, *batch._args(),
                                       *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))
     return out, float(ms.value)
+
+
+def anneal_batch_devices(batch: Batch, devices, out: dict | None = None) -> tuple[dict, float]:
+    """pbsa_anneal_loop_batch_devices: the batch's trials sharded over a
+    device-ordinal list inside the library (one host thread, plan and stream
+    per shard); outputs identical to anneal_batch.  Returns (outputs, the
+    largest shard's device milliseconds)."""
+    lib = load()
+    devs = np.ascontiguousarray([int(d) for d in devices], dtype=np.int32)
+    if devs.size == 0:
+        raise ValueError("need at least one device")
+    for d in set(devs.tolist()):
+        require_device(d)
+    if out is None:
+        out = batch.alloc_outputs()
+    ms = ctypes.c_float(0.0)
+    _check(lib.pbsa_anneal_loop_batch_devices(devs.ctypes.data, int(devs.size), *batch._args(),
+                                              *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))
+    return out, float(ms.value)
+
+
+def device_list() -> list[int] | None:
+    """PBSA_DEVICES=0,1,... (comma-separated ordinals): the device list
+    engine.run_trials shards over when the spec names none; None if unset."""
+    v = os.environ.get("PBSA_DEVICES", "").strip()
+    if not v:
+        return None
+    return [int(x) for x in v.split(",") if x.strip()]
 
 
 class Plan:

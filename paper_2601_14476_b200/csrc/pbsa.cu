@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -2241,6 +2242,11 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
                               double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
                               float *device_ms) {
     pbsa_plan *P = nullptr;
+    const bool trace = std::getenv("PBSA_TRACE_CALL") != nullptr;  // (diagnostic timestamps)
+    auto now_ms = [] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    const double t_enter = now_ms();
     g_oneshot = true;
     int rc = pbsa_plan_create_ex(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm,
                                  ge_i, ge_j, ge_w, lam, delta, period, profile_stride, i0_min,
@@ -2265,18 +2271,33 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
                 CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
                 P->ev_phase.push_back(e);
             }
+            const double t_created = now_ms();
             CK(cudaEventRecord(P->ev_start, P->stream));
             enqueue_run(*P, P->mm_, P->gm_);
+            const double t_enqueued = now_ms();
             CK(cudaEventRecord(P->ev_end, P->stream));
             host_constant_outputs(P, hist, counts, trace_i0);
+            const double t_host = now_ms();
             CK(cudaEventSynchronize(P->ev_end));
+            const double t_dev = now_ms();
             P->ran = true;
             if (device_ms) CK(cudaEventElapsedTime(device_ms, P->ev_start, P->ev_end));
             CK(cudaStreamSynchronize(P->out_stream));
             CK(cudaGetLastError());
+            if (trace) {
+                float dms = 0.f;
+                cudaEventElapsedTime(&dms, P->ev_start, P->ev_end);
+                std::fprintf(stderr, "pbsa one-shot: create %.2f ms, enqueue %.2f, host outputs %.2f, "
+                             "device done at %.2f (device %.2f), outputs done at %.2f\n",
+                             t_created - t_enter, t_enqueued - t_created, t_host - t_enqueued,
+                             t_dev - t_enter, dms, now_ms() - t_enter);
+            }
         });
         const std::string err = g_last_error;
+        const double t_d0 = now_ms();
         pbsa_plan_destroy(P);
+        if (trace) std::fprintf(stderr, "pbsa one-shot: destroy %.2f ms, total %.2f ms\n", now_ms() - t_d0,
+                                now_ms() - t_enter);
         if (rc != PBSA_OK) g_last_error = err;
         return rc;
     }
@@ -2298,6 +2319,65 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
     pbsa_plan_destroy(P);
     if (rc != PBSA_OK) g_last_error = err;
     return rc;
+}
+
+int pbsa_anneal_loop_batch_devices(const int *devices, int ndev, int64_t n, const int64_t *indptr,
+                                   const int64_t *indices, const double *values, const double *h,
+                                   int64_t mm, const int64_t *me_i, const int64_t *me_j,
+                                   const double *me_w, int64_t gm, const int64_t *ge_i,
+                                   const int64_t *ge_j, const int64_t *ge_w, const double *lam,
+                                   const double *delta, const int64_t *period,
+                                   int64_t profile_stride, double i0_min, double beta,
+                                   int64_t cycles, int64_t t_res, int algo, int64_t alpha,
+                                   double p_stall, int64_t trials, const uint64_t *keys,
+                                   int rng_mode, uint64_t rng_seed, int64_t first_trial,
+                                   int8_t *spins, double *inputs, double *hist, int64_t *counts,
+                                   double *trace_i0, double *trace_energy, int64_t *trace_cut,
+                                   int64_t *best_cut, float *device_ms) {
+    if (!devices || ndev < 1) {
+        g_last_error = "need at least one device";
+        return PBSA_EINVAL;
+    }
+    if (trials < 1) {
+        g_last_error = "trials must be in [1, 2^24]";
+        return PBSA_EINVAL;
+    }
+    // contiguous shards, interior edges at multiples of 4 (distributed.shard_range)
+    std::vector<int64_t> edge(ndev + 1);
+    for (int r = 0; r <= ndev; ++r)
+        edge[r] = r == ndev ? trials : (trials * r / ndev) / 4 * 4;
+    std::vector<int> rc(ndev, PBSA_OK);
+    std::vector<float> ms(ndev, 0.f);
+    std::vector<std::string> err(ndev);
+    const int64_t a = std::max<int64_t>(alpha, 1);
+    auto shard = [&](int r) {
+        const int64_t lo = edge[r], hi = edge[r + 1], T = hi - lo;
+        if (T <= 0) return;
+        const size_t po = profile_stride ? (size_t)lo * (size_t)n : 0;
+        rc[r] = pbsa_anneal_loop_batch_ex(
+            devices[r], n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm, ge_i, ge_j, ge_w,
+            lam ? lam + po : nullptr, delta ? delta + po : nullptr, period ? period + po : nullptr,
+            profile_stride, i0_min, beta, cycles, t_res, algo, alpha, p_stall, T, keys + lo, rng_mode,
+            rng_seed, first_trial + lo, spins ? spins + lo * n : nullptr, inputs ? inputs + lo * n : nullptr,
+            hist ? hist + lo * n * a : nullptr, counts ? counts + lo * n : nullptr,
+            trace_i0 ? trace_i0 + lo * cycles : nullptr, trace_energy ? trace_energy + lo * cycles : nullptr,
+            trace_cut ? trace_cut + lo * cycles : nullptr, best_cut ? best_cut + lo : nullptr, &ms[r]);
+        if (rc[r] != PBSA_OK) err[r] = g_last_error;  // (thread-local: copy it out)
+    };
+    std::vector<std::thread> pool;
+    for (int r = 1; r < ndev; ++r) pool.emplace_back(shard, r);
+    shard(0);
+    for (auto &t : pool) t.join();
+    float mx = 0.f;
+    for (int r = 0; r < ndev; ++r) {
+        if (rc[r] != PBSA_OK) {
+            g_last_error = "shard " + std::to_string(r) + " (device " + std::to_string(devices[r]) + "): " + err[r];
+            return rc[r];
+        }
+        mx = std::max(mx, ms[r]);
+    }
+    if (device_ms) *device_ms = mx;
+    return PBSA_OK;
 }
 
 int pbsa_debug_stream_u64(int device, int64_t count, const uint64_t *key, const uint64_t *tag,

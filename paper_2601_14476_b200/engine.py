@@ -43,6 +43,10 @@ class ExperimentSpec:
     # counter hash, bit-exact; "philox" from the native Philox4x32-10 stream
     # (include/pbsa.h PBSA_RNG_PHILOX; plain rule, ideal profile)
     rng: str = "replay"
+    # not in the reference: device ordinals to shard the trials over (one
+    # library-owned host thread and plan per device; results identical to one
+    # device); None reads PBSA_DEVICES, else one device (PBSA_DEVICE / LOCAL_RANK)
+    devices: tuple | None = None
 
     def __post_init__(self) -> None:
         if self.rng not in ("replay", "philox"):
@@ -115,9 +119,15 @@ def run_trial_range(spec: ExperimentSpec, graph: MaxCutGraph, start: int, stop: 
                           algo_code=spec.algo.kind.code, alpha=spec.algo.kernel_alpha,
                           p_stall=spec.algo.p_stall, rng=spec.rng,
                           rng_seed=streams.native_seed(spec.base_seed), first_trial=start)
-    dev = _native.default_device() if device is None else device
+    devs = None
+    if device is None:
+        devs = list(spec.devices) if spec.devices is not None else _native.device_list()
     try:
-        out, _ = _native.anneal_batch(batch, device=dev)
+        if devs is not None and len(devs) > 1:
+            out, _ = _native.anneal_batch_devices(batch, devs)
+        else:
+            dev = device if device is not None else (devs[0] if devs else _native.default_device())
+            out, _ = _native.anneal_batch(batch, device=dev)
     except ValueError as exc:
         raise RuntimeError(f"trials {start}..{stop - 1} of {spec.graph!r} failed: {exc}") from exc
     elapsed = time.perf_counter() - t0

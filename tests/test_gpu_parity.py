@@ -913,3 +913,27 @@ def test_full_batch_variability_configs_match_oracle(bench_graphs, golden_full, 
             assert np.array_equal(rs[k].final_state.spins, golden_bench[p + "spins"]), p
             assert np.array_equal(rs[k].cut_trace, golden_bench[p + "cut"]), p
             assert np.array_equal(rs[k].final_state.inputs, golden_bench[p + "inputs"]), p
+
+
+@pytest.mark.parametrize("rng,sig,trials", [("replay", (0, 0, 0), 301), ("philox", (0, 0, 0), 300),
+                                            ("replay", (0.5, 0.5, 0.5), 130)])
+def test_run_trials_device_list_equals_one_device(bench_graphs, monkeypatch, rng, sig, trials):
+    """engine.run_trials over a device-ordinal list (ExperimentSpec.devices or
+    PBSA_DEVICES; the library shards the batch: pbsa_anneal_loop_batch_devices,
+    4-aligned shards, one host thread and plan per shard) is trial-identical
+    to one device -- here the one visible B200 listed several times."""
+    g = bench_graphs("G81")
+    base = engine.ExperimentSpec(graph="G81", algo=AlgorithmConfig(Algorithm.PSA), cycles=40,
+                                 trials=trials, rng=rng, variability=VariabilityConfig(*sig))
+    one = engine.run_trials(base, {"G81": g}, {"G81": 14004})
+    three = engine.run_trials(dataclasses.replace(base, devices=(0, 0, 0)), {"G81": g}, {"G81": 14004})
+    monkeypatch.setenv("PBSA_DEVICES", "0,0")
+    env2 = engine.run_trials(base, {"G81": g}, {"G81": 14004})
+    for other in (three, env2):
+        assert len(other.results) == trials
+        for a, b in zip(one.results, other.results):
+            assert np.array_equal(a.final_state.spins, b.final_state.spins)
+            assert np.array_equal(a.final_state.inputs, b.final_state.inputs)
+            assert np.array_equal(a.cut_trace, b.cut_trace)
+            assert np.array_equal(a.update_counts, b.update_counts)
+        assert one.mean_cut == other.mean_cut and one.std_cut == other.std_cut
