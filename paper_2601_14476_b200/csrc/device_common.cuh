@@ -82,7 +82,8 @@ struct PackedArgs {
     const uint32_t *sold;
     uint32_t *snew;
     const uint32_t *rowptr;   // [n+1]
-    const uint32_t *adj;      // [nnz] column | (J < 0) << 31
+    const uint32_t *adj;      // [nnz] column | (J < 0) << 31 (n > 32768), else null
+    const uint16_t *adj16;    // [nnz] column | (J < 0) << 15 (n <= 32768), else null
     const uint2 *kfc;         // [Tp] per-trial (F_t, C_t)
     const uint2 *acache;      // [W][chunks][32 trials][32 lanes] absorb(K_t, i) + GAMMA, or null
     const uint64_t *krg;      // [Tp] absorb(key, TAG_R) + GAMMA (exact slow path)
@@ -412,6 +413,76 @@ __device__ __forceinline__ void gather_counts_reg4(const uint32_t *__restrict__ 
     gather_counts_row4<L>(__ldg(reinterpret_cast<const uint4 *>(adj) + i), sw, p);
 }
 
+// The device CSR (model.py:21-33 row order): 16-bit entries column | (J < 0)
+// << 15 whenever n <= 32768 (every G-set graph: G81's 80k couplings in 160 KB,
+// so a CTA's slice, or the whole graph, sits in shared memory), 32-bit column
+// | (J < 0) << 31 beyond.  Kernels branch once per node on which is present.
+__device__ __forceinline__ uint32_t adj16_to32(uint32_t e16) {
+    return (e16 & 0x7fffu) | ((e16 & 0x8000u) << 16);
+}
+
+template <int L>
+__device__ __forceinline__ void gather_counts16(const uint16_t *__restrict__ adj,
+                                                const uint32_t *__restrict__ sw, uint32_t beg,
+                                                uint32_t end, uint32_t (&p)[L]) {
+    count_neighbours<L>(beg, end, [&](uint32_t k) {
+        const uint32_t e = __ldg(adj + k);
+        return __ldg(sw + (e & 0x7fffu)) ^ (0u - (e >> 15));
+    }, p);
+}
+
+template <int L, typename A>
+__device__ __forceinline__ void gather_rows(const A &a, const uint32_t *__restrict__ sw, uint32_t beg,
+                                            uint32_t end, uint32_t (&p)[L]) {
+    if (a.adj16)
+        gather_counts16<L>(a.adj16, sw, beg, end, p);
+    else
+        gather_counts<L>(a.adj, sw, beg, end, p);
+}
+
+// Degree-4 rows: the raw row of node i (16-bit: its four entries in .x, .y)
+// and its 32-bit form for gather_counts_row4.
+template <typename A>
+__device__ __forceinline__ uint4 load_row4(const A &a, int i) {
+    if (a.adj16) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2 *>(a.adj16) + i);
+        return make_uint4(u.x, u.y, 0u, 0u);
+    }
+    return __ldg(reinterpret_cast<const uint4 *>(a.adj) + i);
+}
+
+// 16-bit degree-4 row (entries e.x lo/hi, e.y lo/hi): as gather_counts_row4
+template <int L>
+__device__ __forceinline__ void gather_counts_row4_16(const uint4 e, const uint32_t *__restrict__ sw,
+                                                      uint32_t (&p)[L]) {
+    const uint32_t x0 = __ldg(sw + (e.x & 0x7fffu)) ^ (0u - ((e.x >> 15) & 1u));
+    const uint32_t x1 = __ldg(sw + ((e.x >> 16) & 0x7fffu)) ^ (uint32_t)((int32_t)e.x >> 31);
+    const uint32_t x2 = __ldg(sw + (e.y & 0x7fffu)) ^ (0u - ((e.y >> 15) & 1u));
+    const uint32_t x3 = __ldg(sw + ((e.y >> 16) & 0x7fffu)) ^ (uint32_t)((int32_t)e.y >> 31);
+    const uint32_t s01 = x0 ^ x1, c01 = x0 & x1, s23 = x2 ^ x3, c23 = x2 & x3;
+    const uint32_t s = s01 ^ s23, cs = s01 & s23;
+    const uint32_t t = c01 ^ c23 ^ cs;
+    const uint32_t f = (c01 & c23) | (cs & (c01 ^ c23));
+#pragma unroll
+    for (int r = 0; r < L; ++r) p[r] = r == 0 ? s : r == 1 ? t : r == 2 ? f : 0u;
+}
+
+template <int L, typename A>
+__device__ __forceinline__ void gather_row4(const A &a, const uint4 e, const uint32_t *__restrict__ sw,
+                                            uint32_t (&p)[L]) {
+    if (a.adj16)
+        gather_counts_row4_16<L>(e, sw, p);
+    else
+        gather_counts_row4<L>(e, sw, p);
+}
+
+template <typename A>
+__device__ __forceinline__ uint4 expand_row4(const A &a, uint4 e) {
+    if (!a.adj16) return e;
+    return make_uint4(adj16_to32(e.x & 0xffffu), adj16_to32(e.x >> 16), adj16_to32(e.y & 0xffffu),
+                      adj16_to32(e.y >> 16));
+}
+
 // Cut count g = #{J_ik s_i s_k = +1} = (s_i = +1) ? p : d - p, bit-sliced:
 // d - p = ~p + (d + 1) mod 2^L (p <= d < 2^L), then a per-trial select.
 template <int L>
@@ -528,7 +599,7 @@ struct ResidentArgs {
     const uint32_t *s_in;       // [W][n] initial words
     uint32_t *s_out;            // [W][n] final words
     const uint32_t *rowptr;     // [n+1]
-    const uint32_t *adj;        // [nnz] column | (J < 0) << 31
+    const uint16_t *adj16;      // [nnz] column | (J < 0) << 15 (resident plans have n <= 32768)
     const uint2 *kfc;           // [Tp] folded per-trial constants
     const uint2 *acache;        // [W][chunks][32][32] first-absorb cache, or null
     const uint64_t *krg;        // [Tp] absorb(key, TAG_R) + GAMMA
@@ -566,7 +637,8 @@ struct RLaunch {
 struct ResidentTimingArgs {
     const uint32_t *s_in;
     uint32_t *s_out;
-    const uint32_t *rowptr, *adj;
+    const uint32_t *rowptr;
+    const uint16_t *adj16;      // [nnz] column | (J < 0) << 15
     const uint2 *kfc;
     const uint64_t *krg;
     const __half2 *prof;        // [W][n][32] fp16 pairs (node-major: a node's 32 trials contiguous)

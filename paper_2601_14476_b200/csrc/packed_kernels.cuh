@@ -90,11 +90,10 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
         // fetched one iteration ahead, so only the neighbour loads precede the counts
         // (only the last chunk has lanes past n, and it has no successor)
         const bool R4 = L >= 3 && a.reg4;
-        const uint4 *adj4 = reinterpret_cast<const uint4 *>(a.adj);
         uint4 e_nx = make_uint4(0u, 0u, 0u, 0u);
         uint32_t own_nx = 0;
         if (R4 && q < a.chunks && q * 32 + lane < a.n) {
-            e_nx = __ldg(adj4 + q * 32 + lane);
+            e_nx = load_row4(a, q * 32 + lane);
             own_nx = __ldg(sw + q * 32 + lane);
         }
         for (int ch = q; ch < a.chunks; ch += a.warps_per_word) {
@@ -108,15 +107,15 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                 own = own_nx;
                 const int ni = i + 32 * a.warps_per_word;
                 if (ni < a.n) {
-                    e_nx = __ldg(adj4 + ni);
+                    e_nx = load_row4(a, ni);
                     own_nx = __ldg(sw + ni);
                 }
-                gather_counts_row4<L>(e, sw, p);
+                gather_row4<L>(a, e, sw, p);
                 d = 4;
             } else {
                 const uint32_t beg = __ldg(a.rowptr + i), end = __ldg(a.rowptr + i + 1);
                 own = __ldg(sw + i);
-                gather_counts<L>(a.adj, sw, beg, end, p);
+                gather_rows<L>(a, sw, beg, end, p);
                 d = (int)(end - beg);
             }
             uint32_t g[L];
@@ -527,14 +526,14 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
             int d = (int)(end - beg);
             if (reg4) {
                 if (valid) {
-                    gather_counts_reg4<L>(a.adj, sw, i, p);
+                    gather_row4<L>(a, load_row4(a, i), sw, p);
                     d = 4;
                 } else {
 #pragma unroll
                     for (int r = 0; r < L; ++r) p[r] = 0;
                 }
             } else {
-                gather_counts<L>(a.adj, sw, beg, end, p);
+                gather_rows<L>(a, sw, beg, end, p);
             }
             if (valid) {
                 for (int dv = 0; dv < a.ndiv; ++dv) {
@@ -726,7 +725,6 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
     if (live) {
         const uint32_t *sw = a.sold + (size_t)w * a.n;
         const bool reg4 = L >= 3 && a.reg4;
-        const uint4 *adj4 = reinterpret_cast<const uint4 *>(a.adj);
         const size_t ncl1 = (size_t)a.nclass + 1;
         // class bounds of the lane's fired class k0 + lane in tile ch, packed beg | end << 16
         auto bounds = [&](int ch, int k0) -> uint32_t {
@@ -739,7 +737,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
         uint4 e_nx = make_uint4(0u, 0u, 0u, 0u);
         uint32_t own_nx = 0;
         if (reg4 && q < a.chunks && q * 32 + lane < a.n) {
-            e_nx = __ldg(adj4 + q * 32 + lane);
+            e_nx = load_row4(a, q * 32 + lane);
             own_nx = __ldg(sw + q * 32 + lane);
         }
         uint32_t parity = 0;
@@ -785,11 +783,11 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
                 own = own_nx;
                 const int ni = i + 32 * a.warps_per_word;
                 if (ni < a.n) {
-                    e_nx = __ldg(adj4 + ni);
+                    e_nx = load_row4(a, ni);
                     own_nx = __ldg(sw + ni);
                 }
                 if (valid) {
-                    gather_counts_row4<L>(er, sw, p);
+                    gather_row4<L>(a, er, sw, p);
                     d = 4;
                 } else {
 #pragma unroll
@@ -802,7 +800,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
                     end = __ldg(a.rowptr + i + 1);
                     own = __ldg(sw + i);
                 }
-                gather_counts<L>(a.adj, sw, beg, end, p);
+                gather_rows<L>(a, sw, beg, end, p);
                 d = (int)(end - beg);
             }
             if (a.do_cut && valid) {

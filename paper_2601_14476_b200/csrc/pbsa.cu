@@ -292,7 +292,8 @@ struct pbsa_plan {
     // packed path
     int L = 1, dmax = 0, K = 1;
     int warps_per_word = 1, chunks = 1, packed_blocks = 1;
-    DevBuf<uint32_t> p_spins[2], rowptr, adj;
+    DevBuf<uint32_t> p_spins[2], rowptr, adj;  // adj: 32-bit CSR entries (n > 32768)
+    DevBuf<uint16_t> adj16;                     // 16-bit CSR entries (n <= 32768)
     DevBuf<uint64_t> thr, krg;
     DevBuf<uint2> kfc, acache;
     bool use_cache = false;
@@ -813,14 +814,24 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.L = 1;
         while ((1 << P.L) - 1 < dmax) ++P.L;
         P.K = 2 * P.dmax + 1;
-        std::vector<uint32_t> adjv(nnz);
-        for (int64_t k = 0; k < nnz; ++k)
-            adjv[k] = (uint32_t)indices[k] | (values[k] < 0 ? 0x80000000u : 0u);
+        // device CSR: 16-bit column | sign whenever n <= 32768 (the north_star
+        // format, 2 bytes per coupling), 32-bit column | sign beyond
+        std::vector<uint32_t> adjv;
+        std::vector<uint16_t> adj16;
+        if (n <= 32768) {
+            adj16.resize(nnz);
+            for (int64_t k = 0; k < nnz; ++k)
+                adj16[k] = (uint16_t)((uint32_t)indices[k] | (values[k] < 0 ? 0x8000u : 0u));
+        } else {
+            adjv.resize(nnz);
+            for (int64_t k = 0; k < nnz; ++k)
+                adjv[k] = (uint32_t)indices[k] | (values[k] < 0 ? 0x80000000u : 0u);
+        }
         // degree-4 regular graph (tori): rows at 4i, gathered with one 16-byte load
         P.reg4 = nnz == 4 * n;
         for (int64_t i = 0; i < n && P.reg4; ++i) P.reg4 = indptr[i] == 4 * i;
         if (const char *env = std::getenv("PBSA_REG4")) P.reg4 = P.reg4 && env[0] != '0';
-        P.adj.upload(adjv, st);
+        if (n <= 32768) P.adj16.upload(adj16, st); else P.adj.upload(adjv, st);
         std::vector<uint64_t> krg(P.Tp);
         std::vector<uint2> kfc(P.Tp);
         for (int64_t t = 0; t < P.Tp; ++t) {
@@ -1087,6 +1098,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             bool want = (P.W <= 64 || (P.var_mode && !P.var_uniform && P.W <= 128) ||
                          (P.tapsa_packed && !P.var_mode && P.W <= 128)) && n <= 2500 && nnz >= 8 * n;
             if (const char *env = std::getenv("PBSA_RESIDENT")) want = env[0] == '1';
+            want = want && n <= 32768;  // (the resident kernels stage the 16-bit CSR)
             int csz = 1;  // (measured: 8 for a handful of words, 4 beats 8 at 32 words)
             while (csz < (P.W <= 8 ? 8 : 4) && P.W * csz < sms) csz *= 2;
             if (const char *env = std::getenv("PBSA_RESIDENT_CS")) csz = std::max(1, std::atoi(env));
@@ -1096,7 +1108,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 const int64_t lo = std::min<int64_t>(n, r * per), hi = std::min<int64_t>(n, lo + per);
                 slice = std::max<int64_t>(slice, indptr[hi] - indptr[lo]);
             }
-            P.res_smem += 4 * (size_t)(per + 1 + slice);
+            P.res_smem += 4 * (size_t)(per + 1) + 2 * (size_t)slice + 4;  // (16-bit CSR slice)
             if (tap) P.res_smem += 4 * (size_t)alpha * P.L * per;  // the ring slice
             if (timing) {
                 // two lanes per node when a CTA's slice still takes one pass of <= 16 warps
@@ -1105,7 +1117,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 if (const char *env = std::getenv("PBSA_RES_SPLIT")) P.res_split = env[0] == '1';
                 const int64_t thr = std::min<int64_t>(512, P.res_split ? ((per + 15) / 16) * 32 : ((per + 31) / 32) * 32);
                 P.res_smem = 32 * 8 + 8 * (size_t)n + (thr / 32) * (256 + 4096) + pbsa::kMaxDivisors * 32 +
-                             4 * (size_t)(P.nplanes * per + per + 1 + slice) + 64;
+                             4 * (size_t)(P.nplanes * per + per + 1) + 2 * (size_t)slice + 68;
                 // stage the CTA's fp16 profile slice too when it fits (PBSA_RES_PROF=0 disables)
                 const size_t prof_bytes = 4 * (size_t)per * 32;
                 const char *penv = std::getenv("PBSA_RES_PROF");
@@ -1392,7 +1404,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             r.s_in = P.p_spins[0].p;
             r.s_out = P.p_spins[1].p;
             r.rowptr = P.rowptr.p;
-            r.adj = P.adj.p;
+            r.adj16 = P.adj16.p;
             r.kfc = P.kfc.p;
             r.krg = P.krg.p;
             r.prof = P.prof16.p;
@@ -1443,7 +1455,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             r.s_in = P.p_spins[0].p;
             r.s_out = P.p_spins[1].p;
             r.rowptr = P.rowptr.p;
-            r.adj = P.adj.p;
+            r.adj16 = P.adj16.p;
             r.kfc = P.kfc.p;
             r.acache = P.use_cache ? P.acache.p : nullptr;
             r.krg = P.krg.p;
@@ -1515,7 +1527,8 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     a.sold = P.p_spins[cur].p + w0 * P.n;
                     a.snew = P.p_spins[cur ^ 1].p + w0 * P.n;
                     a.rowptr = P.rowptr.p;
-                    a.adj = P.adj.p;
+                    a.adj = P.adj.n ? P.adj.p : nullptr;
+                    a.adj16 = P.adj16.n ? P.adj16.p : nullptr;
                     a.krg = P.krg.p + w0 * 32;
                     a.kfc = P.kfc.p + w0 * 32;
                     a.acache = P.use_cache ? P.acache.p + (size_t)(w0 - p0) * P.chunks * 1024 : nullptr;
@@ -2177,7 +2190,7 @@ int pbsa_plan_layout(const pbsa_plan *P, int64_t *phase_words, int *chains, int 
 int pbsa_plan_bytes(const pbsa_plan *P, int64_t *h2d_bytes, int64_t *d2h_bytes) {
     return guarded([&] {
         if (!P) fail(PBSA_EINVAL, "null plan");
-        const size_t up = P->p_spins[0].bytes_up + P->rowptr.bytes_up + P->adj.bytes_up + P->kfc.bytes_up +
+        const size_t up = P->p_spins[0].bytes_up + P->rowptr.bytes_up + P->adj.bytes_up + P->adj16.bytes_up + P->kfc.bytes_up +
                           P->thr.bytes_up + P->krg.bytes_up + P->col.bytes_up + P->me_i.bytes_up +
                           P->me_j.bytes_up + P->ge_i.bytes_up + P->ge_j.bytes_up +
                           P->val.bytes_up + P->h.bytes_up + P->me_w.bytes_up + P->lam.bytes_up +

@@ -33,10 +33,10 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
     // flushes L1, which would otherwise re-fetch them from L2 every cycle)
     uint32_t *ringS = S1 + a.n;                 // TAPSA: [alpha][L][per] bit-sliced counts
     uint32_t *rowS = ringS + (TAPSA ? a.alpha * L * per : 0);  // [hi - lo + 1], relative offsets
-    uint32_t *adjS = rowS + (per + 1);          // [rowptr[hi] - rowptr[lo]]
+    uint16_t *adjS = reinterpret_cast<uint16_t *>(rowS + (per + 1));  // [rowptr[hi] - rowptr[lo]], 16-bit entries
     const uint32_t r0 = a.rowptr[lo], r1 = a.rowptr[hi];
     for (int k = tid; k <= hi - lo; k += blockDim.x) rowS[k] = a.rowptr[lo + k] - r0;
-    for (uint32_t k = tid; k < r1 - r0; k += blockDim.x) adjS[k] = a.adj[r0 + k];
+    for (uint32_t k = tid; k < r1 - r0; k += blockDim.x) adjS[k] = a.adj16[r0 + k];
     uint32_t *cs = S0, *ns = S1;
     constexpr int CP = L + 2 + kResidentExtraPlanes;
     // table entry k of a cycle: its source in the cycle's threshold row (-1: unused)
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
             uint32_t p[L];
             count_neighbours<L>(beg, end, [&](uint32_t k) {
                 const uint32_t e = adjS[k];
-                return cs[e & 0x7fffffffu] ^ (uint32_t)((int32_t)e >> 31);
+                return cs[e & 0x7fffu] ^ (0u - (e >> 15));
             }, p);
             const int d = (int)(end - beg);
             uint32_t g[L];
@@ -377,12 +377,12 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
     // fired p-bits then read it at shared-memory latency instead of L2's
     __half2 *profS = reinterpret_cast<__half2 *>(plS + a.nplanes * per);
     uint32_t *rowS = reinterpret_cast<uint32_t *>(profS + (a.prof_smem ? per * 32 : 0));  // [per + 1]
-    uint32_t *adjS = rowS + per + 1;
+    uint16_t *adjS = reinterpret_cast<uint16_t *>(rowS + per + 1);  // 16-bit entries
     for (int k = tid; k < a.n; k += blockDim.x) S0[k] = a.s_in[(size_t)w * a.n + k];
     if (tid < 32) key[tid] = a.kfc[(size_t)w * 32 + tid];
     const uint32_t r0 = a.rowptr[lo], r1 = a.rowptr[hi];
     for (int k = tid; k <= hi - lo; k += blockDim.x) rowS[k] = a.rowptr[lo + k] - r0;
-    for (uint32_t k = tid; k < r1 - r0; k += blockDim.x) adjS[k] = a.adj[r0 + k];
+    for (uint32_t k = tid; k < r1 - r0; k += blockDim.x) adjS[k] = a.adj16[r0 + k];
     for (int k = tid; k < a.nplanes * per; k += blockDim.x) {
         const int pl = k / per, j = k - pl * per;
         plS[k] = lo + j < hi ? a.pplanes[((size_t)w * a.nplanes + pl) * a.n + lo + j] : 0u;
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(512, 1) resident_timing(ResidentTimingArgs a) 
             const uint32_t mid = a.split ? beg + ((end - beg + 1) >> 1) : end;
             count_neighbours<L>(half ? mid : beg, half ? end : mid, [&](uint32_t k) {
                 const uint32_t e = adjS[k];
-                return cs[e & 0x7fffffffu] ^ (uint32_t)((int32_t)e >> 31);
+                return cs[e & 0x7fffu] ^ (0u - (e >> 15));
             }, p);
             if (a.split) {   // the two halves' partial counts, added bit-sliced (the sum is <= d < 2^L)
                 uint32_t carry = 0;

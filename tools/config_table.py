@@ -97,12 +97,19 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default="r01")
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default="", help="comma-separated configs to run (e.g. C5)")
+    ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    only = set(x for x in args.only.split(",") if x)
     orc.build()
     threads = len(os.sched_getaffinity(0))
     rows = []
 
     def add(cfg, name, kind, sig, T, cpu_T, note=""):
+        if only and cfg not in only:
+            return
+        if args.no_cpu:
+            cpu_T = 0
         g, _ = benchmarks.load(name)
         gpu = gpu_run(g, kind, sig, T)
         nat = gpu_run(g, kind, sig, T, rng="philox")
