@@ -54,14 +54,15 @@ __global__ void packed_cache_init(uint2 *__restrict__ acache, const uint64_t *__
 // per (word w, chunk ch) tile counting-sorts the tile's 1024 (lane, trial)
 // slots by period class (lut: clamped period -> class, lanes past n get
 // class nclass and are left out), trial-major inside a class so that a round
-// of 32 consecutive slots touches many lanes' masks.  Each class segment
-// starts at an even record (16-byte aligned for the kernel's bulk copies; an
-// odd class is padded with one ~0 record).  Writes the records (slot, fp16
-// profile pair) and the class starts (boff[nclass] = padded end).
+// of 32 consecutive slots touches many lanes' masks.  Each 16-byte record
+// holds the slot, its fp16 (lam, lam delta) pair and the sub-step-independent
+// first absorb of its replayed draw (as packed_cache_init: y' = s ^ (s >> 30),
+// s = absorb(K_t, i) + GAMMA, stored as (low word, high word * M1L)); boff
+// holds the class starts (boff[nclass] = the tile's record count).
 __global__ void bucket_build(const uint32_t *__restrict__ pplanes, int nplanes,
                              const uint8_t *__restrict__ lut, const __half2 *__restrict__ prof16,
-                             int n, int chunks, int W, int nclass, uint2 *__restrict__ brec,
-                             uint16_t *__restrict__ boff) {
+                             const uint64_t *__restrict__ krg, int n, int chunks, int W, int nclass,
+                             uint4 *__restrict__ brec, uint16_t *__restrict__ boff) {
     __shared__ uint32_t cnt[8][257];
     __shared__ uint8_t slut[256];
     for (int k = threadIdx.x; k < 256; k += blockDim.x) slut[k] = lut[k];
@@ -87,23 +88,21 @@ __global__ void bucket_build(const uint32_t *__restrict__ pplanes, int nplanes,
         atomicAdd(c + cls[b], 1u);
     }
     __syncwarp();
-    uint2 *rec = brec + tile * kBucketTile;
-    // exclusive scan of the padded class sizes -> class starts (cursors); pads
+    uint4 *rec = brec + tile * 1024;
+    // exclusive scan of the class counts -> class starts (cursors)
     uint32_t carry = 0;
     for (int k0 = 0; k0 <= nclass; k0 += 32) {
         const int k = k0 + lane;
         const uint32_t v = k < nclass ? c[k] : 0u;
-        const uint32_t pv = v + (v & 1u);
-        uint32_t incl = pv;
+        uint32_t incl = v;
         for (int sft = 1; sft < 32; sft <<= 1) {
             const uint32_t t = __shfl_up_sync(0xffffffffu, incl, sft);
             if (lane >= sft) incl += t;
         }
         if (k <= nclass) {
-            const uint32_t start = carry + incl - pv;
+            const uint32_t start = carry + incl - v;
             c[k] = start;
             boff[tile * (nclass + 1) + k] = (uint16_t)start;
-            if (v & 1u) rec[start + v] = make_uint2(0xFFFFFFFFu, 0u);
         }
         carry += __shfl_sync(0xffffffffu, incl, 31);
     }
@@ -121,7 +120,10 @@ __global__ void bucket_build(const uint32_t *__restrict__ pplanes, int nplanes,
             const __half2 pv = prof16[((size_t)w * n + i) * 32 + b];
             uint32_t bits;
             memcpy(&bits, &pv, 4);
-            rec[pos] = make_uint2((uint32_t)((lane << 5) | b), bits);
+            const uint64_t s = mix64(krg[(size_t)w * 32 + b] ^ (uint64_t)i) + PB_GAMMA;
+            const uint64_t y = s ^ (s >> 30);
+            rec[pos] = make_uint4((uint32_t)((lane << 5) | b), bits, (uint32_t)y,
+                                  (uint32_t)(y >> 32) * 0x1CE4E5B9u);
         }
     }
 }

@@ -125,8 +125,9 @@ struct PackedArgs {
     int reg4;                 // every degree is 4 (rowptr[i] = 4i): gather_counts_reg4
     // BUCKET (timing spread, packed_sweep_bucket): each (word, 32-node chunk)
     // tile's 1024 (lane, trial) slots sorted by period class
-    const uint2 *brec;        // [W][chunks][kBucketTile] class-sorted slot records: x = lane << 5 |
-                              // trial bit (~0: padding), y = fp16 {lam, lam * delta} of that p-bit
+    const uint4 *brec;        // [W][chunks][1024] class-sorted slot records: x = lane << 5 | trial
+                              // bit, y = fp16 {lam, lam * delta} of that p-bit, (z, w) = its
+                              // first-absorb cache (y' low word, y' high word * M1L)
     const uint16_t *boff;     // [W][chunks][nclass + 1] start of each class in the tile
     int nclass;               // distinct clamped periods present
     const uint8_t *cper;      // [nclass] clamped period of each class
@@ -197,6 +198,17 @@ __device__ __forceinline__ uint32_t packed_hash_hi_y(uint32_t yl, uint32_t yh) {
     const uint32_t zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
     yl = zl ^ __funnelshift_r(zl, zh, 27);
     yh = zh ^ mulhi(zh, 1u << 5);
+    return mulhi(yl, M2L) + yl * M2H + yh * M2L;
+}
+
+// The same from the cached form (y low word, c1 = y high word * M1L).
+__device__ __forceinline__ uint32_t packed_hash_hi_c(uint32_t yl, uint32_t c1) {
+    constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
+    constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
+    const uint32_t zl = yl * M1L;
+    const uint32_t zh = mulhi(yl, M1L) + yl * M1H + c1;
+    yl = zl ^ __funnelshift_r(zl, zh, 27);
+    const uint32_t yh = zh ^ mulhi(zh, 1u << 5);
     return mulhi(yl, M2L) + yl * M2H + yh * M2L;
 }
 
@@ -564,19 +576,19 @@ __device__ __forceinline__ uint32_t var_exact_bits(const PackedArgs &a, uint32_t
 
 constexpr int kMaxDivisors = 256;
 // packed_sweep_bucket shared memory: per-warp keys; per warp a staging list
-// of the tile's fired slot records (bulk-copied, kBucketStage records), its
-// mbarrier, scratch (count planes, own word, degree, flip and exact masks: u32
-// per lane) and the u16 segment table (prefix, start per fired class); the
-// launch's class list and last-firing flags.  Class segments in a tile's
-// record list start at even slots (16-byte aligned bulk copies), so a tile
-// holds at most 1024 + 255 records.
-constexpr int kBucketStage = 512;             // staged records per tile (the rest load directly)
+// of the tile's fired slot records (16 bytes each, bulk-copied, kBucketStage
+// records), its mbarrier, scratch (count planes, own word, degree, flip and
+// exact masks: u32 per lane) and the u16 segment table (prefix, start per
+// fired class); the launch's class list and last-firing flags.
+#ifndef PBSA_BK_STAGE
+#define PBSA_BK_STAGE 384
+#endif
+constexpr int kBucketStage = PBSA_BK_STAGE;            // staged records per tile (the rest load directly)
 constexpr int kBucketMaxDiv = 128;            // fired classes per sub-step the bucket kernel takes
 constexpr int kBucketSegs = kBucketMaxDiv + 1;
-constexpr int kBucketTile = 1280;             // record stride of a tile
 __host__ __device__ constexpr int bucket_scratch(int L) { return ((L < 4 ? 4 : L) + 4) * 32; }
 __host__ __device__ constexpr size_t bucket_warp_bytes(int L) {
-    return (kBucketStage * 8 + 16 + bucket_scratch(L) * 4 + 2 * kBucketSegs * 2 + 15) / 16 * 16;
+    return (kBucketStage * 16 + 16 + bucket_scratch(L) * 4 + 2 * kBucketSegs * 2 + 15) / 16 * 16;
 }
 __host__ __device__ constexpr size_t bucket_smem_bytes(int L) {
     return kPackedWarps * 32 * 8 + kPackedWarps * bucket_warp_bytes(L) + kBucketMaxDiv * 3;

@@ -626,7 +626,8 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
 // p-bits that do not fire.  At plan creation every (word w, 32-node chunk ch)
 // tile's 1024 (lane, trial) slots are counting-sorted by period class
 // (bucket_build): `brec` lists the slots class by class, each with its fp16
-// (lam, lam delta) pair, and `boff` holds the start of each class.  In
+// (lam, lam delta) pair and its draw's first-absorb cache, and `boff` holds
+// the start of each class.  In
 // sub-step `count` exactly the classes whose period divides it fire
 // (_kernels.py:126), so a warp reads only those segments -- coalesced, about
 // E[1/period] of the profile per sub-step -- instead of every fired p-bit's
@@ -698,7 +699,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
     uint2 *key = skey + wib * 32;
     key[lane] = live ? a.kfc[(size_t)w * 32 + lane] : make_uint2(0, 0);
     uint8_t *wbase = swarp + wib * WB;
-    uint2 *stage = reinterpret_cast<uint2 *>(wbase);                           // [kBucketStage]
+    uint4 *stage = reinterpret_cast<uint4 *>(wbase);                           // [kBucketStage]
     uint64_t *mbar = reinterpret_cast<uint64_t *>(stage + kBucketStage);
     uint32_t *splane = reinterpret_cast<uint32_t *>(mbar + 2);                 // [max(L, 4)][32]
     uint32_t *sown = splane + (L < 4 ? 4 : L) * 32, *sdeg = sown + 32, *sflip = sdeg + 32, *sexm = sflip + 32;
@@ -744,7 +745,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
         for (int ch = q; ch < a.chunks; ch += a.warps_per_word, parity ^= 1u) {
             const int i = ch * 32 + lane;
             const bool valid = i < a.n;
-            const uint2 *src = a.brec + ((size_t)w * a.chunks + ch) * kBucketTile;
+            const uint4 *src = a.brec + ((size_t)w * a.chunks + ch) * 1024;
             // 1. the tile's fired segments (sizes even): prefix sums, and the
             // first kBucketStage records bulk-copied into the staging list
             int F = 0;
@@ -763,9 +764,9 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
                 if (k0 + lane < a.ndiv) {
                     pre[k0 + lane] = (uint16_t)excl;
                     beg16[k0 + lane] = (uint16_t)beg;
-                    if (nst > 0) bulk_copy_g2s(stage + excl, src + beg, 8u * (uint32_t)nst, mbar);
+                    if (nst > 0) bulk_copy_g2s(stage + excl, src + beg, 16u * (uint32_t)nst, mbar);
                 }
-                staged += 8u * (uint32_t)__reduce_add_sync(0xffffffffu, (uint32_t)nst);
+                staged += 16u * (uint32_t)__reduce_add_sync(0xffffffffu, (uint32_t)nst);
                 F += __shfl_sync(0xffffffffu, incl, 31);
             }
             if (lane == 0) {
@@ -842,7 +843,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
             // go to lane l's masks (padding records are skipped)
             // branch-free so that a lane's four slots of a round interleave;
             // a padding record (~0) decides nothing (zero masks)
-            auto fire_one = [&](uint2 rec, bool rec_in) {
+            auto fire_one = [&](uint4 rec, bool rec_in) {
                 const bool real = rec.x != 0xFFFFFFFFu;
                 const int b = (int)(rec.x & 31u), l = (int)((rec.x >> 5) & 31u);
                 const int ii = ch * 32 + l;
@@ -864,11 +865,8 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
                     philox4x32_10_rk((uint32_t)ii, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
                                      kNativeTagR, a.rk, o);
                     zh = (b & 2) ? ((b & 1) ? o[3] : o[2]) : ((b & 1) ? o[1] : o[0]);
-                } else {
-                    const uint2 kc = key[b];
-                    uint32_t sl, sh;
-                    packed_first_absorb(kc.x ^ (uint32_t)ii, kc.y, sl, sh);
-                    zh = packed_hash_hi(sl, sh, count);
+                } else {  // the record's first-absorb cache: only the second absorb remains
+                    zh = packed_hash_hi_c(rec.z ^ count, rec.w);
                 }
                 __half2 pv;
                 memcpy(&pv, &rec.y, 4);
@@ -890,11 +888,11 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
                 // while at least 97 remain, then one per lane
                 int j0 = 0;
                 for (; PBSA_BK_ILP && j0 + 96 < Fe; j0 += 128) {
-                    uint2 rec[4];
+                    uint4 rec[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const int j = j0 + 32 * u + lane;
-                        rec[u] = j < Fe ? stage[j] : make_uint2(0xFFFFFFFFu, 0u);
+                        rec[u] = j < Fe ? stage[j] : make_uint4(0xFFFFFFFFu, 0u, 0u, 0u);
                     }
                     uint3 m[4];
 #pragma unroll
@@ -912,7 +910,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
                 int sg = 0;
                 for (int j = lane; j < Fe; j += 32) {
                     while ((int)pre[sg + 1] <= j) ++sg;
-                    const uint2 rec = j < kBucketStage ? stage[j] : __ldg(src + beg16[sg] + (j - (int)pre[sg]));
+                    const uint4 rec = j < kBucketStage ? stage[j] : __ldg(src + beg16[sg] + (j - (int)pre[sg]));
                     apply(fire_one(rec, slast[sg] != 0));
                 }
             }

@@ -318,7 +318,7 @@ struct pbsa_plan {
     int nclass = 0;                    // distinct clamped periods present
     int max_ndiv = 0;                  // most classes firing in one sub-step
     DevBuf<uint8_t> bdivs;             // like vdivs, as class indices
-    DevBuf<uint2> brec;                // [W][chunks][kBucketTile] slot records (slot, fp16 profile pair)
+    DevBuf<uint4> brec;                // [W][chunks][1024] slot records (slot, fp16 profile pair, hash cache)
     DevBuf<uint16_t> boff;             // [W][chunks][nclass + 1] class starts
     DevBuf<uint8_t> blut;              // [256] clamped period -> class
     DevBuf<uint8_t> bcper;             // [nclass] class -> clamped period
@@ -1163,11 +1163,11 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         }
         if (P.bucket) {
             const size_t tiles = (size_t)P.W * P.chunks;
-            P.brec.alloc(tiles * pbsa::kBucketTile);
+            P.brec.alloc(tiles * 1024);
             P.boff.alloc(tiles * (P.nclass + 1));
             pbsa::bucket_build<<<grid_for((int64_t)tiles, 8), 256, 0, st>>>(
-                P.pplanes.p, P.nplanes, P.blut.p, P.prof16.p, (int)n, P.chunks, (int)P.W, P.nclass,
-                P.brec.p, P.boff.p);
+                P.pplanes.p, P.nplanes, P.blut.p, P.prof16.p, P.krg.p, (int)n, P.chunks, (int)P.W,
+                P.nclass, P.brec.p, P.boff.p);
             CK(cudaGetLastError());
             P.prof16.drop();   // (the slot-ordered copy replaces them)
             P.pplanes.drop();
@@ -1563,7 +1563,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                         a.divs = P.var_uniform ? nullptr : (P.bucket ? P.bdivs.p : P.vdivs.p) + pl.div_off;
                         if (P.bucket) {
                             const size_t toff = (size_t)w0 * P.chunks;
-                            a.brec = P.brec.p + toff * pbsa::kBucketTile;
+                            a.brec = P.brec.p + toff * 1024;
                             a.boff = P.boff.p + toff * (P.nclass + 1);
                             a.nclass = P.nclass;
                             a.cper = P.bcper.p;
