@@ -484,7 +484,9 @@ def main():
     # page-locked host arrays the caller allocated once (as a serving loop would)
     pinned = {k: torch.empty(v.shape, dtype=getattr(torch, str(v.dtype)), pin_memory=True).numpy()
               for k, v in batch.alloc_outputs().items()}
-    _native.anneal_batch(batch, device=local, out=pinned)  # warm the allocator pools
+    t0 = time.perf_counter()
+    _native.anneal_batch(batch, device=local, out=pinned)  # the first call builds the plan (reported)
+    e2e_cold_ms = 1e3 * (time.perf_counter() - t0)
     barrier()
     e2e_ms = 0.0
     for _ in range(args.e2e_steps):
@@ -492,6 +494,7 @@ def main():
         out, _ = _native.anneal_batch(batch, device=local, out=pinned)
         int(out["cut_trace"][:, -1].sum())  # the caller reads a result
         e2e_ms += 1e3 * (time.perf_counter() - t0)
+    e2e_h2d, e2e_d2h = _native.last_call_bytes()
     barrier()
 
     step_ms = sum(step_ms_list) / len(step_ms_list)  # mean over steps; max over ranks below
@@ -576,8 +579,10 @@ def main():
                               "inside every timed step",
                        "ms": red_ms if world > 1 else 0.0},
         "e2e": {"value": total_updates / (e2e_step_ms * 1e-3), "unit": UNIT,
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "pbsa_anneal_loop_batch (host buffers)", "ms_per_step": e2e_step_ms},
+                "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
+                "api": "pbsa_anneal_loop_batch (page-locked host buffers; plan kept across calls, every "
+                       "input uploaded and every output written per call)", "ms_per_step": e2e_step_ms,
+                "cold_call_ms": e2e_cold_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_kind,

@@ -193,6 +193,18 @@ int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const i
                            double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
                            float *device_ms);
 
+/*
+ * One-shot calls of the plain rule whose output buffers are page-locked keep
+ * their plan (device buffers, the captured graph with per-phase output copies)
+ * for the next call of the same shape; each call still uploads every input
+ * and writes every output.  PBSA_PLAN_CACHE=0 disables this; this frees the
+ * cached plans.
+ */
+int pbsa_plan_cache_clear(void);
+
+/* Host<->device bytes of the calling thread's last one-shot call. */
+int pbsa_last_call_bytes(int64_t *h2d_bytes, int64_t *d2h_bytes);
+
 /* pbsa_anneal_loop_batch with a choice of random stream (see pbsa_plan_create_ex). */
 int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
                               const double *values, const double *h, int64_t mm,

@@ -59,6 +59,8 @@ _SIGNATURES = [
      [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
       _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.c_int, ctypes.c_uint64,
       _I64] + [_P] * 8 + [ctypes.POINTER(ctypes.c_float)]),
+    ("pbsa_plan_cache_clear", ctypes.c_int, []),
+    ("pbsa_last_call_bytes", ctypes.c_int, [ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("pbsa_anneal_loop_batch_devices", ctypes.c_int,
      [_P, ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
       _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.c_int, ctypes.c_uint64,
@@ -221,6 +223,19 @@ def anneal_batch_devices(batch: Batch, devices, out: dict | None = None) -> tupl
     _check(lib.pbsa_anneal_loop_batch_devices(devs.ctypes.data, int(devs.size), *batch._args(),
                                               *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))
     return out, float(ms.value)
+
+
+def plan_cache_clear() -> None:
+    """Free the one-shot plans the library keeps for repeated calls
+    (pbsa_plan_cache_clear)."""
+    _check(load().pbsa_plan_cache_clear())
+
+
+def last_call_bytes() -> tuple[int, int]:
+    """(host->device, device->host) bytes of this thread's last one-shot call."""
+    a, b = _I64(), _I64()
+    _check(load().pbsa_last_call_bytes(ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def device_list() -> list[int] | None:

@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <condition_variable>
 #include <mutex>
 #include <thread>
 #include <set>
@@ -35,6 +36,13 @@ thread_local std::string g_last_error;
 // word phasing, whose graph (phases x chains x cycles nodes) costs more to
 // instantiate than a single run saves
 thread_local bool g_oneshot = false;
+// set while a cacheable one-shot call builds its plan: the plan keeps the
+// benchmark's launch structure (word phases, chains) captured into one graph,
+// with each phase's output formatting and copies to the caller's (page-locked)
+// buffers captured into it too, so a later call of the same shape replays it
+thread_local bool g_cached_oneshot = false;
+// bytes the calling thread's last one-shot call moved (pbsa_last_call_bytes)
+thread_local int64_t g_call_h2d = 0, g_call_d2h = 0;
 
 struct Error : std::runtime_error {
     int code;
@@ -155,6 +163,13 @@ struct DevBuf {
         if (count) CK(cudaMemcpyAsync(p, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
     }
     void upload(const std::vector<T> &v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+    // new contents for an existing buffer of the same size (its device address,
+    // captured into a cached graph, stays)
+    void overwrite(const std::vector<T> &v, cudaStream_t s) {
+        if (v.size() != n) fail(PBSA_EINVAL, "cached plan buffer size changed");
+        bytes_up = v.size() * sizeof(T);
+        if (n) CK(cudaMemcpyAsync(p, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
     void release() {
         drop();
         bytes_up = 0;
@@ -264,6 +279,26 @@ struct pbsa_plan {
     // phases run one after another and each phase's outputs are formatted and
     // copied to the caller's host buffers on out_stream while the next computes
     bool pipelined = false;
+    bool capturing_outputs = false;    // a cached one-shot plan: phase outputs inside the graph
+    std::vector<std::pair<cudaGraphNode_t, int>> out_nodes;  // its D2H copy nodes and output index
+    std::vector<size_t> out_node_off;  // destination byte offset of each node in its output
+    std::vector<size_t> out_node_bytes;
+    std::vector<const void *> out_node_src;
+    void *out_bound[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // caller buffers the graph writes
+    // cached one-shot plans ship the last raw fields as int16 (trial-major) to a
+    // page-locked staging buffer and widen them to the caller's fp64 inputs on
+    // host threads as each word phase lands (a host node per phase signals it)
+    DevBuf<int16_t> o_raw16;           // [T][n] device
+    int16_t *h_raw = nullptr;          // [T][n] page-locked staging
+    struct PhaseCb {
+        pbsa_plan *P;
+        int k;
+    };
+    std::vector<PhaseCb> cb_args;
+    std::vector<std::pair<int64_t, int64_t>> phase_trials;  // [t0, t1) per phase
+    std::mutex cb_mu;
+    std::condition_variable cb_cv;
+    int cb_done = 0;
     cudaStream_t out_stream = nullptr;
     std::vector<cudaEvent_t> ev_phase;
     PbsaHostOut hout{};
@@ -381,7 +416,13 @@ struct pbsa_plan {
     DevBuf<double> trace_energy;
     int final_parity = 0;  // which spin buffer holds the final state
 
+    cudaGraph_t graph = nullptr;       // kept for a cached plan (its copy nodes are updated)
     ~pbsa_plan() {
+        if (h_raw) {
+            if (out_stream) cudaStreamSynchronize(out_stream);
+            if (stream) cudaStreamSynchronize(stream);
+            cudaFreeHost(h_raw);
+        }
         // drain every stream first: after an error in a pipelined one-shot call
         // the output stream may still be formatting and copying phase outputs
         // into the caller's host buffers, reading buffers released below
@@ -389,6 +430,7 @@ struct pbsa_plan {
         for (cudaStream_t cs : chain_streams) cudaStreamSynchronize(cs);
         if (stream) cudaStreamSynchronize(stream);
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        if (graph) cudaGraphDestroy(graph);
         for (cudaEvent_t e : {ev_start, ev_sweep0, ev_sweep1, ev_end, ev_fork})
             if (e) cudaEventDestroy(e);
         for (cudaEvent_t e : ev_join) cudaEventDestroy(e);
@@ -646,6 +688,64 @@ void setup_active(pbsa_plan &P, int64_t n, const int64_t *indptr, const int64_t 
     P.hist.release();  // the integer ring replaces the fp64 history
 }
 
+// Host-side forms of the per-trial key prefixes and of the packed path's
+// per-trial constants and plain-rule threshold table (create_plan, and the
+// per-call refresh of a cached one-shot plan).
+void host_trial_keys(const uint64_t *keys, int64_t trials, int64_t Tp, std::vector<uint64_t> &kspin,
+                     std::vector<uint64_t> &kr, std::vector<uint64_t> &kst) {
+    kspin.assign(Tp, 0);
+    kr.assign(Tp, 0);
+    kst.assign(Tp, 0);
+    for (int64_t t = 0; t < trials; ++t) {
+        kspin[t] = habsorb(keys[t], 2);
+        kr[t] = habsorb(keys[t], 3);
+        kst[t] = habsorb(keys[t], 4);
+    }
+}
+
+void host_packed_consts(const std::vector<uint64_t> &kr, std::vector<uint64_t> &krg, std::vector<uint2> &kfc) {
+    krg.resize(kr.size());
+    kfc.resize(kr.size());
+    for (size_t t = 0; t < kr.size(); ++t) {
+        krg[t] = kr[t] + kGamma;
+        const uint32_t lo = (uint32_t)krg[t], hi = (uint32_t)(krg[t] >> 32);
+        const uint32_t Y = hi ^ (hi >> 30);
+        kfc[t] = make_uint2(lo ^ ((lo >> 30) | (hi << 2)), Y * 0x1CE4E5B9u);
+    }
+}
+
+std::vector<uint64_t> host_plain_thresholds(const pbsa_plan &P) {
+    // thresholds per (cycle, raw): inp = i0 * raw; act = r + tanh(inp) (lam = 1, delta = 0)
+    // (native mode: the smallest Philox word X that gives +1, threshold_native)
+    std::vector<uint64_t> thr((size_t)P.cycles * P.K);
+    for (int64_t c = 0; c < P.cycles; ++c)
+        for (int raw = -P.dmax; raw <= P.dmax; ++raw) {
+            const double t = pb_libm_tanh(P.i0[c] * (double)raw);
+            thr[(size_t)c * P.K + raw + P.dmax] = P.native ? threshold_native(t) : threshold_h64(t);
+        }
+    return thr;
+}
+
+void host_csr(int64_t n, const int64_t *indptr, const int64_t *indices, const double *values,
+              std::vector<uint32_t> &rowptr, std::vector<uint32_t> &adj32, std::vector<uint16_t> &adj16) {
+    const int64_t nnz = indptr[n];
+    rowptr.resize(n + 1);
+    for (int64_t i = 0; i <= n; ++i) rowptr[i] = (uint32_t)indptr[i];
+    // device CSR: 16-bit column | sign whenever n <= 32768 (the north_star
+    // format, 2 bytes per coupling), 32-bit column | sign beyond
+    adj16.clear();
+    adj32.clear();
+    if (n <= 32768) {
+        adj16.resize(nnz);
+        for (int64_t k = 0; k < nnz; ++k)
+            adj16[k] = (uint16_t)((uint32_t)indices[k] | (values[k] < 0 ? 0x8000u : 0u));
+    } else {
+        adj32.resize(nnz);
+        for (int64_t k = 0; k < nnz; ++k)
+            adj32[k] = (uint32_t)indices[k] | (values[k] < 0 ? 0x80000000u : 0u);
+    }
+}
+
 void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                  const int64_t *indices, const double *values, const double *hv, int64_t mm,
                  const int64_t *mei, const int64_t *mej, const double *mew, int64_t gm,
@@ -795,12 +895,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     cudaStream_t st = P.stream;
 
     // per-trial key prefixes (streams.py: draws are absorb^3(key, tag, a, b))
-    std::vector<uint64_t> kspin(P.Tp, 0), kr(P.Tp, 0), kst(P.Tp, 0);
-    for (int64_t t = 0; t < trials; ++t) {
-        kspin[t] = habsorb(keys[t], 2);
-        kr[t] = habsorb(keys[t], 3);
-        kst[t] = habsorb(keys[t], 4);
-    }
+    std::vector<uint64_t> kspin, kr, kst;
+    host_trial_keys(keys, trials, P.Tp, kspin, kr, kst);
     P.kspin.upload(kspin, st);
     P.kr_host = kr;
 
@@ -814,32 +910,17 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.L = 1;
         while ((1 << P.L) - 1 < dmax) ++P.L;
         P.K = 2 * P.dmax + 1;
-        // device CSR: 16-bit column | sign whenever n <= 32768 (the north_star
-        // format, 2 bytes per coupling), 32-bit column | sign beyond
-        std::vector<uint32_t> adjv;
+        std::vector<uint32_t> rowv, adjv;
         std::vector<uint16_t> adj16;
-        if (n <= 32768) {
-            adj16.resize(nnz);
-            for (int64_t k = 0; k < nnz; ++k)
-                adj16[k] = (uint16_t)((uint32_t)indices[k] | (values[k] < 0 ? 0x8000u : 0u));
-        } else {
-            adjv.resize(nnz);
-            for (int64_t k = 0; k < nnz; ++k)
-                adjv[k] = (uint32_t)indices[k] | (values[k] < 0 ? 0x80000000u : 0u);
-        }
+        host_csr(n, indptr, indices, values, rowv, adjv, adj16);
         // degree-4 regular graph (tori): rows at 4i, gathered with one 16-byte load
         P.reg4 = nnz == 4 * n;
         for (int64_t i = 0; i < n && P.reg4; ++i) P.reg4 = indptr[i] == 4 * i;
         if (const char *env = std::getenv("PBSA_REG4")) P.reg4 = P.reg4 && env[0] != '0';
         if (n <= 32768) P.adj16.upload(adj16, st); else P.adj.upload(adjv, st);
-        std::vector<uint64_t> krg(P.Tp);
-        std::vector<uint2> kfc(P.Tp);
-        for (int64_t t = 0; t < P.Tp; ++t) {
-            krg[t] = kr[t] + kGamma;
-            const uint32_t lo = (uint32_t)krg[t], hi = (uint32_t)(krg[t] >> 32);
-            const uint32_t Y = hi ^ (hi >> 30);
-            kfc[t] = make_uint2(lo ^ ((lo >> 30) | (hi << 2)), Y * 0x1CE4E5B9u);
-        }
+        std::vector<uint64_t> krg;
+        std::vector<uint2> kfc;
+        host_packed_consts(kr, krg, kfc);
         P.krg.upload(krg, st);
         P.kfc.upload(kfc, st);
         if (P.spsa_packed) {
@@ -878,14 +959,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             P.thr.upload(thr, st);
             P.ring.alloc((size_t)P.W * alpha * P.L * n);
         } else {
-            // thresholds per (cycle, raw): inp = i0 * raw; act = r + tanh(inp) (lam = 1, delta = 0)
-            // (native mode: the smallest Philox word X that gives +1, threshold_native)
-            std::vector<uint64_t> thr((size_t)cycles * P.K);
-            for (int64_t c = 0; c < cycles; ++c)
-                for (int raw = -P.dmax; raw <= P.dmax; ++raw) {
-                    const double t = pb_libm_tanh(P.i0[c] * (double)raw);
-                    thr[(size_t)c * P.K + raw + P.dmax] = P.native ? threshold_native(t) : threshold_h64(t);
-                }
+            const std::vector<uint64_t> thr = host_plain_thresholds(P);
             P.thr.upload(thr, st);
             if (P.spsa_packed) {
                 std::vector<uint32_t> hi(thr.size());
@@ -1023,12 +1097,15 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // (PBSA_PIPELINE=0 disables): four word phases, each phase's outputs
         // copied back while the next anneals (decided again below once the
         // resident choice is known)
-        P.pipelined = g_oneshot && !many_launches && !P.var_mode && !P.tapsa_packed && !P.spsa_packed &&
-                      !P.tapsa_hist_from_raw && P.W >= 16;
+        P.pipelined = (g_oneshot || g_cached_oneshot) && !many_launches && !P.var_mode && !P.tapsa_packed &&
+                      !P.spsa_packed && !P.tapsa_hist_from_raw && P.W >= 16;
         if (const char *env = std::getenv("PBSA_PIPELINE")) P.pipelined = P.pipelined && env[0] != '0';
+        // a cached one-shot plan keeps the benchmark's phases and chains (its
+        // launches are replayed from a graph, so their count costs nothing)
+        P.capturing_outputs = g_cached_oneshot && P.pipelined;
         // (up to four phases, but each phase at least two waves of word-warps:
         // measured G81 x 512 one-shot, four phases of 4 words 36.6 ms)
-        if (P.pipelined) {
+        if (P.pipelined && !P.capturing_outputs) {
             const int64_t fill = (2LL * sm_count * 32 + (n + 31) / 32 - 1) / ((n + 31) / 32);
             P.phase_words = std::min<int64_t>(P.W, std::max<int64_t>((P.W + 3) / 4, fill));
         }
@@ -1066,7 +1143,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // couple (fewer graph nodes to instantiate)
         int chains = (many_launches || (P.spsa_packed && !g_oneshot && P.W >= 64)) ? 4
                                                                      : (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
-        if (P.pipelined) chains = 2;  // launched directly: keep the launch count low
+        if (P.pipelined && !P.capturing_outputs) chains = 2;  // launched directly: keep the launch count low
         if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
         chains = (int)std::min<int64_t>(chains, P.W);
         if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
@@ -1154,7 +1231,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                 if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             }
         }
-        if (P.resident) P.pipelined = false;
+        if (P.resident) P.pipelined = P.capturing_outputs = false;
         // timing spread on the launched path: sort every tile's slots into
         // period buckets once (PBSA_BUCKET=0 keeps packed_sweep_timing)
         if (many_launches && !P.resident && P.max_ndiv <= pbsa::kBucketMaxDiv) {
@@ -1325,13 +1402,25 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
 // The sweep-interval events are external event nodes inside a captured graph;
 // a directly launched (pipelined) run records them normally.
 cudaError_t record_sweep_event(const pbsa_plan &P, cudaEvent_t ev, cudaStream_t st) {
-    return P.pipelined ? cudaEventRecord(ev, st) : cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+    return P.pipelined && !P.capturing_outputs ? cudaEventRecord(ev, st)
+                                               : cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
 }
 
 // Pipelined one-shot: once the words [w0, w1) have finished their last cut
 // pass, format their trials' outputs (traces, spins, inputs) and copy them to
 // the caller's host buffers on out_stream, while the main stream anneals the
 // next phase.  Outputs of the plain rule on the packed path only.
+// host node of a cached one-shot graph: phase k's int16 raw fields are in the
+// staging buffer (runs on a driver thread: no CUDA calls, only a signal)
+void CUDART_CB phase_landed(void *arg) {
+    auto *cb = static_cast<pbsa_plan::PhaseCb *>(arg);
+    {
+        std::lock_guard<std::mutex> lk(cb->P->cb_mu);
+        cb->P->cb_done = std::max(cb->P->cb_done, cb->k + 1);
+    }
+    cb->P->cb_cv.notify_all();
+}
+
 void enqueue_phase_outputs(pbsa_plan &P, int64_t w0, int64_t w1, int parity, int k) {
     const int TB = 256;
     cudaStream_t os = P.out_stream;
@@ -1367,7 +1456,18 @@ void enqueue_phase_outputs(pbsa_plan &P, int64_t w0, int64_t w1, int parity, int
         CK(cudaMemcpyAsync(h.spins + t0 * n, P.o_spins.p + t0 * n, Tr * n, cudaMemcpyDeviceToHost, os));
         ++P.launches;
     }
-    if (h.inputs) {
+    if (h.inputs && P.capturing_outputs) {
+        // int16 raw fields, trial-major, to the staging buffer; the host widens them
+        dim3 tb(32, 8), g((unsigned)((Tr + 31) / 32), (unsigned)((n + 31) / 32));
+        pbsa::transpose_tile<int16_t><<<g, tb, 0, os>>>(P.raw_last.p + t0, P.o_raw16.p + t0 * n, (int)n,
+                                                         (int)P.Tp, (int)Tr);
+        CK(cudaMemcpyAsync(P.h_raw + t0 * n, P.o_raw16.p + t0 * n, Tr * n * sizeof(int16_t),
+                           cudaMemcpyDeviceToHost, os));
+        P.phase_trials.push_back({t0, t1});
+        P.cb_args.push_back({&P, (int)P.cb_args.size()});
+        CK(cudaLaunchHostFunc(os, phase_landed, &P.cb_args.back()));
+        ++P.launches;
+    } else if (h.inputs) {
         pbsa::inputs_from_raw<<<grid_for(n * Tr, TB), TB, 0, os>>>(P.raw_last.p + t0, P.o_inputs.p + t0 * n,
                                                                    P.i0[C - 1], (int)n, (int)P.Tp, (int)Tr, 1.0);
         CK(cudaMemcpyAsync(h.inputs + t0 * n, P.o_inputs.p + t0 * n, Tr * n * sizeof(double),
@@ -1900,7 +2000,7 @@ int pbsa_plan_create_ex(int device, int64_t n, const int64_t *indptr, const int6
         DeviceGuard dg(device);
         P->mm_ = mm;
         P->gm_ = gm;
-        if (P->pipelined) {  // one-shot pipelined: launched directly by the call
+        if (P->pipelined) {  // one-shot pipelined: launched directly (or captured with its outputs) by the call
             *out = P.release();
             return;
         }
@@ -2242,6 +2342,229 @@ int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const i
                                      trace_i0, trace_energy, trace_cut, best_cut, device_ms);
 }
 
+}  // extern "C"
+
+namespace {
+
+// ------------------------------------------------------ one-shot plan cache
+// A one-shot call of the plain rule with page-locked output buffers keeps its
+// plan -- device buffers and the captured graph of the whole anneal with each
+// word phase's output formatting and copies into the caller's buffers -- for
+// the next call of the same shape.  Every call still uploads all of its
+// inputs (CSR, per-trial keys and constants, threshold table) into the plan's
+// buffers, replays the graph and writes all eight outputs; only buffer
+// allocation and graph construction are amortised.  PBSA_PLAN_CACHE=0 turns
+// it off; pbsa_plan_cache_clear() frees the cached plans.
+struct CachedPlan {
+    std::vector<uint64_t> key;
+    pbsa_plan *P;
+    uint64_t used;
+};
+std::mutex &plan_cache_mu() {
+    static std::mutex *m = new std::mutex;  // (leaked: no destructor at exit)
+    return *m;
+}
+std::vector<CachedPlan> &plan_cache() {
+    static auto *v = new std::vector<CachedPlan>;
+    return *v;
+}
+uint64_t g_cache_clock = 0;
+constexpr size_t kPlanCacheCap = 2;
+
+uint64_t hash_bytes(const void *p, size_t bytes, uint64_t h) {
+    if (!p) return hmix64(h ^ 0x5bd1e995u);
+    const uint8_t *b = static_cast<const uint8_t *>(p);
+    size_t k = 0;
+    for (; k + 8 <= bytes; k += 8) {
+        uint64_t w;
+        std::memcpy(&w, b + k, 8);
+        h = (h ^ w) * 0x9E3779B97F4A7C15ULL;
+        h ^= h >> 29;
+    }
+    uint64_t w = 0;
+    std::memcpy(&w, b + k, bytes - k);
+    return hmix64(h ^ w ^ (uint64_t)bytes);
+}
+
+bool pinned_or_null(const void *p) {
+    if (!p) return true;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+pbsa_plan *plan_cache_take(const std::vector<uint64_t> &key) {
+    std::lock_guard<std::mutex> lk(plan_cache_mu());
+    auto &c = plan_cache();
+    for (size_t k = 0; k < c.size(); ++k)
+        if (c[k].key == key) {
+            pbsa_plan *P = c[k].P;
+            c.erase(c.begin() + k);
+            return P;
+        }
+    return nullptr;
+}
+
+void plan_cache_put(std::vector<uint64_t> key, pbsa_plan *P) {
+    std::vector<pbsa_plan *> evicted;
+    {
+        std::lock_guard<std::mutex> lk(plan_cache_mu());
+        auto &c = plan_cache();
+        for (const CachedPlan &e : c)
+            if (e.key == key) {  // another thread's plan of this shape is cached already
+                evicted.push_back(P);
+                P = nullptr;
+                break;
+            }
+        if (P) c.push_back({std::move(key), P, ++g_cache_clock});
+        while (c.size() > kPlanCacheCap) {
+            size_t old = 0;
+            for (size_t k = 1; k < c.size(); ++k)
+                if (c[k].used < c[old].used) old = k;
+            evicted.push_back(c[old].P);
+            c.erase(c.begin() + old);
+        }
+    }
+    for (pbsa_plan *e : evicted) pbsa_plan_destroy(e);
+}
+
+// the outputs the graph writes, in PbsaHostOut order, with their byte sizes
+void graph_outputs(const pbsa_plan &P, const PbsaHostOut &h, void *(&ptr)[5], size_t (&bytes)[5]) {
+    const size_t T = (size_t)P.T, n = (size_t)P.n, C = (size_t)P.cycles;
+    ptr[0] = h.spins;        bytes[0] = T * n;
+    ptr[1] = h.inputs;       bytes[1] = T * n * 8;
+    ptr[2] = h.trace_energy; bytes[2] = T * C * 8;
+    ptr[3] = h.trace_cut;    bytes[3] = T * C * 8;
+    ptr[4] = h.best;         bytes[4] = T * 8;
+}
+
+// Capture a cached one-shot plan's anneal with its phase outputs into one graph
+// and index the graph's device-to-host copy nodes by output.
+void capture_with_outputs(pbsa_plan &P, const PbsaHostOut &hout) {
+    DeviceGuard dg(P.device);
+    AllocStream as(P.stream);
+    P.hout = hout;
+    if (hout.spins) P.o_spins.alloc((size_t)P.T * P.n);
+    if (hout.inputs) {
+        P.o_raw16.alloc((size_t)P.T * P.n);
+        CK(cudaMallocHost(reinterpret_cast<void **>(&P.h_raw), (size_t)P.T * P.n * sizeof(int16_t)));
+    }
+    CK(cudaStreamCreateWithFlags(&P.out_stream, cudaStreamNonBlocking));
+    const int64_t nph = (P.W + P.phase_words - 1) / P.phase_words;
+    P.cb_args.reserve(nph);  // (host nodes keep pointers into it)
+    for (int64_t k = 0; k < nph; ++k) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        P.ev_phase.push_back(e);
+    }
+    cudaEvent_t ej;
+    CK(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+    P.ev_phase.push_back(ej);  // (the join of the output stream; destroyed with the plan)
+    CK(cudaStreamSynchronize(P.stream));  // buffers exist before the capture starts
+    CK(cudaStreamBeginCapture(P.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        enqueue_run(P, P.mm_, P.gm_);
+        CK(cudaEventRecord(ej, P.out_stream));
+        CK(cudaStreamWaitEvent(P.stream, ej, 0));
+    } catch (...) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(P.stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    CK(cudaStreamEndCapture(P.stream, &P.graph));
+    void *ptr[5];
+    size_t bytes[5];
+    graph_outputs(P, hout, ptr, bytes);
+    size_t nn = 0;
+    CK(cudaGraphGetNodes(P.graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CK(cudaGraphGetNodes(P.graph, nodes.data(), &nn));
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType ty;
+        CK(cudaGraphNodeGetType(nd, &ty));
+        if (ty != cudaGraphNodeTypeMemcpy) continue;
+        cudaMemcpy3DParms mp{};
+        CK(cudaGraphMemcpyNodeGetParams(nd, &mp));
+        const char *dst = static_cast<const char *>(mp.dstPtr.ptr);
+        for (int k = 0; k < 5; ++k) {
+            const char *b = static_cast<const char *>(ptr[k]);
+            if (b && dst >= b && dst < b + bytes[k]) {
+                P.out_nodes.push_back({nd, k});
+                P.out_node_off.push_back((size_t)(dst - b));
+                P.out_node_bytes.push_back(mp.extent.width * mp.extent.height * mp.extent.depth);
+                P.out_node_src.push_back(mp.srcPtr.ptr);
+                break;
+            }
+        }
+    }
+    for (int k = 0; k < 5; ++k) P.out_bound[k] = ptr[k];
+    CK(cudaGraphInstantiate(&P.graph_exec, P.graph, 0));
+}
+
+// Point the graph's copy nodes at this call's output buffers.
+void bind_outputs(pbsa_plan &P, const PbsaHostOut &hout) {
+    void *ptr[5];
+    size_t bytes[5];
+    graph_outputs(P, hout, ptr, bytes);
+    for (size_t j = 0; j < P.out_nodes.size(); ++j) {
+        const int k = P.out_nodes[j].second;
+        if (ptr[k] == P.out_bound[k]) continue;
+        CK(cudaGraphExecMemcpyNodeSetParams1D(P.graph_exec, P.out_nodes[j].first,
+                                              static_cast<char *>(ptr[k]) + P.out_node_off[j],
+                                              P.out_node_src[j], P.out_node_bytes[j],
+                                              cudaMemcpyDeviceToHost));
+    }
+    for (int k = 0; k < 5; ++k) P.out_bound[k] = ptr[k];
+    P.hout = hout;
+}
+
+// This call's inputs into a cached plan's buffers (same sizes: the cache key
+// fixes every shape), exactly as create_plan derives and uploads them.
+void refresh_inputs(pbsa_plan &P, int64_t n, const int64_t *indptr, const int64_t *indices,
+                    const double *values, const uint64_t *keys) {
+    DeviceGuard dg(P.device);
+    cudaStream_t st = P.stream;
+    std::vector<uint64_t> kspin, kr, kst, krg;
+    std::vector<uint2> kfc;
+    host_trial_keys(keys, P.T, P.Tp, kspin, kr, kst);
+    host_packed_consts(kr, krg, kfc);
+    std::vector<uint32_t> rowv, adj32;
+    std::vector<uint16_t> adj16;
+    host_csr(n, indptr, indices, values, rowv, adj32, adj16);
+    P.kspin.overwrite(kspin, st);
+    P.krg.overwrite(krg, st);
+    P.kfc.overwrite(kfc, st);
+    P.rowptr.overwrite(rowv, st);
+    if (P.adj16.n) P.adj16.overwrite(adj16, st); else P.adj.overwrite(adj32, st);
+    P.thr.overwrite(host_plain_thresholds(P), st);
+    P.kr_host = kr;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pbsa_last_call_bytes(int64_t *h2d_bytes, int64_t *d2h_bytes) {
+    if (h2d_bytes) *h2d_bytes = g_call_h2d;
+    if (d2h_bytes) *d2h_bytes = g_call_d2h;
+    return PBSA_OK;
+}
+
+int pbsa_plan_cache_clear(void) {
+    std::vector<pbsa_plan *> all;
+    {
+        std::lock_guard<std::mutex> lk(plan_cache_mu());
+        for (CachedPlan &e : plan_cache()) all.push_back(e.P);
+        plan_cache().clear();
+    }
+    for (pbsa_plan *P : all) pbsa_plan_destroy(P);
+    return PBSA_OK;
+}
+
 int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
                               const double *values, const double *h, int64_t mm,
                               const int64_t *me_i, const int64_t *me_j, const double *me_w,
@@ -2260,6 +2583,126 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
     };
     const double t_enter = now_ms();
+    const char *cenv = std::getenv("PBSA_PLAN_CACHE");
+    const bool cacheable = (!cenv || cenv[0] != '0') && lam == nullptr && indptr && n >= 1 && trials >= 1 &&
+                           mm >= 0 && gm >= 0 && pinned_or_null(spins) && pinned_or_null(inputs) &&
+                           pinned_or_null(trace_energy) && pinned_or_null(trace_cut) && pinned_or_null(best_cut);
+    if (cacheable) {
+        // the key: every scalar and the content of the model and graph (which
+        // fix the path, launch structure and every value baked into the graph);
+        // the per-trial keys are inputs uploaded on every call
+        uint64_t hm = hash_bytes(indptr, (size_t)(n + 1) * 8, 1);
+        const int64_t nnz = indptr[n];
+        hm = hash_bytes(indices, (size_t)nnz * 8, hm);
+        hm = hash_bytes(values, (size_t)nnz * 8, hm);
+        hm = hash_bytes(h, (size_t)n * 8, hm);
+        hm = hash_bytes(me_i, (size_t)mm * 8, hm);
+        hm = hash_bytes(me_j, (size_t)mm * 8, hm);
+        hm = hash_bytes(me_w, (size_t)mm * 8, hm);
+        hm = hash_bytes(ge_i, (size_t)gm * 8, hm);
+        hm = hash_bytes(ge_j, (size_t)gm * 8, hm);
+        hm = hash_bytes(ge_w, (size_t)gm * 8, hm);
+        uint64_t ps, i0b, bb;
+        std::memcpy(&ps, &p_stall, 8);
+        std::memcpy(&i0b, &i0_min, 8);
+        std::memcpy(&bb, &beta, 8);
+        const uint64_t outs = (spins ? 1 : 0) | (inputs ? 2 : 0) | (trace_energy ? 4 : 0) | (trace_cut ? 8 : 0) |
+                              (best_cut ? 16 : 0);
+        std::vector<uint64_t> key = {(uint64_t)device, (uint64_t)n, (uint64_t)mm, (uint64_t)gm, (uint64_t)cycles,
+                                     (uint64_t)t_res, (uint64_t)algo, (uint64_t)alpha, ps, (uint64_t)trials,
+                                     (uint64_t)rng_mode, rng_seed, (uint64_t)first_trial, i0b, bb, outs, hm};
+        const PbsaHostOut hout{spins, inputs, trace_energy, trace_cut, best_cut};
+        P = plan_cache_take(key);
+        int rc;
+        if (P) {
+            rc = guarded([&] {
+                refresh_inputs(*P, n, indptr, indices, values, keys);
+                bind_outputs(*P, hout);
+            });
+        } else {
+            g_cached_oneshot = true;
+            rc = pbsa_plan_create_ex(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm,
+                                     ge_i, ge_j, ge_w, lam, delta, period, profile_stride, i0_min,
+                                     beta, cycles, t_res, algo, alpha, p_stall, trials, keys, rng_mode,
+                                     rng_seed, first_trial, &P);
+            g_cached_oneshot = false;
+            if (rc != PBSA_OK) return rc;
+            if (!P->capturing_outputs) {  // not the plain launched path: run it once, uncached
+                rc = guarded([&] {
+                    DeviceGuard dg(P->device);
+                    CK(cudaEventRecord(P->ev_start, P->stream));
+                    CK(cudaGraphLaunch(P->graph_exec, P->stream));
+                    CK(cudaEventRecord(P->ev_end, P->stream));
+                    host_constant_outputs(P, hist, counts, trace_i0);
+                    CK(cudaEventSynchronize(P->ev_end));
+                    P->ran = true;
+                    if (device_ms) CK(cudaEventElapsedTime(device_ms, P->ev_start, P->ev_end));
+                    download_impl(P, spins, inputs, hist, counts, trace_i0, trace_energy, trace_cut,
+                                  best_cut, true);
+                });
+                const std::string err = g_last_error;
+                pbsa_plan_destroy(P);
+                if (rc != PBSA_OK) g_last_error = err;
+                return rc;
+            }
+            rc = guarded([&] { capture_with_outputs(*P, hout); });
+        }
+        if (rc == PBSA_OK)
+            rc = guarded([&] {
+                DeviceGuard dg(P->device);
+                {
+                    std::lock_guard<std::mutex> lk(P->cb_mu);
+                    P->cb_done = 0;
+                }
+                const double t_ready = now_ms();
+                CK(cudaEventRecord(P->ev_start, P->stream));
+                CK(cudaGraphLaunch(P->graph_exec, P->stream));
+                CK(cudaEventRecord(P->ev_end, P->stream));
+                const double t_launched = now_ms();
+                host_constant_outputs(P, hist, counts, trace_i0);  // host threads while the device runs
+                const double t_host = now_ms();
+                // fp64 inputs = i0_last * raw (_kernels.py:146) of each phase as it lands
+                const double i0_last = P->i0[P->cycles - 1];
+                for (size_t k = 0; inputs && k < P->phase_trials.size(); ++k) {
+                    {
+                        std::unique_lock<std::mutex> lk(P->cb_mu);
+                        P->cb_cv.wait(lk, [&] { return P->cb_done > (int)k; });
+                    }
+                    const int64_t a0 = P->phase_trials[k].first * n, a1 = P->phase_trials[k].second * n;
+                    const int16_t *src = P->h_raw;
+                    parallel_for(a1 - a0, 1 << 18, [&](int64_t lo, int64_t hi) {
+                        for (int64_t j = a0 + lo; j < a0 + hi; ++j) inputs[j] = i0_last * (double)src[j];
+                    });
+                }
+                CK(cudaEventSynchronize(P->ev_end));
+                P->ran = true;
+                float dms = 0.f;
+                CK(cudaEventElapsedTime(&dms, P->ev_start, P->ev_end));
+                if (device_ms) *device_ms = dms;
+                CK(cudaGetLastError());
+                if (trace)
+                    std::fprintf(stderr, "pbsa one-shot (cached plan): prepare %.2f ms, launch %.2f, host outputs %.2f, "
+                                 "done at %.2f (device %.2f)\n", t_ready - t_enter, t_launched - t_ready,
+                                 t_host - t_launched, now_ms() - t_enter, dms);
+            });
+        if (rc != PBSA_OK) {
+            const std::string err = g_last_error;
+            pbsa_plan_destroy(P);
+            g_last_error = err;
+            return rc;
+        }
+        {
+            int64_t up = (int64_t)(P->kspin.bytes_up + P->krg.bytes_up + P->kfc.bytes_up + P->rowptr.bytes_up +
+                                   P->adj16.bytes_up + P->adj.bytes_up + P->thr.bytes_up);
+            int64_t down = 0;
+            for (size_t j = 0; j < P->out_node_bytes.size(); ++j) down += (int64_t)P->out_node_bytes[j];
+            if (inputs) down += P->T * P->n * (int64_t)sizeof(int16_t);
+            g_call_h2d = up;
+            g_call_d2h = down;
+        }
+        plan_cache_put(std::move(key), P);
+        return PBSA_OK;
+    }
     g_oneshot = true;
     int rc = pbsa_plan_create_ex(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm,
                                  ge_i, ge_j, ge_w, lam, delta, period, profile_stride, i0_min,
@@ -2308,6 +2751,7 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
         });
         const std::string err = g_last_error;
         const double t_d0 = now_ms();
+        pbsa_plan_bytes(P, &g_call_h2d, &g_call_d2h);
         pbsa_plan_destroy(P);
         if (trace) std::fprintf(stderr, "pbsa one-shot: destroy %.2f ms, total %.2f ms\n", now_ms() - t_d0,
                                 now_ms() - t_enter);
@@ -2329,6 +2773,7 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
                       true);
     });
     const std::string err = g_last_error;
+    pbsa_plan_bytes(P, &g_call_h2d, &g_call_d2h);
     pbsa_plan_destroy(P);
     if (rc != PBSA_OK) g_last_error = err;
     return rc;
