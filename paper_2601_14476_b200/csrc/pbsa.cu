@@ -408,6 +408,11 @@ struct pbsa_plan {
     int64_t apmax = 1;                    // largest clamped period
     std::vector<int32_t> apcl;            // [T][n] clamped periods (host counts)
     std::vector<uint64_t> kr_host;        // [Tp] absorb(key, TAG_R)
+    // cached one-shot plans: host copies of the key-independent uploads (the
+    // cache key fixes their content; each call uploads them again)
+    std::vector<uint32_t> h_rowptr, h_adj32;
+    std::vector<uint16_t> h_adj16;
+    std::vector<uint64_t> h_thr;
     uint32_t tmask = 0;
 
     DevBuf<uint64_t> kspin;
@@ -1105,6 +1110,13 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         P.capturing_outputs = g_cached_oneshot && P.pipelined;
         // (up to four phases, but each phase at least two waves of word-warps:
         // measured G81 x 512 one-shot, four phases of 4 words 36.6 ms)
+        // a cached one-shot plan of an unphased batch still splits it in two when
+        // each half fills two waves of word-warps: the second half's outputs are
+        // then the only ones left to copy after the anneal
+        if (P.capturing_outputs && (P.phase_words == 0 || P.phase_words >= P.W)) {
+            const int64_t fill = ((int64_t)sm_count * 32 + (n + 31) / 32 - 1) / ((n + 31) / 32);
+            if (P.W >= 4 * fill) P.phase_words = (P.W + 1) / 2;  // (measured: halves of one wave lose)
+        }
         if (P.pipelined && !P.capturing_outputs) {
             const int64_t fill = (2LL * sm_count * 32 + (n + 31) / 32 - 1) / ((n + 31) / 32);
             P.phase_words = std::min<int64_t>(P.W, std::max<int64_t>((P.W + 3) / 4, fill));
@@ -2532,15 +2544,16 @@ void refresh_inputs(pbsa_plan &P, int64_t n, const int64_t *indptr, const int64_
     std::vector<uint2> kfc;
     host_trial_keys(keys, P.T, P.Tp, kspin, kr, kst);
     host_packed_consts(kr, krg, kfc);
-    std::vector<uint32_t> rowv, adj32;
-    std::vector<uint16_t> adj16;
-    host_csr(n, indptr, indices, values, rowv, adj32, adj16);
+    if (P.h_rowptr.empty()) {  // the model's CSR and the schedule's table (fixed by the key)
+        host_csr(n, indptr, indices, values, P.h_rowptr, P.h_adj32, P.h_adj16);
+        P.h_thr = host_plain_thresholds(P);
+    }
     P.kspin.overwrite(kspin, st);
     P.krg.overwrite(krg, st);
     P.kfc.overwrite(kfc, st);
-    P.rowptr.overwrite(rowv, st);
-    if (P.adj16.n) P.adj16.overwrite(adj16, st); else P.adj.overwrite(adj32, st);
-    P.thr.overwrite(host_plain_thresholds(P), st);
+    P.rowptr.overwrite(P.h_rowptr, st);
+    if (P.adj16.n) P.adj16.overwrite(P.h_adj16, st); else P.adj.overwrite(P.h_adj32, st);
+    P.thr.overwrite(P.h_thr, st);
     P.kr_host = kr;
 }
 
