@@ -329,7 +329,7 @@ struct CutPlanes {
 };
 
 #ifndef PBSA_BUCKET_MIN_BLOCKS
-#define PBSA_BUCKET_MIN_BLOCKS 8
+#define PBSA_BUCKET_MIN_BLOCKS 6  // (85 registers: G55 C3 -5 %, G81 even)
 #endif
 #ifndef PBSA_PACKED_MIN_BLOCKS
 #define PBSA_PACKED_MIN_BLOCKS 8

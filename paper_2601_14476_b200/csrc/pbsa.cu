@@ -1149,6 +1149,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         if (dm > cap) fail(PBSA_EINVAL, "degree too large for the packed cut counter");
         const int64_t max_tasks = cap / dm;  // chunks one warp may take
         wpw = std::max<int64_t>(wpw, std::min<int64_t>((P.chunks + max_tasks - 1) / max_tasks, P.chunks));
+        if (const char *env = std::getenv("PBSA_WARPS_PER_WORD"))  // (experiments; bounded like the default)
+            wpw = std::max<int64_t>(std::min<int64_t>(std::atoi(env), P.chunks),
+                                    (P.chunks + max_tasks - 1) / max_tasks);
         P.warps_per_word = (int)wpw;
         // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
         // small batches need many chains to hide launch gaps; large ones only a
