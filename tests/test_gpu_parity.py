@@ -972,3 +972,65 @@ def test_cached_one_shot_plan_equals_uncached(bench_graphs, monkeypatch, name, t
         assert np.array_equal(r2[k], ref2[k]), k
         assert np.array_equal(r3[k], ref1[k]), k
     _native.plan_cache_clear()
+
+
+@pytest.mark.parametrize("sig", [(0.0, 0.0, 0.0), (0.4, 0.3, 0.6)])
+def test_wide_graph_uses_32_bit_csr_and_matches_oracle(oracle, sig):
+    """n > 32768: the device CSR falls back from 16-bit to 32-bit column |
+    sign entries (the packed sweep and the bucket kernel branch per node);
+    ideal and timing-spread profiles against the oracle."""
+    from paper_2601_14476_b200.model import MaxCutGraph
+    rng = np.random.default_rng(3)
+    n = 33000
+    a, b = rng.integers(0, n, 70000), rng.integers(0, n, 70000)
+    pairs = sorted({(int(min(x, y)), int(max(x, y))) for x, y in zip(a, b) if x != y})
+    g = MaxCutGraph.from_edges(n, [(i, j, int(rng.choice([-1, 1]))) for i, j in pairs])
+    model = maxcut_to_ising(g)
+    assert model.n == 33000
+    sch = derive_schedule(model, 12, 10)
+    T = 40
+    seeds = [streams.trial_seed(2, k) for k in range(T)]
+    vc = VariabilityConfig(*sig)
+    profs = None if vc.is_ideal else [
+        sample_variability(vc, g.n, np.random.default_rng(streams.profile_seed(s))) for s in seeds]
+    keys = [streams.run_key(s) for s in seeds]
+    b = _native.Batch(model, sch, keys, profile_rows=profile_rows(profs, model.n), graph=g)
+    plan = _native.Plan(b)
+    assert plan.info()["path"] == "packed"
+    plan.run()
+    got = plan.download()
+    plan.close()
+    want = oracle.anneal_batch(model, sch, "psa", profs or VariabilityProfile.ideal(model.n), keys,
+                               graph=g)
+    for k in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
+
+
+def test_cached_one_shot_plans_are_keyed_by_model_and_schedule(bench_graphs, monkeypatch):
+    """Kept plans never leak between shapes: two structure-matched graphs of
+    the same size (G81 analog and a relabelled torus) and two schedules give
+    the results of fresh uncached calls."""
+    import torch
+    g = bench_graphs("G81")
+    perm = np.random.default_rng(5).permutation(g.n)
+    from paper_2601_14476_b200.model import MaxCutGraph
+    g2 = MaxCutGraph.from_edges(g.n, [(int(min(perm[i], perm[j])), int(max(perm[i], perm[j])), int(w))
+                                      for i, j, w in zip(g.edge_i, g.edge_j, g.edge_w)])
+    keys = streams.run_keys(streams.trial_seeds(0, 600))
+    batches = []
+    for graph in (g, g2):
+        model = maxcut_to_ising(graph)
+        for cycles in (30, 31):
+            batches.append(_native.Batch(model, derive_schedule(model, cycles, 10), keys, graph=graph))
+    _native.plan_cache_clear()
+    got = []
+    for b in batches + batches:
+        out = {k: torch.empty(v.shape, dtype=getattr(torch, str(v.dtype)), pin_memory=True).numpy()
+               for k, v in b.alloc_outputs().items()}
+        got.append({k: v.copy() for k, v in _native.anneal_batch(b, out=out)[0].items()})
+    monkeypatch.setenv("PBSA_PLAN_CACHE", "0")
+    for j, b in enumerate(batches + batches):
+        want, _ = _native.anneal_batch(b)
+        for k in _native.OUT_ORDER:
+            assert np.array_equal(got[j][k], want[k]), (j, k)
+    _native.plan_cache_clear()
