@@ -34,13 +34,13 @@ __global__ void init_general(int8_t *__restrict__ s, const uint64_t *__restrict_
 // 8 KB tiles per (word w, 32-node chunk) laid out [trial b][lane] so the sweep
 // reads trial b of its node at a fixed offset and every load is 256 B coalesced.
 __global__ void packed_cache_init(uint2 *__restrict__ acache, const uint64_t *__restrict__ krg,
-                                  int n, int chunks, int W) {
+                                  int n, int chunks, int W, const uint32_t *__restrict__ order) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= (int64_t)W * chunks * 1024) return;
     const int lane = (int)(g & 31), b = (int)((g >> 5) & 31);
     const int64_t tile = g >> 10;
     const int ch = (int)(tile % chunks), w = (int)(tile / chunks);
-    const int i = ch * 32 + lane;
+    const int i = order ? (int)order[ch * 32 + lane] : ch * 32 + lane;  // (the sweep's node of this lane)
     uint64_t s = 0;
     if (i < n) s = mix64(krg[w * 32 + b] ^ (uint64_t)i) + PB_GAMMA;
     // store y' = s ^ (s >> 30): the sweep only XORs the sub-step counter into
@@ -62,7 +62,8 @@ __global__ void packed_cache_init(uint2 *__restrict__ acache, const uint64_t *__
 __global__ void bucket_build(const uint32_t *__restrict__ pplanes, int nplanes,
                              const uint8_t *__restrict__ lut, const __half2 *__restrict__ prof16,
                              const uint64_t *__restrict__ krg, int n, int chunks, int W, int nclass,
-                             uint4 *__restrict__ brec, uint16_t *__restrict__ boff) {
+                             uint4 *__restrict__ brec, uint16_t *__restrict__ boff,
+                             const uint32_t *__restrict__ order) {
     __shared__ uint32_t cnt[8][257];
     __shared__ uint8_t slut[256];
     for (int k = threadIdx.x; k < 256; k += blockDim.x) slut[k] = lut[k];
@@ -71,7 +72,7 @@ __global__ void bucket_build(const uint32_t *__restrict__ pplanes, int nplanes,
     const int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
     if (tile >= (int64_t)W * chunks) return;
     const int w = (int)(tile / chunks), ch = (int)(tile % chunks);
-    const int i = ch * 32 + lane;
+    const int i = order ? (int)order[ch * 32 + lane] : ch * 32 + lane;  // (the sweep's node of this lane)
     const bool valid = i < n;
     uint32_t pl[8];
     for (int k = 0; k < 8; ++k)

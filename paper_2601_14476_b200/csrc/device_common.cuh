@@ -132,6 +132,7 @@ struct PackedArgs {
     int nclass;               // distinct clamped periods present
     const uint8_t *cper;      // [nclass] clamped period of each class
     uint32_t maxcount;        // cycles * t_res
+    const uint32_t *order;    // [chunks * 32] node processed by (chunk, lane) (degree order; n = none), or null
 };
 
 // Exact H >= thr for H = mix64(x); thr == ~0 encodes "never" (tanh == -1),
@@ -433,6 +434,16 @@ __device__ __forceinline__ uint32_t adj16_to32(uint32_t e16) {
     return (e16 & 0x7fffu) | ((e16 & 0x8000u) << 16);
 }
 
+// Node handled by lane `lane` of 32-node chunk `ch`: the identity, or, on
+// irregular graphs, a degree-sorted processing order (nodes of similar degree
+// share a warp, so its gather loop runs ~ their degree instead of the maximum
+// of 32 random degrees).  Labels, spin layout and draws are unchanged.
+template <typename A>
+__device__ __forceinline__ int node_at(const A &a, int ch, int lane) {
+    const int k = ch * 32 + lane;
+    return a.order ? (int)__ldg(a.order + k) : k;
+}
+
 template <int L>
 __device__ __forceinline__ void gather_counts16(const uint16_t *__restrict__ adj,
                                                 const uint32_t *__restrict__ sw, uint32_t beg,
@@ -586,7 +597,7 @@ constexpr int kMaxDivisors = 256;
 constexpr int kBucketStage = PBSA_BK_STAGE;            // staged records per tile (the rest load directly)
 constexpr int kBucketMaxDiv = 128;            // fired classes per sub-step the bucket kernel takes
 constexpr int kBucketSegs = kBucketMaxDiv + 1;
-__host__ __device__ constexpr int bucket_scratch(int L) { return ((L < 4 ? 4 : L) + 4) * 32; }
+__host__ __device__ constexpr int bucket_scratch(int L) { return ((L < 4 ? 4 : L) + 5) * 32; }
 __host__ __device__ constexpr size_t bucket_warp_bytes(int L) {
     return (kBucketStage * 16 + 16 + bucket_scratch(L) * 4 + 2 * kBucketSegs * 2 + 15) / 16 * 16;
 }

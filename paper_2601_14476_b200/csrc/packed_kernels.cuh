@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             own_nx = __ldg(sw + q * 32 + lane);
         }
         for (int ch = q; ch < a.chunks; ch += a.warps_per_word) {
-            const int i = ch * 32 + lane;
+            const int i = node_at(a, ch, lane);
             if (i >= a.n) continue;
             uint32_t p[L];
             int d;
@@ -505,7 +505,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
     if (live) {
         const uint32_t *sw = a.sold + (size_t)w * a.n;
         for (int ch = q; ch < a.chunks; ch += a.warps_per_word) {
-            const int i = ch * 32 + lane;
+            const int i = node_at(a, ch, lane);
             const bool valid = i < a.n;
             // (the gather is issued with the period planes: with a timing
             // spread almost every warp has some firing trial)
@@ -572,7 +572,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
             // two list entries per lane and round, their profile loads in flight together
             auto fire_one = [&](uint32_t e, __half2 lv) {
                 const int b = (int)(e & 31u), l = (int)((e >> 5) & 31u), raw = (int)(e >> 10) - 1024;
-                const int ii = ch * 32 + l;
+                const int ii = node_at(a, ch, l);
                 const float ir = a.i0f * (float)raw;
                 uint32_t zh;
                 if (NATIVE) {  // one Philox block per fired trial (fired trials are sparse)
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
                 if (a.inp_out) a.inp_out[((size_t)w * 32 + b) * a.n + ii] = __dmul_rn(a.i0, (double)raw);
             };
             auto prof_of = [&](uint32_t e) {
-                return __ldg(a.prof16 + ((size_t)w * a.n + ch * 32 + ((e >> 5) & 31u)) * 32 + (e & 31u));
+                return __ldg(a.prof16 + ((size_t)w * a.n + node_at(a, ch, (int)((e >> 5) & 31u))) * 32 + (e & 31u));
             };
             // four list entries per lane and round, their profile loads in flight together
             for (int k = lane; k < F; k += 128) {
@@ -703,7 +703,8 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
     uint64_t *mbar = reinterpret_cast<uint64_t *>(stage + kBucketStage);
     uint32_t *splane = reinterpret_cast<uint32_t *>(mbar + 2);                 // [max(L, 4)][32]
     uint32_t *sown = splane + (L < 4 ? 4 : L) * 32, *sdeg = sown + 32, *sflip = sdeg + 32, *sexm = sflip + 32;
-    uint16_t *pre = reinterpret_cast<uint16_t *>(sexm + 32), *beg16 = pre + kBucketSegs;
+    uint32_t *snode = sexm + 32;  // node of each lane of the tile
+    uint16_t *pre = reinterpret_cast<uint16_t *>(snode + 32), *beg16 = pre + kBucketSegs;
     if (lane == 0) mbar_init(mbar, 1);
     // fired classes of this sub-step; a class whose period p has count + p >=
     // cycles * t_res fires here for the last time, so only its slots record
@@ -743,7 +744,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
         }
         uint32_t parity = 0;
         for (int ch = q; ch < a.chunks; ch += a.warps_per_word, parity ^= 1u) {
-            const int i = ch * 32 + lane;
+            const int i = node_at(a, ch, lane);
             const bool valid = i < a.n;
             const uint4 *src = a.brec + ((size_t)w * a.chunks + ch) * 1024;
             // 1. the tile's fired segments (sizes even): prefix sums, and the
@@ -834,6 +835,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
             }
             sown[lane] = own;
             sdeg[lane] = (uint32_t)d;
+            snode[lane] = (uint32_t)i;
             sflip[lane] = 0;
             sexm[lane] = 0;
             mbar_wait_parity(mbar, parity);  // the staged records have landed
@@ -846,7 +848,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
             auto fire_one = [&](uint4 rec, bool rec_in) {
                 const bool real = rec.x != 0xFFFFFFFFu;
                 const int b = (int)(rec.x & 31u), l = (int)((rec.x >> 5) & 31u);
-                const int ii = ch * 32 + l;
+                const int ii = (int)snode[l];
                 int raw;
                 if (PBSA_BK_NIB && L <= 3) {
                     raw = (int)((splane[(b >> 3) * 32 + l] >> (4 * (b & 7))) & 15u) - 7;

@@ -329,6 +329,7 @@ struct pbsa_plan {
     int warps_per_word = 1, chunks = 1, packed_blocks = 1;
     DevBuf<uint32_t> p_spins[2], rowptr, adj;  // adj: 32-bit CSR entries (n > 32768)
     DevBuf<uint16_t> adj16;                     // 16-bit CSR entries (n <= 32768)
+    DevBuf<uint32_t> order;                     // [chunks * 32] degree-sorted processing order, or empty
     DevBuf<uint64_t> thr, krg;
     DevBuf<uint2> kfc, acache;
     bool use_cache = false;
@@ -1247,6 +1248,33 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             }
         }
         if (P.resident) P.pipelined = P.capturing_outputs = false;
+        // irregular graphs on the launched path: warps take nodes in degree
+        // order, so a chunk's lanes have similar degrees and the gather loop
+        // runs ~ their degree, not the largest of 32 random ones (labels, spin
+        // layout and draws are unchanged; PBSA_DEGREE_ORDER=0/1 overrides)
+        if (!P.resident && !P.reg4) {
+            std::vector<uint32_t> ord(n);
+            for (int64_t i = 0; i < n; ++i) ord[i] = (uint32_t)i;
+            std::stable_sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) {
+                return indptr[x + 1] - indptr[x] > indptr[y + 1] - indptr[y];
+            });
+            double sum_max = 0, sum_deg = (double)nnz;
+            for (int64_t c0 = 0; c0 < n; c0 += 32) {
+                int64_t mx = 0;
+                for (int64_t i = c0; i < std::min<int64_t>(n, c0 + 32); ++i)
+                    mx = std::max<int64_t>(mx, indptr[i + 1] - indptr[i]);
+                sum_max += (double)mx * (double)(std::min<int64_t>(n, c0 + 32) - c0);
+            }
+            // (measured, 1024 trials: sparse random graphs gain -- G55 12.6 -> 11.0 ms, G60
+            // 15.1 -> 13.1 ms -- while dense ones lose to the scattered own-word and
+            // spin-store accesses -- G22 9.0 -> 10.9 ms, G1 12.2 -> 13.6 ms)
+            bool want = sum_max > 1.15 * sum_deg && nnz < 8 * n;
+            if (const char *env = std::getenv("PBSA_DEGREE_ORDER")) want = env[0] == '1';
+            if (want) {
+                ord.resize((size_t)P.chunks * 32, (uint32_t)n);
+                P.order.upload(ord, st);
+            }
+        }
         // timing spread on the launched path: sort every tile's slots into
         // period buckets once (PBSA_BUCKET=0 keeps packed_sweep_timing)
         if (many_launches && !P.resident && P.max_ndiv <= pbsa::kBucketMaxDiv) {
@@ -1259,7 +1287,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             P.boff.alloc(tiles * (P.nclass + 1));
             pbsa::bucket_build<<<grid_for((int64_t)tiles, 8), 256, 0, st>>>(
                 P.pplanes.p, P.nplanes, P.blut.p, P.prof16.p, P.krg.p, (int)n, P.chunks, (int)P.W,
-                P.nclass, P.brec.p, P.boff.p);
+                P.nclass, P.brec.p, P.boff.p, P.order.n ? P.order.p : nullptr);
             CK(cudaGetLastError());
             P.prof16.drop();   // (the slot-ordered copy replaces them)
             P.pplanes.drop();
@@ -1563,7 +1591,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
         } else if (P.resident) {
             if (P.use_cache) {
                 pbsa::packed_cache_init<<<grid_for(P.W * P.chunks * 1024, TB), TB, 0, st>>>(
-                    P.acache.p, P.krg.p, (int)P.n, P.chunks, (int)P.W);
+                    P.acache.p, P.krg.p, (int)P.n, P.chunks, (int)P.W, nullptr);
                 ++P.launches;
             }
             pbsa::ResidentArgs r{};
@@ -1622,7 +1650,8 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
             const int64_t p1 = std::min<int64_t>(P.W, p0 + P.phase_words);
             if (P.use_cache) {
                 pbsa::packed_cache_init<<<grid_for((p1 - p0) * P.chunks * 1024, TB), TB, 0, st>>>(
-                    P.acache.p, P.krg.p + p0 * 32, (int)P.n, P.chunks, (int)(p1 - p0));
+                    P.acache.p, P.krg.p + p0 * 32, (int)P.n, P.chunks, (int)(p1 - p0),
+                    P.order.n ? P.order.p : nullptr);
                 ++P.launches;
             }
             if (G > 1) {
@@ -1644,6 +1673,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     a.rowptr = P.rowptr.p;
                     a.adj = P.adj.n ? P.adj.p : nullptr;
                     a.adj16 = P.adj16.n ? P.adj16.p : nullptr;
+                    a.order = P.order.n ? P.order.p : nullptr;
                     a.krg = P.krg.p + w0 * 32;
                     a.kfc = P.kfc.p + w0 * 32;
                     a.acache = P.use_cache ? P.acache.p + (size_t)(w0 - p0) * P.chunks * 1024 : nullptr;
