@@ -92,6 +92,7 @@ struct PackedArgs {
     int16_t *raw_out;         // [n][Tp] raw field of this update, or null
     int n, W, Tp, K, dmax;
     int warps_per_word;       // warps sharing one word index
+    int cta_flush;            // every warp of a block has the same word: one cut flush per block
     int chunks;               // ceil(n / 32)
     uint32_t count;           // global sub-step counter c * t_res (< 2^30)
     int do_update;            // 0: only accumulate pacc (final cut pass)
@@ -146,6 +147,9 @@ __device__ __forceinline__ bool hash_ge_exact(uint64_t x, uint64_t thr) {
 #endif
 constexpr int kPackedThreads = PBSA_PACKED_THREADS;
 constexpr int kPackedWarps = kPackedThreads / 32;
+// packed_sweep's block-level cut reduction buffer: per warp up to 9 count
+// planes and the degree sum, 32 lanes each
+constexpr size_t kPackedFlushBytes = (size_t)kPackedWarps * 10 * 32 * 4 + 16;
 
 __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
 

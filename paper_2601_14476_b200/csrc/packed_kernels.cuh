@@ -453,6 +453,32 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             }
         }
     }
+    if (a.cta_flush) {
+        // every warp of the block works on word w (warps_per_word is a multiple
+        // of the block's warps): add the warps' bit-sliced counters in shared
+        // memory and flush once per block instead of once per warp
+        uint32_t *sC = scount + 4;                                   // [warps][CP][32]
+        int *sD = reinterpret_cast<int *>(sC + kPackedWarps * CP * 32);  // [warps][32]
+#pragma unroll
+        for (int r = 0; r < CP; ++r) sC[(wib * CP + r) * 32 + lane] = C[r];
+        sD[wib * 32 + lane] = dsum;
+        __syncthreads();
+        if (wib == 0) {
+            constexpr int CQ = CP + 3;  // sums of up to 8 warps
+            uint32_t S[CQ];
+#pragma unroll
+            for (int r = 0; r < CQ; ++r) S[r] = r < CP ? C[r] : 0u;
+            for (int v = 1; v < kPackedWarps; ++v) {
+                uint32_t x[CP];
+#pragma unroll
+                for (int r = 0; r < CP; ++r) x[r] = sC[(v * CP + r) * 32 + lane];
+                vc_add<CP, CQ>(S, x);
+                dsum += sD[v * 32 + lane];
+            }
+            warp_cut_flush(S, dsum, lane, live ? a.pacc + (size_t)w * 32 : nullptr);
+        }
+        return;
+    }
     warp_cut_flush(C, dsum, lane, live ? a.pacc + (size_t)w * 32 : nullptr);
 }
 

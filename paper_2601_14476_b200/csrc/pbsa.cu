@@ -327,6 +327,7 @@ struct pbsa_plan {
     // packed path
     int L = 1, dmax = 0, K = 1;
     int warps_per_word = 1, chunks = 1, packed_blocks = 1;
+    bool cta_flush = false;           // packed_sweep: one cut flush per block (warps_per_word % warps == 0)
     DevBuf<uint32_t> p_spins[2], rowptr, adj;  // adj: 32-bit CSR entries (n > 32768)
     DevBuf<uint16_t> adj16;                     // 16-bit CSR entries (n <= 32768)
     DevBuf<uint32_t> order;                     // [chunks * 32] degree-sorted processing order, or empty
@@ -1133,7 +1134,8 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         if (P.use_cache) P.acache.alloc(cache_entries);
         PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
                                               P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16;
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
+                             pbsa::kPackedFlushBytes;
         const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
         set_packed_smem(kern, smem_up);
         set_packed_smem(packed_kernel_for(P.L, false, false), smem);
@@ -1150,6 +1152,11 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         if (dm > cap) fail(PBSA_EINVAL, "degree too large for the packed cut counter");
         const int64_t max_tasks = cap / dm;  // chunks one warp may take
         wpw = std::max<int64_t>(wpw, std::min<int64_t>((P.chunks + max_tasks - 1) / max_tasks, P.chunks));
+        // a multiple of the block's warps, so each block works on one word and
+        // reduces the cut once (PBSA_CTA_FLUSH=0 keeps one flush per warp)
+        P.cta_flush = true;
+        if (const char *env = std::getenv("PBSA_CTA_FLUSH")) P.cta_flush = env[0] != '0';
+        if (P.cta_flush) wpw = (wpw + pbsa::kPackedWarps - 1) / pbsa::kPackedWarps * pbsa::kPackedWarps;
         if (const char *env = std::getenv("PBSA_WARPS_PER_WORD"))  // (experiments; bounded like the default)
             wpw = std::max<int64_t>(std::min<int64_t>(std::atoi(env), P.chunks),
                                     (P.chunks + max_tasks - 1) / max_tasks);
@@ -1533,7 +1540,8 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                         : packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
                                                             P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16;
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
+                             pbsa::kPackedFlushBytes;
         CK(record_sweep_event(P, P.ev_sweep0, st));
         // Word phases run one after another so that a phase's first-absorb
         // cache (PW words x n x 256 B) stays L2-resident across its cycles;
@@ -1687,6 +1695,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                     a.K = P.K;
                     a.dmax = P.dmax;
                     a.warps_per_word = P.warps_per_word;
+                    a.cta_flush = (P.cta_flush && P.warps_per_word % pbsa::kPackedWarps == 0) ? 1 : 0;
                     a.chunks = P.chunks;
                     a.count = pl.count;
                     a.do_update = pl.update;
