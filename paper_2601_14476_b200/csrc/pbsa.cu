@@ -29,6 +29,8 @@
 #include "aux_kernels.cuh"
 #include "dispatch.h"
 
+extern char **environ;
+
 namespace {
 
 thread_local std::string g_last_error;
@@ -2663,6 +2665,12 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
         std::memcpy(&bb, &beta, 8);
         const uint64_t outs = (spins ? 1 : 0) | (inputs ? 2 : 0) | (trace_energy ? 4 : 0) | (trace_cut ? 8 : 0) |
                               (best_cut ? 16 : 0);
+        // (and the PBSA_* tuning variables, read at plan creation: a plan built
+        // under other settings is another plan)
+        for (char **e = environ; e && *e; ++e)
+            if (std::strncmp(*e, "PBSA_", 5) == 0 && std::strncmp(*e, "PBSA_TRACE_CALL=", 16) != 0 &&
+                std::strncmp(*e, "PBSA_DEVICES=", 13) != 0 && std::strncmp(*e, "PBSA_LIB=", 9) != 0)
+                hm = hash_bytes(*e, std::strlen(*e), hm);
         std::vector<uint64_t> key = {(uint64_t)device, (uint64_t)n, (uint64_t)mm, (uint64_t)gm, (uint64_t)cycles,
                                      (uint64_t)t_res, (uint64_t)algo, (uint64_t)alpha, ps, (uint64_t)trials,
                                      (uint64_t)rng_mode, rng_seed, (uint64_t)first_trial, i0b, bb, outs, hm};
