@@ -95,7 +95,7 @@ def denom(name):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--tag", default="r01")
+    ap.add_argument("--tag", default="r02")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--only", default="", help="comma-separated configs to run (e.g. C5)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -151,6 +151,8 @@ def main():
     add("C3'", "G1", Algorithm.SPSA, (0, 0, 0), 1024, 16, "stalled rule (p=0.5)")
     for name in ([] if q else ["G1", "G47", "G22", "G48", "G55", "G60", "G67", "G77", "G81"]):
         add("C5", name, Algorithm.PSA, (0, 0, 0), 1024, 8)
+    for name in ([] if q else ["G1", "G22", "G55", "G60", "G67"]):
+        add("C5", name, Algorithm.PSA, (0, 0, 0), 4096, 0, "the C4 batch size")
 
     out = ROOT / "profiles" / f"{args.tag}_configs.json"
     out.write_text(json.dumps(rows, indent=1))
@@ -158,7 +160,10 @@ def main():
              "Kernels: `packed` (one launch per sub-step), `packed_timing`, `resident` / `resident_timing` (one "
              "cluster launch per run, state in shared memory: their roofline is the SMEM ceiling, "
              f"{SMEM_PEAK / 1000:.1f} TB/s), `active_fast` / `active` (general path). Bytes per update: "
-             "SURVEY 8(d) B, plus 8 B for a varied profile.", "",
+             "SURVEY 8(d) B, plus 8 B for a varied profile. That model counts one byte per neighbour "
+             "and update (int8 spins); the packed kernels read one 4-byte word per neighbour for 32 trials, "
+             "so dense graphs at large batches exceed 1.0 of it (G1/G22 x 4096): there the kernel is "
+             "instruction-bound, not byte-bound.", "",
              "Philox columns: the same run with the native Philox4x32-10 stream (`rng=\"philox\"`; "
              "every rule on the packed path).", "",
              "| cfg | graph (n) | rule | sigma | trials | kernel | GPU ms/run | GPU upd/s | frac of roofline (bound) | CPU upd/s | GPU/CPU | mean cut / best-known | Philox kernel | Philox ms | Philox upd/s | Philox mean cut / best-known |",
