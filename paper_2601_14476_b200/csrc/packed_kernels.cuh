@@ -644,7 +644,8 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
             __syncwarp();
         }
     }
-    warp_cut_flush(C, dsum, lane, live ? a.pacc + (size_t)w * 32 : nullptr);
+    if (a.do_cut)  // (the cut is taken on a cycle's first sub-step only)
+        warp_cut_flush(C, dsum, lane, live ? a.pacc + (size_t)w * 32 : nullptr);
 }
 
 // ------------------------------------------- packed sweep over period buckets
@@ -955,7 +956,8 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
     }
-    warp_cut_flush(C, dsum, lane, live ? a.pacc + (size_t)w * 32 : nullptr);
+    if (a.do_cut)  // (the cut is taken on a cycle's first sub-step only)
+        warp_cut_flush(C, dsum, lane, live ? a.pacc + (size_t)w * 32 : nullptr);
 }
 
 }  // namespace pbsa
