@@ -194,6 +194,38 @@ int pbsa_anneal_loop_batch(int device, int64_t n, const int64_t *indptr, const i
                            float *device_ms);
 
 /*
+ * Native variability profiles (Philox stream only; no reference counterpart):
+ * instead of lam/delta/period arrays the caller gives the three standard
+ * deviations native_sigmas = {sigma_lambda, sigma_delta, sigma_nu} of
+ * pbit.py:57-75 and the plan draws every p-bit's profile on the device from
+ * Philox4x32-10 (counter (node, trial_hi, trial_lo, 5) under rng_seed, two
+ * Box-Muller pairs): lam = 1 + s_l z1, delta = s_d z2, period = max(1,
+ * rint(t_res (1 + s_n z3))).  No host sampling, no profile upload; the
+ * packed path's plain rule only (else -1).  pbsa_native_profiles returns the
+ * profiles a plan with the same seed and first_trial draws (periods clamped
+ * to cycles * t_res, which fires identically).
+ */
+int pbsa_plan_create_np(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                        const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                        const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                        const int64_t *ge_j, const int64_t *ge_w, const double *native_sigmas,
+                        double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                        int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                        uint64_t rng_seed, int64_t first_trial, pbsa_plan **out);
+int pbsa_anneal_loop_batch_np(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                              const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                              const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                              const int64_t *ge_j, const int64_t *ge_w, const double *native_sigmas,
+                              double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                              int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                              uint64_t rng_seed, int64_t first_trial, int8_t *spins, double *inputs,
+                              double *hist, int64_t *counts, double *trace_i0, double *trace_energy,
+                              int64_t *trace_cut, int64_t *best_cut, float *device_ms);
+int pbsa_native_profiles(int device, uint64_t rng_seed, int64_t first_trial, int64_t trials, int64_t n,
+                         int64_t t_res, int64_t cycles, const double *native_sigmas, double *lam,
+                         double *delta, int64_t *period);
+
+/*
  * One-shot calls of the plain rule whose output buffers are page-locked keep
  * their plan (device buffers, the captured graph with per-phase output copies)
  * for the next call of the same shape; each call still uploads every input

@@ -60,6 +60,16 @@ _SIGNATURES = [
       _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.c_int, ctypes.c_uint64,
       _I64] + [_P] * 8 + [ctypes.POINTER(ctypes.c_float)]),
     ("pbsa_plan_cache_clear", ctypes.c_int, []),
+    ("pbsa_plan_create_np", ctypes.c_int,
+     [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P,
+      _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.c_uint64, _I64,
+      ctypes.POINTER(_P)]),
+    ("pbsa_anneal_loop_batch_np", ctypes.c_int,
+     [ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P,
+      _F64, _F64, _I64, _I64, ctypes.c_int, _I64, _F64, _I64, _P, ctypes.c_uint64, _I64]
+     + [_P] * 8 + [ctypes.POINTER(ctypes.c_float)]),
+    ("pbsa_native_profiles", ctypes.c_int,
+     [ctypes.c_int, ctypes.c_uint64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
     ("pbsa_last_call_bytes", ctypes.c_int, [ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("pbsa_anneal_loop_batch_devices", ctypes.c_int,
      [_P, ctypes.c_int, _I64, _P, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P, _P, _I64,
@@ -139,9 +149,20 @@ class Batch:
     """Host-side arguments of one batched anneal_loop call (_kernels.py:69-91)."""
 
     def __init__(self, model, schedule, keys, profile_rows=None, graph=None, algo_code=0,
-                 alpha=1, p_stall=0.5, rng="replay", rng_seed=0, first_trial=0):
+                 alpha=1, p_stall=0.5, rng="replay", rng_seed=0, first_trial=0, native_sigmas=None):
         if rng not in RNG_MODES:
             raise ValueError(f"rng must be one of {sorted(RNG_MODES)}, got {rng!r}")
+        # native_sigmas: (sigma_lambda, sigma_delta, sigma_nu) -- the profiles
+        # are drawn on the device (pbsa_plan_create_np; Philox stream only)
+        self.native_sigmas = None
+        if native_sigmas is not None:
+            if profile_rows is not None:
+                raise ValueError("native_sigmas replace profile_rows; give one")
+            if rng != "philox":
+                raise ValueError("native profiles need rng='philox'")
+            self.native_sigmas = np.ascontiguousarray([float(x) for x in native_sigmas], dtype=np.float64)
+            if self.native_sigmas.size != 3:
+                raise ValueError("native_sigmas holds (sigma_lambda, sigma_delta, sigma_nu)")
         self.rng, self.rng_seed, self.first_trial = rng, int(rng_seed), int(first_trial)
         self.n = int(model.n)
         self.indptr = _c(model.indptr, np.int64)
@@ -180,6 +201,16 @@ class Batch:
                 self.p_stall, self.T, _ptr(self.keys), RNG_MODES[self.rng],
                 self.rng_seed & 0xFFFFFFFFFFFFFFFF, self.first_trial)
 
+    def _args_np(self):
+        """pbsa_*_np arguments: the model, the sigmas in place of the profile
+        arrays, the schedule and rule, keys, seed and first trial."""
+        return (self.n, _ptr(self.indptr), _ptr(self.indices), _ptr(self.values), _ptr(self.h),
+                int(self.me_i.size), _ptr(self.me_i), _ptr(self.me_j), _ptr(self.me_w),
+                int(self.ge_i.size), _ptr(self.ge_i), _ptr(self.ge_j), _ptr(self.ge_w),
+                self.native_sigmas.ctypes.data, self.i0_min, self.beta, self.cycles, self.t_res,
+                self.algo, self.alpha, self.p_stall, self.T, _ptr(self.keys),
+                self.rng_seed & 0xFFFFFFFFFFFFFFFF, self.first_trial)
+
     def alloc_outputs(self) -> dict:
         T, n, C = self.T, self.n, self.cycles
         return dict(spins=np.empty((T, n), np.int8), inputs=np.empty((T, n)),
@@ -201,8 +232,12 @@ def anneal_batch(batch: Batch, device: int = 0, out: dict | None = None) -> tupl
     if out is None:
         out = batch.alloc_outputs()
     ms = ctypes.c_float(0.0)
-    _check(lib.pbsa_anneal_loop_batch_ex(device, *batch._args(),
-                                      *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))
+    if batch.native_sigmas is not None:
+        _check(lib.pbsa_anneal_loop_batch_np(device, *batch._args_np(),
+                                             *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))
+    else:
+        _check(lib.pbsa_anneal_loop_batch_ex(device, *batch._args(),
+                                             *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))
     return out, float(ms.value)
 
 
@@ -223,6 +258,22 @@ def anneal_batch_devices(batch: Batch, devices, out: dict | None = None) -> tupl
     _check(lib.pbsa_anneal_loop_batch_devices(devs.ctypes.data, int(devs.size), *batch._args(),
                                               *(_ptr(out[k]) for k in OUT_ORDER), ctypes.byref(ms)))
     return out, float(ms.value)
+
+
+def native_profiles(rng_seed: int, first_trial: int, trials: int, n: int, t_res: int, cycles: int,
+                    sigmas, device: int = 0):
+    """The (lam, delta, period) [trials][n] arrays a native-profile plan with
+    this seed and first trial draws on the device (pbsa_native_profiles;
+    periods clamped to cycles * t_res, which fires identically)."""
+    lib = load()
+    require_device(device)
+    sig = np.ascontiguousarray([float(x) for x in sigmas], dtype=np.float64)
+    lam, delta = np.empty((trials, n)), np.empty((trials, n))
+    period = np.empty((trials, n), np.int64)
+    _check(lib.pbsa_native_profiles(device, int(rng_seed) & 0xFFFFFFFFFFFFFFFF, int(first_trial), int(trials),
+                                    int(n), int(t_res), int(cycles), sig.ctypes.data, _ptr(lam), _ptr(delta),
+                                    _ptr(period)))
+    return lam, delta, period
 
 
 def plan_cache_clear() -> None:
@@ -255,7 +306,10 @@ class Plan:
         require_device(device)
         self.batch, self.device = batch, device
         h = _P()
-        _check(lib.pbsa_plan_create_ex(device, *batch._args(), ctypes.byref(h)))
+        if batch.native_sigmas is not None:
+            _check(lib.pbsa_plan_create_np(device, *batch._args_np(), ctypes.byref(h)))
+        else:
+            _check(lib.pbsa_plan_create_ex(device, *batch._args(), ctypes.byref(h)))
         self._h = h
 
     def run(self) -> float:

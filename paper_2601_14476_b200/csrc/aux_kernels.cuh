@@ -129,6 +129,72 @@ __global__ void bucket_build(const uint32_t *__restrict__ pplanes, int nplanes,
     }
 }
 
+// Native variability profiles (rng = Philox, ExperimentSpec.native_profiles):
+// the reference draws lam ~ N(1, s_l^2), delta ~ N(0, s_d^2) and the period
+// max(1, rint(t_res (1 + nu))), nu ~ N(0, s_n^2), per p-bit with numpy
+// (pbit.py:57-75); here the three normals of (global trial g, node i) come
+// from one Philox4x32-10 block -- counter (i, g_hi, g_lo, tag 5) under the
+// plan's native seed -- through two Box-Muller pairs (u = (X + 1/2) 2^-32),
+// generated on the device at plan creation (no host sampling, no profile
+// upload).  Padding trials get the ideal profile; periods are clamped to
+// cycles * t_res, and a clamped period of 256 or more sets *overflow.
+constexpr uint32_t kNativeTagProfile = 5u;
+
+__device__ __forceinline__ void native_profile_of(uint32_t k0, uint32_t k1, uint64_t g, uint32_t i,
+                                                  double sl, double sd, double sn, int t_res,
+                                                  double &lam, double &del, int64_t &per) {
+    uint32_t o[4];
+    philox4x32_10(i, (uint32_t)(g >> 32), (uint32_t)g, kNativeTagProfile, k0, k1, o);
+    const double u0 = ((double)o[0] + 0.5) * 0x1p-32, u1 = ((double)o[1] + 0.5) * 0x1p-32;
+    const double u2 = ((double)o[2] + 0.5) * 0x1p-32, u3 = ((double)o[3] + 0.5) * 0x1p-32;
+    const double r0 = sqrt(-2.0 * log(u0)), r1 = sqrt(-2.0 * log(u2));
+    double s0, c0;
+    sincospi(2.0 * u1, &s0, &c0);
+    const double z3 = r1 * cospi(2.0 * u3);
+    lam = 1.0 + sl * (r0 * c0);
+    del = sd * (r0 * s0);
+    const double nu = sn * z3;
+    per = (int64_t)fmax(1.0, rint((double)t_res * (1.0 + nu)));
+}
+
+__global__ void native_profiles(uint32_t k0, uint32_t k1, uint64_t first_trial, int64_t T, int64_t Tp, int n,
+                                int t_res, double sl, double sd, double sn, int64_t maxcount,
+                                double *__restrict__ l64, double *__restrict__ d64,
+                                uint8_t *__restrict__ pcl, int *__restrict__ overflow) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Tp * (int64_t)n) return;
+    const int64_t t = g / n;
+    const int i = (int)(g % n);
+    if (t >= T) {
+        l64[g] = 1.0;
+        d64[g] = 0.0;
+        return;
+    }
+    double lam, del;
+    int64_t per;
+    native_profile_of(k0, k1, first_trial + (uint64_t)t, (uint32_t)i, sl, sd, sn, t_res, lam, del, per);
+    l64[g] = lam;
+    d64[g] = del;
+    const int64_t pc = per < maxcount ? per : maxcount;
+    if (pc >= 256) atomicOr(overflow, 1);
+    pcl[g] = (uint8_t)(pc < 256 ? pc : 255);
+}
+
+// The prefilter's profile pairs from the exact profile, rounded as the host
+// rounds them: fp16 node-major [W][n][32] (timing spread) or fp32 [Tp][n].
+__global__ void profile_pairs(const double *__restrict__ l64, const double *__restrict__ d64, int64_t Tp, int n,
+                              __half2 *__restrict__ prof16, float2 *__restrict__ prof) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= Tp * (int64_t)n) return;
+    const int64_t t = g / n;
+    const int i = (int)(g % n);
+    const double lam = l64[g], ld = lam * d64[g];
+    if (prof16)
+        prof16[((size_t)(t >> 5) * n + i) * 32 + (t & 31)] = __floats2half2_rn((float)lam, (float)ld);
+    else
+        prof[g] = make_float2((float)lam, (float)ld);
+}
+
 // Packed spins [W][n] -> int8 [T][n]
 __global__ void unpack_spins(const uint32_t *__restrict__ s, int8_t *__restrict__ out, int n,
                              int W, int T) {

@@ -762,7 +762,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                  const double *delta, const int64_t *period, int64_t pstride, double i0_min,
                  double beta, int64_t cycles, int64_t t_res, int algo, int64_t alpha,
                  double p_stall, int64_t trials, const uint64_t *keys, int rng_mode,
-                 uint64_t rng_seed, int64_t first_trial) {
+                 uint64_t rng_seed, int64_t first_trial, const double *native_sig = nullptr) {
     // ------------------------------------------------------- validation
     if (rng_mode != PBSA_RNG_REPLAY && rng_mode != PBSA_RNG_PHILOX)
         fail(PBSA_EINVAL, "rng_mode must be 0 (replay) or 1 (philox)");
@@ -785,6 +785,14 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     if (pstride != 0 && pstride != n) fail(PBSA_EINVAL, "profile_stride must be 0 or n");
     if ((lam == nullptr) != (delta == nullptr) || (lam == nullptr) != (period == nullptr))
         fail(PBSA_EINVAL, "lam, delta and period must all be given or all be NULL");
+    const bool native_prof = native_sig && (native_sig[0] != 0.0 || native_sig[1] != 0.0 || native_sig[2] != 0.0);
+    if (native_sig) {
+        if (lam) fail(PBSA_EINVAL, "native profiles take sigmas, not lam/delta/period arrays");
+        if (rng_mode != PBSA_RNG_PHILOX) fail(PBSA_EINVAL, "native profiles need rng_mode=philox");
+        for (int k = 0; k < 3; ++k)
+            if (!(std::isfinite(native_sig[k]) && native_sig[k] >= 0.0))
+                fail(PBSA_EINVAL, "native profile sigmas must be finite and >= 0");
+    }
     if (indptr[0] != 0) fail(PBSA_EINVAL, "indptr[0] must be 0");
     for (int64_t i = 0; i < n; ++i)
         if (indptr[i + 1] < indptr[i]) fail(PBSA_EINVAL, "indptr must be non-decreasing");
@@ -827,6 +835,41 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         }
     }
 
+    DeviceGuard dg(device);
+    CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
+    P.stream_holder.s = P.stream;
+    raise_pool_threshold(device);
+    AllocStream as(P.stream);
+    for (cudaEvent_t *e : {&P.ev_start, &P.ev_sweep0, &P.ev_sweep1, &P.ev_end}) CK(cudaEventCreate(e));
+    cudaStream_t st = P.stream;
+
+    // native profiles: drawn on the device (lam, delta fp64 [Tp][n] straight into
+    // the plan's exact-recheck buffers); the clamped periods come back to the
+    // host, which plans the sub-step launches and the period buckets from them
+    int64_t native_pmax = 0;
+    bool native_overflow = false;
+    if (native_prof) {
+        P.lam64.alloc((size_t)P.Tp * n);
+        P.del64.alloc((size_t)P.Tp * n);
+        DevBuf<uint8_t> pcl_dev;
+        pcl_dev.alloc((size_t)P.Tp * n);
+        DevBuf<int> ovf;
+        ovf.alloc(1);
+        CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), st));
+        pbsa::native_profiles<<<grid_for(P.Tp * n, 256), 256, 0, st>>>(
+            (uint32_t)rng_seed, (uint32_t)(rng_seed >> 32), (uint64_t)first_trial, trials, P.Tp, (int)n,
+            (int)t_res, native_sig[0], native_sig[1], native_sig[2], cycles * t_res, P.lam64.p, P.del64.p,
+            pcl_dev.p, ovf.p);
+        CK(cudaGetLastError());
+        P.pcl.resize((size_t)trials * n);
+        int ov = 0;
+        CK(cudaMemcpyAsync(P.pcl.data(), pcl_dev.p, P.pcl.size(), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&ov, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        native_overflow = ov != 0;
+        for (uint8_t pc : P.pcl) native_pmax = std::max<int64_t>(native_pmax, pc);
+    }
+
     // --------------------------------------------------- path selection
     bool unit_J = true, zero_h = true;
     int64_t dmax = 0;
@@ -836,7 +879,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         if (hv[i] != 0.0) zero_h = false;
         dmax = std::max<int64_t>(dmax, indptr[i + 1] - indptr[i]);
     }
-    bool ideal = true;
+    bool ideal = !native_prof;
     if (lam) {
         for (int64_t k = 0; k < prow * n && ideal; ++k)
             if (lam[k] != 1.0 || delta[k] != 0.0 || period[k] != t_res) ideal = false;
@@ -864,12 +907,16 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     // clamped periods below 256 (bit-sliced in at most 8 planes)
     const int64_t maxcount = cycles * t_res;
     // (PBSA_PACKED_VAR=0 sends variability runs to the active-list kernels)
-    bool var_ok = lam && !ideal && (algo == 0 || (algo == 2 && p_stall == 0.0));
+    bool var_ok = (lam || native_prof) && !ideal && (algo == 0 || (algo == 2 && p_stall == 0.0));
     const char *venv = std::getenv("PBSA_PACKED_VAR");
     if (venv) var_ok = var_ok && venv[0] != '0';
     int64_t pmax = 0;
     bool var_uniform = true;
-    if (var_ok) {
+    if (var_ok && native_prof) {
+        pmax = native_pmax;
+        var_uniform = native_sig[2] == 0.0;
+        var_ok = !native_overflow;
+    } else if (var_ok) {
         for (int64_t k = 0; k < prow * n && var_ok; ++k) {
             var_ok = std::isfinite(lam[k]) && std::isfinite(delta[k]);
             const int64_t pc = std::min<int64_t>(period[k], maxcount);
@@ -880,6 +927,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     }
     const bool packed = (((rule_is_psa || tapsa_packed || spsa_packed) && ideal) || var_ok) && unit_J &&
                         zero_h && graph_is_model && dmax <= 127 && small_counters;
+    if (native_prof && !(packed && var_ok))
+        fail(PBSA_EINVAL, "native profiles run on the packed path only: a +-1 MAX-CUT model of degree "
+                          "<= 127, the plain rule, and clamped periods below 256");
     if (rng_mode == PBSA_RNG_PHILOX && !packed)
         fail(PBSA_EINVAL, "rng_mode=philox runs on the packed path only: a +-1 MAX-CUT model of "
                           "degree <= 127 with pSA/TApSA/SpSA on an ideal profile, or the plain rule "
@@ -895,13 +945,6 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
     P.tapsa_hist_from_raw = packed && algo == 1 && !P.tapsa_packed;
     P.path = packed ? PBSA_PATH_PACKED : PBSA_PATH_GENERAL;
 
-    DeviceGuard dg(device);
-    CK(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking));
-    P.stream_holder.s = P.stream;
-    raise_pool_threshold(device);
-    AllocStream as(P.stream);
-    for (cudaEvent_t *e : {&P.ev_start, &P.ev_sweep0, &P.ev_sweep1, &P.ev_end}) CK(cudaEventCreate(e));
-    cudaStream_t st = P.stream;
 
     // per-trial key prefixes (streams.py: draws are absorb^3(key, tag, a, b))
     std::vector<uint64_t> kspin, kr, kst;
@@ -995,33 +1038,42 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             // DRAM bursts that the [W][32][n] layout spreads over 32 rows
             const int64_t Tp = P.Tp;
             const bool node_major = !P.var_uniform;
-            std::vector<float2> pf(node_major ? 0 : (size_t)Tp * n, make_float2(1.0f, 0.0f));
-            std::vector<__half2> pf16(node_major ? (size_t)Tp * n : 0, __floats2half2_rn(1.0f, 0.0f));
-            std::vector<double> l64((size_t)Tp * n, 1.0), d64((size_t)Tp * n, 0.0);
-            parallel_for(trials, 16, [&](int64_t t0, int64_t t1) {
-                for (int64_t t = t0; t < t1; ++t)
-                    for (int64_t i = 0; i < n; ++i) {
-                        const size_t src = (size_t)(pstride ? t * n : 0) + i, dst = (size_t)t * n + i;
-                        const size_t pdst = node_major ? ((size_t)(t >> 5) * n + i) * 32 + (t & 31) : dst;
-                        l64[dst] = lam[src];
-                        d64[dst] = delta[src];
-                        // timing kernels: fp16 pair (overflow -> inf -> the exact recheck)
-                        if (node_major)
-                            pf16[pdst] = __floats2half2_rn((float)lam[src], (float)(lam[src] * delta[src]));
-                        else
-                            pf[pdst] = make_float2((float)lam[src], (float)(lam[src] * delta[src]));
-                    }
-            });
-            if (node_major) P.prof16.upload(pf16, st); else P.prof.upload(pf, st);
-            P.lam64.upload(l64, st);
-            P.del64.upload(d64, st);
+            if (native_prof) {  // pairs from the device-drawn exact profile
+                if (node_major) P.prof16.alloc((size_t)Tp * n); else P.prof.alloc((size_t)Tp * n);
+                pbsa::profile_pairs<<<grid_for(Tp * n, 256), 256, 0, st>>>(
+                    P.lam64.p, P.del64.p, Tp, (int)n, node_major ? P.prof16.p : nullptr,
+                    node_major ? nullptr : P.prof.p);
+                CK(cudaGetLastError());
+            } else {
+                std::vector<float2> pf(node_major ? 0 : (size_t)Tp * n, make_float2(1.0f, 0.0f));
+                std::vector<__half2> pf16(node_major ? (size_t)Tp * n : 0, __floats2half2_rn(1.0f, 0.0f));
+                std::vector<double> l64((size_t)Tp * n, 1.0), d64((size_t)Tp * n, 0.0);
+                parallel_for(trials, 16, [&](int64_t t0, int64_t t1) {
+                    for (int64_t t = t0; t < t1; ++t)
+                        for (int64_t i = 0; i < n; ++i) {
+                            const size_t src = (size_t)(pstride ? t * n : 0) + i, dst = (size_t)t * n + i;
+                            const size_t pdst = node_major ? ((size_t)(t >> 5) * n + i) * 32 + (t & 31) : dst;
+                            l64[dst] = lam[src];
+                            d64[dst] = delta[src];
+                            // timing kernels: fp16 pair (overflow -> inf -> the exact recheck)
+                            if (node_major)
+                                pf16[pdst] = __floats2half2_rn((float)lam[src], (float)(lam[src] * delta[src]));
+                            else
+                                pf[pdst] = make_float2((float)lam[src], (float)(lam[src] * delta[src]));
+                        }
+                });
+                if (node_major) P.prof16.upload(pf16, st); else P.prof.upload(pf, st);
+                P.lam64.upload(l64, st);
+                P.del64.upload(d64, st);
+
+            }
             P.inp_var.alloc((size_t)Tp * n);
             if (!P.var_uniform) {
                 // clamped periods (a period >= cycles * t_res fires only at count 0),
                 // bit-sliced per word: plane k bit b = bit k of trial 32w+b's period
                 P.nplanes = 1;
                 while ((1LL << P.nplanes) <= P.pmax) ++P.nplanes;
-                P.pcl.assign((size_t)trials * n, 0);
+                if (!native_prof) P.pcl.assign((size_t)trials * n, 0);
                 std::vector<uint32_t> planes((size_t)P.W * P.nplanes * n, 0u);
                 parallel_for(P.W, 1, [&](int64_t w0, int64_t w1) {
                     for (int64_t w = w0; w < w1; ++w)
@@ -1029,7 +1081,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                             const int64_t t = w * 32 + b;
                             for (int64_t i = 0; i < n; ++i) {
                                 int64_t pc = t_res;
-                                if (t < trials) {
+                                if (t < trials && native_prof) {
+                                    pc = P.pcl[(size_t)t * n + i];
+                                } else if (t < trials) {
                                     pc = std::min<int64_t>(period[(pstride ? t * n : 0) + i], maxcount);
                                     P.pcl[(size_t)t * n + i] = (uint8_t)pc;
                                 }
@@ -2037,14 +2091,18 @@ int pbsa_plan_create(int device, int64_t n, const int64_t *indptr, const int64_t
                                0, 0, out);
 }
 
-int pbsa_plan_create_ex(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
-                        const double *values, const double *h, int64_t mm, const int64_t *me_i,
-                        const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
-                        const int64_t *ge_j, const int64_t *ge_w, const double *lam,
-                        const double *delta, const int64_t *period, int64_t profile_stride,
-                        double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
-                        int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
-                        int rng_mode, uint64_t rng_seed, int64_t first_trial, pbsa_plan **out) {
+}  // extern "C"
+
+namespace {
+int plan_create_impl(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                     const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                     const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                     const int64_t *ge_j, const int64_t *ge_w, const double *lam,
+                     const double *delta, const int64_t *period, int64_t profile_stride,
+                     double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                     int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                     int rng_mode, uint64_t rng_seed, int64_t first_trial, const double *native_sig,
+                     pbsa_plan **out) {
     return guarded([&] {
         if (!out) fail(PBSA_EINVAL, "null plan out-pointer");
         *out = nullptr;
@@ -2052,7 +2110,7 @@ int pbsa_plan_create_ex(int device, int64_t n, const int64_t *indptr, const int6
         std::unique_ptr<pbsa_plan> P(new pbsa_plan());
         create_plan(*P, device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm, ge_i,
                     ge_j, ge_w, lam, delta, period, profile_stride, i0_min, beta, cycles, t_res,
-                    algo, alpha, p_stall, trials, keys, rng_mode, rng_seed, first_trial);
+                    algo, alpha, p_stall, trials, keys, rng_mode, rng_seed, first_trial, native_sig);
         DeviceGuard dg(device);
         P->mm_ = mm;
         P->gm_ = gm;
@@ -2077,6 +2135,39 @@ int pbsa_plan_create_ex(int device, int64_t n, const int64_t *indptr, const int6
         CK(e);
         *out = P.release();
     });
+}
+}  // namespace
+
+extern "C" {
+
+int pbsa_plan_create_ex(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                        const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                        const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                        const int64_t *ge_j, const int64_t *ge_w, const double *lam,
+                        const double *delta, const int64_t *period, int64_t profile_stride,
+                        double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                        int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                        int rng_mode, uint64_t rng_seed, int64_t first_trial, pbsa_plan **out) {
+    return plan_create_impl(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm, ge_i, ge_j,
+                            ge_w, lam, delta, period, profile_stride, i0_min, beta, cycles, t_res, algo,
+                            alpha, p_stall, trials, keys, rng_mode, rng_seed, first_trial, nullptr, out);
+}
+
+int pbsa_plan_create_np(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                        const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                        const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                        const int64_t *ge_j, const int64_t *ge_w, const double *native_sigmas,
+                        double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                        int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                        uint64_t rng_seed, int64_t first_trial, pbsa_plan **out) {
+    if (!native_sigmas) {
+        g_last_error = "null native_sigmas";
+        return PBSA_EINVAL;
+    }
+    return plan_create_impl(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm, ge_i, ge_j,
+                            ge_w, nullptr, nullptr, nullptr, 0, i0_min, beta, cycles, t_res, algo, alpha,
+                            p_stall, trials, keys, PBSA_RNG_PHILOX, rng_seed, first_trial, native_sigmas,
+                            out);
 }
 
 int pbsa_plan_run(pbsa_plan *P, float *device_ms) {
@@ -2840,6 +2931,89 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
     pbsa_plan_destroy(P);
     if (rc != PBSA_OK) g_last_error = err;
     return rc;
+}
+
+int pbsa_anneal_loop_batch_np(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                              const double *values, const double *h, int64_t mm, const int64_t *me_i,
+                              const int64_t *me_j, const double *me_w, int64_t gm, const int64_t *ge_i,
+                              const int64_t *ge_j, const int64_t *ge_w, const double *native_sigmas,
+                              double i0_min, double beta, int64_t cycles, int64_t t_res, int algo,
+                              int64_t alpha, double p_stall, int64_t trials, const uint64_t *keys,
+                              uint64_t rng_seed, int64_t first_trial, int8_t *spins, double *inputs,
+                              double *hist, int64_t *counts, double *trace_i0, double *trace_energy,
+                              int64_t *trace_cut, int64_t *best_cut, float *device_ms) {
+    if (!native_sigmas) {
+        g_last_error = "null native_sigmas";
+        return PBSA_EINVAL;
+    }
+    if (native_sigmas[0] == 0.0 && native_sigmas[1] == 0.0 && native_sigmas[2] == 0.0)  // the ideal profile
+        return pbsa_anneal_loop_batch_ex(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm, ge_i,
+                                         ge_j, ge_w, nullptr, nullptr, nullptr, 0, i0_min, beta, cycles, t_res,
+                                         algo, alpha, p_stall, trials, keys, PBSA_RNG_PHILOX, rng_seed,
+                                         first_trial, spins, inputs, hist, counts, trace_i0, trace_energy,
+                                         trace_cut, best_cut, device_ms);
+    pbsa_plan *P = nullptr;
+    g_oneshot = true;
+    int rc = pbsa_plan_create_np(device, n, indptr, indices, values, h, mm, me_i, me_j, me_w, gm, ge_i,
+                                 ge_j, ge_w, native_sigmas, i0_min, beta, cycles, t_res, algo, alpha,
+                                 p_stall, trials, keys, rng_seed, first_trial, &P);
+    g_oneshot = false;
+    if (rc != PBSA_OK) return rc;
+    rc = guarded([&] {
+        if (!P->graph_exec) fail(PBSA_EINVAL, "native-profile plan was not captured");
+        DeviceGuard dg(P->device);
+        CK(cudaEventRecord(P->ev_start, P->stream));
+        CK(cudaGraphLaunch(P->graph_exec, P->stream));
+        CK(cudaEventRecord(P->ev_end, P->stream));
+        host_constant_outputs(P, hist, counts, trace_i0);
+        CK(cudaEventSynchronize(P->ev_end));
+        P->ran = true;
+        if (device_ms) CK(cudaEventElapsedTime(device_ms, P->ev_start, P->ev_end));
+        download_impl(P, spins, inputs, hist, counts, trace_i0, trace_energy, trace_cut, best_cut, true);
+    });
+    const std::string err = g_last_error;
+    pbsa_plan_bytes(P, &g_call_h2d, &g_call_d2h);
+    pbsa_plan_destroy(P);
+    if (rc != PBSA_OK) g_last_error = err;
+    return rc;
+}
+
+int pbsa_native_profiles(int device, uint64_t rng_seed, int64_t first_trial, int64_t trials, int64_t n,
+                         int64_t t_res, int64_t cycles, const double *native_sigmas, double *lam,
+                         double *delta, int64_t *period) {
+    return guarded([&] {
+        if (!native_sigmas || !lam || !delta || !period) fail(PBSA_EINVAL, "null pointer");
+        if (trials < 1 || n < 1 || t_res < 1 || cycles < 1) fail(PBSA_EINVAL, "sizes must be >= 1");
+        DeviceGuard dg(device);
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        StreamHolder sh;
+        sh.s = st;
+        AllocStream as(st);
+        const size_t cnt = (size_t)trials * n;
+        DevBuf<double> l64, d64;
+        DevBuf<uint8_t> pcl;
+        DevBuf<int> ovf;
+        l64.alloc(cnt);
+        d64.alloc(cnt);
+        pcl.alloc(cnt);
+        ovf.alloc(1);
+        CK(cudaMemsetAsync(ovf.p, 0, sizeof(int), st));
+        pbsa::native_profiles<<<grid_for((int64_t)cnt, 256), 256, 0, st>>>(
+            (uint32_t)rng_seed, (uint32_t)(rng_seed >> 32), (uint64_t)first_trial, trials, trials, (int)n,
+            (int)t_res, native_sigmas[0], native_sigmas[1], native_sigmas[2], cycles * t_res, l64.p, d64.p,
+            pcl.p, ovf.p);
+        CK(cudaGetLastError());
+        std::vector<uint8_t> pc(cnt);
+        int ov = 0;
+        CK(cudaMemcpyAsync(lam, l64.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(delta, d64.p, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(pc.data(), pcl.p, cnt, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&ov, ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (ov) fail(PBSA_EINVAL, "a native period reaches 256 after clamping to cycles * t_res");
+        for (size_t k = 0; k < cnt; ++k) period[k] = pc[k];
+    });
 }
 
 int pbsa_anneal_loop_batch_devices(const int *devices, int ndev, int64_t n, const int64_t *indptr,

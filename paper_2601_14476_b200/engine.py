@@ -47,10 +47,16 @@ class ExperimentSpec:
     # library-owned host thread and plan per device; results identical to one
     # device); None reads PBSA_DEVICES, else one device (PBSA_DEVICE / LOCAL_RANK)
     devices: tuple | None = None
+    # not in the reference: with rng="philox", draw every trial's variability
+    # profile on the device from the native stream (pbsa_plan_create_np) instead
+    # of numpy's generator -- statistically, not bitwise, the reference's
+    native_profiles: bool = False
 
     def __post_init__(self) -> None:
         if self.rng not in ("replay", "philox"):
             raise ValueError(f"rng must be 'replay' or 'philox', got {self.rng!r}")
+        if self.native_profiles and self.rng != "philox":
+            raise ValueError("native_profiles needs rng='philox'")
         if self.cycles < 2:
             raise ValueError("cycles must be >= 2")
         if self.trials < 1:
@@ -110,7 +116,12 @@ def run_trial_range(spec: ExperimentSpec, graph: MaxCutGraph, start: int, stop: 
     all_seeds = streams.trial_seeds(spec.base_seed, stop, 0)
     seeds = all_seeds[start:stop]
     t0 = time.perf_counter()
-    if spec.resample_variability:
+    cfg = spec.variability
+    native = spec.native_profiles and not (cfg.sigma_lambda == 0.0 and cfg.sigma_delta == 0.0 and
+                                           cfg.sigma_nu == 0.0)
+    if native:  # drawn on the device from the native stream
+        profs = None
+    elif spec.resample_variability:
         profs = trial_profiles(spec, model.n, seeds)
     else:
         profs = trial_profiles(spec, model.n, all_seeds[:1])
@@ -118,11 +129,15 @@ def run_trial_range(spec: ExperimentSpec, graph: MaxCutGraph, start: int, stop: 
                           profile_rows=profile_rows(profs, model.n), graph=graph,
                           algo_code=spec.algo.kind.code, alpha=spec.algo.kernel_alpha,
                           p_stall=spec.algo.p_stall, rng=spec.rng,
-                          rng_seed=streams.native_seed(spec.base_seed), first_trial=start)
+                          rng_seed=streams.native_seed(spec.base_seed), first_trial=start,
+                          native_sigmas=(cfg.sigma_lambda, cfg.sigma_delta, cfg.sigma_nu) if native else None)
     devs = None
     if device is None:
         devs = list(spec.devices) if spec.devices is not None else _native.device_list()
     try:
+        if devs is not None and len(devs) > 1 and native:
+            # (the library's device fan-out takes profile arrays: shard here)
+            return _native_shards(spec, graph, start, stop, devs), time.perf_counter() - t0
         if devs is not None and len(devs) > 1:
             out, _ = _native.anneal_batch_devices(batch, devs)
         else:
@@ -132,6 +147,20 @@ def run_trial_range(spec: ExperimentSpec, graph: MaxCutGraph, start: int, stop: 
         raise RuntimeError(f"trials {start}..{stop - 1} of {spec.graph!r} failed: {exc}") from exc
     elapsed = time.perf_counter() - t0
     return results_from_batch(out, seeds, schedule, True), elapsed
+
+
+def _native_shards(spec: ExperimentSpec, graph: MaxCutGraph, start: int, stop: int, devs):
+    """Native-profile trials [start, stop) over several devices: 4-aligned
+    shards (the Philox groups), one host thread per device, trial order kept."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from .distributed import shard_range
+    spans = [shard_range(stop - start, r, len(devs)) for r in range(len(devs))]
+    with ThreadPoolExecutor(len(devs)) as ex:
+        parts = list(ex.map(lambda a: run_trial_range(spec, graph, start + a[0][0], start + a[0][1],
+                                                      device=a[1])[0] if a[0][1] > a[0][0] else [],
+                            zip(spans, devs)))
+    return [r for part in parts for r in part]
 
 
 def run_trials(spec: ExperimentSpec, graphs: Mapping[str, MaxCutGraph],

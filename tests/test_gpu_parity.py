@@ -1066,3 +1066,62 @@ def test_degree_order_is_bitwise_neutral(oracle, bench_graphs, monkeypatch, name
                                graph=g, **extra)
     for k in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
         assert np.array_equal(got[k], want[k]), k
+
+
+# ------------------------------------------ native (device-drawn) variability profiles
+
+def test_native_profiles_are_the_reference_distributions():
+    """pbsa_native_profiles: lam ~ N(1, s_l^2), delta ~ N(0, s_d^2),
+    period = max(1, rint(t_res (1 + N(0, s_n^2)))) (pbit.py:57-75) -- moments,
+    the period histogram against numpy's draw of the same law, shard
+    invariance (trial k's profile depends only on its global index)."""
+    sig = (0.5, 0.3, 0.5)
+    lam, delta, per = _native.native_profiles(0xABC, 0, 512, 4000, 10, 1000, sig)
+    assert abs(lam.mean() - 1.0) < 0.003 and abs(lam.std() - 0.5) < 0.003
+    assert abs(delta.mean()) < 0.002 and abs(delta.std() - 0.3) < 0.002
+    ref = sample_variability(VariabilityConfig(*sig), 2_048_000, np.random.default_rng(3)).period
+    for p in range(1, 25):
+        assert abs((per == p).mean() - (ref == p).mean()) < 0.003, p
+    lam2, delta2, per2 = _native.native_profiles(0xABC, 256, 256, 4000, 10, 1000, sig)
+    assert np.array_equal(lam[256:], lam2) and np.array_equal(per[256:], per2)
+    assert np.array_equal(delta[256:], delta2)
+
+
+@pytest.mark.parametrize("name,sig,trials,cycles", [("G81", (0.5, 0.5, 0.5), 96, 30),
+                                                    ("G55", (0.7, 0.2, 0.0), 64, 40),
+                                                    ("G1", (0.0, 0.0, 0.8), 40, 30)])
+def test_native_profile_runs_match_oracle_on_their_profiles(oracle, bench_graphs, name, sig, trials,
+                                                            cycles):
+    """A native-profile plan (profiles drawn on the device at plan creation,
+    bucket / plain variability kernels) equals the oracle's Philox run on the
+    same profiles, fetched with pbsa_native_profiles."""
+    g = bench_graphs(name)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, cycles, 10)
+    seed = 0x51DE_5EED
+    keys = [streams.run_key(streams.trial_seed(9, k)) for k in range(trials)]
+    b = _native.Batch(model, sch, keys, graph=g, rng="philox", rng_seed=seed, native_sigmas=sig)
+    got, _ = _native.anneal_batch(b)
+    lam, delta, per = _native.native_profiles(seed, 0, trials, g.n, 10, cycles, sig)
+    profs = [VariabilityProfile(lam[k], delta[k], per[k], 10) for k in range(trials)]
+    want = oracle.anneal_batch(model, sch, "psa", profs, keys, graph=g, rng="philox", rng_seed=seed)
+    for k in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
+
+
+@pytest.mark.parametrize("name,sig,trials", [("G81", (0.5, 0.5, 0.5), 256), ("G1", (0.0, 0.0, 0.5), 128),
+                                             ("G55", (1.0, 0.0, 0.0), 256)])
+def test_native_profile_cut_statistics_match_reference(bench_graphs, golden_analogs, name, sig, trials):
+    """ExperimentSpec(rng='philox', native_profiles=True): the profiles come
+    from the device, not numpy; mean final cut and mean per-trial best cut
+    within 0.5 % of the best-known cut of the reference's replayed run."""
+    g = bench_graphs(name)
+    best_known = golden_analogs[name]["best_known_analog"]
+    spec = engine.ExperimentSpec(graph=name, algo=AlgorithmConfig(Algorithm.PSA),
+                                 variability=VariabilityConfig(*sig), cycles=1000, trials=trials)
+    rep = engine.run_trials(spec, {name: g})
+    nat = engine.run_trials(dataclasses.replace(spec, rng="philox", native_profiles=True), {name: g})
+    assert abs(nat.mean_cut - rep.mean_cut) <= 0.005 * best_known, (nat.mean_cut, rep.mean_cut)
+    b_rep = np.mean([r.best_cut for r in rep.results])
+    b_nat = np.mean([r.best_cut for r in nat.results])
+    assert abs(b_nat - b_rep) <= 0.005 * best_known, (b_nat, b_rep)
