@@ -180,6 +180,11 @@ __global__ void native_profiles(uint32_t k0, uint32_t k1, uint64_t first_trial, 
     pcl[g] = (uint8_t)(pc < 256 ? pc : 255);
 }
 
+__global__ void fill_f64(double *__restrict__ p, int64_t n, double v) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n) p[g] = v;
+}
+
 // The prefilter's profile pairs from the exact profile, rounded as the host
 // rounds them: fp16 node-major [W][n][32] (timing spread) or fp32 [Tp][n].
 __global__ void profile_pairs(const double *__restrict__ l64, const double *__restrict__ d64, int64_t Tp, int n,

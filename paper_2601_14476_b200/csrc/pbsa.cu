@@ -282,6 +282,7 @@ struct pbsa_plan {
     // copied to the caller's host buffers on out_stream while the next computes
     bool pipelined = false;
     bool capturing_outputs = false;    // a cached one-shot plan: phase outputs inside the graph
+    bool direct = false;               // one-shot: launched directly, no graph (instantiation costs more)
     std::vector<std::pair<cudaGraphNode_t, int>> out_nodes;  // its D2H copy nodes and output index
     std::vector<size_t> out_node_off;  // destination byte offset of each node in its output
     std::vector<size_t> out_node_bytes;
@@ -1038,7 +1039,22 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             // DRAM bursts that the [W][32][n] layout spreads over 32 rows
             const int64_t Tp = P.Tp;
             const bool node_major = !P.var_uniform;
-            if (native_prof) {  // pairs from the device-drawn exact profile
+            if (!native_prof && pstride == n) {
+                // per-trial rows already in the plan's [trial][node] layout: upload
+                // the exact profile as given (padding rows ideal) and round the
+                // prefilter pairs on the device (no host copies or conversion)
+                P.lam64.alloc((size_t)Tp * n);
+                P.del64.alloc((size_t)Tp * n);
+                CK(cudaMemcpyAsync(P.lam64.p, lam, (size_t)trials * n * sizeof(double), cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(P.del64.p, delta, (size_t)trials * n * sizeof(double), cudaMemcpyHostToDevice, st));
+                P.lam64.bytes_up = P.del64.bytes_up = (size_t)trials * n * sizeof(double);
+                if (Tp > trials) {
+                    pbsa::fill_f64<<<grid_for((Tp - trials) * n, 256), 256, 0, st>>>(
+                        P.lam64.p + (size_t)trials * n, (Tp - trials) * n, 1.0);
+                    CK(cudaMemsetAsync(P.del64.p + (size_t)trials * n, 0, (size_t)(Tp - trials) * n * sizeof(double), st));
+                }
+            }
+            if (native_prof || pstride == n) {  // pairs from the device copy of the exact profile
                 if (node_major) P.prof16.alloc((size_t)Tp * n); else P.prof.alloc((size_t)Tp * n);
                 pbsa::profile_pairs<<<grid_for(Tp * n, 256), 256, 0, st>>>(
                     P.lam64.p, P.del64.p, Tp, (int)n, node_major ? P.prof16.p : nullptr,
@@ -1508,8 +1524,9 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
 // The sweep-interval events are external event nodes inside a captured graph;
 // a directly launched (pipelined) run records them normally.
 cudaError_t record_sweep_event(const pbsa_plan &P, cudaEvent_t ev, cudaStream_t st) {
-    return P.pipelined && !P.capturing_outputs ? cudaEventRecord(ev, st)
-                                               : cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+    return (P.pipelined || P.direct) && !P.capturing_outputs
+               ? cudaEventRecord(ev, st)
+               : cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
 }
 
 // Pipelined one-shot: once the words [w0, w1) have finished their last cut
@@ -1723,115 +1740,122 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                 for (cudaStream_t cs : P.chain_streams) CK(cudaStreamWaitEvent(cs, P.ev_fork, 0));
             }
             const int64_t per = (p1 - p0 + G - 1) / G;
-            for (int g = 0; g < G; ++g) {
-                const int64_t w0 = p0 + g * per, w1 = std::min<int64_t>(p1, w0 + per);
-                if (w0 >= w1) continue;
-                cudaStream_t cs = g == 0 ? st : P.chain_streams[g - 1];
-                const int blocks = (int)grid_for((w1 - w0) * P.warps_per_word, pbsa::kPackedWarps);
-                cur = 0;
-                for (const pbsa_plan::PLaunch &pl : P.plaunch) {
-                    const int64_t c = pl.cycle;
-                    pbsa::PackedArgs a{};
-                    a.sold = P.p_spins[cur].p + w0 * P.n;
-                    a.snew = P.p_spins[cur ^ 1].p + w0 * P.n;
-                    a.rowptr = P.rowptr.p;
-                    a.adj = P.adj.n ? P.adj.p : nullptr;
-                    a.adj16 = P.adj16.n ? P.adj16.p : nullptr;
-                    a.order = P.order.n ? P.order.p : nullptr;
-                    a.krg = P.krg.p + w0 * 32;
-                    a.kfc = P.kfc.p + w0 * 32;
-                    a.acache = P.use_cache ? P.acache.p + (size_t)(w0 - p0) * P.chunks * 1024 : nullptr;
-                    const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
-                    a.thr = P.thr.p + (size_t)cc * P.K;
-                    a.pacc = P.pacc.p + (size_t)c * P.Tp + w0 * 32;
-                    a.raw_out = (c == P.cycles - 1 && !P.var_mode) ? P.raw_last.p + w0 * 32 : nullptr;
-                    a.n = (int)P.n;
-                    a.W = (int)(w1 - w0);
-                    a.Tp = (int)P.Tp;
-                    a.K = P.K;
-                    a.dmax = P.dmax;
-                    a.warps_per_word = P.warps_per_word;
-                    a.cta_flush = (P.cta_flush && P.warps_per_word % pbsa::kPackedWarps == 0) ? 1 : 0;
-                    a.chunks = P.chunks;
-                    a.count = pl.count;
-                    a.do_update = pl.update;
-                    a.reg4 = P.reg4 ? 1 : 0;
-                    if (P.native) {
-                        a.nk0 = (uint32_t)P.nseed;
-                        a.nk1 = (uint32_t)(P.nseed >> 32);
-                        a.ngroup = (uint32_t)((P.first_trial + w0 * 32) / 4);
-                        pbsa::philox_round_keys(a.nk0, a.nk1, a.rk);
-                    }
-                    a.do_cut = pl.do_cut;
-                    if (P.var_mode) {
-                        const size_t off = (size_t)w0 * 32 * P.n;
-                        a.prof = P.var_uniform ? P.prof.p + off : nullptr;
-                        a.prof16 = P.var_uniform ? nullptr : P.prof16.p + off;
-                        a.lam64 = P.lam64.p + off;
-                        a.del64 = P.del64.p + off;
-                        a.pplanes = P.var_uniform ? nullptr : P.pplanes.p + (size_t)w0 * P.nplanes * P.n;
-                        a.divs = P.var_uniform ? nullptr : (P.bucket ? P.bdivs.p : P.vdivs.p) + pl.div_off;
-                        if (P.bucket) {
-                            const size_t toff = (size_t)w0 * P.chunks;
-                            a.brec = P.brec.p + toff * 1024;
-                            a.boff = P.boff.p + toff * (P.nclass + 1);
-                            a.nclass = P.nclass;
-                            a.cper = P.bcper.p;
-                            a.maxcount = (uint32_t)(P.cycles * P.t_res);
+            // launches interleaved across the chains (round robin), so a directly
+            // launched run fills every chain's queue evenly; a captured graph is
+            // the same either way (each chain keeps its own order)
+            std::vector<int> cur_g(G, 0);
+            for (const pbsa_plan::PLaunch &pl : P.plaunch) {
+                for (int g = 0; g < G; ++g) {
+                    const int64_t w0 = p0 + g * per, w1 = std::min<int64_t>(p1, w0 + per);
+                    if (w0 >= w1) continue;
+                    cudaStream_t cs = g == 0 ? st : P.chain_streams[g - 1];
+                    const int blocks = (int)grid_for((w1 - w0) * P.warps_per_word, pbsa::kPackedWarps);
+                    int &cur = cur_g[g];
+                        const int64_t c = pl.cycle;
+                        pbsa::PackedArgs a{};
+                        a.sold = P.p_spins[cur].p + w0 * P.n;
+                        a.snew = P.p_spins[cur ^ 1].p + w0 * P.n;
+                        a.rowptr = P.rowptr.p;
+                        a.adj = P.adj.n ? P.adj.p : nullptr;
+                        a.adj16 = P.adj16.n ? P.adj16.p : nullptr;
+                        a.order = P.order.n ? P.order.p : nullptr;
+                        a.krg = P.krg.p + w0 * 32;
+                        a.kfc = P.kfc.p + w0 * 32;
+                        a.acache = P.use_cache ? P.acache.p + (size_t)(w0 - p0) * P.chunks * 1024 : nullptr;
+                        const int64_t cc = std::min<int64_t>(c, P.cycles - 1);
+                        a.thr = P.thr.p + (size_t)cc * P.K;
+                        a.pacc = P.pacc.p + (size_t)c * P.Tp + w0 * 32;
+                        a.raw_out = (c == P.cycles - 1 && !P.var_mode) ? P.raw_last.p + w0 * 32 : nullptr;
+                        a.n = (int)P.n;
+                        a.W = (int)(w1 - w0);
+                        a.Tp = (int)P.Tp;
+                        a.K = P.K;
+                        a.dmax = P.dmax;
+                        a.warps_per_word = P.warps_per_word;
+                        a.cta_flush = (P.cta_flush && P.warps_per_word % pbsa::kPackedWarps == 0) ? 1 : 0;
+                        a.chunks = P.chunks;
+                        a.count = pl.count;
+                        a.do_update = pl.update;
+                        a.reg4 = P.reg4 ? 1 : 0;
+                        if (P.native) {
+                            a.nk0 = (uint32_t)P.nseed;
+                            a.nk1 = (uint32_t)(P.nseed >> 32);
+                            a.ngroup = (uint32_t)((P.first_trial + w0 * 32) / 4);
+                            pbsa::philox_round_keys(a.nk0, a.nk1, a.rk);
                         }
-                        a.ndiv = pl.ndiv;
-                        a.nplanes = P.nplanes;
-                        a.i0 = P.i0[cc];
-                        a.i0f = (float)P.i0[cc];
-                        a.margin = P.var_margin;
-                        a.inp_out = pl.inp ? P.inp_var.p + off : nullptr;
-                    }
-                    if (P.spsa_packed) {
-                        a.sidx = P.sidx.p + (size_t)w0 * 32 * P.n;
-                        a.thr_hi_all = P.thr_hi.p;
-                        a.kfs = P.kfs.p + w0 * 32;
-                        a.kst = P.kstg.p + w0 * 32;
-                        a.thr_all = P.thr.p;
-                        a.p_stall64 = P.p_stall64;
-                        a.cycle = (int)cc;
-                        a.Kc = P.K;
-                        a.sidx_full = P.sidx_full ? 1 : 0;
-                    }
-                    if (P.tapsa_packed) {
-                        a.ring = P.ring.p + (size_t)w0 * P.alpha * P.L * P.n;
-                        a.alpha = (int)P.alpha;
-                        a.slot = (int)(cc % P.alpha);
-                        a.filled = (int)std::min<int64_t>(cc + 1, P.alpha);
-                    }
-                    {
-                        // programmatic dependent launch: the next sub-step's prologue
-                        // overlaps this one's tail (the kernel waits on griddepcontrol)
-                        cudaLaunchConfig_t cfg{};
-                        cfg.gridDim = dim3((unsigned)blocks);
-                        cfg.blockDim = dim3(pbsa::kPackedThreads);
-                        cfg.dynamicSmemBytes = (pl.update && P.var_mode && !P.var_uniform)
-                                                   ? (P.bucket ? pbsa::bucket_smem_bytes(P.L) : pbsa::kTimingSmem)
-                                                   : smem;
-                        cfg.stream = cs;
-                        cudaLaunchAttribute attr[1];
-                        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-                        attr[0].val.programmaticStreamSerializationAllowed = P.use_pdl ? 1 : 0;
-                        cfg.attrs = attr;
-                        cfg.numAttrs = 1;
-                        CK(cudaLaunchKernelEx(&cfg, pl.update ? kern_up : kern_cut, a));
-                    }
-                    CK(cudaGetLastError());
-                    ++P.launches;
-                    if (pl.update) {
-                        if (g == 0 && p0 == 0) ++P.sweep_launches;
-                        cur ^= 1;
-                    }
-                }
-                if (g > 0) {
-                    CK(cudaEventRecord(P.ev_join[g - 1], cs));
-                    CK(cudaStreamWaitEvent(st, P.ev_join[g - 1], 0));
+                        a.do_cut = pl.do_cut;
+                        if (P.var_mode) {
+                            const size_t off = (size_t)w0 * 32 * P.n;
+                            a.prof = P.var_uniform ? P.prof.p + off : nullptr;
+                            a.prof16 = P.var_uniform ? nullptr : P.prof16.p + off;
+                            a.lam64 = P.lam64.p + off;
+                            a.del64 = P.del64.p + off;
+                            a.pplanes = P.var_uniform ? nullptr : P.pplanes.p + (size_t)w0 * P.nplanes * P.n;
+                            a.divs = P.var_uniform ? nullptr : (P.bucket ? P.bdivs.p : P.vdivs.p) + pl.div_off;
+                            if (P.bucket) {
+                                const size_t toff = (size_t)w0 * P.chunks;
+                                a.brec = P.brec.p + toff * 1024;
+                                a.boff = P.boff.p + toff * (P.nclass + 1);
+                                a.nclass = P.nclass;
+                                a.cper = P.bcper.p;
+                                a.maxcount = (uint32_t)(P.cycles * P.t_res);
+                            }
+                            a.ndiv = pl.ndiv;
+                            a.nplanes = P.nplanes;
+                            a.i0 = P.i0[cc];
+                            a.i0f = (float)P.i0[cc];
+                            a.margin = P.var_margin;
+                            a.inp_out = pl.inp ? P.inp_var.p + off : nullptr;
+                        }
+                        if (P.spsa_packed) {
+                            a.sidx = P.sidx.p + (size_t)w0 * 32 * P.n;
+                            a.thr_hi_all = P.thr_hi.p;
+                            a.kfs = P.kfs.p + w0 * 32;
+                            a.kst = P.kstg.p + w0 * 32;
+                            a.thr_all = P.thr.p;
+                            a.p_stall64 = P.p_stall64;
+                            a.cycle = (int)cc;
+                            a.Kc = P.K;
+                            a.sidx_full = P.sidx_full ? 1 : 0;
+                        }
+                        if (P.tapsa_packed) {
+                            a.ring = P.ring.p + (size_t)w0 * P.alpha * P.L * P.n;
+                            a.alpha = (int)P.alpha;
+                            a.slot = (int)(cc % P.alpha);
+                            a.filled = (int)std::min<int64_t>(cc + 1, P.alpha);
+                        }
+                        {
+                            // programmatic dependent launch: the next sub-step's prologue
+                            // overlaps this one's tail (the kernel waits on griddepcontrol)
+                            cudaLaunchConfig_t cfg{};
+                            cfg.gridDim = dim3((unsigned)blocks);
+                            cfg.blockDim = dim3(pbsa::kPackedThreads);
+                            cfg.dynamicSmemBytes = (pl.update && P.var_mode && !P.var_uniform)
+                                                       ? (P.bucket ? pbsa::bucket_smem_bytes(P.L) : pbsa::kTimingSmem)
+                                                       : smem;
+                            cfg.stream = cs;
+                            cudaLaunchAttribute attr[1];
+                            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                            attr[0].val.programmaticStreamSerializationAllowed = P.use_pdl ? 1 : 0;
+                            cfg.attrs = attr;
+                            cfg.numAttrs = 1;
+                            CK(cudaLaunchKernelEx(&cfg, pl.update ? kern_up : kern_cut, a));
+                        }
+                        CK(cudaGetLastError());
+                        ++P.launches;
+                        if (pl.update) {
+                            if (g == 0 && p0 == 0) ++P.sweep_launches;
+                            cur ^= 1;
+                        }
                 }
             }
+            for (int g = 1; g < G; ++g) {
+                const int64_t w0 = p0 + g * per;
+                if (w0 >= std::min<int64_t>(p1, w0 + per)) continue;
+                CK(cudaEventRecord(P.ev_join[g - 1], P.chain_streams[g - 1]));
+                CK(cudaStreamWaitEvent(st, P.ev_join[g - 1], 0));
+            }
+            cur = cur_g[0];
             if (P.pipelined) enqueue_phase_outputs(P, p0, p1, cur, (int)(p0 / P.phase_words));
         }
         CK(record_sweep_event(P, P.ev_sweep1, st));
@@ -2057,6 +2081,16 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
 }
 
 void host_constant_outputs(pbsa_plan *P, double *hist, int64_t *counts, double *trace_i0);
+// The whole anneal on the plan stream: the captured graph, or (one-shot
+// plans) the launches themselves.
+void launch_run(pbsa_plan &P) {
+    if (P.direct) {
+        enqueue_run(P, P.mm_, P.gm_);
+        CK(cudaGetLastError());
+    } else {
+        CK(cudaGraphLaunch(P.graph_exec, P.stream));
+    }
+}
 void download_impl(pbsa_plan *P, int8_t *spins, double *inputs, double *hist, int64_t *counts,
                    double *trace_i0, double *trace_energy, int64_t *trace_cut, int64_t *best_cut,
                    bool consts_done);
@@ -2114,7 +2148,11 @@ int plan_create_impl(int device, int64_t n, const int64_t *indptr, const int64_t
         DeviceGuard dg(device);
         P->mm_ = mm;
         P->gm_ = gm;
-        if (P->pipelined) {  // one-shot pipelined: launched directly (or captured with its outputs) by the call
+        // a one-shot call's plan is launched directly: instantiating a graph of
+        // ~10^4 launch nodes (a timing spread, several chains) costs more than
+        // launching them once
+        if (g_oneshot && !P->pipelined) P->direct = true;
+        if (P->pipelined || P->direct) {  // one-shot: launched directly (or captured with its outputs) by the call
             *out = P.release();
             return;
         }
@@ -2175,7 +2213,7 @@ int pbsa_plan_run(pbsa_plan *P, float *device_ms) {
         if (!P) fail(PBSA_EINVAL, "null plan");
         DeviceGuard dg(P->device);
         CK(cudaEventRecord(P->ev_start, P->stream));
-        CK(cudaGraphLaunch(P->graph_exec, P->stream));
+        launch_run(*P);
         CK(cudaEventRecord(P->ev_end, P->stream));
         CK(cudaEventSynchronize(P->ev_end));
         P->ran = true;
@@ -2785,7 +2823,7 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
                 rc = guarded([&] {
                     DeviceGuard dg(P->device);
                     CK(cudaEventRecord(P->ev_start, P->stream));
-                    CK(cudaGraphLaunch(P->graph_exec, P->stream));
+                    launch_run(*P);
                     CK(cudaEventRecord(P->ev_end, P->stream));
                     host_constant_outputs(P, hist, counts, trace_i0);
                     CK(cudaEventSynchronize(P->ev_end));
@@ -2917,7 +2955,7 @@ int pbsa_anneal_loop_batch_ex(int device, int64_t n, const int64_t *indptr, cons
     rc = guarded([&] {
         DeviceGuard dg(P->device);
         CK(cudaEventRecord(P->ev_start, P->stream));
-        CK(cudaGraphLaunch(P->graph_exec, P->stream));
+        launch_run(*P);
         CK(cudaEventRecord(P->ev_end, P->stream));
         host_constant_outputs(P, hist, counts, trace_i0);
         CK(cudaEventSynchronize(P->ev_end));
@@ -2960,10 +2998,9 @@ int pbsa_anneal_loop_batch_np(int device, int64_t n, const int64_t *indptr, cons
     g_oneshot = false;
     if (rc != PBSA_OK) return rc;
     rc = guarded([&] {
-        if (!P->graph_exec) fail(PBSA_EINVAL, "native-profile plan was not captured");
         DeviceGuard dg(P->device);
         CK(cudaEventRecord(P->ev_start, P->stream));
-        CK(cudaGraphLaunch(P->graph_exec, P->stream));
+        launch_run(*P);
         CK(cudaEventRecord(P->ev_end, P->stream));
         host_constant_outputs(P, hist, counts, trace_i0);
         CK(cudaEventSynchronize(P->ev_end));
