@@ -6,6 +6,11 @@
 
 namespace pbsa {
 
+// PBSA_CACHE_PREFETCH: 1 prefetches a warp's first hash-cache tile into L1
+// ahead of the dependent-launch wait, 2 also each next tile; 0 none
+#ifndef PBSA_CACHE_PREFETCH
+#define PBSA_CACHE_PREFETCH 2
+#endif
 template <int L, bool UPDATE, bool CACHED, int ALG = 0>
 __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed_sweep(PackedArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
@@ -66,6 +71,13 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     if (SPSA) skeys[wib * 32 + lane] = live ? a.kfs[(size_t)w * 32 + lane] : make_uint2(0, 0);
     uint32_t *scount = reinterpret_cast<uint32_t *>(skeys + kPackedWarps * 32);
     if (threadIdx.x == 0) scount[0] = a.count;
+    // the first chunk's 8 KB hash-cache tile into L1 before waiting on the
+    // previous sub-step (it does not depend on the spins): 64 lines, two per lane
+    if (CACHED && PBSA_CACHE_PREFETCH && live && q < a.chunks) {
+        const char *tile = reinterpret_cast<const char *>(a.acache + ((size_t)w * a.chunks + q) * 1024);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(tile + lane * 128));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(tile + 4096 + lane * 128));
+    }
     __syncthreads();
     // Programmatic dependent launch: everything above reads only host-written
     // constants, so it overlaps the previous sub-step's tail; the spin state
@@ -97,6 +109,12 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             own_nx = __ldg(sw + q * 32 + lane);
         }
         for (int ch = q; ch < a.chunks; ch += a.warps_per_word) {
+            if (CACHED && PBSA_CACHE_PREFETCH > 1 && ch + a.warps_per_word < a.chunks) {  // the next tile
+                const char *tile = reinterpret_cast<const char *>(
+                    a.acache + ((size_t)w * a.chunks + ch + a.warps_per_word) * 1024);
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(tile + lane * 128));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(tile + 4096 + lane * 128));
+            }
             const int i = node_at(a, ch, lane);
             if (i >= a.n) continue;
             uint32_t p[L];
