@@ -93,6 +93,7 @@ struct PackedArgs {
     int n, W, Tp, K, dmax;
     int warps_per_word;       // warps sharing one word index
     int cta_flush;            // every warp of a block has the same word: one cut flush per block
+    int cache_prefetch;       // prefetch hash-cache tiles into L1 (phased plans: the cache is L2-resident)
     int chunks;               // ceil(n / 32)
     uint32_t count;           // global sub-step counter c * t_res (< 2^30)
     int do_update;            // 0: only accumulate pacc (final cut pass)

@@ -6,13 +6,52 @@
 
 namespace pbsa {
 
+// hash-cache loads: 0 evict-first (ld.global.cs), 1 read-only path (ld.global.nc;
+// measured +1 % over 0 once the tiles are prefetched into L1),
+// 2 default caching
+#ifndef PBSA_CACHE_LD
+#define PBSA_CACHE_LD 1
+#endif
+__device__ __forceinline__ uint2 cache_ld(const uint2 *p) {
+    if (PBSA_CACHE_LD == 1) return __ldg(p);
+    if (PBSA_CACHE_LD == 2) return *p;
+    return __ldcs(p);
+}
 // PBSA_CACHE_PREFETCH: 1 prefetches a warp's first hash-cache tile into L1
-// ahead of the dependent-launch wait, 2 also each next tile; 0 none
+// ahead of the dependent-launch wait, 2 also each next tile; 0 none.  At run
+// time only for phased plans (the phase's cache is L2-resident: G81 C4
+// +4 %); unphased batches stream the cache and lose with it (G55 x 4096 -17 %)
 #ifndef PBSA_CACHE_PREFETCH
 #define PBSA_CACHE_PREFETCH 2
 #endif
+// Blocks per SM the plain cached sweep is compiled for, per count width
+// (registers = 64K / (128 x blocks)): measured per instance, since more
+// registers let the compiler keep more of a chunk's 32 hash-cache loads in
+// flight while fewer cost warps (A/B on one B200: see DESIGN.md section 4).
+#ifndef PBSA_MB_L3
+#define PBSA_MB_L3 7
+#endif
+#ifndef PBSA_MB_L4
+#define PBSA_MB_L4 8
+#endif
+#ifndef PBSA_MB_L5
+#define PBSA_MB_L5 PBSA_PACKED_MIN_BLOCKS
+#endif
+#ifndef PBSA_MB_L6
+#define PBSA_MB_L6 PBSA_PACKED_MIN_BLOCKS
+#endif
+#ifndef PBSA_MB_L7
+#define PBSA_MB_L7 6
+#endif
+template <int L, bool UPDATE, bool CACHED, int ALG>
+constexpr int packed_min_blocks() {
+    return !(UPDATE && CACHED && ALG == 0) ? PBSA_PACKED_MIN_BLOCKS
+           : L == 3 ? PBSA_MB_L3 : L == 4 ? PBSA_MB_L4 : L == 5 ? PBSA_MB_L5 : L == 6 ? PBSA_MB_L6
+           : L == 7 ? PBSA_MB_L7 : PBSA_PACKED_MIN_BLOCKS;
+}
+
 template <int L, bool UPDATE, bool CACHED, int ALG = 0>
-__global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed_sweep(PackedArgs a) {
+__global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, CACHED, ALG>())) packed_sweep(PackedArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
     extern __shared__ unsigned long long smem_u64[];
     // Threshold table, 128 B aligned.  L <= 4 (degree <= 15): one 16-entry row
@@ -73,7 +112,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
     if (threadIdx.x == 0) scount[0] = a.count;
     // the first chunk's 8 KB hash-cache tile into L1 before waiting on the
     // previous sub-step (it does not depend on the spins): 64 lines, two per lane
-    if (CACHED && PBSA_CACHE_PREFETCH && live && q < a.chunks) {
+    if (CACHED && PBSA_CACHE_PREFETCH && a.cache_prefetch && live && q < a.chunks) {
         const char *tile = reinterpret_cast<const char *>(a.acache + ((size_t)w * a.chunks + q) * 1024);
         asm volatile("prefetch.global.L1 [%0];" ::"l"(tile + lane * 128));
         asm volatile("prefetch.global.L1 [%0];" ::"l"(tile + 4096 + lane * 128));
@@ -109,7 +148,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
             own_nx = __ldg(sw + q * 32 + lane);
         }
         for (int ch = q; ch < a.chunks; ch += a.warps_per_word) {
-            if (CACHED && PBSA_CACHE_PREFETCH > 1 && ch + a.warps_per_word < a.chunks) {  // the next tile
+            if (CACHED && PBSA_CACHE_PREFETCH > 1 && a.cache_prefetch && ch + a.warps_per_word < a.chunks) {
                 const char *tile = reinterpret_cast<const char *>(
                     a.acache + ((size_t)w * a.chunks + ch + a.warps_per_word) * 1024);
                 asm volatile("prefetch.global.L1 [%0];" ::"l"(tile + lane * 128));
@@ -172,7 +211,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                                              kNativeTagR, a.rk, X);
                         zh = X[b & 3];
                     } else if (CACHED) {
-                        const uint2 v = __ldcs(ctile + b * 32);
+                        const uint2 v = cache_ld(ctile + b * 32);
                         zh = packed_hash_hi_y(v.x ^ count, v.y);
                     } else {
                         const uint2 kc = key[b];
@@ -244,7 +283,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                                              kNativeTagR, a.rk, X);
                         native_decide(X[b & 3], t, word);
                     } else if (CACHED) {
-                        const uint2 v = __ldcs(ctile + b * 32);
+                        const uint2 v = cache_ld(ctile + b * 32);
                         tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
                     } else {
                         const uint2 kc = key[b];
@@ -372,7 +411,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                                                  kNativeTagR, a.rk, X);
                             native_decide(X[b & 3], t, word);
                         } else if (CACHED) {
-                            const uint2 v = __ldcs(ctile + b * 32);
+                            const uint2 v = cache_ld(ctile + b * 32);
                             tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
                         } else {
                             const uint2 kc = key[b];
@@ -441,7 +480,7 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS) packed
                         asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
                             : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
                     } else if (CACHED) {
-                        const uint2 v = __ldcs(ctile + b * 32);
+                        const uint2 v = cache_ld(ctile + b * 32);
                         tie = min(tie, packed_decide_n2(v.x ^ count, v.y, t, word));
                     } else {
                         const uint2 kc = key[b];

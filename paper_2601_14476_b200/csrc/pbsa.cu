@@ -1773,6 +1773,8 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                         a.dmax = P.dmax;
                         a.warps_per_word = P.warps_per_word;
                         a.cta_flush = (P.cta_flush && P.warps_per_word % pbsa::kPackedWarps == 0) ? 1 : 0;
+                    a.cache_prefetch = P.phase_words < P.W ? 1 : 0;
+                    if (const char *env = std::getenv("PBSA_CACHE_PREFETCH")) a.cache_prefetch = env[0] == '1';
                         a.chunks = P.chunks;
                         a.count = pl.count;
                         a.do_update = pl.update;
