@@ -474,6 +474,47 @@ using pbsa_dispatch::PackedKernel;
 using pbsa_dispatch::ResidentKernel;
 using pbsa_dispatch::ResidentTimingKernel;
 
+// Word-phase width for the packed sweep (W = one phase), from a wave model
+// fitted on the C5 rows x 4096 (profiles/r02_summary.md, "phase width"): the
+// launches of one phase hold phase_words x warps_per_word warps; the modelled
+// throughput is (warps in flight / resident warps, at most 1) x (chunks /
+// (warps x busiest warp's chunks)) x c/(c + 0.25) with c the chunks per warp (a
+// launch's fixed cost per warp, ~190 instructions, is about a quarter of a
+// chunk), x 0.85 for one phase whose hash cache (8 KiB per word and chunk)
+// exceeds l2_budget; several phases must fit it.  l2_budget 0 allows one phase
+// only.  *balance: spread the chunks over the fewest warps with the same
+// busiest-warp count.
+int64_t choose_phases(int64_t chunks, int64_t W, int64_t resident_warps, size_t l2_budget, bool *balance) {
+    double best = -1;
+    int64_t best_pw = W;
+    *balance = false;
+    const int64_t max_phases = l2_budget ? std::max<int64_t>(1, W / 4) : 1;
+    for (int64_t nph = 1; nph <= max_phases; ++nph) {
+        const int64_t pw = (W + nph - 1) / nph;
+        if ((W + pw - 1) / pw != nph) continue;  // equal phases only
+        const bool fits = (size_t)pw * (size_t)chunks * 8192 <= l2_budget;
+        if (nph > 1 && !fits) continue;
+        for (int bal = 0; bal < 2; ++bal) {
+            int64_t wpw = std::min<int64_t>(std::max<int64_t>(1, resident_warps / pw), chunks);
+            if (bal) {
+                const int64_t per = (chunks + wpw - 1) / wpw;
+                wpw = (chunks + per - 1) / per;
+            }
+            wpw = (wpw + pbsa::kPackedWarps - 1) / pbsa::kPackedWarps * pbsa::kPackedWarps;
+            const int64_t per = (chunks + wpw - 1) / wpw;
+            double eff = std::min(1.0, (double)(pw * wpw) / (double)resident_warps) * (double)chunks /
+                         (double)(wpw * per) * (double)per / ((double)per + 0.25);
+            if (!fits) eff *= 0.85;
+            if (eff > best + 1e-9) {
+                best = eff;
+                best_pw = pw;
+                *balance = bal != 0;
+            }
+        }
+    }
+    return best_pw;
+}
+
 // The sweep kernels live in the per-L translation units (dispatch.h).
 PackedKernel packed_kernel_for(int L, bool update, bool cached, bool tapsa = false,
                                bool spsa = false, int var = 0, bool native = false) {
@@ -1151,27 +1192,38 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // cache the sub-step-independent first absorb of every (trial, node)
         // draw when it fits the budget (PBSA_PACKED_CACHE=0/1 overrides)
         // phase width in words (PBSA_PACKED_PHASE_WORDS overrides; 0 = all)
-        // Large batches run in word phases of 13 words (416 trials): each phase's
-        // cache (~67 MB for G81) stays L2-resident across its cycles, which keeps
-        // HBM (and the 1 kW power cap) out of the loop; 13 words x ~315 warps
-        // per word fill one wave with ~2 tasks per warp.  Small batches: one phase.
+        // Large batches run in word phases whose hash cache stays L2-resident
+        // across their cycles (G81: 13 words, ~67 MB), which keeps HBM (and the
+        // 1 kW power cap) out of the loop.  The width comes from a wave model
+        // (choose_phases): fill the resident warps, give every warp the same
+        // chunk count, keep that count >= 2, fit the phase's cache in 5/8 of L2.
         // A timing spread multiplies the launches by t_res: one phase, four chains.
         const bool many_launches = P.var_mode && !P.var_uniform;
-        // Only graphs whose 13 words already fill a wave of resident threads
-        // (sms x 1024) are phased, and only batches of four phases or more
-        // (measured: G55 x 4096 and G81 x 1024 run faster unphased).
-        int sm_count = 148;
+        int sm_count = 148, l2_bytes = 0;
         CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
-        const bool big_graph = 13 * n >= (int64_t)sm_count * 1024;
+        CK(cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device));
+        const int sms = sm_count;
         // (SpSA streams its per-p-bit drive index, which no phase keeps in L2: unphased)
         // (native Philox draws keep no cache, so nothing gains from phases: measured
         // G81 x 4096 9.1e11 updates/s unphased vs 7.8e11 in phases of 13)
-        P.phase_words = (!g_oneshot && !many_launches && big_graph && P.W >= 4 * 13 && !P.spsa_packed &&
-                         !P.native) ? 13 : 0;
-        if (P.phase_words > 0) {  // equal phases
-            const int64_t nph = (P.W + P.phase_words - 1) / P.phase_words;
-            P.phase_words = (P.W + nph - 1) / nph;
+        const bool may_phase = !g_oneshot && !many_launches && P.W >= 4 * 13 && !P.spsa_packed && !P.native;
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
+                             pbsa::kPackedFlushBytes;
+        const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
+        int occ = 0;
+        {
+            // (the kernel instance, so its occupancy, does not depend on the phase width)
+            PackedKernel k0 = packed_kernel_for(P.L, true, !many_launches && !P.native, P.tapsa_packed, P.spsa_packed,
+                                                P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
+            set_packed_smem(k0, smem_up);
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k0, pbsa::kPackedThreads, smem_up));
+            occ = std::max(occ, 1);
         }
+        P.chunks = (int)((n + 31) / 32);
+        bool balance_chunks = false;
+        P.phase_words = choose_phases(P.chunks, P.W, (int64_t)sm_count * occ * pbsa::kPackedWarps,
+                                      may_phase ? (size_t)l2_bytes * 5 / 8 : 0, &balance_chunks);
+        if (P.phase_words >= P.W) P.phase_words = 0;
         // one-shot calls of the plain rule on the launched path run pipelined
         // (PBSA_PIPELINE=0 disables): four word phases, each phase's outputs
         // copied back while the next anneals (decided again below once the
@@ -1206,19 +1258,24 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         if (P.use_cache) P.acache.alloc(cache_entries);
         PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
                                               P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
-                             pbsa::kPackedFlushBytes;
-        const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
         set_packed_smem(kern, smem_up);
         set_packed_smem(packed_kernel_for(P.L, false, false), smem);
-        int occ = 0, sms = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pbsa::kPackedThreads, smem_up));
-        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
         occ = std::max(occ, 1);
-        P.chunks = (int)((n + 31) / 32);
-        const int64_t target_warps = (int64_t)sms * occ * pbsa::kPackedWarps;
+        const int64_t target_warps = (int64_t)sm_count * occ * pbsa::kPackedWarps;
         int64_t wpw = std::max<int64_t>(1, target_warps / P.phase_words);  // one phase at a time
         wpw = std::min<int64_t>(wpw, P.chunks);
+        // equal chunk counts per warp: a launch lasts as long as its busiest
+        // warp, so spread the chunks over the fewest warps that give the same
+        // maximum, when choose_phases scores that higher (PBSA_BALANCE_CHUNKS=0/1)
+        {
+            bool balance = balance_chunks;
+            if (const char *env = std::getenv("PBSA_BALANCE_CHUNKS")) balance = env[0] != '0';
+            if (balance) {
+                const int64_t per = (P.chunks + wpw - 1) / wpw;
+                wpw = (P.chunks + per - 1) / per;
+            }
+        }
         // the per-thread bit-sliced cut counter holds sum(degree) < 2^(L+2)
         const int64_t cap = (1LL << (P.L + 2)) - 1, dm = std::max<int64_t>(dmax, 1);
         if (dm > cap) fail(PBSA_EINVAL, "degree too large for the packed cut counter");

@@ -24,4 +24,6 @@ plan = _native.Plan(b)
 ms = plan.run()
 ms = plan.run()
 s, best, ups = plan.summary()
-print(f"{name} {sig} T={T} cycles={cyc} {rng}: {ms:.2f} ms, {ups / ms * 1e3:.3g} upd/s, {plan.info()}")
+lay = plan.layout()
+print(f"{name} {sig} T={T} cycles={cyc} {rng}: {ms:.2f} ms, {ups / ms * 1e3:.3g} upd/s, pw={lay['phase_words']} "
+      f"chains={lay['chains']} wpw={lay['warps_per_word']} {plan.info()}")
