@@ -1,9 +1,12 @@
 // aux_kernels.cuh -- non-template kernels of the host runtime: spin init, first-absorb
-// cache, general (int8) path, output formatting, debug hooks.  Included by pbsa.cu only.
+// cache, general (int8) path, output formatting, debug hooks.  Included by the
+// runtime units through runtime.h: the kernels have internal linkage (an
+// unnamed namespace), each unit launching its own copy.
 #pragma once
 #include "device_common.cuh"
 
 namespace pbsa {
+namespace {
 
 __global__ void init_packed(uint32_t *__restrict__ s, const uint64_t *__restrict__ kspin,
                             int n, int W) {
@@ -769,5 +772,5 @@ __global__ void debug_tanh(int64_t cnt, const double *x, double *out) {
     if (g < cnt) out[g] = pb_libm_tanh(x[g]);
 }
 
+}  // namespace
 }  // namespace pbsa
-

@@ -1,6 +1,6 @@
 // dispatch.h -- host-side kernel selection.  The sweep kernels are templates
 // on the count width L (degree < 2^L); each L is instantiated in its own
-// translation unit (kernels_L<1..7>.cu, built in parallel) and pbsa.cu picks
+// translation unit (kernels_L<1..7>.cu, built in parallel) and plan.cu picks
 // the function pointer for a plan through these declarations.
 #pragma once
 #include "device_common.cuh"
