@@ -43,11 +43,24 @@ __device__ __forceinline__ uint2 cache_ld(const uint2 *p) {
 #ifndef PBSA_MB_L7
 #define PBSA_MB_L7 6
 #endif
+// The Philox plain (ALG 4) and varied-profile (5) update sweeps spill at 64
+// registers: 72 for L = 3 (G81 C4 Philox +1 %), 80 otherwise (G55 x 4096 +12 %,
+// G1 x 4096 +27 %, G81 sigma_lam,delta +5 %).  TApSA / SpSA / replayed
+// varied-profile sweeps lose with fewer blocks (G81 TApSA -11 %): 64.
+#ifndef PBSA_MB_PHILOX_L3
+#define PBSA_MB_PHILOX_L3 7
+#endif
+#ifndef PBSA_MB_PHILOX
+#define PBSA_MB_PHILOX 6
+#endif
 template <int L, bool UPDATE, bool CACHED, int ALG>
 constexpr int packed_min_blocks() {
-    return !(UPDATE && CACHED && ALG == 0) ? PBSA_PACKED_MIN_BLOCKS
-           : L == 3 ? PBSA_MB_L3 : L == 4 ? PBSA_MB_L4 : L == 5 ? PBSA_MB_L5 : L == 6 ? PBSA_MB_L6
-           : L == 7 ? PBSA_MB_L7 : PBSA_PACKED_MIN_BLOCKS;
+    return (UPDATE && CACHED && ALG == 0)
+               ? (L == 3 ? PBSA_MB_L3 : L == 4 ? PBSA_MB_L4 : L == 5 ? PBSA_MB_L5 : L == 6 ? PBSA_MB_L6
+                  : L == 7 ? PBSA_MB_L7 : PBSA_PACKED_MIN_BLOCKS)
+           : (UPDATE && ALG == 4) ? (L == 3 ? PBSA_MB_PHILOX_L3 : PBSA_MB_PHILOX)
+           : (UPDATE && ALG == 5) ? PBSA_MB_PHILOX
+                                  : PBSA_PACKED_MIN_BLOCKS;
 }
 
 template <int L, bool UPDATE, bool CACHED, int ALG = 0>
