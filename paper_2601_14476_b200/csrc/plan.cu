@@ -10,8 +10,8 @@ namespace pbsa_rt {
 // throughput is (warps in flight / resident warps, at most 1) x (chunks /
 // (warps x busiest warp's chunks)) x c/(c + 0.25) with c the chunks per warp (a
 // launch's fixed cost per warp, ~190 instructions, is about a quarter of a
-// chunk), x 0.85 for one phase whose hash cache (8 KiB per word and chunk)
-// exceeds l2_budget; several phases must fit it.  l2_budget 0 allows one phase
+// chunk), x (l2_budget / cache)^0.35 for one phase whose hash cache (8 KiB per
+// word and chunk) exceeds l2_budget; several phases must fit it.  l2_budget 0 allows one phase
 // only.  *balance: spread the chunks over the fewest warps with the same
 // busiest-warp count.
 int64_t choose_phases(int64_t chunks, int64_t W, int64_t resident_warps, size_t l2_budget, bool *balance) {
@@ -34,7 +34,7 @@ int64_t choose_phases(int64_t chunks, int64_t W, int64_t resident_warps, size_t 
             const int64_t per = (chunks + wpw - 1) / wpw;
             double eff = std::min(1.0, (double)(pw * wpw) / (double)resident_warps) * (double)chunks /
                          (double)(wpw * per) * (double)per / ((double)per + 0.25);
-            if (!fits) eff *= 0.85;
+            if (!fits) eff *= std::pow((double)l2_budget / ((double)pw * (double)chunks * 8192.0), 0.35);
             if (eff > best + 1e-9) {
                 best = eff;
                 best_pw = pw;
@@ -672,7 +672,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // (SpSA streams its per-p-bit drive index, which no phase keeps in L2: unphased)
         // (native Philox draws keep no cache, so nothing gains from phases: measured
         // G81 x 4096 9.1e11 updates/s unphased vs 7.8e11 in phases of 13)
-        const bool may_phase = !g_oneshot && !many_launches && P.W >= 4 * 13 && !P.spsa_packed && !P.native;
+        const bool may_phase = !g_oneshot && !many_launches && !P.spsa_packed && !P.native;
         const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
                              pbsa::kPackedFlushBytes;
         const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
