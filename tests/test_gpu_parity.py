@@ -1125,3 +1125,38 @@ def test_native_profile_cut_statistics_match_reference(bench_graphs, golden_anal
     b_rep = np.mean([r.best_cut for r in rep.results])
     b_nat = np.mean([r.best_cut for r in nat.results])
     assert abs(b_nat - b_rep) <= 0.005 * best_known, (b_nat, b_rep)
+
+
+# ------------------------------------------------ launch shapes of the packed sweep
+
+@pytest.mark.parametrize("name,trials", [("G77", 1024), ("G81", 512), ("G55", 4096)])
+def test_launch_shapes_are_bitwise_neutral(oracle, bench_graphs, monkeypatch, name, trials):
+    """The word-phase width and chunk balance the wave model picks
+    (plan.cu choose_phases), and forced alternatives (one phase, other widths,
+    balance on/off): every shape equals the oracle bit for bit."""
+    g = bench_graphs(name)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 6, 10)
+    seeds = [streams.trial_seed(6, k) for k in range(trials)]
+    keys = [streams.run_key(s) for s in seeds]
+    b = _native.Batch(model, sch, keys, graph=g)
+    want = oracle.anneal_batch(model, sch, "psa", VariabilityProfile.ideal(model.n), keys, graph=g)
+    W = trials // 32
+    shapes = [{}, {"PBSA_PACKED_PHASE_WORDS": "0", "PBSA_BALANCE_CHUNKS": "0"},
+              {"PBSA_PACKED_PHASE_WORDS": str(max(1, W // 3)), "PBSA_BALANCE_CHUNKS": "1"},
+              {"PBSA_PACKED_PHASE_WORDS": str(max(1, W // 2 + 1)), "PBSA_BALANCE_CHUNKS": "0"}]
+    seen = set()
+    for env in shapes:
+        for k in ("PBSA_PACKED_PHASE_WORDS", "PBSA_BALANCE_CHUNKS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        plan = _native.Plan(b)
+        lay = plan.layout()
+        plan.run()
+        got = plan.download()
+        plan.close()
+        seen.add((lay["phase_words"], lay["warps_per_word"]))
+        for k in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
+            assert np.array_equal(got[k], want[k]), (env, lay, k)
+    assert len(seen) >= 3, seen
