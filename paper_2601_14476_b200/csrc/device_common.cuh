@@ -334,8 +334,14 @@ struct CutPlanes {
     static constexpr int value = L + 2;
 };
 
+// blocks per SM of the period-bucket kernel: 8 (64 registers) for the tori
+// (L <= 3), 6 (85 registers) otherwise; measured with 256 staged records:
+// G81 C3 -5.6 % against 6 blocks, G55 C3 +0 / -19 % with 7 / 8 blocks
 #ifndef PBSA_BUCKET_MIN_BLOCKS
-#define PBSA_BUCKET_MIN_BLOCKS 6  // (85 registers: G55 C3 -5 %, G81 even)
+#define PBSA_BUCKET_MIN_BLOCKS 6
+#endif
+#ifndef PBSA_BUCKET_MIN_BLOCKS_L3
+#define PBSA_BUCKET_MIN_BLOCKS_L3 8
 #endif
 #ifndef PBSA_PACKED_MIN_BLOCKS
 #define PBSA_PACKED_MIN_BLOCKS 8
@@ -597,7 +603,7 @@ constexpr int kMaxDivisors = 256;
 // exact masks: u32 per lane) and the u16 segment table (prefix, start per
 // fired class); the launch's class list and last-firing flags.
 #ifndef PBSA_BK_STAGE
-#define PBSA_BK_STAGE 384
+#define PBSA_BK_STAGE 256  // (384: G81 C3 +5.6 %, G55 C3 +10 % time)
 #endif
 constexpr int kBucketStage = PBSA_BK_STAGE;            // staged records per tile (the rest load directly)
 constexpr int kBucketMaxDiv = 128;            // fired classes per sub-step the bucket kernel takes

@@ -779,7 +779,7 @@ __device__ __forceinline__ void bulk_copy_g2s(void *dst, const void *src, uint32
 #define PBSA_BK_ILP 1
 #endif
 template <int L, bool NATIVE = false>
-__global__ void __launch_bounds__(kPackedThreads, PBSA_BUCKET_MIN_BLOCKS)
+__global__ void __launch_bounds__(kPackedThreads, L <= 3 ? PBSA_BUCKET_MIN_BLOCKS_L3 : PBSA_BUCKET_MIN_BLOCKS)
     packed_sweep_bucket(PackedArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
     extern __shared__ unsigned long long smem_u64[];
