@@ -180,14 +180,14 @@ __device__ __forceinline__ void packed_first_absorb(uint32_t ylo, uint32_t C, ui
 // Second absorb from y = x ^ (x >> 30), x = s ^ count, up to the high word of
 // the last multiply, then the decision bit shifted into `word` through the
 // carry of zh + ~thi.  Returns the (zh ^ thi) tie witness (< 2: recompute).
-__device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t yh, uint2 t,
+__device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t c1, uint2 t,
                                                     uint32_t &word) {
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
     uint32_t zl = yl * M1L;
-    uint32_t zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
+    uint32_t zh = mulhi(yl, M1L) + yl * M1H + c1;
     yl = zl ^ __funnelshift_r(zl, zh, 27);
-    yh = zh ^ mulhi(zh, 1u << 5);
+    const uint32_t yh = zh ^ mulhi(zh, 1u << 5);
     zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
     uint32_t dummy;
     asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %4;"
@@ -196,18 +196,8 @@ __device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t yh, ui
 }
 
 // High word zh of the last multiply of the second absorb, from its input
-// y = x ^ (x >> 30); the draw's top word is zh ^ (zh >> 31), within 1 of zh.
-__device__ __forceinline__ uint32_t packed_hash_hi_y(uint32_t yl, uint32_t yh) {
-    constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
-    constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
-    const uint32_t zl = yl * M1L;
-    const uint32_t zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
-    yl = zl ^ __funnelshift_r(zl, zh, 27);
-    yh = zh ^ mulhi(zh, 1u << 5);
-    return mulhi(yl, M2L) + yl * M2H + yh * M2L;
-}
-
-// The same from the cached form (y low word, c1 = y high word * M1L).
+// y = x ^ (x >> 30) given as (low word, high word * M1L); the draw's top word
+// is zh ^ (zh >> 31), within 1 of zh.
 __device__ __forceinline__ uint32_t packed_hash_hi_c(uint32_t yl, uint32_t c1) {
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
@@ -218,9 +208,20 @@ __device__ __forceinline__ uint32_t packed_hash_hi_c(uint32_t yl, uint32_t c1) {
     return mulhi(yl, M2L) + yl * M2H + yh * M2L;
 }
 
+// The hash cache entry of a (trial, node): (low word, high word x M1L) of
+// y' = s ^ (s >> 30) with PBSA_CACHE_C1 (one multiply per update fewer), else
+// (low word, high word); cache_c1 gives the c1 term either way.
+#ifndef PBSA_CACHE_C1
+#define PBSA_CACHE_C1 1
+#endif
+__device__ __forceinline__ uint32_t cache_c1(uint32_t hi) { return PBSA_CACHE_C1 ? hi : hi * 0x1CE4E5B9u; }
+__host__ __device__ __forceinline__ uint32_t cache_hi_entry(uint32_t yh) {
+    return PBSA_CACHE_C1 ? yh * 0x1CE4E5B9u : yh;
+}
+
 // Same from the first absorb s (x = s ^ count; count < 2^30 only touches the low word).
 __device__ __forceinline__ uint32_t packed_hash_hi(uint32_t sl, uint32_t sh, uint32_t count) {
-    return packed_hash_hi_y(sl ^ count ^ __funnelshift_r(sl, sh, 30), sh ^ mulhi(sh, 1u << 2));
+    return packed_hash_hi_c(sl ^ count ^ __funnelshift_r(sl, sh, 30), (sh ^ mulhi(sh, 1u << 2)) * 0x1CE4E5B9u);
 }
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -275,8 +276,8 @@ __device__ __forceinline__ uint32_t var_prefilter(__half2 h, float ir, uint32_t 
 // Second absorb (x = s ^ count; count < 2^30 only touches the low word).
 __device__ __forceinline__ uint32_t packed_second_decide(uint32_t sl, uint32_t sh, uint32_t count,
                                                          uint2 t, uint32_t &word) {
-    return packed_decide_y(sl ^ count ^ __funnelshift_r(sl, sh, 30), sh ^ mulhi(sh, 1u << 2), t,
-                           word);
+    return packed_decide_y(sl ^ count ^ __funnelshift_r(sl, sh, 30), (sh ^ mulhi(sh, 1u << 2)) * 0x1CE4E5B9u,
+                           t, word);
 }
 
 // Plain-rule variant with the table entry t = (lo, hi) of the 33-bit
@@ -285,14 +286,14 @@ __device__ __forceinline__ uint32_t packed_second_decide(uint32_t sl, uint32_t s
 // or the final xorshift's bit 0 matter) is the only case that needs the
 // exact 64-bit test, and every other carry is the exact decision -- also for
 // thi <= 1, which the 33rd bit keeps.  Returns D.
-__device__ __forceinline__ uint32_t packed_decide_n2(uint32_t yl, uint32_t yh, uint2 t,
+__device__ __forceinline__ uint32_t packed_decide_n2(uint32_t yl, uint32_t c1, uint2 t,
                                                      uint32_t &word) {
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
     uint32_t zl = yl * M1L;
-    uint32_t zh = mulhi(yl, M1L) + yl * M1H + yh * M1L;
+    uint32_t zh = mulhi(yl, M1L) + yl * M1H + c1;
     yl = zl ^ __funnelshift_r(zl, zh, 27);
-    yh = zh ^ mulhi(zh, 1u << 5);
+    const uint32_t yh = zh ^ mulhi(zh, 1u << 5);
     zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
     uint32_t D;
     asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
@@ -302,8 +303,8 @@ __device__ __forceinline__ uint32_t packed_decide_n2(uint32_t yl, uint32_t yh, u
 
 __device__ __forceinline__ uint32_t packed_second_decide_n2(uint32_t sl, uint32_t sh, uint32_t count,
                                                             uint2 t, uint32_t &word) {
-    return packed_decide_n2(sl ^ count ^ __funnelshift_r(sl, sh, 30), sh ^ mulhi(sh, 1u << 2), t,
-                            word);
+    return packed_decide_n2(sl ^ count ^ __funnelshift_r(sl, sh, 30), (sh ^ mulhi(sh, 1u << 2)) * 0x1CE4E5B9u,
+                            t, word);
 }
 
 // Native decision: shift (X >= T) into `word` as the carry of X + (2^32 - T),

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                         zh = X[b & 3];
                     } else if (CACHED) {
                         const uint2 v = __ldcs(ctile + b * 32);
-                        zh = packed_hash_hi_y(v.x ^ count, v.y);
+                        zh = packed_hash_hi_c(v.x ^ count, cache_c1(v.y));
                     } else {
                         const uint2 kc = key[b];
                         uint32_t sl, sh;
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                         native_decide(X[b & 3], t, word);
                     } else if (CACHED) {
                         const uint2 v = __ldcs(ctile + b * 32);
-                        tie = min(tie, packed_decide_y(v.x ^ count, v.y, t, word));
+                        tie = min(tie, packed_decide_y(v.x ^ count, cache_c1(v.y), t, word));
                     } else {
                         const uint2 kc = key[b];
                         uint32_t sl, sh;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                         : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
                 } else if (CACHED) {
                     const uint2 v = __ldcs(ctile + b * 32);
-                    tie = min(tie, packed_decide_n2(v.x ^ count, v.y, t, word));
+                    tie = min(tie, packed_decide_n2(v.x ^ count, cache_c1(v.y), t, word));
                 } else {
                     const uint2 kc = key[b];
                     uint32_t sl, sh;
