@@ -154,6 +154,22 @@ constexpr size_t kPackedFlushBytes = (size_t)kPackedWarps * 10 * 32 * 4 + 16;
 
 __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
 
+// (lo, hi + add) of a 32 x 32 product: one IMAD.WIDE (+ the add) instead of a
+// multiply and a multiply-high (PBSA_WIDE_MUL=0: the two-instruction form)
+#ifndef PBSA_WIDE_MUL
+#define PBSA_WIDE_MUL 1
+#endif
+__device__ __forceinline__ void mul_lohi(uint32_t a, uint32_t m, uint32_t add, uint32_t &lo, uint32_t &hi) {
+#if PBSA_WIDE_MUL
+    const uint64_t p = (uint64_t)a * m;
+    lo = (uint32_t)p;
+    hi = (uint32_t)(p >> 32) + add;
+#else
+    lo = a * m;
+    hi = mulhi(a, m) + add;
+#endif
+}
+
 // First absorb of a trial's draw: s = absorb(K, i) + GAMMA, as (lo, hi).
 // y = (ylo, Y) with ylo = F_t ^ i; Y * M1L is folded into C = C_t.
 // Right shifts of high words go through IMAD.HI (x >> s == umulhi(x, 2^(32-s)))
@@ -163,13 +179,12 @@ __device__ __forceinline__ void packed_first_absorb(uint32_t ylo, uint32_t C, ui
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
     constexpr uint32_t GL = 0x7F4A7C15u, GH = 0x9E3779B9u;
-    uint32_t zl = ylo * M1L;
-    uint32_t zh = mulhi(ylo, M1L) + ylo * M1H + C;
+    uint32_t zl, zh;
+    mul_lohi(ylo, M1L, ylo * M1H + C, zl, zh);
     // z ^= z >> 27 ; z *= M2
     uint32_t yl = zl ^ __funnelshift_r(zl, zh, 27);
     uint32_t yh = zh ^ mulhi(zh, 1u << 5);
-    zl = yl * M2L;
-    zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
+    mul_lohi(yl, M2L, yl * M2H + yh * M2L, zl, zh);
     // z ^= z >> 31  -> A ; s = A + GAMMA
     yl = zl ^ __funnelshift_r(zl, zh, 31);
     yh = zh ^ mulhi(zh, 1u << 1);
@@ -184,8 +199,8 @@ __device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t c1, ui
                                                     uint32_t &word) {
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
-    uint32_t zl = yl * M1L;
-    uint32_t zh = mulhi(yl, M1L) + yl * M1H + c1;
+    uint32_t zl, zh;
+    mul_lohi(yl, M1L, yl * M1H + c1, zl, zh);
     yl = zl ^ __funnelshift_r(zl, zh, 27);
     const uint32_t yh = zh ^ mulhi(zh, 1u << 5);
     zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
@@ -201,8 +216,8 @@ __device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t c1, ui
 __device__ __forceinline__ uint32_t packed_hash_hi_c(uint32_t yl, uint32_t c1) {
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
-    const uint32_t zl = yl * M1L;
-    const uint32_t zh = mulhi(yl, M1L) + yl * M1H + c1;
+    uint32_t zl, zh;
+    mul_lohi(yl, M1L, yl * M1H + c1, zl, zh);
     yl = zl ^ __funnelshift_r(zl, zh, 27);
     const uint32_t yh = zh ^ mulhi(zh, 1u << 5);
     return mulhi(yl, M2L) + yl * M2H + yh * M2L;
@@ -290,8 +305,8 @@ __device__ __forceinline__ uint32_t packed_decide_n2(uint32_t yl, uint32_t c1, u
                                                      uint32_t &word) {
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
-    uint32_t zl = yl * M1L;
-    uint32_t zh = mulhi(yl, M1L) + yl * M1H + c1;
+    uint32_t zl, zh;
+    mul_lohi(yl, M1L, yl * M1H + c1, zl, zh);
     yl = zl ^ __funnelshift_r(zl, zh, 27);
     const uint32_t yh = zh ^ mulhi(zh, 1u << 5);
     zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
