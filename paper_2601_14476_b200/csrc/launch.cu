@@ -96,7 +96,7 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                                         : packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
                                                             P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
         PackedKernel kern_cut = packed_kernel_for(P.L, false, false);
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 32) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
                              pbsa::kPackedFlushBytes;
         CK(record_sweep_event(P, P.ev_sweep0, st));
         // Word phases run one after another so that a phase's first-absorb

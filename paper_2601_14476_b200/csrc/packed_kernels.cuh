@@ -24,6 +24,9 @@ __device__ __forceinline__ uint2 cache_ld(const uint2 *p) {
 #ifndef PBSA_CACHE_PREFETCH
 #define PBSA_CACHE_PREFETCH 2
 #endif
+#ifndef PBSA_PRMT_ADDR
+#define PBSA_PRMT_ADDR 1
+#endif
 // Blocks per SM the plain cached sweep is compiled for, per count width
 // (registers = 64K / (128 x blocks)): measured per instance, since more
 // registers let the compiler keep more of a chunk's 32 hash-cache loads in
@@ -78,9 +81,12 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
     constexpr bool VAR = ALG == 3 || ALG == 5;
     constexpr bool NATIVE = ALG >= 4;
     constexpr bool NIB = L <= 4 && !TAPSA;
+    // NIB rows: one per degree, kNibRow entries of 8 B (256 B with PBSA_PRMT_ADDR,
+    // so a row base has a zero low byte and one PRMT forms a trial's address)
+    constexpr int kNibRow = PBSA_PRMT_ADDR ? 32 : 16;
     uint2 *sthr = reinterpret_cast<uint2 *>(
         (reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
-    const int tab_entries = VAR ? 0 : TAPSA ? a.K : NIB ? (a.dmax + 1) * 16 : a.K;
+    const int tab_entries = VAR ? 0 : TAPSA ? a.K : NIB ? (a.dmax + 1) * kNibRow : a.K;
     uint2 *skey = sthr + tab_entries;                     // [warps][32] {F, C}
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
             int raw = k - a.dmax;
             bool ok = true;
             if (NIB) {
-                const int d = k >> 4, pp = k & 15;
+                const int d = k / kNibRow, pp = k % kNibRow;
                 raw = 2 * pp - d;
                 ok = pp <= d;
             }
@@ -411,7 +417,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                         if ((stallw >> b) & 1u) {
                             t = NATIVE ? make_uint2(tlo[j], th[j]) : make_uint2(~th[j], th[j]);
                         } else {
-                            t = NIB ? sthr[d * 16 + pop] : sthr[2 * pop - d + a.dmax];
+                            t = NIB ? sthr[d * kNibRow + pop] : sthr[2 * pop - d + a.dmax];
                             nidx = (uint32_t)(base + 2 * pop);
                         }
                         // every lane stores (stalled p-bits their unchanged index): whole
@@ -453,10 +459,24 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                 const uint32_t ui = (uint32_t)i;
                 uint32_t X[4];  // NATIVE: the current Philox block (trials 4k .. 4k + 3)
                 // NIB: transpose the L count planes into 32 nibbles (N[k] nibble j =
-                // count of trial 8k + j), a few ops per 32 trials instead of 2L per trial
+                // count of trial 8k + j), a few ops per 32 trials instead of 2L per trial;
+                // PBSA_PRMT_ADDR: into bytes holding 8 x count (B[k] byte j = trial
+                // 4k + j; four trials' bits spread by one multiply), so that a trial's
+                // table address is one PRMT of its byte with the row base
                 uint32_t N[4] = {0u, 0u, 0u, 0u};
+                uint32_t B8[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
                 uint32_t rb = 0;
-                if (NIB) {
+                if (NIB && PBSA_PRMT_ADDR) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+#pragma unroll
+                        for (int r = 0; r < L; ++r) {
+                            const uint32_t x4 = (p[r] >> (4 * k)) & 0xFu;
+                            B8[k] |= (x4 * (0x00204081u << (r + 3))) & (0x01010101u << (r + 3));
+                        }
+                    }
+                    rb = (uint32_t)__cvta_generic_to_shared(sthr) + (uint32_t)d * (8u * kNibRow);
+                } else if (NIB) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
 #pragma unroll
@@ -473,7 +493,10 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
 #pragma unroll
                 for (int b = 31; b >= 0; --b) {
                     uint2 t;
-                    if (NIB) {
+                    if (NIB && PBSA_PRMT_ADDR) {
+                        const uint32_t addr = __byte_perm(B8[b >> 2], rb, 0x7650u | (uint32_t)(b & 3));
+                        asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(t.x), "=r"(t.y) : "r"(addr));
+                    } else if (NIB) {
                         const int k = b >> 3, j = b & 7;
                         const uint32_t x = j == 0 ? (N[k] << 3) : (N[k] >> (4 * j - 3));
                         const uint32_t addr = (x & 0x78u) | rb;

@@ -673,7 +673,7 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         // (native Philox draws keep no cache, so nothing gains from phases: measured
         // G81 x 4096 9.1e11 updates/s unphased vs 7.8e11 in phases of 13)
         const bool may_phase = !g_oneshot && !many_launches && !P.spsa_packed && !P.native;
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 16) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
+        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 32) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
                              pbsa::kPackedFlushBytes;
         const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
         int occ = 0;
