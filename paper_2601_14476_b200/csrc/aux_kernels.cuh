@@ -49,7 +49,7 @@ __global__ void packed_cache_init(uint2 *__restrict__ acache, const uint64_t *__
     // store y' = s ^ (s >> 30): the sweep only XORs the sub-step counter into
     // its low word (count < 2^30 never reaches the shifted bits)
     const uint64_t y = s ^ (s >> 30);
-    acache[g] = make_uint2((uint32_t)y, cache_hi_entry((uint32_t)(y >> 32)));
+    acache[tile * 1024 + cache_lane(lane) + cache_off(b)] = make_uint2((uint32_t)y, cache_hi_entry((uint32_t)(y >> 32)));
 }
 
 

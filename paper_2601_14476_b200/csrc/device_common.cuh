@@ -229,6 +229,16 @@ __device__ __forceinline__ uint32_t packed_hash_hi_c(uint32_t yl, uint32_t c1) {
 #ifndef PBSA_CACHE_C1
 #define PBSA_CACHE_C1 1
 #endif
+// Layout of a (word, 32-node chunk) tile of the hash cache (1024 entries of
+// 8 B): with PBSA_CACHE_PAIRS trial pairs are interleaved per lane,
+// [b / 2][lane][b % 2], so the plain sweep loads two trials with one 16-byte
+// load; else [b][lane].  cache_lane / cache_off give a lane's base and trial b's
+// offset in entries.
+#ifndef PBSA_CACHE_PAIRS
+#define PBSA_CACHE_PAIRS 1
+#endif
+__host__ __device__ __forceinline__ int cache_lane(int lane) { return PBSA_CACHE_PAIRS ? 2 * lane : lane; }
+__host__ __device__ __forceinline__ int cache_off(int b) { return PBSA_CACHE_PAIRS ? (b >> 1) * 64 + (b & 1) : b * 32; }
 __device__ __forceinline__ uint32_t cache_c1(uint32_t hi) { return PBSA_CACHE_C1 ? hi : hi * 0x1CE4E5B9u; }
 __host__ __device__ __forceinline__ uint32_t cache_hi_entry(uint32_t yh) {
     return PBSA_CACHE_C1 ? yh * 0x1CE4E5B9u : yh;

@@ -17,6 +17,12 @@ __device__ __forceinline__ uint2 cache_ld(const uint2 *p) {
     if (PBSA_CACHE_LD == 2) return *p;
     return __ldcs(p);
 }
+__device__ __forceinline__ uint4 cache_ld2(const uint2 *p) {  // trials b - 1, b (b odd)
+    const uint4 *q = reinterpret_cast<const uint4 *>(p);
+    if (PBSA_CACHE_LD == 1) return __ldg(q);
+    if (PBSA_CACHE_LD == 2) return *q;
+    return __ldcs(q);
+}
 // PBSA_CACHE_PREFETCH: 1 prefetches a warp's first hash-cache tile into L1
 // ahead of the dependent-launch wait, 2 also each next tile; 0 none.  At run
 // time only for phased plans (the phase's cache is L2-resident: G81 C4
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                 // slower here; the timing kernels, whose reads are scattered, use it.)
                 const uint32_t ui = (uint32_t)i;
                 const float2 *pr = a.prof + (size_t)w * 32 * a.n + i;
-                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
+                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + cache_lane(lane) : nullptr;
                 uint32_t word = 0, exact = 0;
                 uint32_t X[4];  // NATIVE: the current Philox block (trials 4k .. 4k + 3)
                 auto decide = [&](int b, float2 lv) {
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                                              kNativeTagR, a.rk, X);
                         zh = X[b & 3];
                     } else if (CACHED) {
-                        const uint2 v = cache_ld(ctile + b * 32);
+                        const uint2 v = cache_ld(ctile + cache_off(b));
                         zh = packed_hash_hi_c(v.x ^ count, cache_c1(v.y));
                     } else {
                         const uint2 kc = key[b];
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                 // thresholds indexed by acc + f dmax = 2 S + f (dmax - d) (f = filled)
                 const int off = a.filled * (a.dmax - d);
                 const uint32_t rb = (uint32_t)__cvta_generic_to_shared(sthr) + 8u * (uint32_t)off;
-                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
+                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + cache_lane(lane) : nullptr;
                 uint32_t word = 0, tie = 0xffffffffu;
                 const uint32_t ui = (uint32_t)i;
                 uint32_t X[4];  // NATIVE: the current Philox block
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                                              kNativeTagR, a.rk, X);
                         native_decide(X[b & 3], t, word);
                     } else if (CACHED) {
-                        const uint2 v = cache_ld(ctile + b * 32);
+                        const uint2 v = cache_ld(ctile + cache_off(b));
                         tie = min(tie, packed_decide_y(v.x ^ count, cache_c1(v.y), t, word));
                     } else {
                         const uint2 kc = key[b];
@@ -336,7 +342,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                 // u = u01(key, TAG_STALL, i, count) < p_stall; the first update is always fresh.
                 uint32_t *sidx = a.sidx + (size_t)w * 32 * a.n + i;
                 const int base = a.cycle * a.Kc + a.dmax - d;      // fresh index = base + 2 pop
-                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
+                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + cache_lane(lane) : nullptr;
                 const uint32_t ui = (uint32_t)i;
                 // pass 1: stall bits of the 32 trials (exactly, before any index is replaced)
                 uint32_t stallw = 0;
@@ -430,7 +436,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                                                  kNativeTagR, a.rk, X);
                             native_decide(X[b & 3], t, word);
                         } else if (CACHED) {
-                            const uint2 v = cache_ld(ctile + b * 32);
+                            const uint2 v = cache_ld(ctile + cache_off(b));
                             tie = min(tie, packed_decide_y(v.x ^ count, cache_c1(v.y), t, word));
                         } else {
                             const uint2 kc = key[b];
@@ -454,10 +460,11 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                 const uint2 *tb = sthr + (a.dmax - d);   // entry for raw = 2 pop - d
                 // cache tile of (word w, chunk ch): [b][lane], so trial b of this
                 // lane sits at a compile-time offset b * 256 B
-                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + lane : nullptr;
+                const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + cache_lane(lane) : nullptr;
                 uint32_t word = 0, tie = 0xffffffffu;
                 const uint32_t ui = (uint32_t)i;
                 uint32_t X[4];  // NATIVE: the current Philox block (trials 4k .. 4k + 3)
+                uint4 cpair = make_uint4(0u, 0u, 0u, 0u);  // CACHED: the current trial pair
                 // NIB: transpose the L count planes into 32 nibbles (N[k] nibble j =
                 // count of trial 8k + j), a few ops per 32 trials instead of 2L per trial;
                 // PBSA_PRMT_ADDR: into bytes holding 8 x count (B[k] byte j = trial
@@ -515,8 +522,13 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                         uint32_t dummy;
                         asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
                             : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
+                    } else if (CACHED && PBSA_CACHE_PAIRS) {
+                        // one 16-byte load per trial pair (b odd: trials b, b - 1)
+                        if (b & 1) cpair = cache_ld2(ctile + cache_off(b - 1));
+                        const uint32_t vx = (b & 1) ? cpair.z : cpair.x, vy = (b & 1) ? cpair.w : cpair.y;
+                        tie = min(tie, packed_decide_n2(vx ^ count, cache_c1(vy), t, word));
                     } else if (CACHED) {
-                        const uint2 v = cache_ld(ctile + b * 32);
+                        const uint2 v = cache_ld(ctile + cache_off(b));
                         tie = min(tie, packed_decide_n2(v.x ^ count, cache_c1(v.y), t, word));
                     } else {
                         const uint2 kc = key[b];

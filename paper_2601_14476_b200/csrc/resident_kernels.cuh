@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
             vc_add<L, CP>(C, g);
             if (c == a.cycles) continue;  // final cut pass
             const uint32_t ui = (uint32_t)i;
-            const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + (i >> 5)) * 1024 + (i & 31) : nullptr;
+            const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + (i >> 5)) * 1024 + cache_lane(i & 31) : nullptr;
             if (VARU) {  // the packed ALG=3 decision (sigmoid prefilter, exact recheck)
                 const double i0 = a.i0[cc];
                 const float i0f = (float)i0;
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                             philox4x32_10_rk(ui, count, grp + (uint32_t)(b >> 2), kNativeTagR, a.rk, X);
                         zh = X[b & 3];
                     } else if (CACHED) {
-                        const uint2 v = __ldcs(ctile + b * 32);
+                        const uint2 v = __ldcs(ctile + cache_off(b));
                         zh = packed_hash_hi_c(v.x ^ count, cache_c1(v.y));
                     } else {
                         const uint2 kc = key[b];
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                             philox4x32_10_rk(ui, count, grp + (uint32_t)(b >> 2), kNativeTagR, a.rk, X);
                         native_decide(X[b & 3], t, word);
                     } else if (CACHED) {
-                        const uint2 v = __ldcs(ctile + b * 32);
+                        const uint2 v = __ldcs(ctile + cache_off(b));
                         tie = min(tie, packed_decide_y(v.x ^ count, cache_c1(v.y), t, word));
                     } else {
                         const uint2 kc = key[b];
@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                     asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
                         : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
                 } else if (CACHED) {
-                    const uint2 v = __ldcs(ctile + b * 32);
+                    const uint2 v = __ldcs(ctile + cache_off(b));
                     tie = min(tie, packed_decide_n2(v.x ^ count, cache_c1(v.y), t, word));
                 } else {
                     const uint2 kc = key[b];
