@@ -109,13 +109,12 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
             thi = (uint32_t)(tfull >> 32);
         } else {
             int raw = k - a.dmax;
-            bool ok = true;
             if (NIB) {
                 const int d = k / kNibRow, pp = k % kNibRow;
+                if (pp > d) continue;  // (a count never exceeds the degree: never read)
                 raw = 2 * pp - d;
-                ok = pp <= d;
             }
-            tfull = ok ? a.thr[raw + a.dmax] : 0ULL;
+            tfull = a.thr[raw + a.dmax];
             thi = (uint32_t)(tfull >> 32);
         }
         if (NATIVE && !VAR) {  // (lo, hi) of the 33-bit 2^32 - T: carry of X + it is X >= T
