@@ -94,6 +94,7 @@ struct PackedArgs {
     int warps_per_word;       // warps sharing one word index
     int cta_flush;            // every warp of a block has the same word: one cut flush per block
     int cache_prefetch;       // prefetch hash-cache tiles into L1 (phased plans: the cache is L2-resident)
+    int grid2d;               // 2-D grid (warps_per_word / kPackedWarps, words): one word per block
     int chunks;               // ceil(n / 32)
     uint32_t count;           // global sub-step counter c * t_res (< 2^30)
     int do_update;            // 0: only accumulate pacc (final cut pass)
@@ -154,20 +155,23 @@ constexpr size_t kPackedFlushBytes = (size_t)kPackedWarps * 10 * 32 * 4 + 16;
 
 __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umulhi(a, b); }
 
-// (lo, hi + add) of a 32 x 32 product: one IMAD.WIDE (+ the add) instead of a
-// multiply and a multiply-high (PBSA_WIDE_MUL=0: the two-instruction form)
+// (lo, hi + add) of a 32 x 32 product.  WIDE: one IMAD.WIDE (+ the add)
+// instead of a multiply and a multiply-high -- used by the plain sweep's
+// decision only (C4 +1.5 %); in the period-bucket kernel it cost registers
+// (G55 C3 +7 % time), elsewhere it compiled to the same code.
 #ifndef PBSA_WIDE_MUL
 #define PBSA_WIDE_MUL 1
 #endif
+template <bool WIDE = false>
 __device__ __forceinline__ void mul_lohi(uint32_t a, uint32_t m, uint32_t add, uint32_t &lo, uint32_t &hi) {
-#if PBSA_WIDE_MUL
-    const uint64_t p = (uint64_t)a * m;
-    lo = (uint32_t)p;
-    hi = (uint32_t)(p >> 32) + add;
-#else
-    lo = a * m;
-    hi = mulhi(a, m) + add;
-#endif
+    if (WIDE) {
+        const uint64_t p = (uint64_t)a * m;
+        lo = (uint32_t)p;
+        hi = (uint32_t)(p >> 32) + add;
+    } else {
+        lo = a * m;
+        hi = mulhi(a, m) + add;
+    }
 }
 
 // First absorb of a trial's draw: s = absorb(K, i) + GAMMA, as (lo, hi).
@@ -316,7 +320,7 @@ __device__ __forceinline__ uint32_t packed_decide_n2(uint32_t yl, uint32_t c1, u
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
     uint32_t zl, zh;
-    mul_lohi(yl, M1L, yl * M1H + c1, zl, zh);
+    mul_lohi<PBSA_WIDE_MUL != 0>(yl, M1L, yl * M1H + c1, zl, zh);
     yl = zl ^ __funnelshift_r(zl, zh, 27);
     const uint32_t yh = zh ^ mulhi(zh, 1u << 5);
     zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;

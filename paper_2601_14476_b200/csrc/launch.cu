@@ -257,6 +257,9 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                         a.warps_per_word = P.warps_per_word;
                         a.cta_flush = (P.cta_flush && P.warps_per_word % pbsa::kPackedWarps == 0) ? 1 : 0;
                     a.cache_prefetch = P.phase_words < P.W ? 1 : 0;
+                    // (the bucket kernel keeps the 1-D grid: G55 C3 measured 7 % slower 2-D)
+                    a.grid2d = a.cta_flush && !(P.bucket && pl.update);
+                    if (const char *env = std::getenv("PBSA_GRID2D")) a.grid2d = a.cta_flush && env[0] == '1';
                     if (const char *env = std::getenv("PBSA_CACHE_PREFETCH")) a.cache_prefetch = env[0] == '1';
                         a.chunks = P.chunks;
                         a.count = pl.count;
@@ -313,7 +316,10 @@ void enqueue_run(pbsa_plan &P, int64_t mm, int64_t gm) {
                             // programmatic dependent launch: the next sub-step's prologue
                             // overlaps this one's tail (the kernel waits on griddepcontrol)
                             cudaLaunchConfig_t cfg{};
-                            cfg.gridDim = dim3((unsigned)blocks);
+                            // one word per block: a 2-D grid (blocks of a word, words)
+                            cfg.gridDim = a.grid2d ? dim3((unsigned)(P.warps_per_word / pbsa::kPackedWarps),
+                                                             (unsigned)(w1 - w0))
+                                                      : dim3((unsigned)blocks);
                             cfg.blockDim = dim3(pbsa::kPackedThreads);
                             cfg.dynamicSmemBytes = (pl.update && P.var_mode && !P.var_uniform)
                                                        ? (P.bucket ? pbsa::bucket_smem_bytes(P.L) : pbsa::kTimingSmem)

@@ -23,6 +23,19 @@ __device__ __forceinline__ uint4 cache_ld2(const uint2 *p) {  // trials b - 1, b
     if (PBSA_CACHE_LD == 2) return *q;
     return __ldcs(q);
 }
+// A warp's word w (within the launch) and its slot q among the word's
+// warps_per_word warps.  With one word per block the grid may be 2-D,
+// (warps_per_word / kPackedWarps, words), and no division is needed.
+__device__ __forceinline__ void word_and_slot(const PackedArgs &a, int wib, int &w, int &q) {
+    if (a.grid2d) {
+        w = (int)blockIdx.y;
+        q = (int)blockIdx.x * kPackedWarps + wib;
+    } else {
+        const int g = (int)blockIdx.x * kPackedWarps + wib;
+        w = g / a.warps_per_word;
+        q = g % a.warps_per_word;
+    }
+}
 // PBSA_CACHE_PREFETCH: 1 prefetches a warp's first hash-cache tile into L1
 // ahead of the dependent-launch wait, 2 also each next tile; 0 none.  At run
 // time only for phased plans (the phase's cache is L2-resident: G81 C4
@@ -75,7 +88,9 @@ constexpr int packed_min_blocks() {
 template <int L, bool UPDATE, bool CACHED, int ALG = 0>
 __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, CACHED, ALG>())) packed_sweep(PackedArgs a) {
     asm volatile("griddepcontrol.launch_dependents;");
-    extern __shared__ unsigned long long smem_u64[];
+    // (declared 1 KB-aligned: the table base is then a known shared-window
+    // address, so its accesses compile to STS / LDS rather than generic ones)
+    extern __shared__ __align__(1024) unsigned long long smem_pk[];
     // Threshold table, 128 B aligned.  L <= 4 (degree <= 15): one 16-entry row
     // per degree d indexed by the neighbour count p (raw = 2p - d), so a
     // trial's entry address is (p * 8) | row base, formed with one LOP3.
@@ -90,15 +105,13 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
     // NIB rows: one per degree, kNibRow entries of 8 B (256 B with PBSA_PRMT_ADDR,
     // so a row base has a zero low byte and one PRMT forms a trial's address)
     constexpr int kNibRow = PBSA_PRMT_ADDR ? 32 : 16;
-    uint2 *sthr = reinterpret_cast<uint2 *>(
-        (reinterpret_cast<uintptr_t>(smem_u64) + 511) & ~(uintptr_t)511);
+    uint2 *sthr = reinterpret_cast<uint2 *>(smem_pk);
     const int tab_entries = VAR ? 0 : TAPSA ? a.K : NIB ? (a.dmax + 1) * kNibRow : a.K;
     uint2 *skey = sthr + tab_entries;                     // [warps][32] {F, C}
 
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int gwarp = blockIdx.x * kPackedWarps + wib;
-    const int w = gwarp / a.warps_per_word;
-    const int q = gwarp % a.warps_per_word;
+    int w, q;
+    word_and_slot(a, wib, w, q);
     const bool live = w < a.W;
 
     for (int k = threadIdx.x; k < tab_entries; k += blockDim.x) {
@@ -609,9 +622,8 @@ __global__ void __launch_bounds__(kPackedThreads, PBSA_PACKED_MIN_BLOCKS)
     uint32_t *sexm = sres + kPackedWarps * 32;                                   // [warps][32]
     uint32_t *sfl = sexm + kPackedWarps * 32;                                    // [warps][1024]
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int gwarp = blockIdx.x * kPackedWarps + wib;
-    const int w = gwarp / a.warps_per_word;
-    const int q = gwarp % a.warps_per_word;
+    int w, q;
+    word_and_slot(a, wib, w, q);
     const bool live = w < a.W;
     uint2 *key = skey + wib * 32;
     key[lane] = live ? a.kfc[(size_t)w * 32 + lane] : make_uint2(0, 0);
@@ -823,9 +835,8 @@ __global__ void __launch_bounds__(kPackedThreads, L <= 3 ? PBSA_BUCKET_MIN_BLOCK
     uint16_t *sdiv = reinterpret_cast<uint16_t *>(swarp + kPackedWarps * WB);  // [kBucketMaxDiv]
     uint8_t *slast = reinterpret_cast<uint8_t *>(sdiv + kBucketMaxDiv);       // [kBucketMaxDiv]
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int gwarp = blockIdx.x * kPackedWarps + wib;
-    const int w = gwarp / a.warps_per_word;
-    const int q = gwarp % a.warps_per_word;
+    int w, q;
+    word_and_slot(a, wib, w, q);
     const bool live = w < a.W;
     uint2 *key = skey + wib * 32;
     key[lane] = live ? a.kfc[(size_t)w * 32 + lane] : make_uint2(0, 0);
