@@ -316,6 +316,13 @@ uint64_t pbsa_threshold_host(double t);
  *     the device, philox.cuh). */
 uint64_t pbsa_threshold_native_host(double t);
 void pbsa_philox_host(const uint32_t *ctr, const uint32_t *key, uint32_t *out);
+/*   pbsa_choose_phases_host -- the packed sweep's word-phase width for a batch
+ *     of W words of `chunks` 32-node chunks on a device with resident_warps
+ *     resident sweep warps and an L2 budget in bytes (0: one phase), as plan
+ *     creation picks it (csrc/plan.cu choose_phases); *balance receives
+ *     whether the chunks are spread evenly over fewer warps. */
+int64_t pbsa_choose_phases_host(int64_t chunks, int64_t W, int64_t resident_warps, int64_t l2_budget,
+                                int *balance);
 
 #ifdef __cplusplus
 }

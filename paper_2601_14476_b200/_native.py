@@ -85,6 +85,7 @@ _SIGNATURES = [
     ("pbsa_threshold_host", ctypes.c_uint64, [_F64]),
     ("pbsa_threshold_native_host", ctypes.c_uint64, [_F64]),
     ("pbsa_philox_host", None, [_P, _P, _P]),
+    ("pbsa_choose_phases_host", _I64, [_I64, _I64, _I64, _I64, ctypes.POINTER(ctypes.c_int)]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGNATURES]

@@ -1045,3 +1045,12 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
 }
 
 }  // namespace pbsa_rt
+
+// Host export of the launch-shape model (include/pbsa.h), for the CPU tests.
+extern "C" int64_t pbsa_choose_phases_host(int64_t chunks, int64_t W, int64_t resident_warps, int64_t l2_budget,
+                                           int *balance) {
+    bool b = false;
+    const int64_t pw = pbsa_rt::choose_phases(chunks, W, resident_warps, (size_t)std::max<int64_t>(0, l2_budget), &b);
+    if (balance) *balance = b ? 1 : 0;
+    return pw;
+}

@@ -132,3 +132,36 @@ def test_native_threshold_matches_native_decision():
             assert _native_decision(float(t), T)
         if T > 0:
             assert not _native_decision(float(t), T - 1)
+
+
+def test_launch_shape_model_picks_the_measured_best_phase_widths():
+    """The word-phase width plan creation picks (plan.cu choose_phases, host
+    export) for B200 parameters -- 148 SMs x blocks per SM x 4 warps, 5/8 of
+    the 126.5 MiB L2 -- against the widths measured fastest on one B200
+    (profiles/r02_summary.md, "Word-phase width"): G81 13, G77 19, G67 26,
+    G60 43, one phase for G55 and G48 at 4096 trials; two phases of 16 words
+    for the 1024-trial G81 shard, one phase at 512 trials."""
+    import ctypes
+    lib = _native.load()
+    budget = 132644864 * 5 // 8
+
+    def pick(n, words, blocks):
+        bal = ctypes.c_int()
+        pw = lib.pbsa_choose_phases_host((n + 31) // 32, words, 148 * blocks * 4, budget, ctypes.byref(bal))
+        return pw, bal.value
+
+    assert pick(20000, 128, 7) == (13, 1)
+    assert pick(14000, 128, 7)[0] == 19
+    assert pick(10000, 128, 7)[0] == 26
+    assert pick(7000, 128, 8)[0] == 43
+    assert pick(5000, 128, 8)[0] == 128
+    assert pick(3000, 128, 7)[0] == 128
+    assert pick(20000, 32, 7)[0] == 16
+    assert pick(20000, 16, 7)[0] == 16
+    # no L2 budget: always one phase; otherwise equal phases only
+    for n, words in ((20000, 128), (9000, 100), (800, 7)):
+        bal = ctypes.c_int()
+        assert lib.pbsa_choose_phases_host((n + 31) // 32, words, 4144, 0, ctypes.byref(bal)) == words
+        pw = lib.pbsa_choose_phases_host((n + 31) // 32, words, 4144, budget, ctypes.byref(bal))
+        nph = -(-words // pw)
+        assert -(-words // nph) == pw
