@@ -868,8 +868,8 @@ def test_full_batch_one_shot_call_matches_oracle(bench_graphs, golden_full):
 
 
 @pytest.mark.parametrize("tag,name,sig,trials,env,kernel", [
-    ("c3_g22", "G22", (0.5, 0.5, 0.5), 4096, {}, "resident_timing"),
-    ("c3_g22", "G22", (0.5, 0.5, 0.5), 4096, {"PBSA_RESIDENT": "0"}, "packed_bucket"),
+    ("c3_g22", "G22", (0.5, 0.5, 0.5), 4096, {}, "packed_bucket"),
+    ("c3_g22", "G22", (0.5, 0.5, 0.5), 4096, {"PBSA_RESIDENT": "1"}, "resident_timing"),
     ("c3_g55", "G55", (0.5, 0.5, 0.5), 4096, {}, "packed_bucket"),
     ("c3_g55", "G55", (0.5, 0.5, 0.5), 4096, {"PBSA_BUCKET": "0"}, "packed_timing"),
     ("c2_g1_nu1", "G1", (0.0, 0.0, 1.0), 1024, {}, "resident_timing"),
