@@ -790,14 +790,14 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
             // or larger problems are faster with launched sweeps
             // (TApSA: the launched sweep re-reads the ring every cycle; resident wins to
             // 128 words: G1 x 4096 alpha 4 27.2 -> 20.5 ms, G47 18.2 -> 16.5, G22 even)
-            // (timing spread: against the period-bucket kernel, 300 cycles -- resident
-            // G1 x 1024 / 2048 16 / 33 ms vs 37 / 41, G22 x 1024 20 vs 28; bucket G22
-            // x 2048 / 4096 33 / 61 vs 41 / 70, G47 x 2048 / 4096 27 / 32 vs 30 / 40,
-            // G1 x 4096 45 vs 46: resident up to 32 words, 64 for degree >= 32)
-            const bool timing_res = P.W <= 32 || (P.W <= 64 && nnz >= 32 * n);
-            bool want = ((P.var_mode && !P.var_uniform) ? timing_res
-                         : (P.W <= 64 || (P.tapsa_packed && !P.var_mode && P.W <= 128))) &&
-                        n <= 2500 && nnz >= 8 * n;
+            // (round 2, after the launched sweeps' instruction trims: resident up to 32
+            // words, 64 at mean degree >= 32.  Timing spread vs the period-bucket
+            // kernel, 300 cycles: resident G1 x 1024 / 2048 16 / 33 ms vs 37 / 41, G22
+            // x 1024 20 vs 28; bucket G22 x 2048 / 4096 33 / 61 vs 41 / 70, G47 x 2048 /
+            // 4096 27 / 32 vs 30 / 40.  Plain rule, 1000 cycles: resident G1 x 2048
+            // 11.0 vs 13.9 ms, G22 x 1024 7.7 vs 8.7; launched G22 x 2048 11.2 vs 14.9)
+            const bool small = P.W <= 32 || (P.W <= 64 && nnz >= 32 * n);
+            bool want = (small || (P.tapsa_packed && !P.var_mode && P.W <= 128)) && n <= 2500 && nnz >= 8 * n;
             if (const char *env = std::getenv("PBSA_RESIDENT")) want = env[0] == '1';
             want = want && n <= 32768;  // (the resident kernels stage the 16-bit CSR)
             int csz = 1;  // (measured: 8 for a handful of words, 4 beats 8 at 32 words)
