@@ -162,6 +162,9 @@ __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umu
 #ifndef PBSA_WIDE_MUL
 #define PBSA_WIDE_MUL 1
 #endif
+#ifndef PBSA_WIDE_Y
+#define PBSA_WIDE_Y 0
+#endif
 template <bool WIDE = false>
 __device__ __forceinline__ void mul_lohi(uint32_t a, uint32_t m, uint32_t add, uint32_t &lo, uint32_t &hi) {
     if (WIDE) {
@@ -204,7 +207,7 @@ __device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t c1, ui
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
     uint32_t zl, zh;
-    mul_lohi(yl, M1L, yl * M1H + c1, zl, zh);
+    mul_lohi<PBSA_WIDE_Y != 0>(yl, M1L, yl * M1H + c1, zl, zh);
     yl = zl ^ __funnelshift_r(zl, zh, 27);
     const uint32_t yh = zh ^ mulhi(zh, 1u << 5);
     zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
@@ -236,10 +239,12 @@ __device__ __forceinline__ uint32_t packed_hash_hi_c(uint32_t yl, uint32_t c1) {
 // Layout of a (word, 32-node chunk) tile of the hash cache (1024 entries of
 // 8 B): with PBSA_CACHE_PAIRS trial pairs are interleaved per lane,
 // [b / 2][lane][b % 2], so the plain sweep loads two trials with one 16-byte
-// load; else [b][lane].  cache_lane / cache_off give a lane's base and trial b's
-// offset in entries.
+// load; else [b][lane] (the default: the pairs were neutral on C4 and made the
+// single-trial loads of TApSA / SpSA / the resident kernels half-coalesced,
+// G81 TApSA +8 % time).  cache_lane / cache_off give a lane's base and trial
+// b's offset in entries.
 #ifndef PBSA_CACHE_PAIRS
-#define PBSA_CACHE_PAIRS 1
+#define PBSA_CACHE_PAIRS 0
 #endif
 __host__ __device__ __forceinline__ int cache_lane(int lane) { return PBSA_CACHE_PAIRS ? 2 * lane : lane; }
 __host__ __device__ __forceinline__ int cache_off(int b) { return PBSA_CACHE_PAIRS ? (b >> 1) * 64 + (b & 1) : b * 32; }

@@ -75,6 +75,9 @@ __device__ __forceinline__ void word_and_slot(const PackedArgs &a, int wib, int 
 #ifndef PBSA_MB_PHILOX
 #define PBSA_MB_PHILOX 6
 #endif
+#ifndef PBSA_MB_TAPSA
+#define PBSA_MB_TAPSA 7  // (TApSA G81 / G55 x 4096 -3 / -5 % time against 8)
+#endif
 template <int L, bool UPDATE, bool CACHED, int ALG>
 constexpr int packed_min_blocks() {
     return (UPDATE && CACHED && ALG == 0)
@@ -82,6 +85,7 @@ constexpr int packed_min_blocks() {
                   : L == 7 ? PBSA_MB_L7 : PBSA_PACKED_MIN_BLOCKS)
            : (UPDATE && ALG == 4) ? (L == 3 ? PBSA_MB_PHILOX_L3 : PBSA_MB_PHILOX)
            : (UPDATE && ALG == 5) ? PBSA_MB_PHILOX
+           : (UPDATE && ALG == 1) ? PBSA_MB_TAPSA
                                   : PBSA_PACKED_MIN_BLOCKS;
 }
 
