@@ -263,6 +263,402 @@ void host_csr(int64_t n, const int64_t *indptr, const int64_t *indices, const do
     }
 }
 
+// Packed path with a varied profile: the fp32 / fp16 prefilter pairs and the
+// exact fp64 profile on the device, and with a timing spread the bit-sliced
+// clamped periods, their class table and the launch list of every sub-step
+// some present period divides (_kernels.py:110-127).
+void packed_variability_setup(pbsa_plan &P, int64_t n, int64_t trials, int64_t cycles, int64_t t_res,
+                              const double *lam, const double *delta, const int64_t *period, int64_t pstride,
+                              bool native_prof, cudaStream_t st) {
+    const int64_t maxcount = cycles * t_res;
+    std::vector<uint8_t> divs;
+    // per-p-bit profile, trial-major [Tp][n] (padding trials: ideal).  The
+    // fp32 pair of the timing kernels is [W][n][32] instead: their fired
+    // p-bits are a sparse random ~15 % of each (word, node), so keeping a
+    // node's 32 trials in 256 contiguous bytes lets nearby fires share
+    // DRAM bursts that the [W][32][n] layout spreads over 32 rows
+    const int64_t Tp = P.Tp;
+    const bool node_major = !P.var_uniform;
+    if (!native_prof && pstride == n) {
+        // per-trial rows already in the plan's [trial][node] layout: upload
+        // the exact profile as given (padding rows ideal) and round the
+        // prefilter pairs on the device (no host copies or conversion)
+        P.lam64.alloc((size_t)Tp * n);
+        P.del64.alloc((size_t)Tp * n);
+        CK(cudaMemcpyAsync(P.lam64.p, lam, (size_t)trials * n * sizeof(double), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(P.del64.p, delta, (size_t)trials * n * sizeof(double), cudaMemcpyHostToDevice, st));
+        P.lam64.bytes_up = P.del64.bytes_up = (size_t)trials * n * sizeof(double);
+        if (Tp > trials) {
+            pbsa::fill_f64<<<grid_for((Tp - trials) * n, 256), 256, 0, st>>>(
+                P.lam64.p + (size_t)trials * n, (Tp - trials) * n, 1.0);
+            CK(cudaMemsetAsync(P.del64.p + (size_t)trials * n, 0, (size_t)(Tp - trials) * n * sizeof(double), st));
+        }
+    }
+    if (native_prof || pstride == n) {  // pairs from the device copy of the exact profile
+        if (node_major) P.prof16.alloc((size_t)Tp * n); else P.prof.alloc((size_t)Tp * n);
+        pbsa::profile_pairs<<<grid_for(Tp * n, 256), 256, 0, st>>>(
+            P.lam64.p, P.del64.p, Tp, (int)n, node_major ? P.prof16.p : nullptr,
+            node_major ? nullptr : P.prof.p);
+        CK(cudaGetLastError());
+    } else {
+        std::vector<float2> pf(node_major ? 0 : (size_t)Tp * n, make_float2(1.0f, 0.0f));
+        std::vector<__half2> pf16(node_major ? (size_t)Tp * n : 0, __floats2half2_rn(1.0f, 0.0f));
+        std::vector<double> l64((size_t)Tp * n, 1.0), d64((size_t)Tp * n, 0.0);
+        parallel_for(trials, 16, [&](int64_t t0, int64_t t1) {
+            for (int64_t t = t0; t < t1; ++t)
+                for (int64_t i = 0; i < n; ++i) {
+                    const size_t src = (size_t)(pstride ? t * n : 0) + i, dst = (size_t)t * n + i;
+                    const size_t pdst = node_major ? ((size_t)(t >> 5) * n + i) * 32 + (t & 31) : dst;
+                    l64[dst] = lam[src];
+                    d64[dst] = delta[src];
+                    // timing kernels: fp16 pair (overflow -> inf -> the exact recheck)
+                    if (node_major)
+                        pf16[pdst] = __floats2half2_rn((float)lam[src], (float)(lam[src] * delta[src]));
+                    else
+                        pf[pdst] = make_float2((float)lam[src], (float)(lam[src] * delta[src]));
+                }
+        });
+        if (node_major) P.prof16.upload(pf16, st); else P.prof.upload(pf, st);
+        P.lam64.upload(l64, st);
+        P.del64.upload(d64, st);
+
+    }
+    P.inp_var.alloc((size_t)Tp * n);
+    if (!P.var_uniform) {
+        // clamped periods (a period >= cycles * t_res fires only at count 0),
+        // bit-sliced per word: plane k bit b = bit k of trial 32w+b's period
+        P.nplanes = 1;
+        while ((1LL << P.nplanes) <= P.pmax) ++P.nplanes;
+        if (!native_prof) P.pcl.assign((size_t)trials * n, 0);
+        std::vector<uint32_t> planes((size_t)P.W * P.nplanes * n, 0u);
+        parallel_for(P.W, 1, [&](int64_t w0, int64_t w1) {
+            for (int64_t w = w0; w < w1; ++w)
+                for (int b = 0; b < 32; ++b) {
+                    const int64_t t = w * 32 + b;
+                    for (int64_t i = 0; i < n; ++i) {
+                        int64_t pc = t_res;
+                        if (t < trials && native_prof) {
+                            pc = P.pcl[(size_t)t * n + i];
+                        } else if (t < trials) {
+                            pc = std::min<int64_t>(period[(pstride ? t * n : 0) + i], maxcount);
+                            P.pcl[(size_t)t * n + i] = (uint8_t)pc;
+                        }
+                        for (int k = 0; k < P.nplanes; ++k)
+                            planes[((size_t)w * P.nplanes + k) * n + i] |= (uint32_t)((pc >> k) & 1) << b;
+                    }
+                }
+        });
+        P.pplanes.upload(planes, st);
+        std::vector<char> present(256, 0);
+        for (uint8_t pc : P.pcl) present[pc] = 1;  // (padding trials never matter)
+        std::vector<uint8_t> lut(256, 0), cdivs, cper;
+        for (int pc = 1; pc < 256; ++pc)
+            if (present[pc]) {
+                lut[pc] = (uint8_t)P.nclass++;
+                cper.push_back((uint8_t)pc);
+            }
+        P.blut.upload(lut, st);
+        P.bcper.upload(cper, st);
+        // ... or, with a timing spread, every sub-step some present period
+        // divides (the first sub-step of each cycle always runs: it takes the cut)
+        for (int64_t c = 0; c < cycles; ++c)
+            for (int64_t s = 0; s < t_res; ++s) {
+                const int64_t count = c * t_res + s;
+                const int64_t off = (int64_t)divs.size();
+                for (int64_t pc = 1; pc <= P.pmax; ++pc)
+                    if (present[pc] && count % pc == 0) {
+                        divs.push_back((uint8_t)pc);
+                        cdivs.push_back(lut[pc]);
+                    }
+                const int nd = (int)((int64_t)divs.size() - off);
+                if (nd > pbsa::kMaxDivisors) fail(PBSA_EINVAL, "too many dividing periods");
+                P.max_ndiv = std::max(P.max_ndiv, nd);
+                if (s == 0 || nd > 0)
+                    P.plaunch.push_back({(uint32_t)count, c, s == 0, nd, off, true,
+                                         count >= maxcount - P.pmax});
+            }
+        if (divs.empty()) {
+            divs.push_back(0);
+            cdivs.push_back(0);
+        }
+        P.vdivs.upload(divs, st);
+        P.bdivs.upload(cdivs, st);
+    }
+}
+
+// Launch shape of the packed sweep: word phases (choose_phases), the
+// first-absorb hash cache, warps per word, chains of word groups.
+void packed_launch_shape(pbsa_plan &P, int device, int64_t n, int64_t dmax) {
+    // launch shape: one wave of resident warps, each owning one word
+    // cache the sub-step-independent first absorb of every (trial, node)
+    // draw when it fits the budget (PBSA_PACKED_CACHE=0/1 overrides)
+    // phase width in words (PBSA_PACKED_PHASE_WORDS overrides; 0 = all)
+    // Large batches run in word phases whose hash cache stays L2-resident
+    // across their cycles (G81: 13 words, ~67 MB), which keeps HBM (and the
+    // 1 kW power cap) out of the loop.  The width comes from a wave model
+    // (choose_phases): fill the resident warps, give every warp the same
+    // chunk count, keep that count >= 2, fit the phase's cache in 5/8 of L2.
+    // A timing spread multiplies the launches by t_res: one phase, four chains.
+    const bool many_launches = P.var_mode && !P.var_uniform;
+    int sm_count = 148, l2_bytes = 0;
+    CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device));
+    const int sms = sm_count;
+    // (SpSA streams its per-p-bit drive index, which no phase keeps in L2: unphased)
+    // (native Philox draws keep no cache, so nothing gains from phases: measured
+    // G81 x 4096 9.1e11 updates/s unphased vs 7.8e11 in phases of 13)
+    const bool may_phase = !g_oneshot && !many_launches && !P.spsa_packed && !P.native;
+    const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 32) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
+                         pbsa::kPackedFlushBytes;
+    const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
+    int occ = 0;
+    {
+        // (the kernel instance, so its occupancy, does not depend on the phase width)
+        PackedKernel k0 = packed_kernel_for(P.L, true, !many_launches && !P.native, P.tapsa_packed, P.spsa_packed,
+                                            P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
+        set_packed_smem(k0, smem_up);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k0, pbsa::kPackedThreads, smem_up));
+        occ = std::max(occ, 1);
+    }
+    P.chunks = (int)((n + 31) / 32);
+    bool balance_chunks = false;
+    P.phase_words = choose_phases(P.chunks, P.W, (int64_t)sm_count * occ * pbsa::kPackedWarps,
+                                  may_phase ? (size_t)l2_bytes * 5 / 8 : 0, &balance_chunks);
+    if (P.phase_words >= P.W) P.phase_words = 0;
+    // one-shot calls of the plain rule on the launched path run pipelined
+    // (PBSA_PIPELINE=0 disables): four word phases, each phase's outputs
+    // copied back while the next anneals (decided again below once the
+    // resident choice is known)
+    P.pipelined = (g_oneshot || g_cached_oneshot) && !many_launches && !P.var_mode && !P.tapsa_packed &&
+                  !P.spsa_packed && !P.tapsa_hist_from_raw && P.W >= 16;
+    if (const char *env = std::getenv("PBSA_PIPELINE")) P.pipelined = P.pipelined && env[0] != '0';
+    // a cached one-shot plan keeps the benchmark's phases and chains (its
+    // launches are replayed from a graph, so their count costs nothing)
+    P.capturing_outputs = g_cached_oneshot && P.pipelined;
+    // (up to four phases, but each phase at least two waves of word-warps:
+    // measured G81 x 512 one-shot, four phases of 4 words 36.6 ms)
+    // a cached one-shot plan of an unphased batch still splits it in two when
+    // each half fills two waves of word-warps: the second half's outputs are
+    // then the only ones left to copy after the anneal
+    if (P.capturing_outputs && (P.phase_words == 0 || P.phase_words >= P.W)) {
+        const int64_t fill = ((int64_t)sm_count * 32 + (n + 31) / 32 - 1) / ((n + 31) / 32);
+        if (P.W >= 4 * fill) P.phase_words = (P.W + 1) / 2;  // (measured: halves of one wave lose)
+    }
+    if (P.pipelined && !P.capturing_outputs) {
+        const int64_t fill = (2LL * sm_count * 32 + (n + 31) / 32 - 1) / ((n + 31) / 32);
+        P.phase_words = std::min<int64_t>(P.W, std::max<int64_t>((P.W + 3) / 4, fill));
+    }
+    if (const char *env = std::getenv("PBSA_PACKED_PHASE_WORDS")) P.phase_words = std::atoi(env);
+    if (const char *env = std::getenv("PBSA_PDL")) P.use_pdl = env[0] != '0';
+    if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;
+    const size_t cache_entries = (size_t)P.phase_words * ((n + 31) / 32) * 1024;
+    // (with a timing spread the fired trials of a word are sparse: no cache)
+    P.use_cache = cache_entries * 8 <= (32ULL << 30) && !many_launches;
+    if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1' && !many_launches;
+    if (P.native) P.use_cache = false;  // Philox draws cache nothing
+    if (P.use_cache) P.acache.alloc(cache_entries);
+    PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
+                                          P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
+    set_packed_smem(kern, smem_up);
+    set_packed_smem(packed_kernel_for(P.L, false, false), smem);
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pbsa::kPackedThreads, smem_up));
+    occ = std::max(occ, 1);
+    const int64_t target_warps = (int64_t)sm_count * occ * pbsa::kPackedWarps;
+    int64_t wpw = std::max<int64_t>(1, target_warps / P.phase_words);  // one phase at a time
+    wpw = std::min<int64_t>(wpw, P.chunks);
+    // equal chunk counts per warp: a launch lasts as long as its busiest
+    // warp, so spread the chunks over the fewest warps that give the same
+    // maximum, when choose_phases scores that higher (PBSA_BALANCE_CHUNKS=0/1)
+    {
+        bool balance = balance_chunks;
+        if (const char *env = std::getenv("PBSA_BALANCE_CHUNKS")) balance = env[0] != '0';
+        if (balance) {
+            const int64_t per = (P.chunks + wpw - 1) / wpw;
+            wpw = (P.chunks + per - 1) / per;
+        }
+    }
+    // the per-thread bit-sliced cut counter holds sum(degree) < 2^(L+2)
+    const int64_t cap = (1LL << (P.L + 2)) - 1, dm = std::max<int64_t>(dmax, 1);
+    if (dm > cap) fail(PBSA_EINVAL, "degree too large for the packed cut counter");
+    const int64_t max_tasks = cap / dm;  // chunks one warp may take
+    wpw = std::max<int64_t>(wpw, std::min<int64_t>((P.chunks + max_tasks - 1) / max_tasks, P.chunks));
+    // a multiple of the block's warps, so each block works on one word and
+    // reduces the cut once (PBSA_CTA_FLUSH=0 keeps one flush per warp)
+    P.cta_flush = true;
+    if (const char *env = std::getenv("PBSA_CTA_FLUSH")) P.cta_flush = env[0] != '0';
+    if (P.cta_flush) wpw = (wpw + pbsa::kPackedWarps - 1) / pbsa::kPackedWarps * pbsa::kPackedWarps;
+    if (const char *env = std::getenv("PBSA_WARPS_PER_WORD"))  // (experiments; bounded like the default)
+        wpw = std::max<int64_t>(std::min<int64_t>(std::atoi(env), P.chunks),
+                                (P.chunks + max_tasks - 1) / max_tasks);
+    P.warps_per_word = (int)wpw;
+    // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
+    // small batches need many chains to hide launch gaps; large ones only a
+    // couple (fewer graph nodes to instantiate)
+    int chains = (many_launches || (P.spsa_packed && !g_oneshot && P.W >= 64)) ? 4
+                                                                 : (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
+    if (P.pipelined && !P.capturing_outputs) chains = 2;  // launched directly: keep the launch count low
+    if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
+    chains = (int)std::min<int64_t>(chains, P.W);
+    if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
+    for (int g = 1; g < chains; ++g) {
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        P.chain_streams.push_back(cs);
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        P.ev_join.push_back(e);
+    }
+    P.packed_blocks = (int)grid_for(P.W * wpw, pbsa::kPackedWarps);
+}
+
+// Resident cluster kernels for small batches of small dense graphs: a
+// word's double-buffered state in shared memory, one launch per run.
+void resident_setup(pbsa_plan &P, int device, int64_t n, const int64_t *indptr, int64_t alpha, int64_t cycles,
+                    cudaStream_t st) {
+    const int64_t nnz = indptr[n];
+    int sms = 148;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    // resident mode (plain rule, ideal profile): a word's double-buffered
+    // state in shared memory; cluster size so that W clusters cover the SMs
+    {
+        const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode;
+        const bool timing = P.var_mode && !P.var_uniform;
+        const bool varu = P.var_mode && P.var_uniform;
+        const bool tap = P.tapsa_packed && !P.var_mode;
+        const int tab = tap ? P.K : (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
+        P.res_smem = 512 + 2 * (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;  // two tables
+        int max_smem = 0;
+        CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        // measured: small batches (<= 64 words) of small dense graphs (n <= 2500,
+        // mean degree >= 8: G1, G47, G22) run 1.1-2.2x faster resident; sparse
+        // or larger problems are faster with launched sweeps
+        // (TApSA: the launched sweep re-reads the ring every cycle; resident wins to
+        // 128 words: G1 x 4096 alpha 4 27.2 -> 20.5 ms, G47 18.2 -> 16.5, G22 even)
+        // (round 2, after the launched sweeps' instruction trims: resident up to 32
+        // words, 64 at mean degree >= 32.  Timing spread vs the period-bucket
+        // kernel, 300 cycles: resident G1 x 1024 / 2048 16 / 33 ms vs 37 / 41, G22
+        // x 1024 20 vs 28; bucket G22 x 2048 / 4096 33 / 61 vs 41 / 70, G47 x 2048 /
+        // 4096 27 / 32 vs 30 / 40.  Plain rule, 1000 cycles: resident G1 x 2048
+        // 11.0 vs 13.9 ms, G22 x 1024 7.7 vs 8.7; launched G22 x 2048 11.2 vs 14.9)
+        const bool small = P.W <= 32 || (P.W <= 64 && nnz >= 32 * n);
+        bool want = (small || (P.tapsa_packed && !P.var_mode && P.W <= 128)) && n <= 2500 && nnz >= 8 * n;
+        if (const char *env = std::getenv("PBSA_RESIDENT")) want = env[0] == '1';
+        want = want && n <= 32768;  // (the resident kernels stage the 16-bit CSR)
+        int csz = 1;  // (measured: 8 for a handful of words, 4 beats 8 at 32 words)
+        while (csz < (P.W <= 8 ? 8 : 4) && P.W * csz < sms) csz *= 2;
+        if (const char *env = std::getenv("PBSA_RESIDENT_CS")) csz = std::max(1, std::atoi(env));
+        const int64_t per = (n + csz - 1) / csz;
+        int64_t slice = 0;  // largest CTA slice of the adjacency
+        for (int64_t r = 0; r < csz; ++r) {
+            const int64_t lo = std::min<int64_t>(n, r * per), hi = std::min<int64_t>(n, lo + per);
+            slice = std::max<int64_t>(slice, indptr[hi] - indptr[lo]);
+        }
+        P.res_smem += 4 * (size_t)(per + 1) + 2 * (size_t)slice + 4;  // (16-bit CSR slice)
+        if (tap) P.res_smem += 4 * (size_t)alpha * P.L * per;  // the ring slice
+        if (timing) {
+            // two lanes per node when a CTA's slice still takes one pass of <= 16 warps
+            // (measured: G1 C2 sigma_nu 1.0 70 -> 63 ms; a second pass costs more: G22)
+            P.res_split = (per + 15) / 16 <= 16;
+            if (const char *env = std::getenv("PBSA_RES_SPLIT")) P.res_split = env[0] == '1';
+            const int64_t thr = std::min<int64_t>(512, P.res_split ? ((per + 15) / 16) * 32 : ((per + 31) / 32) * 32);
+            P.res_smem = 32 * 8 + 8 * (size_t)n + (thr / 32) * (256 + 4096) + pbsa::kMaxDivisors * 32 +
+                         4 * (size_t)(P.nplanes * per + per + 1) + 2 * (size_t)slice + 68;
+            // stage the CTA's fp16 profile slice too when it fits (PBSA_RES_PROF=0 disables)
+            const size_t prof_bytes = 4 * (size_t)per * 32;
+            const char *penv = std::getenv("PBSA_RES_PROF");
+            P.res_prof_smem = (!penv || penv[0] != '0') && P.res_smem + prof_bytes <= (size_t)max_smem;
+            if (P.res_prof_smem) P.res_smem += prof_bytes;
+        }
+        // (per-thread cut counters take up to 32 nodes: 16 warps x 16 nodes x 32)
+        if (timing && want && P.res_smem <= (size_t)max_smem && per <= 16 * 16 * 32) {
+            P.resident = true;
+            P.res_timing = true;
+            P.res_cs = csz;
+            P.res_threads = (int)std::min<int64_t>(512, P.res_split ? ((per + 15) / 16) * 32 : ((per + 31) / 32) * 32);
+            std::vector<pbsa::RLaunch> rl;
+            for (const pbsa_plan::PLaunch &pl : P.plaunch)
+                rl.push_back({pl.count, (int)pl.cycle, pl.do_cut, pl.ndiv, (int)pl.div_off, pl.inp ? 1 : 0,
+                              P.i0[std::min<int64_t>(pl.cycle, cycles - 1)]});
+            P.rlaunch.upload(rl, st);
+            if (!P.i0_dev.n) P.i0_dev.upload(P.i0, st);
+            ResidentTimingKernel rk = resident_timing_for(P.L, P.native);
+            CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
+            if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        } else if ((plain || varu || tap) && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
+            // (the per-thread cut counter takes up to 32 nodes)
+            const int thr = (int)std::min<int64_t>(512, ((per + 31) / 32) * 32);
+            P.resident = true;
+            P.res_cs = csz;
+            P.res_threads = thr;
+            if (P.use_cache && P.phase_words < P.W) P.acache.alloc((size_t)P.W * P.chunks * 1024);
+            P.phase_words = P.W;
+            P.res_tapsa = tap;
+            ResidentKernel rk = resident_kernel_for(P.L, P.use_cache, varu, P.native, tap);
+            CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
+            if (varu && !P.i0_dev.n) P.i0_dev.upload(P.i0, st);
+            if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        }
+    }
+    if (P.resident) P.pipelined = P.capturing_outputs = false;
+}
+
+// Launched path: degree-sorted processing order of irregular graphs, and
+// the period-bucket slot records of a timing spread.
+void order_and_bucket_setup(pbsa_plan &P, int64_t n, const int64_t *indptr, cudaStream_t st) {
+    const int64_t nnz = indptr[n];
+    const bool many_launches = P.var_mode && !P.var_uniform;
+    // irregular graphs on the launched path: warps take nodes in degree
+    // order, so a chunk's lanes have similar degrees and the gather loop
+    // runs ~ their degree, not the largest of 32 random ones (labels, spin
+    // layout and draws are unchanged; PBSA_DEGREE_ORDER=0/1 overrides)
+    if (!P.resident && !P.reg4) {
+        std::vector<uint32_t> ord(n);
+        for (int64_t i = 0; i < n; ++i) ord[i] = (uint32_t)i;
+        std::stable_sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) {
+            return indptr[x + 1] - indptr[x] > indptr[y + 1] - indptr[y];
+        });
+        double sum_max = 0, sum_deg = (double)nnz;
+        for (int64_t c0 = 0; c0 < n; c0 += 32) {
+            int64_t mx = 0;
+            for (int64_t i = c0; i < std::min<int64_t>(n, c0 + 32); ++i)
+                mx = std::max<int64_t>(mx, indptr[i + 1] - indptr[i]);
+            sum_max += (double)mx * (double)(std::min<int64_t>(n, c0 + 32) - c0);
+        }
+        // (measured, 1024 trials: sparse random graphs gain -- G55 12.6 -> 11.0 ms, G60
+        // 15.1 -> 13.1 ms -- while dense ones lose to the scattered own-word and
+        // spin-store accesses -- G22 9.0 -> 10.9 ms, G1 12.2 -> 13.6 ms)
+        bool want = sum_max > 1.15 * sum_deg && nnz < 8 * n;
+        if (const char *env = std::getenv("PBSA_DEGREE_ORDER")) want = env[0] == '1';
+        if (want) {
+            ord.resize((size_t)P.chunks * 32, (uint32_t)n);
+            P.order.upload(ord, st);
+        }
+    }
+    // timing spread on the launched path: sort every tile's slots into
+    // period buckets once (PBSA_BUCKET=0 keeps packed_sweep_timing)
+    if (many_launches && !P.resident && P.max_ndiv <= pbsa::kBucketMaxDiv) {
+        const char *benv = std::getenv("PBSA_BUCKET");
+        P.bucket = !benv || benv[0] != '0';
+    }
+    if (P.bucket) {
+        const size_t tiles = (size_t)P.W * P.chunks;
+        P.brec.alloc(tiles * 1024);
+        P.boff.alloc(tiles * (P.nclass + 1));
+        pbsa::bucket_build<<<grid_for((int64_t)tiles, 8), 256, 0, st>>>(
+            P.pplanes.p, P.nplanes, P.blut.p, P.prof16.p, P.krg.p, (int)n, P.chunks, (int)P.W,
+            P.nclass, P.brec.p, P.boff.p, P.order.n ? P.order.p : nullptr);
+        CK(cudaGetLastError());
+        P.prof16.drop();   // (the slot-ordered copy replaces them)
+        P.pplanes.drop();
+        const PackedKernel bk = bucket_kernel_for(P.L, P.native);
+        set_packed_smem(bk, pbsa::bucket_smem_bytes(P.L));
+        int bocc = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bk, pbsa::kPackedThreads,
+                                                         pbsa::bucket_smem_bytes(P.L)));
+        (void)bocc;
+    }
+}
+
 void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
                  const int64_t *indices, const double *values, const double *hv, int64_t mm,
                  const int64_t *mei, const int64_t *mej, const double *mew, int64_t gm,
@@ -532,382 +928,20 @@ void create_plan(pbsa_plan &P, int device, int64_t n, const int64_t *indptr,
         if (!P.var_mode) P.raw_last.alloc((size_t)n * P.Tp);
 
         // launch sequence: one sweep per cycle (counter c * t_res) ...
-        std::vector<uint8_t> divs;
         if (!P.var_mode || P.var_uniform) {
             for (int64_t c = 0; c < cycles; ++c)
                 P.plaunch.push_back({(uint32_t)(c * t_res), c, 1, 0, 0, true,
                                      c == cycles - 1});
         }
-        if (P.var_mode) {
-            // per-p-bit profile, trial-major [Tp][n] (padding trials: ideal).  The
-            // fp32 pair of the timing kernels is [W][n][32] instead: their fired
-            // p-bits are a sparse random ~15 % of each (word, node), so keeping a
-            // node's 32 trials in 256 contiguous bytes lets nearby fires share
-            // DRAM bursts that the [W][32][n] layout spreads over 32 rows
-            const int64_t Tp = P.Tp;
-            const bool node_major = !P.var_uniform;
-            if (!native_prof && pstride == n) {
-                // per-trial rows already in the plan's [trial][node] layout: upload
-                // the exact profile as given (padding rows ideal) and round the
-                // prefilter pairs on the device (no host copies or conversion)
-                P.lam64.alloc((size_t)Tp * n);
-                P.del64.alloc((size_t)Tp * n);
-                CK(cudaMemcpyAsync(P.lam64.p, lam, (size_t)trials * n * sizeof(double), cudaMemcpyHostToDevice, st));
-                CK(cudaMemcpyAsync(P.del64.p, delta, (size_t)trials * n * sizeof(double), cudaMemcpyHostToDevice, st));
-                P.lam64.bytes_up = P.del64.bytes_up = (size_t)trials * n * sizeof(double);
-                if (Tp > trials) {
-                    pbsa::fill_f64<<<grid_for((Tp - trials) * n, 256), 256, 0, st>>>(
-                        P.lam64.p + (size_t)trials * n, (Tp - trials) * n, 1.0);
-                    CK(cudaMemsetAsync(P.del64.p + (size_t)trials * n, 0, (size_t)(Tp - trials) * n * sizeof(double), st));
-                }
-            }
-            if (native_prof || pstride == n) {  // pairs from the device copy of the exact profile
-                if (node_major) P.prof16.alloc((size_t)Tp * n); else P.prof.alloc((size_t)Tp * n);
-                pbsa::profile_pairs<<<grid_for(Tp * n, 256), 256, 0, st>>>(
-                    P.lam64.p, P.del64.p, Tp, (int)n, node_major ? P.prof16.p : nullptr,
-                    node_major ? nullptr : P.prof.p);
-                CK(cudaGetLastError());
-            } else {
-                std::vector<float2> pf(node_major ? 0 : (size_t)Tp * n, make_float2(1.0f, 0.0f));
-                std::vector<__half2> pf16(node_major ? (size_t)Tp * n : 0, __floats2half2_rn(1.0f, 0.0f));
-                std::vector<double> l64((size_t)Tp * n, 1.0), d64((size_t)Tp * n, 0.0);
-                parallel_for(trials, 16, [&](int64_t t0, int64_t t1) {
-                    for (int64_t t = t0; t < t1; ++t)
-                        for (int64_t i = 0; i < n; ++i) {
-                            const size_t src = (size_t)(pstride ? t * n : 0) + i, dst = (size_t)t * n + i;
-                            const size_t pdst = node_major ? ((size_t)(t >> 5) * n + i) * 32 + (t & 31) : dst;
-                            l64[dst] = lam[src];
-                            d64[dst] = delta[src];
-                            // timing kernels: fp16 pair (overflow -> inf -> the exact recheck)
-                            if (node_major)
-                                pf16[pdst] = __floats2half2_rn((float)lam[src], (float)(lam[src] * delta[src]));
-                            else
-                                pf[pdst] = make_float2((float)lam[src], (float)(lam[src] * delta[src]));
-                        }
-                });
-                if (node_major) P.prof16.upload(pf16, st); else P.prof.upload(pf, st);
-                P.lam64.upload(l64, st);
-                P.del64.upload(d64, st);
-
-            }
-            P.inp_var.alloc((size_t)Tp * n);
-            if (!P.var_uniform) {
-                // clamped periods (a period >= cycles * t_res fires only at count 0),
-                // bit-sliced per word: plane k bit b = bit k of trial 32w+b's period
-                P.nplanes = 1;
-                while ((1LL << P.nplanes) <= P.pmax) ++P.nplanes;
-                if (!native_prof) P.pcl.assign((size_t)trials * n, 0);
-                std::vector<uint32_t> planes((size_t)P.W * P.nplanes * n, 0u);
-                parallel_for(P.W, 1, [&](int64_t w0, int64_t w1) {
-                    for (int64_t w = w0; w < w1; ++w)
-                        for (int b = 0; b < 32; ++b) {
-                            const int64_t t = w * 32 + b;
-                            for (int64_t i = 0; i < n; ++i) {
-                                int64_t pc = t_res;
-                                if (t < trials && native_prof) {
-                                    pc = P.pcl[(size_t)t * n + i];
-                                } else if (t < trials) {
-                                    pc = std::min<int64_t>(period[(pstride ? t * n : 0) + i], maxcount);
-                                    P.pcl[(size_t)t * n + i] = (uint8_t)pc;
-                                }
-                                for (int k = 0; k < P.nplanes; ++k)
-                                    planes[((size_t)w * P.nplanes + k) * n + i] |= (uint32_t)((pc >> k) & 1) << b;
-                            }
-                        }
-                });
-                P.pplanes.upload(planes, st);
-                std::vector<char> present(256, 0);
-                for (uint8_t pc : P.pcl) present[pc] = 1;  // (padding trials never matter)
-                std::vector<uint8_t> lut(256, 0), cdivs, cper;
-                for (int pc = 1; pc < 256; ++pc)
-                    if (present[pc]) {
-                        lut[pc] = (uint8_t)P.nclass++;
-                        cper.push_back((uint8_t)pc);
-                    }
-                P.blut.upload(lut, st);
-                P.bcper.upload(cper, st);
-                // ... or, with a timing spread, every sub-step some present period
-                // divides (the first sub-step of each cycle always runs: it takes the cut)
-                for (int64_t c = 0; c < cycles; ++c)
-                    for (int64_t s = 0; s < t_res; ++s) {
-                        const int64_t count = c * t_res + s;
-                        const int64_t off = (int64_t)divs.size();
-                        for (int64_t pc = 1; pc <= P.pmax; ++pc)
-                            if (present[pc] && count % pc == 0) {
-                                divs.push_back((uint8_t)pc);
-                                cdivs.push_back(lut[pc]);
-                            }
-                        const int nd = (int)((int64_t)divs.size() - off);
-                        if (nd > pbsa::kMaxDivisors) fail(PBSA_EINVAL, "too many dividing periods");
-                        P.max_ndiv = std::max(P.max_ndiv, nd);
-                        if (s == 0 || nd > 0)
-                            P.plaunch.push_back({(uint32_t)count, c, s == 0, nd, off, true,
-                                                 count >= maxcount - P.pmax});
-                    }
-                if (divs.empty()) {
-                    divs.push_back(0);
-                    cdivs.push_back(0);
-                }
-                P.vdivs.upload(divs, st);
-                P.bdivs.upload(cdivs, st);
-            }
-        }
+        if (P.var_mode)
+            packed_variability_setup(P, n, trials, cycles, t_res, lam, delta, period, pstride, native_prof, st);
         P.plaunch.push_back({(uint32_t)(cycles * t_res), cycles, 1, 0, 0, false, false});
 
-        // launch shape: one wave of resident warps, each owning one word
-        // cache the sub-step-independent first absorb of every (trial, node)
-        // draw when it fits the budget (PBSA_PACKED_CACHE=0/1 overrides)
-        // phase width in words (PBSA_PACKED_PHASE_WORDS overrides; 0 = all)
-        // Large batches run in word phases whose hash cache stays L2-resident
-        // across their cycles (G81: 13 words, ~67 MB), which keeps HBM (and the
-        // 1 kW power cap) out of the loop.  The width comes from a wave model
-        // (choose_phases): fill the resident warps, give every warp the same
-        // chunk count, keep that count >= 2, fit the phase's cache in 5/8 of L2.
-        // A timing spread multiplies the launches by t_res: one phase, four chains.
-        const bool many_launches = P.var_mode && !P.var_uniform;
-        int sm_count = 148, l2_bytes = 0;
-        CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
-        CK(cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device));
-        const int sms = sm_count;
-        // (SpSA streams its per-p-bit drive index, which no phase keeps in L2: unphased)
-        // (native Philox draws keep no cache, so nothing gains from phases: measured
-        // G81 x 4096 9.1e11 updates/s unphased vs 7.8e11 in phases of 13)
-        const bool may_phase = !g_oneshot && !many_launches && !P.spsa_packed && !P.native;
-        const size_t smem = (size_t)std::max(P.K, (P.dmax + 1) * 32) * 8 + 512 + 2 * pbsa::kPackedWarps * 32 * 8 + 16 +
-                             pbsa::kPackedFlushBytes;
-        const size_t smem_up = many_launches ? pbsa::kTimingSmem : smem;
-        int occ = 0;
-        {
-            // (the kernel instance, so its occupancy, does not depend on the phase width)
-            PackedKernel k0 = packed_kernel_for(P.L, true, !many_launches && !P.native, P.tapsa_packed, P.spsa_packed,
-                                                P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
-            set_packed_smem(k0, smem_up);
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k0, pbsa::kPackedThreads, smem_up));
-            occ = std::max(occ, 1);
-        }
-        P.chunks = (int)((n + 31) / 32);
-        bool balance_chunks = false;
-        P.phase_words = choose_phases(P.chunks, P.W, (int64_t)sm_count * occ * pbsa::kPackedWarps,
-                                      may_phase ? (size_t)l2_bytes * 5 / 8 : 0, &balance_chunks);
-        if (P.phase_words >= P.W) P.phase_words = 0;
-        // one-shot calls of the plain rule on the launched path run pipelined
-        // (PBSA_PIPELINE=0 disables): four word phases, each phase's outputs
-        // copied back while the next anneals (decided again below once the
-        // resident choice is known)
-        P.pipelined = (g_oneshot || g_cached_oneshot) && !many_launches && !P.var_mode && !P.tapsa_packed &&
-                      !P.spsa_packed && !P.tapsa_hist_from_raw && P.W >= 16;
-        if (const char *env = std::getenv("PBSA_PIPELINE")) P.pipelined = P.pipelined && env[0] != '0';
-        // a cached one-shot plan keeps the benchmark's phases and chains (its
-        // launches are replayed from a graph, so their count costs nothing)
-        P.capturing_outputs = g_cached_oneshot && P.pipelined;
-        // (up to four phases, but each phase at least two waves of word-warps:
-        // measured G81 x 512 one-shot, four phases of 4 words 36.6 ms)
-        // a cached one-shot plan of an unphased batch still splits it in two when
-        // each half fills two waves of word-warps: the second half's outputs are
-        // then the only ones left to copy after the anneal
-        if (P.capturing_outputs && (P.phase_words == 0 || P.phase_words >= P.W)) {
-            const int64_t fill = ((int64_t)sm_count * 32 + (n + 31) / 32 - 1) / ((n + 31) / 32);
-            if (P.W >= 4 * fill) P.phase_words = (P.W + 1) / 2;  // (measured: halves of one wave lose)
-        }
-        if (P.pipelined && !P.capturing_outputs) {
-            const int64_t fill = (2LL * sm_count * 32 + (n + 31) / 32 - 1) / ((n + 31) / 32);
-            P.phase_words = std::min<int64_t>(P.W, std::max<int64_t>((P.W + 3) / 4, fill));
-        }
-        if (const char *env = std::getenv("PBSA_PACKED_PHASE_WORDS")) P.phase_words = std::atoi(env);
-        if (const char *env = std::getenv("PBSA_PDL")) P.use_pdl = env[0] != '0';
-        if (P.phase_words <= 0 || P.phase_words > P.W) P.phase_words = P.W;
-        const size_t cache_entries = (size_t)P.phase_words * ((n + 31) / 32) * 1024;
-        // (with a timing spread the fired trials of a word are sparse: no cache)
-        P.use_cache = cache_entries * 8 <= (32ULL << 30) && !many_launches;
-        if (const char *env = std::getenv("PBSA_PACKED_CACHE")) P.use_cache = env[0] == '1' && !many_launches;
-        if (P.native) P.use_cache = false;  // Philox draws cache nothing
-        if (P.use_cache) P.acache.alloc(cache_entries);
-        PackedKernel kern = packed_kernel_for(P.L, true, P.use_cache, P.tapsa_packed, P.spsa_packed,
-                                              P.var_mode ? (P.var_uniform ? 1 : 2) : 0, P.native);
-        set_packed_smem(kern, smem_up);
-        set_packed_smem(packed_kernel_for(P.L, false, false), smem);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pbsa::kPackedThreads, smem_up));
-        occ = std::max(occ, 1);
-        const int64_t target_warps = (int64_t)sm_count * occ * pbsa::kPackedWarps;
-        int64_t wpw = std::max<int64_t>(1, target_warps / P.phase_words);  // one phase at a time
-        wpw = std::min<int64_t>(wpw, P.chunks);
-        // equal chunk counts per warp: a launch lasts as long as its busiest
-        // warp, so spread the chunks over the fewest warps that give the same
-        // maximum, when choose_phases scores that higher (PBSA_BALANCE_CHUNKS=0/1)
-        {
-            bool balance = balance_chunks;
-            if (const char *env = std::getenv("PBSA_BALANCE_CHUNKS")) balance = env[0] != '0';
-            if (balance) {
-                const int64_t per = (P.chunks + wpw - 1) / wpw;
-                wpw = (P.chunks + per - 1) / per;
-            }
-        }
-        // the per-thread bit-sliced cut counter holds sum(degree) < 2^(L+2)
-        const int64_t cap = (1LL << (P.L + 2)) - 1, dm = std::max<int64_t>(dmax, 1);
-        if (dm > cap) fail(PBSA_EINVAL, "degree too large for the packed cut counter");
-        const int64_t max_tasks = cap / dm;  // chunks one warp may take
-        wpw = std::max<int64_t>(wpw, std::min<int64_t>((P.chunks + max_tasks - 1) / max_tasks, P.chunks));
-        // a multiple of the block's warps, so each block works on one word and
-        // reduces the cut once (PBSA_CTA_FLUSH=0 keeps one flush per warp)
-        P.cta_flush = true;
-        if (const char *env = std::getenv("PBSA_CTA_FLUSH")) P.cta_flush = env[0] != '0';
-        if (P.cta_flush) wpw = (wpw + pbsa::kPackedWarps - 1) / pbsa::kPackedWarps * pbsa::kPackedWarps;
-        if (const char *env = std::getenv("PBSA_WARPS_PER_WORD"))  // (experiments; bounded like the default)
-            wpw = std::max<int64_t>(std::min<int64_t>(std::atoi(env), P.chunks),
-                                    (P.chunks + max_tasks - 1) / max_tasks);
-        P.warps_per_word = (int)wpw;
-        // concurrent chains of word groups (PBSA_PACKED_CHAINS overrides; 1 disables)
-        // small batches need many chains to hide launch gaps; large ones only a
-        // couple (fewer graph nodes to instantiate)
-        int chains = (many_launches || (P.spsa_packed && !g_oneshot && P.W >= 64)) ? 4
-                                                                     : (int)std::max<int64_t>(1, std::min<int64_t>(16, 256 / P.phase_words));
-        if (P.pipelined && !P.capturing_outputs) chains = 2;  // launched directly: keep the launch count low
-        if (const char *env = std::getenv("PBSA_PACKED_CHAINS")) chains = std::max(1, std::atoi(env));
-        chains = (int)std::min<int64_t>(chains, P.W);
-        if (chains > 1) CK(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
-        for (int g = 1; g < chains; ++g) {
-            cudaStream_t cs;
-            CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-            P.chain_streams.push_back(cs);
-            cudaEvent_t e;
-            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            P.ev_join.push_back(e);
-        }
-        P.packed_blocks = (int)grid_for(P.W * wpw, pbsa::kPackedWarps);
-        // resident mode (plain rule, ideal profile): a word's double-buffered
-        // state in shared memory; cluster size so that W clusters cover the SMs
-        {
-            const bool plain = !P.tapsa_packed && !P.spsa_packed && !P.var_mode;
-            const bool timing = P.var_mode && !P.var_uniform;
-            const bool varu = P.var_mode && P.var_uniform;
-            const bool tap = P.tapsa_packed && !P.var_mode;
-            const int tab = tap ? P.K : (P.L <= 4 ? (P.dmax + 1) * 16 : P.K);
-            P.res_smem = 512 + 2 * (size_t)tab * 8 + 32 * 8 + 8 * (size_t)n;  // two tables
-            int max_smem = 0;
-            CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-            // measured: small batches (<= 64 words) of small dense graphs (n <= 2500,
-            // mean degree >= 8: G1, G47, G22) run 1.1-2.2x faster resident; sparse
-            // or larger problems are faster with launched sweeps
-            // (TApSA: the launched sweep re-reads the ring every cycle; resident wins to
-            // 128 words: G1 x 4096 alpha 4 27.2 -> 20.5 ms, G47 18.2 -> 16.5, G22 even)
-            // (round 2, after the launched sweeps' instruction trims: resident up to 32
-            // words, 64 at mean degree >= 32.  Timing spread vs the period-bucket
-            // kernel, 300 cycles: resident G1 x 1024 / 2048 16 / 33 ms vs 37 / 41, G22
-            // x 1024 20 vs 28; bucket G22 x 2048 / 4096 33 / 61 vs 41 / 70, G47 x 2048 /
-            // 4096 27 / 32 vs 30 / 40.  Plain rule, 1000 cycles: resident G1 x 2048
-            // 11.0 vs 13.9 ms, G22 x 1024 7.7 vs 8.7; launched G22 x 2048 11.2 vs 14.9)
-            const bool small = P.W <= 32 || (P.W <= 64 && nnz >= 32 * n);
-            bool want = (small || (P.tapsa_packed && !P.var_mode && P.W <= 128)) && n <= 2500 && nnz >= 8 * n;
-            if (const char *env = std::getenv("PBSA_RESIDENT")) want = env[0] == '1';
-            want = want && n <= 32768;  // (the resident kernels stage the 16-bit CSR)
-            int csz = 1;  // (measured: 8 for a handful of words, 4 beats 8 at 32 words)
-            while (csz < (P.W <= 8 ? 8 : 4) && P.W * csz < sms) csz *= 2;
-            if (const char *env = std::getenv("PBSA_RESIDENT_CS")) csz = std::max(1, std::atoi(env));
-            const int64_t per = (n + csz - 1) / csz;
-            int64_t slice = 0;  // largest CTA slice of the adjacency
-            for (int64_t r = 0; r < csz; ++r) {
-                const int64_t lo = std::min<int64_t>(n, r * per), hi = std::min<int64_t>(n, lo + per);
-                slice = std::max<int64_t>(slice, indptr[hi] - indptr[lo]);
-            }
-            P.res_smem += 4 * (size_t)(per + 1) + 2 * (size_t)slice + 4;  // (16-bit CSR slice)
-            if (tap) P.res_smem += 4 * (size_t)alpha * P.L * per;  // the ring slice
-            if (timing) {
-                // two lanes per node when a CTA's slice still takes one pass of <= 16 warps
-                // (measured: G1 C2 sigma_nu 1.0 70 -> 63 ms; a second pass costs more: G22)
-                P.res_split = (per + 15) / 16 <= 16;
-                if (const char *env = std::getenv("PBSA_RES_SPLIT")) P.res_split = env[0] == '1';
-                const int64_t thr = std::min<int64_t>(512, P.res_split ? ((per + 15) / 16) * 32 : ((per + 31) / 32) * 32);
-                P.res_smem = 32 * 8 + 8 * (size_t)n + (thr / 32) * (256 + 4096) + pbsa::kMaxDivisors * 32 +
-                             4 * (size_t)(P.nplanes * per + per + 1) + 2 * (size_t)slice + 68;
-                // stage the CTA's fp16 profile slice too when it fits (PBSA_RES_PROF=0 disables)
-                const size_t prof_bytes = 4 * (size_t)per * 32;
-                const char *penv = std::getenv("PBSA_RES_PROF");
-                P.res_prof_smem = (!penv || penv[0] != '0') && P.res_smem + prof_bytes <= (size_t)max_smem;
-                if (P.res_prof_smem) P.res_smem += prof_bytes;
-            }
-            // (per-thread cut counters take up to 32 nodes: 16 warps x 16 nodes x 32)
-            if (timing && want && P.res_smem <= (size_t)max_smem && per <= 16 * 16 * 32) {
-                P.resident = true;
-                P.res_timing = true;
-                P.res_cs = csz;
-                P.res_threads = (int)std::min<int64_t>(512, P.res_split ? ((per + 15) / 16) * 32 : ((per + 31) / 32) * 32);
-                std::vector<pbsa::RLaunch> rl;
-                for (const pbsa_plan::PLaunch &pl : P.plaunch)
-                    rl.push_back({pl.count, (int)pl.cycle, pl.do_cut, pl.ndiv, (int)pl.div_off, pl.inp ? 1 : 0,
-                                  P.i0[std::min<int64_t>(pl.cycle, cycles - 1)]});
-                P.rlaunch.upload(rl, st);
-                if (!P.i0_dev.n) P.i0_dev.upload(P.i0, st);
-                ResidentTimingKernel rk = resident_timing_for(P.L, P.native);
-                CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
-                if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            } else if ((plain || varu || tap) && want && P.res_smem <= (size_t)max_smem && per <= 32 * 512) {
-                // (the per-thread cut counter takes up to 32 nodes)
-                const int thr = (int)std::min<int64_t>(512, ((per + 31) / 32) * 32);
-                P.resident = true;
-                P.res_cs = csz;
-                P.res_threads = thr;
-                if (P.use_cache && P.phase_words < P.W) P.acache.alloc((size_t)P.W * P.chunks * 1024);
-                P.phase_words = P.W;
-                P.res_tapsa = tap;
-                ResidentKernel rk = resident_kernel_for(P.L, P.use_cache, varu, P.native, tap);
-                CK(cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.res_smem));
-                if (varu && !P.i0_dev.n) P.i0_dev.upload(P.i0, st);
-                if (csz > 8) CK(cudaFuncSetAttribute(rk, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            }
-        }
-        if (P.resident) P.pipelined = P.capturing_outputs = false;
-        // irregular graphs on the launched path: warps take nodes in degree
-        // order, so a chunk's lanes have similar degrees and the gather loop
-        // runs ~ their degree, not the largest of 32 random ones (labels, spin
-        // layout and draws are unchanged; PBSA_DEGREE_ORDER=0/1 overrides)
-        if (!P.resident && !P.reg4) {
-            std::vector<uint32_t> ord(n);
-            for (int64_t i = 0; i < n; ++i) ord[i] = (uint32_t)i;
-            std::stable_sort(ord.begin(), ord.end(), [&](uint32_t x, uint32_t y) {
-                return indptr[x + 1] - indptr[x] > indptr[y + 1] - indptr[y];
-            });
-            double sum_max = 0, sum_deg = (double)nnz;
-            for (int64_t c0 = 0; c0 < n; c0 += 32) {
-                int64_t mx = 0;
-                for (int64_t i = c0; i < std::min<int64_t>(n, c0 + 32); ++i)
-                    mx = std::max<int64_t>(mx, indptr[i + 1] - indptr[i]);
-                sum_max += (double)mx * (double)(std::min<int64_t>(n, c0 + 32) - c0);
-            }
-            // (measured, 1024 trials: sparse random graphs gain -- G55 12.6 -> 11.0 ms, G60
-            // 15.1 -> 13.1 ms -- while dense ones lose to the scattered own-word and
-            // spin-store accesses -- G22 9.0 -> 10.9 ms, G1 12.2 -> 13.6 ms)
-            bool want = sum_max > 1.15 * sum_deg && nnz < 8 * n;
-            if (const char *env = std::getenv("PBSA_DEGREE_ORDER")) want = env[0] == '1';
-            if (want) {
-                ord.resize((size_t)P.chunks * 32, (uint32_t)n);
-                P.order.upload(ord, st);
-            }
-        }
-        // timing spread on the launched path: sort every tile's slots into
-        // period buckets once (PBSA_BUCKET=0 keeps packed_sweep_timing)
-        if (many_launches && !P.resident && P.max_ndiv <= pbsa::kBucketMaxDiv) {
-            const char *benv = std::getenv("PBSA_BUCKET");
-            P.bucket = !benv || benv[0] != '0';
-        }
-        if (P.bucket) {
-            const size_t tiles = (size_t)P.W * P.chunks;
-            P.brec.alloc(tiles * 1024);
-            P.boff.alloc(tiles * (P.nclass + 1));
-            pbsa::bucket_build<<<grid_for((int64_t)tiles, 8), 256, 0, st>>>(
-                P.pplanes.p, P.nplanes, P.blut.p, P.prof16.p, P.krg.p, (int)n, P.chunks, (int)P.W,
-                P.nclass, P.brec.p, P.boff.p, P.order.n ? P.order.p : nullptr);
-            CK(cudaGetLastError());
-            P.prof16.drop();   // (the slot-ordered copy replaces them)
-            P.pplanes.drop();
-            const PackedKernel bk = bucket_kernel_for(P.L, P.native);
-            set_packed_smem(bk, pbsa::bucket_smem_bytes(P.L));
-            int bocc = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bocc, bk, pbsa::kPackedThreads,
-                                                             pbsa::bucket_smem_bytes(P.L)));
-            (void)bocc;
-        }
+        packed_launch_shape(P, device, n, dmax);
+        resident_setup(P, device, n, indptr, alpha, cycles, st);
+        order_and_bucket_setup(P, n, indptr, st);
         P.updates_per_run = (int64_t)n * trials * cycles;
-        if (many_launches) {  // sum over p-bits of #{count < cycles t_res : period | count}
+        if (P.var_mode && !P.var_uniform) {  // sum over p-bits of #{count < cycles t_res : period | count}
             int64_t ups = 0;
             for (uint8_t pc : P.pcl) ups += (maxcount + pc - 1) / pc;
             P.updates_per_run = ups;
