@@ -9,4 +9,4 @@ done
 for cs in 1 2; do
   echo "G55 C3 x4096 resident CS=$cs: $(PBSA_RESIDENT=1 PBSA_RESIDENT_CS=$cs timeout 200 python tools/timing_run.py G55 0.5,0.5,0.5 4096 1000 2>&1 | cut -c1-150 | tail -1)"
 done
-timeout 300 python tools/tapsa_ab.py G1:4096:4 G22:4096:4 G47:4096:4 G1:4096:8 2>&1
+timeout 300 python tools/experiments/tapsa_ab.py G1:4096:4 G22:4096:4 G47:4096:4 G1:4096:8 2>&1

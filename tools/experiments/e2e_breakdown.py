@@ -1,7 +1,7 @@
 """Where the end-to-end time of one pbsa_anneal_loop_batch-equivalent call goes."""
 import sys, time
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import numpy as np
 import torch
 from paper_2601_14476_b200 import _native, benchmarks, streams

@@ -8,5 +8,5 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/f
 timeout 1500 python tools/config_table.py --tag r01 > gpurun_out/final/configs.log 2>&1
 cp profiles/r01_configs.* gpurun_out/final/
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:resident_sweep --launch-count 1 \
-  -o gpurun_out/final/r01_resident_tapsa_g1 python tools/tapsa_ab.py G1:100:4 > gpurun_out/final/ncu_tapsa.log 2>&1
+  -o gpurun_out/final/r01_resident_tapsa_g1 python tools/experiments/tapsa_ab.py G1:100:4 > gpurun_out/final/ncu_tapsa.log 2>&1
 ls -la gpurun_out/final

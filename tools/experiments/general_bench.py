@@ -2,7 +2,7 @@
 (BASELINE C2/C3 shapes). Prints device ms and updates/s per config."""
 import sys, time
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import numpy as np
 from paper_2601_14476_b200 import _native, benchmarks, streams
 from paper_2601_14476_b200.annealer import Algorithm, AlgorithmConfig, derive_schedule, profile_rows

@@ -2,7 +2,7 @@
 (usage: oneshot_time.py [T] [graph])."""
 import sys, time
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import torch
 from paper_2601_14476_b200 import _native, benchmarks, streams
 from paper_2601_14476_b200.annealer import derive_schedule

@@ -1,7 +1,7 @@
 """Device time of one G81 x T plan run (phases/chains via PBSA_* env vars)."""
 import sys, time
 from pathlib import Path
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 from paper_2601_14476_b200 import _native, benchmarks, streams
 from paper_2601_14476_b200.annealer import derive_schedule
 from paper_2601_14476_b200.model import maxcut_to_ising

@@ -3,7 +3,7 @@ import os
 import sys
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 from paper_2601_14476_b200 import _native, benchmarks, streams
 from paper_2601_14476_b200.annealer import derive_schedule
 from paper_2601_14476_b200.model import maxcut_to_ising
