@@ -403,7 +403,10 @@ __device__ __forceinline__ void csa(uint32_t &h, uint32_t &l, uint32_t a, uint32
 // given by nb(k).  Degrees >= 8 go through a Harley-Seal carry-save tree
 // (seven CSAs per eight neighbours, ~2 ops each, plus one ripple of the
 // weight-8 digit) instead of an L-plane ripple per neighbour.
-template <int L, typename NB>
+#ifndef PBSA_MASKED_TAIL
+#define PBSA_MASKED_TAIL 1
+#endif
+template <int L, bool MASKED = true, typename NB>
 __device__ __forceinline__ void count_neighbours(uint32_t beg, uint32_t end, NB nb, uint32_t (&p)[L]) {
 #pragma unroll
     for (int r = 0; r < L; ++r) p[r] = 0;
@@ -417,30 +420,48 @@ __device__ __forceinline__ void count_neighbours(uint32_t beg, uint32_t end, NB 
         }
     };
     uint32_t k = beg;
+    // (called for L >= 3 only; the clamped plane indices keep the L < 3
+    // instances well-formed)
+    constexpr int P1 = L > 1 ? 1 : 0, P2 = L > 2 ? 2 : 0;
+    auto batch8 = [&](const uint32_t (&x)[8]) {
+        uint32_t twosA, twosB, foursA, foursB, eights;
+        csa(twosA, p[0], x[0], x[1]);
+        csa(twosB, p[0], x[2], x[3]);
+        csa(foursA, p[P1], twosA, twosB);
+        csa(twosA, p[0], x[4], x[5]);
+        csa(twosB, p[0], x[6], x[7]);
+        csa(foursB, p[P1], twosA, twosB);
+        csa(eights, p[P2], foursA, foursB);
+        ripple(eights, 3);
+    };
     if (L >= 4) {
         for (; k + 8 <= end; k += 8) {
             uint32_t x[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) x[j] = nb(k + j);
-            uint32_t twosA, twosB, foursA, foursB, eights;
-            csa(twosA, p[0], x[0], x[1]);
-            csa(twosB, p[0], x[2], x[3]);
-            csa(foursA, p[1], twosA, twosB);
-            csa(twosA, p[0], x[4], x[5]);
-            csa(twosB, p[0], x[6], x[7]);
-            csa(foursB, p[1], twosA, twosB);
-            csa(eights, p[2], foursA, foursB);
-            ripple(eights, 3);
+            batch8(x);
         }
     }
-    for (; k < end; ++k) ripple(nb(k), 0);
+    if (L >= 3 && MASKED && PBSA_MASKED_TAIL) {
+        // the remaining (< 8) entries as one masked batch, their loads in flight
+        // together instead of one dependent load pair per entry; absent entries
+        // add zero (and a sum below 2^L leaves the weight-8 digit zero for L = 3)
+        if (k < end) {
+            uint32_t x[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[j] = k + j < end ? nb(k + j) : 0u;
+            batch8(x);
+        }
+    } else {
+        for (; k < end; ++k) ripple(nb(k), 0);
+    }
 }
 
-template <int L>
+template <int L, bool MASKED = true>
 __device__ __forceinline__ void gather_counts(const uint32_t *__restrict__ adj,
                                               const uint32_t *__restrict__ sw, uint32_t beg,
                                               uint32_t end, uint32_t (&p)[L]) {
-    count_neighbours<L>(beg, end, [&](uint32_t k) {
+    count_neighbours<L, MASKED>(beg, end, [&](uint32_t k) {
         const uint32_t e = __ldg(adj + k);
         return __ldg(sw + (e & 0x7fffffffu)) ^ (uint32_t)((int32_t)e >> 31);
     }, p);
@@ -490,23 +511,23 @@ __device__ __forceinline__ int node_at(const A &a, int ch, int lane) {
     return a.order ? (int)__ldg(a.order + k) : k;
 }
 
-template <int L>
+template <int L, bool MASKED = true>
 __device__ __forceinline__ void gather_counts16(const uint16_t *__restrict__ adj,
                                                 const uint32_t *__restrict__ sw, uint32_t beg,
                                                 uint32_t end, uint32_t (&p)[L]) {
-    count_neighbours<L>(beg, end, [&](uint32_t k) {
+    count_neighbours<L, MASKED>(beg, end, [&](uint32_t k) {
         const uint32_t e = __ldg(adj + k);
         return __ldg(sw + (e & 0x7fffu)) ^ (0u - (e >> 15));
     }, p);
 }
 
-template <int L, typename A>
+template <int L, bool MASKED = true, typename A>
 __device__ __forceinline__ void gather_rows(const A &a, const uint32_t *__restrict__ sw, uint32_t beg,
                                             uint32_t end, uint32_t (&p)[L]) {
     if (a.adj16)
-        gather_counts16<L>(a.adj16, sw, beg, end, p);
+        gather_counts16<L, MASKED>(a.adj16, sw, beg, end, p);
     else
-        gather_counts<L>(a.adj, sw, beg, end, p);
+        gather_counts<L, MASKED>(a.adj, sw, beg, end, p);
 }
 
 // Degree-4 rows: the raw row of node i (16-bit: its four entries in .x, .y)
