@@ -1160,3 +1160,33 @@ def test_launch_shapes_are_bitwise_neutral(oracle, bench_graphs, monkeypatch, na
         for k in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
             assert np.array_equal(got[k], want[k]), (env, lay, k)
     assert len(seen) >= 3, seen
+
+
+@pytest.mark.parametrize("name,trials,sig,kernel", [
+    ("G1", 128, (0, 0, 0), "resident"),
+    ("G81", 4096, (0, 0, 0), "packed"),
+    ("G55", 4096, (0.5, 0.5, 0.5), "packed_bucket"),
+    ("G22", 1024, (0.0, 0.0, 0.5), "resident_timing"),
+    ("G60", 1000, (0.5, 0.5, 0.0), "packed")])
+def test_shortest_runs_match_oracle(oracle, bench_graphs, name, trials, sig, kernel):
+    """Two cycles (the shortest schedule the API admits) on every kernel
+    family at its production batch shape: the first cycle's sweep, the one
+    cut pass per phase and the last-cycle outputs (inputs, counts) meet with
+    no steady state in between; equal to the oracle bit for bit."""
+    g = bench_graphs(name)
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 2, 10)
+    seeds = [streams.trial_seed(8, k) for k in range(trials)]
+    vc = VariabilityConfig(*sig)
+    profs = None if vc.is_ideal else [
+        sample_variability(vc, g.n, np.random.default_rng(streams.profile_seed(s))) for s in seeds]
+    keys = [streams.run_key(s) for s in seeds]
+    b = _native.Batch(model, sch, keys, profile_rows=profile_rows(profs, model.n), graph=g)
+    plan = _native.Plan(b)
+    assert plan.info()["kernel"] == kernel, plan.info()
+    plan.run()
+    got = plan.download()
+    plan.close()
+    want = oracle.anneal_batch(model, sch, "psa", profs or VariabilityProfile.ideal(model.n), keys, graph=g)
+    for k in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
