@@ -1,0 +1,8 @@
+# shared-memory carveout of the launched sweep (PBSA_CARVEOUT: auto / driver / fixed)
+for cv in auto -1 30 45; do
+  if [ $cv = auto ]; then unset PBSA_CARVEOUT; else export PBSA_CARVEOUT=$cv; fi
+  echo "carveout=$cv"
+  timeout 200 python bench.py --steps 5 --no-var-leg --no-cpu-baseline --e2e-steps 1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('C4 %.4g philox %.4g' % (d['value'], d['philox']['value']))"
+  timeout 100 python tools/timing_run.py G55 0,0,0 4096 1000 | cut -c40-70
+  timeout 100 python tools/timing_run.py G81 0,0,0 1024 1000 | cut -c40-70
+done
