@@ -251,7 +251,10 @@ int enqueue_packed_phases(pbsa_plan &P, PackedKernel kern_up, PackedKernel kern_
                     a.dmax = P.dmax;
                     a.warps_per_word = P.warps_per_word;
                     a.cta_flush = (P.cta_flush && P.warps_per_word % pbsa::kPackedWarps == 0) ? 1 : 0;
-                a.cache_prefetch = P.phase_words < P.W ? 1 : 0;
+                // (L1 prefetch of the hash-cache tiles: off since the instruction trims
+                // of late round 2 -- C4 9.25e11 with it, 9.47e11 without; the loads hit
+                // L1 3 % of the time either way.  PBSA_CACHE_PREFETCH=1 enables it)
+                a.cache_prefetch = 0;
                 // (the bucket kernel keeps the 1-D grid: G55 C3 measured 7 % slower 2-D)
                 a.grid2d = a.cta_flush && !(P.bucket && pl.update);
                 if (const char *env = std::getenv("PBSA_GRID2D")) a.grid2d = a.cta_flush && env[0] == '1';

@@ -38,8 +38,8 @@ __device__ __forceinline__ void word_and_slot(const PackedArgs &a, int wib, int 
 }
 // PBSA_CACHE_PREFETCH: 1 prefetches a warp's first hash-cache tile into L1
 // ahead of the dependent-launch wait, 2 also each next tile; 0 none.  At run
-// time only for phased plans (the phase's cache is L2-resident: G81 C4
-// +4 %); unphased batches stream the cache and lose with it (G55 x 4096 -17 %)
+// time off by default (a.cache_prefetch: it measured +4 % on C4 mid-round 2
+// and -2.3 % after the instruction trims)
 #ifndef PBSA_CACHE_PREFETCH
 #define PBSA_CACHE_PREFETCH 2
 #endif

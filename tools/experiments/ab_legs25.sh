@@ -1,0 +1,4 @@
+# hash-cache load flavour without the L1 prefetch (PBSA_CACHE_LD 1 = ld.global.nc, 0 = .cs, 2 = default)
+timeout 200 python bench.py --steps 5 --no-var-leg --no-cpu-baseline --no-philox-leg --e2e-steps 1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print('C4 %.4g' % d['value'])"
+timeout 100 python tools/timing_run.py G81 0,0,0 1024 1000 | cut -c40-70
+timeout 100 python tools/timing_run.py G55 0,0,0 4096 1000 | cut -c40-70
