@@ -239,15 +239,28 @@ __device__ __forceinline__ uint32_t packed_hash_hi_c(uint32_t yl, uint32_t c1) {
 // Layout of a (word, 32-node chunk) tile of the hash cache (1024 entries of
 // 8 B): with PBSA_CACHE_PAIRS trial pairs are interleaved per lane,
 // [b / 2][lane][b % 2], so the plain sweep loads two trials with one 16-byte
-// load; else [b][lane] (the default: the pairs were neutral on C4 and made the
-// single-trial loads of TApSA / SpSA / the resident kernels half-coalesced,
-// G81 TApSA +8 % time).  cache_lane / cache_off give a lane's base and trial
-// b's offset in entries.
+// load, and every consumer loads pairs (cache_get); else [b][lane].
+// cache_lane / cache_off give a lane's base and trial b's offset in entries.
 #ifndef PBSA_CACHE_PAIRS
-#define PBSA_CACHE_PAIRS 0
+#define PBSA_CACHE_PAIRS 1
 #endif
 __host__ __device__ __forceinline__ int cache_lane(int lane) { return PBSA_CACHE_PAIRS ? 2 * lane : lane; }
 __host__ __device__ __forceinline__ int cache_off(int b) { return PBSA_CACHE_PAIRS ? (b >> 1) * 64 + (b & 1) : b * 32; }
+// Trial b's cache entry inside a loop over a lane's 32 trials.  With the pair
+// layout the 16-byte load of (b & ~1, b | 1) happens at the first trial of the
+// pair the loop visits (ASC: even b, else odd b) and `pr` carries it to the
+// second; CS selects evict-first loads (the resident kernels), else the
+// read-only path.
+template <bool ASC, bool CS = false>
+__device__ __forceinline__ uint2 cache_get(const uint2 *ctile, int b, uint4 &pr) {
+    if (!PBSA_CACHE_PAIRS) return CS ? __ldcs(ctile + cache_off(b)) : __ldg(ctile + cache_off(b));
+    if ((b & 1) == (ASC ? 0 : 1)) {
+        const uint4 *q = reinterpret_cast<const uint4 *>(ctile + cache_off(b & ~1));
+        pr = CS ? __ldcs(q) : __ldg(q);
+    }
+    return (b & 1) ? make_uint2(pr.z, pr.w) : make_uint2(pr.x, pr.y);
+}
+
 __device__ __forceinline__ uint32_t cache_c1(uint32_t hi) { return PBSA_CACHE_C1 ? hi : hi * 0x1CE4E5B9u; }
 __host__ __device__ __forceinline__ uint32_t cache_hi_entry(uint32_t yh) {
     return PBSA_CACHE_C1 ? yh * 0x1CE4E5B9u : yh;

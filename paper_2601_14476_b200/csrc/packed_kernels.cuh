@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                 const uint2 *ctile = CACHED ? a.acache + ((size_t)w * a.chunks + ch) * 1024 + cache_lane(lane) : nullptr;
                 uint32_t word = 0, exact = 0;
                 uint32_t X[4];  // NATIVE: the current Philox block (trials 4k .. 4k + 3)
+                uint4 cpair = make_uint4(0u, 0u, 0u, 0u);  // CACHED: the current trial pair
                 auto decide = [&](int b, float2 lv) {
                     int pop = 0;
 #pragma unroll
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                                              kNativeTagR, a.rk, X);
                         zh = X[b & 3];
                     } else if (CACHED) {
-                        const uint2 v = cache_ld(ctile + cache_off(b));
+                        const uint2 v = cache_get<true>(ctile, b, cpair);
                         zh = packed_hash_hi_c(v.x ^ count, cache_c1(v.y));
                     } else {
                         const uint2 kc = key[b];
@@ -309,6 +310,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                 uint32_t word = 0, tie = 0xffffffffu;
                 const uint32_t ui = (uint32_t)i;
                 uint32_t X[4];  // NATIVE: the current Philox block
+                uint4 cpair = make_uint4(0u, 0u, 0u, 0u);  // CACHED: the current trial pair
 #pragma unroll
                 for (int b = 31; b >= 0; --b) {
                     const int k = b >> 2, j = b & 3;
@@ -324,7 +326,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                                              kNativeTagR, a.rk, X);
                         native_decide(X[b & 3], t, word);
                     } else if (CACHED) {
-                        const uint2 v = cache_ld(ctile + cache_off(b));
+                        const uint2 v = cache_get<false>(ctile, b, cpair);
                         tie = min(tie, packed_decide_y(v.x ^ count, cache_c1(v.y), t, word));
                     } else {
                         const uint2 kc = key[b];
@@ -404,6 +406,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                 // loads are issued together before the group's decisions.
                 uint32_t word = 0, tie = 0xffffffffu;
                 uint32_t X[4];  // NATIVE: the current Philox block of the activation draws
+                uint4 cpair = make_uint4(0u, 0u, 0u, 0u);  // CACHED: the current trial pair
                 // groups of GS trials (native: 4, its stalled drives need both threshold words)
                 constexpr int GS = NATIVE ? 4 : 8;
                 for (int gq = 32 / GS - 1; gq >= 0; --gq) {
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                                                  kNativeTagR, a.rk, X);
                             native_decide(X[b & 3], t, word);
                         } else if (CACHED) {
-                            const uint2 v = cache_ld(ctile + cache_off(b));
+                            const uint2 v = cache_get<false>(ctile, b, cpair);
                             tie = min(tie, packed_decide_y(v.x ^ count, cache_c1(v.y), t, word));
                         } else {
                             const uint2 kc = key[b];
@@ -538,13 +541,8 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                         uint32_t dummy;
                         asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
                             : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
-                    } else if (CACHED && PBSA_CACHE_PAIRS) {
-                        // one 16-byte load per trial pair (b odd: trials b, b - 1)
-                        if (b & 1) cpair = cache_ld2(ctile + cache_off(b - 1));
-                        const uint32_t vx = (b & 1) ? cpair.z : cpair.x, vy = (b & 1) ? cpair.w : cpair.y;
-                        tie = min(tie, packed_decide_n2(vx ^ count, cache_c1(vy), t, word));
                     } else if (CACHED) {
-                        const uint2 v = cache_ld(ctile + cache_off(b));
+                        const uint2 v = cache_get<false>(ctile, b, cpair);
                         tie = min(tie, packed_decide_n2(v.x ^ count, cache_c1(v.y), t, word));
                     } else {
                         const uint2 kc = key[b];

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                 const float2 *pr = a.prof + (size_t)w * 32 * a.n + i;
                 uint32_t word = 0, exact = 0;
                 uint32_t X[4];
+                uint4 cpair = make_uint4(0u, 0u, 0u, 0u);  // CACHED: the current trial pair
 #pragma unroll
                 for (int b = 0; b < 32; ++b) {
                     int pop = 0;
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                             philox4x32_10_rk(ui, count, grp + (uint32_t)(b >> 2), kNativeTagR, a.rk, X);
                         zh = X[b & 3];
                     } else if (CACHED) {
-                        const uint2 v = __ldcs(ctile + cache_off(b));
+                        const uint2 v = cache_get<true, true>(ctile, b, cpair);
                         zh = packed_hash_hi_c(v.x ^ count, cache_c1(v.y));
                     } else {
                         const uint2 kc = key[b];
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                 const uint32_t rb = (uint32_t)__cvta_generic_to_shared(sthr) + 8u * (uint32_t)off;
                 uint32_t word = 0, tie = 0xffffffffu;
                 uint32_t X[4];
+                uint4 cpair = make_uint4(0u, 0u, 0u, 0u);  // CACHED: the current trial pair
 #pragma unroll
                 for (int b = 31; b >= 0; --b) {
                     const int k = b >> 2, j = b & 3;
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                             philox4x32_10_rk(ui, count, grp + (uint32_t)(b >> 2), kNativeTagR, a.rk, X);
                         native_decide(X[b & 3], t, word);
                     } else if (CACHED) {
-                        const uint2 v = __ldcs(ctile + cache_off(b));
+                        const uint2 v = cache_get<false, true>(ctile, b, cpair);
                         tie = min(tie, packed_decide_y(v.x ^ count, cache_c1(v.y), t, word));
                     } else {
                         const uint2 kc = key[b];
@@ -269,6 +271,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
             }
             const uint2 *tb = sthr + (a.dmax - d);
             uint32_t X[4];
+            uint4 cpair = make_uint4(0u, 0u, 0u, 0u);  // CACHED: the current trial pair
 #pragma unroll
             for (int b = 31; b >= 0; --b) {
                 uint2 t;
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                     asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
                         : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
                 } else if (CACHED) {
-                    const uint2 v = __ldcs(ctile + cache_off(b));
+                    const uint2 v = cache_get<false, true>(ctile, b, cpair);
                     tie = min(tie, packed_decide_n2(v.x ^ count, cache_c1(v.y), t, word));
                 } else {
                     const uint2 kc = key[b];
