@@ -162,9 +162,6 @@ __device__ __forceinline__ uint32_t mulhi(uint32_t a, uint32_t b) { return __umu
 #ifndef PBSA_WIDE_MUL
 #define PBSA_WIDE_MUL 1
 #endif
-#ifndef PBSA_WIDE_Y
-#define PBSA_WIDE_Y 0
-#endif
 template <bool WIDE = false>
 __device__ __forceinline__ void mul_lohi(uint32_t a, uint32_t m, uint32_t add, uint32_t &lo, uint32_t &hi) {
     if (WIDE) {
@@ -207,13 +204,12 @@ __device__ __forceinline__ uint32_t packed_decide_y(uint32_t yl, uint32_t c1, ui
     constexpr uint32_t M1L = 0x1CE4E5B9u, M1H = 0xBF58476Du;
     constexpr uint32_t M2L = 0x32684F87u, M2H = 0x94D4A04Cu;
     uint32_t zl, zh;
-    mul_lohi<PBSA_WIDE_Y != 0>(yl, M1L, yl * M1H + c1, zl, zh);
+    mul_lohi(yl, M1L, yl * M1H + c1, zl, zh);
     yl = zl ^ __funnelshift_r(zl, zh, 27);
     const uint32_t yh = zh ^ mulhi(zh, 1u << 5);
     zh = mulhi(yl, M2L) + yl * M2H + yh * M2L;
-    uint32_t dummy;
-    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %4;"
-        : "=r"(dummy), "=r"(word) : "r"(zh), "r"(t.x), "r"(word));
+    asm("{\n\t.reg .u32 lo;\n\tadd.cc.u32 lo, %1, %2;\n\taddc.u32 %0, %3, %3;\n\t}"
+        : "=r"(word) : "r"(zh), "r"(t.x), "r"(word));
     return zh ^ t.y;
 }
 
@@ -357,9 +353,8 @@ __device__ __forceinline__ uint32_t packed_second_decide_n2(uint32_t sl, uint32_
 // Native decision: shift (X >= T) into `word` as the carry of X + (2^32 - T),
 // t = (lo, hi) of the 33-bit 2^32 - T (T = 2^32 never fires, T = 0 always).
 __device__ __forceinline__ void native_decide(uint32_t X, uint2 t, uint32_t &word) {
-    uint32_t dummy;
-    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
-        : "=r"(dummy), "=r"(word) : "r"(X), "r"(t.x), "r"(word), "r"(word + t.y));
+    asm("{\n\t.reg .u32 lo;\n\tadd.cc.u32 lo, %1, %2;\n\taddc.u32 %0, %3, %4;\n\t}"
+        : "=r"(word) : "r"(X), "r"(t.x), "r"(word), "r"(word + t.y));
 }
 
 // Bit-sliced counter: add the L-bit per-trial numbers x[] into C[] (CL planes).

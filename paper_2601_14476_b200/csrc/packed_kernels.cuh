@@ -538,9 +538,7 @@ __global__ void __launch_bounds__(kPackedThreads, (packed_min_blocks<L, UPDATE, 
                         if ((b & 3) == 3)
                             philox4x32_10_rk(ui, count, a.ngroup + 8u * (uint32_t)w + (uint32_t)(b >> 2),
                                              kNativeTagR, a.rk, X);
-                        uint32_t dummy;
-                        asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
-                            : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
+                        native_decide(X[b & 3], t, word);
                     } else if (CACHED) {
                         const uint2 v = cache_get<false>(ctile, b, cpair);
                         tie = min(tie, packed_decide_n2(v.x ^ count, cache_c1(v.y), t, word));

@@ -403,7 +403,6 @@ void packed_launch_shape(pbsa_plan &P, int device, int64_t n, int64_t dmax) {
     int sm_count = 148, l2_bytes = 0;
     CK(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
     CK(cudaDeviceGetAttribute(&l2_bytes, cudaDevAttrL2CacheSize, device));
-    const int sms = sm_count;
     // (SpSA streams its per-p-bit drive index, which no phase keeps in L2: unphased)
     // (native Philox draws keep no cache, so nothing gains from phases: measured
     // G81 x 4096 9.1e11 updates/s unphased vs 7.8e11 in phases of 13)

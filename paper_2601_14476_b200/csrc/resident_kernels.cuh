@@ -289,9 +289,7 @@ __global__ void __launch_bounds__(512, 1) resident_sweep(ResidentArgs a) {
                 if (NATIVE) {
                     if ((b & 3) == 3)
                         philox4x32_10_rk(ui, count, grp + (uint32_t)(b >> 2), kNativeTagR, a.rk, X);
-                    uint32_t dummy;
-                    asm("add.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %4, %5;"
-                        : "=r"(dummy), "=r"(word) : "r"(X[b & 3]), "r"(t.x), "r"(word), "r"(word + t.y));
+                    native_decide(X[b & 3], t, word);
                 } else if (CACHED) {
                     const uint2 v = cache_get<false, true>(ctile, b, cpair);
                     tie = min(tie, packed_decide_n2(v.x ^ count, cache_c1(v.y), t, word));
