@@ -1144,10 +1144,16 @@ def test_launch_shapes_are_bitwise_neutral(oracle, bench_graphs, monkeypatch, na
     W = trials // 32
     shapes = [{}, {"PBSA_PACKED_PHASE_WORDS": "0", "PBSA_BALANCE_CHUNKS": "0"},
               {"PBSA_PACKED_PHASE_WORDS": str(max(1, W // 3)), "PBSA_BALANCE_CHUNKS": "1"},
-              {"PBSA_PACKED_PHASE_WORDS": str(max(1, W // 2 + 1)), "PBSA_BALANCE_CHUNKS": "0"}]
+              {"PBSA_PACKED_PHASE_WORDS": str(max(1, W // 2 + 1)), "PBSA_BALANCE_CHUNKS": "0"},
+              # the 1-D grid (per-warp division) and the L1 tile prefetch paths
+              {"PBSA_GRID2D": "0", "PBSA_CACHE_PREFETCH": "1"},
+              # one cut flush per warp instead of per block (warps per word not a multiple of 4)
+              {"PBSA_CTA_FLUSH": "0", "PBSA_WARPS_PER_WORD": "37"}]
+    knobs = ("PBSA_PACKED_PHASE_WORDS", "PBSA_BALANCE_CHUNKS", "PBSA_GRID2D", "PBSA_CACHE_PREFETCH",
+             "PBSA_CTA_FLUSH", "PBSA_WARPS_PER_WORD")
     seen = set()
     for env in shapes:
-        for k in ("PBSA_PACKED_PHASE_WORDS", "PBSA_BALANCE_CHUNKS"):
+        for k in knobs:
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
