@@ -1196,3 +1196,28 @@ def test_shortest_runs_match_oracle(oracle, bench_graphs, name, trials, sig, ker
     want = oracle.anneal_batch(model, sch, "psa", profs or VariabilityProfile.ideal(model.n), keys, graph=g)
     for k in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
         assert np.array_equal(got[k], want[k]), k
+
+
+@pytest.mark.parametrize("env", [{}, {"PBSA_GRID2D": "1"}, {"PBSA_BUCKET": "0"}])
+def test_bucket_kernel_shapes_match_oracle(oracle, bench_graphs, monkeypatch, env):
+    """The period-bucket kernel on the 2-D grid (default 1-D) and the
+    fallback timing kernel, on a timing-spread batch: equal to the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = bench_graphs("G55")
+    model = maxcut_to_ising(g)
+    sch = derive_schedule(model, 4, 10)
+    seeds = [streams.trial_seed(9, k) for k in range(256)]
+    vc = VariabilityConfig(0.5, 0.5, 0.5)
+    profs = [sample_variability(vc, g.n, np.random.default_rng(streams.profile_seed(s))) for s in seeds]
+    keys = [streams.run_key(s) for s in seeds]
+    b = _native.Batch(model, sch, keys, profile_rows=profile_rows(profs, model.n), graph=g)
+    plan = _native.Plan(b)
+    want_kernel = "packed_timing" if env.get("PBSA_BUCKET") == "0" else "packed_bucket"
+    assert plan.info()["kernel"] == want_kernel, plan.info()
+    plan.run()
+    got = plan.download()
+    plan.close()
+    want = oracle.anneal_batch(model, sch, "psa", profs, keys, graph=g)
+    for k in ("spins", "inputs", "counts", "energy_trace", "cut_trace", "best_cut"):
+        assert np.array_equal(got[k], want[k]), k
