@@ -2,6 +2,8 @@
 // (plain / TApSA / SpSA / varied profile, replayed or Philox draws) and the
 // timing-spread sweep.  Instantiated per degree width L in kernels_L*.cu.
 #pragma once
+#include <type_traits>
+
 #include "device_common.cuh"
 
 namespace pbsa {
@@ -870,14 +872,31 @@ __global__ void __launch_bounds__(kPackedThreads, L <= 3 ? PBSA_BUCKET_MIN_BLOCK
         const uint32_t *sw = a.sold + (size_t)w * a.n;
         const bool reg4 = L >= 3 && a.reg4;
         const size_t ncl1 = (size_t)a.nclass + 1;
-        // class bounds of the lane's fired class k0 + lane in tile ch, packed beg | end << 16
-        auto bounds = [&](int ch, int k0) -> uint32_t {
+        // class bounds (begin, end) of the lane's fired class k0 + lane in tile ch.
+        // The next tile's are loaded a tile ahead; on the tori (L <= 3) they stay
+        // the two loaded values until used (combining them at once waited on the
+        // loads: G81 C3 +1 %), otherwise packed beg | end << 16 (one register
+        // fewer: the L = 4 kernel keeps 7 blocks per SM, G55 C3 +6 %)
+        using Bounds = std::conditional_t<(L <= 3), uint2, uint32_t>;
+        auto bounds = [&](int ch, int k0) -> Bounds {
             const int k = k0 + lane;
-            if (ch >= a.chunks || k >= a.ndiv) return 0u;
+            if (ch >= a.chunks || k >= a.ndiv) return Bounds{};
             const uint16_t *row = a.boff + ((size_t)w * a.chunks + ch) * ncl1 + sdiv[k];
-            return (uint32_t)__ldg(row) | ((uint32_t)__ldg(row + 1) << 16);
+            if constexpr (L <= 3)
+                return make_uint2((uint32_t)__ldg(row), (uint32_t)__ldg(row + 1));
+            else
+                return (uint32_t)__ldg(row) | ((uint32_t)__ldg(row + 1) << 16);
         };
-        uint32_t bb_nx = bounds(q, 0);
+        auto bounds_beg_end = [](Bounds v, int &beg, int &end) {
+            if constexpr (L <= 3) {
+                beg = (int)v.x;
+                end = (int)v.y;
+            } else {
+                beg = (int)(v & 0xFFFFu);
+                end = (int)(v >> 16);
+            }
+        };
+        Bounds bb_nx = bounds(q, 0);
         uint4 e_nx = make_uint4(0u, 0u, 0u, 0u);
         uint32_t own_nx = 0;
         if (reg4 && q < a.chunks && q * 32 + lane < a.n) {
@@ -894,8 +913,10 @@ __global__ void __launch_bounds__(kPackedThreads, L <= 3 ? PBSA_BUCKET_MIN_BLOCK
             int F = 0;
             uint32_t staged = 0;  // bytes in flight
             for (int k0 = 0; k0 < a.ndiv; k0 += 32) {
-                const uint32_t bb = k0 == 0 ? bb_nx : bounds(ch, k0);
-                const int beg = (int)(bb & 0xFFFFu), sz = (int)(bb >> 16) - beg;
+                const Bounds bb = k0 == 0 ? bb_nx : bounds(ch, k0);
+                int beg, bend;
+                bounds_beg_end(bb, beg, bend);
+                const int sz = bend - beg;
                 int incl = sz;
 #pragma unroll
                 for (int sft = 1; sft < 32; sft <<= 1) {
