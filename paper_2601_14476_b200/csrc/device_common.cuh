@@ -550,6 +550,17 @@ __device__ __forceinline__ uint4 load_row4(const A &a, int i) {
 }
 
 // 16-bit degree-4 row (entries e.x lo/hi, e.y lo/hi): as gather_counts_row4
+// bit-sliced x0 + x1 + x2 + x3 (<= 4 < 2^L, L >= 3 since dmax = 4)
+template <int L>
+__device__ __forceinline__ void add4_planes(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3, uint32_t (&p)[L]) {
+    const uint32_t s01 = x0 ^ x1, c01 = x0 & x1, s23 = x2 ^ x3, c23 = x2 & x3;
+    const uint32_t s = s01 ^ s23, cs = s01 & s23;
+    const uint32_t t = c01 ^ c23 ^ cs;
+    const uint32_t f = (c01 & c23) | (cs & (c01 ^ c23));
+#pragma unroll
+    for (int r = 0; r < L; ++r) p[r] = r == 0 ? s : r == 1 ? t : r == 2 ? f : 0u;
+}
+
 template <int L>
 __device__ __forceinline__ void gather_counts_row4_16(const uint4 e, const uint32_t *__restrict__ sw,
                                                       uint32_t (&p)[L]) {

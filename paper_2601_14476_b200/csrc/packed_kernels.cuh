@@ -826,6 +826,9 @@ __device__ __forceinline__ void bulk_copy_g2s(void *dst, const void *src, uint32
 #ifndef PBSA_BK_ILP
 #define PBSA_BK_ILP 1
 #endif
+#ifndef PBSA_BK_NB_EARLY
+#define PBSA_BK_NB_EARLY 1
+#endif
 template <int L, bool NATIVE = false>
 __global__ void __launch_bounds__(kPackedThreads, L <= 3 ? PBSA_BUCKET_MIN_BLOCKS_L3 : PBSA_BUCKET_MIN_BLOCKS)
     packed_sweep_bucket(PackedArgs a) {
@@ -908,6 +911,16 @@ __global__ void __launch_bounds__(kPackedThreads, L <= 3 ? PBSA_BUCKET_MIN_BLOCK
             const int i = node_at(a, ch, lane);
             const bool valid = i < a.n;
             const uint4 *src = a.brec + ((size_t)w * a.chunks + ch) * 1024;
+            // degree-4 16-bit rows: the tile's four neighbour words are loaded
+            // before the segment scan, which then runs while they are in flight
+            uint32_t xr[4] = {0u, 0u, 0u, 0u};
+            const bool early_nb = PBSA_BK_NB_EARLY && L <= 3 && reg4 && a.adj16 && valid;  // (L > 3: registers)
+            if (early_nb) {
+                xr[0] = __ldg(sw + (e_nx.x & 0x7fffu));
+                xr[1] = __ldg(sw + ((e_nx.x >> 16) & 0x7fffu));
+                xr[2] = __ldg(sw + (e_nx.y & 0x7fffu));
+                xr[3] = __ldg(sw + ((e_nx.y >> 16) & 0x7fffu));
+            }
             // 1. the tile's fired segments (sizes even): prefix sums, and the
             // first kBucketStage records bulk-copied into the staging list
             int F = 0;
@@ -951,7 +964,11 @@ __global__ void __launch_bounds__(kPackedThreads, L <= 3 ? PBSA_BUCKET_MIN_BLOCK
                     e_nx = load_row4(a, ni);
                     own_nx = __ldg(sw + ni);
                 }
-                if (valid) {
+                if (early_nb) {
+                    add4_planes<L>(xr[0] ^ (0u - ((er.x >> 15) & 1u)), xr[1] ^ (uint32_t)((int32_t)er.x >> 31),
+                                   xr[2] ^ (0u - ((er.y >> 15) & 1u)), xr[3] ^ (uint32_t)((int32_t)er.y >> 31), p);
+                    d = 4;
+                } else if (valid) {
                     gather_row4<L>(a, er, sw, p);
                     d = 4;
                 } else {
